@@ -1,0 +1,179 @@
+/*
+ * wqb200.h -- C-ABI of the B200 (sm_100a, FP64) IgA-SGBEM V-matrix assembly.
+ *
+ * This is the drop-in boundary beneath the reference's Python entry points in
+ * wqbem.assembly (reference: pkg/src/wqbem/assembly.py).  The reference has no
+ * FFI of its own; each entry point below names the reference function whose
+ * O(N^2) work it replaces (file:line under /root/reference/pkg/src/wqbem/).
+ *
+ * Conventions
+ *   - All buffers are caller-allocated, contiguous DEVICE memory (FP64 values,
+ *     int64 indices), row-major.  No torch types cross this boundary.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and performs no host synchronisation.
+ *   - Return 0 on success, a negative WQ_E* code on failure; the message is
+ *     available from wq_last_error() (thread-local).
+ *   - Geometry failures detected on the device (R <= 0 on the kernel grid,
+ *     geometry.py:246-247) are OR-ed into *flag (device int); the caller maps
+ *     a non-zero flag to GeometryError after synchronising.
+ *   - Results are deterministic: no floating-point atomics anywhere.
+ */
+#ifndef WQB200_H
+#define WQB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WQ_OK 0
+#define WQ_EINVAL (-1)
+#define WQ_ECUDA (-2)
+#define WQ_EUNSUPPORTED (-3)
+
+#define WQ_FLAG_R_NONPOSITIVE 1
+
+/* rows/cols per CTA output tile of wq_ik1 / wq_ik2_circ (callers size max_span with it) */
+#define WQ_TILE 32
+
+/* K1 parameter-distance modes (geometry.py:127-139) */
+#define WQ_K1_TABLE 0        /* 1/p^2 looked up by node-index gap (exactly uniform nodes) */
+#define WQ_K1_OPEN 1         /* p = |t - s| */
+#define WQ_K1_CLOSED 2       /* p = (L/pi)|sin(pi |t - s| / L)| */
+
+/* Smooth part: nodes, banded rule matrix G = W*J (assembly.py:160) */
+typedef struct {
+  int64_t n_rows;          /* N: test functions (rows of G)                   */
+  int64_t nq;              /* number of shared quadrature nodes               */
+  int64_t wg;              /* padded band width of G                          */
+  int64_t closed;          /* 1 on closed curves                              */
+  int64_t k1_mode;         /* WQ_K1_*                                         */
+  double period;           /* L = b - a                                       */
+  const double* s;         /* (nq) node parameters                            */
+  const double* fx;        /* (nq) f(s) x                                     */
+  const double* fy;        /* (nq) f(s) y                                     */
+  const double* J;         /* (nq) parametric speed                           */
+  const double* invp2;     /* (nq) 1/p^2 per index gap (WQ_K1_TABLE) or NULL   */
+  const int64_t* g_start;  /* (N) unwrapped first node of row i (monotone)    */
+  const double* g_w;       /* (N, wg) G[i, (g_start[i]+w) mod nq]             */
+} wq_smooth_t;
+
+/* Version / identification. */
+int wq_version(void);
+const char* wq_last_error(void);
+
+/* FP64 pipe probe for the roofline denominator: blocks x 256 threads x
+ * iters x 64 DFMA (2 flops each).  out: >= blocks doubles (never written
+ * in practice). */
+int wq_fp64_peak(int64_t iters, int blocks, double* out, void* stream);
+
+/*
+ * IK1 rows/cols block (replaces assemble_ik1, assembly.py:175-183, with the
+ * K1 grid of geometry.py:225-248 evaluated in-kernel and never stored):
+ *   X[i, j] (+)= sum_q sum_r G[i,q] K1(eta_q, eta_r) G[j,r]
+ * for i in [row0,row1), j in [col0,col1); X points at element (row0, col0),
+ * leading dimension ldx.  accumulate != 0 adds into X.
+ * max_span = max over tiles of the node span (host-computed, see Python).
+ */
+int wq_ik1(const wq_smooth_t* sm, int64_t row0, int64_t row1, int64_t col0, int64_t col1,
+           double* X, int64_t ldx, int accumulate, int64_t max_span, int* flag, void* stream);
+
+/*
+ * Gap-indexed pair log-moment table (replaces uniform_pair_log_moments,
+ * quadrature.py:472-504 / _unit_pair_stack :441-469):
+ *   far gaps: 30x30 Gauss of ln|v-u-delta| (quadrature.py:413-438);
+ *   |gap| <= 1: analytic closed-form unit table supplied by the host
+ *   (near_unit, 3 x (da+1) x (db+1), rows keff = -1, 0, +1);
+ *   closed meshes: + periodic correction ln|sinc| (quadrature.py:253-256,464-467);
+ *   then M_h = h^(2+a+b) (M_1 + ln h c_a c_b).
+ * n_gap = nel (closed, index (f-e) mod nel) or 2 nel - 1 (open, f-e+nel-1).
+ * gx, gw: Gauss nodes/weights on (-1/2, 1/2), n_gauss of them.
+ */
+int wq_pair_table(int64_t nel, int closed, int da, int db, double h,
+                  const double* near_unit, const double* gx, const double* gw, int n_gauss,
+                  const double* ca, const double* cb, double* m2, void* stream);
+
+/* Closed uniform simple-knot meshes: circulant log-part tables.
+ *   Z[g][al]  = sum_b sum_be M2[(g-b) mod n][al][be] v0[be][b]
+ *   dd[k]     = sum_a sum_{al<=d} v0[al][a] Z[(k+a) mod n][al]       (D circulant)
+ *   Zp[g][al] = sum_{|k|<=K} Z[(g+k) mod n][al] hinv[k]               (Theta H^{-1})
+ *   ff        = hinv * dd * hinv                                       (H^{-1} D H^{-1})
+ * hinv_taps has 2K+1 entries, hinv_taps[K+k] = H^{-1}[0,k].
+ * work: n doubles of scratch.
+ */
+int wq_circ_tables(int64_t n, int da, int db, const double* m2, const double* v0,
+                   const double* hinv_taps, int64_t K, double* Zp, double* ff, double* work,
+                   double* Zwork, void* stream);
+
+/* Log-part description shared by the circulant path and the general path. */
+typedef struct {
+  int64_t n_rows;          /* N  (coarse functions)                          */
+  int64_t n_fine;          /* N_E (fine functions) = n_el on closed meshes    */
+  int64_t da;              /* P = p + 12 (row polynomial degree)              */
+  int64_t tu;              /* elements per coarse support (p+1)*nref          */
+  int64_t ws;              /* padded band width of S columns                  */
+  const int64_t* e_start;  /* (N) unwrapped first fine element of supp(B_i)   */
+  const double* U;         /* (N, tu, da+1): u[e_start+a][:, a_i]             */
+  const int64_t* s_start;  /* (N) unwrapped first fine row of column i of S   */
+  const double* s_w;       /* (N, ws): S[s_start+t, i]                        */
+} wq_logpart_t;
+
+/*
+ * Circulant log part (replaces assemble_ik2, assembly.py:186-245, X-form):
+ *   Phi[m,i] = 2 sum_a sum_al U[i][a][al] Zp[(m - e_start[i] - a) mod n][al]
+ *              - sum_t S[s_start[i]+t, i] ff[(m - s_start[i] - t) mod n]
+ *   X[i, j] (+)= sum_t S[s_start[j]+t, j] Phi[s_start[j]+t, i]
+ * i in [row0,row1), j in [col0,col1); X points at (row0,col0), ld ldx.
+ */
+int wq_ik2_circ(const wq_logpart_t* lp, const double* Zp, const double* ff,
+                int64_t row0, int64_t row1, int64_t col0, int64_t col1,
+                double* X, int64_t ldx, int accumulate, void* stream);
+
+/* General (open-mesh) log part, dense intermediates. */
+typedef struct {
+  int64_t n_rows, n_fine, n_el, n_gap, da, db, closed;
+  int64_t wu;                 /* max (e,a) incidences per coarse function      */
+  int64_t wv;                 /* max (f,b) incidences per fine function        */
+  const int64_t* u_el;        /* (N, wu)  element of incidence, -1 = none      */
+  const int64_t* u_loc;       /* (N, wu)  local index a                         */
+  const int64_t* v_el;        /* (N_E, wv)                                      */
+  const int64_t* v_loc;       /* (N_E, wv)                                      */
+  const double* u;            /* (n_el, da+1, pu+1) coefficients               */
+  int64_t pu;                 /* coarse degree p                                */
+  const double* v;            /* (n_el, db+1, db+1)                             */
+  const double* m2;           /* (n_gap, da+1, db+1)                            */
+} wq_pairs_t;
+
+/* Theta^T (N_E x N) and D (N_E x N_E) by element-pair gathers (assembly.py:215-232). */
+int wq_theta_t(const wq_pairs_t* pp, double* thetaT, void* stream);
+int wq_dmat(const wq_pairs_t* pp, double* D, void* stream);
+
+/* In-place banded SPD solve on every column of X (n x ncols, ld ldx):
+ * X <- H^{-1} X with H = L L^T, Lb[k][j] = L[k][k-j], j = 0..bw. */
+int wq_band_solve_cols(int64_t n, int64_t bw, const double* Lb, double* X, int64_t ncols,
+                       int64_t ldx, void* stream);
+
+/* out = in^T for an (rows x cols) matrix. */
+int wq_transpose(const double* in, int64_t rows, int64_t cols, double* out, void* stream);
+
+/* Phi[m][i] = alpha * P[m][i] - sum_t F[m][(s_start[i]+t) mod nf] S[s_start[i]+t, i]  (in place on P) */
+int wq_gather_fs(const wq_logpart_t* lp, double alpha, const double* F, double* P, void* stream);
+
+/* X[j][i] (+)= sum_t S[s_start[j]+t, j] Phi[(s_start[j]+t) mod nf][i], all i, j rows [row0,row1). */
+int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64_t row1,
+                  double* X, int64_t ldx, int accumulate, void* stream);
+
+/* Epilogue (assembly.py:262-271): A = alpha * (X + X^T), in place, n x n. */
+int wq_symmetrize(double* X, int64_t n, double alpha, void* stream);
+
+/* max |X| and max |X - X^T| (symmetry defect numerator), out[0..1]. */
+int wq_absmax_defect(const double* X, int64_t n, double* out, void* stream);
+
+/* Weighted RHS (assembly.py:312-319): b[i] = sum_w G[i, w] g[(g_start[i]+w) mod nq]. */
+int wq_b1w(const wq_smooth_t* sm, const double* g, double* b, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,653 @@
+"""CPU ORACLE (test infrastructure only) -- numpy restatement of the reference
+IgA-SGBEM weighted-quadrature V-matrix assembly (``wqbem``, arXiv 1703.10016).
+
+This module is the CHECKER.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import it; the
+product package ``paper_1703_10016_b200`` never does, and fails loudly when
+its CUDA library is missing.
+
+Parity pinning: every function below is checked against golden fixtures
+produced by running the unmodified reference (``tests/golden/make_golden.py``)
+and against the reference's own independent oracles
+(``pkg/tests/oracles.py:64-155``, stored in ``tests/golden/naive_*.npz``).
+
+Two layers:
+
+* ``dense_*``: a literal restatement of the reference algorithm
+  (dense G, dense K1 grid, element-pair tensors, QR fit) for small N;
+* ``xform_*``: the scalable restatement used as the oracle where the
+  reference cannot run (config 4 row blocks): the X-form
+  ``X = IK1 + (2 Theta - C^T D) C``, ``A = -(X + X^T)/(4 pi)`` with the fit
+  ``C = H^{-1} S`` through the banded normal equations, and the
+  circulant specialisation on closed uniform simple-knot meshes.
+
+Citations are ``file:line`` under ``/root/reference/pkg/src/wqbem/``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from functools import lru_cache
+from math import comb
+
+import numpy as np
+import scipy.linalg
+from scipy.interpolate import BSpline
+
+TWO_PI = 2.0 * np.pi
+JFIT_DEGREE = 12          # assembly.py:82
+DIAG_REL = 1e-7           # geometry.py:37
+PAIR_FAR_ORDER = 30       # quadrature.py:369
+PERIODIC_CORR_ORDER = 24  # quadrature.py:53
+DEDUP_RTOL = 1e-12        # quadrature.py:47
+GRADE_LEVELS, GRADE_RATIO = 14, 0.3  # assembly.py:76-77
+
+
+# --------------------------------------------------------------------------
+# splines (splines.py:41-257)
+# --------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class Basis:
+    """Degree + extended knot vector + closed flag (splines.py:41-152)."""
+
+    degree: int
+    knots: np.ndarray
+    closed: bool = False
+
+    @property
+    def nplain(self):
+        return len(self.knots) - self.degree - 1
+
+    @property
+    def a(self):
+        return float(self.knots[self.degree])
+
+    @property
+    def b(self):
+        return float(self.knots[self.nplain])
+
+    @property
+    def length(self):
+        return self.b - self.a
+
+    @property
+    def seam_multiplicity(self):  # splines.py:74-78
+        tol = 1e-12 * max(float(self.knots[-1] - self.knots[0]), 1.0)
+        return int(np.count_nonzero(np.abs(self.knots - self.a) <= tol))
+
+    @property
+    def wrap(self):  # splines.py:80-83
+        return self.degree + 1 - self.seam_multiplicity if self.closed else 0
+
+    @property
+    def dim(self):
+        return self.nplain - self.wrap
+
+    def _bd(self):
+        inner = self.knots[self.degree: self.nplain + 1]
+        return np.unique(inner, return_counts=True)
+
+    @property
+    def breakpoints(self):
+        return self._bd()[0]
+
+    @property
+    def multiplicities(self):
+        return self._bd()[1]
+
+    @property
+    def elements(self):
+        bp = self.breakpoints
+        return np.column_stack([bp[:-1], bp[1:]])
+
+    @property
+    def n_elements(self):
+        return len(self.breakpoints) - 1
+
+    def min_smoothness(self):  # splines.py:131-143
+        _, mult = self._bd()
+        inner = list(mult[1:-1])
+        if self.closed:
+            inner.append(self.seam_multiplicity)
+        return self.degree if not inner else self.degree - max(inner)
+
+
+def as_basis(obj) -> Basis:
+    return Basis(int(obj.degree), np.asarray(obj.knots, float), bool(obj.closed))
+
+
+def open_basis(degree, breakpoints, multiplicities=None) -> Basis:
+    """Clamped knot vector (splines.py:168-196)."""
+    bp = np.asarray(breakpoints, float)
+    inner = bp[1:-1]
+    mult = np.ones(len(inner), int) if multiplicities is None else np.asarray(multiplicities, int)
+    if len(mult) == len(bp):
+        mult = mult[1:-1]
+    knots = np.concatenate([np.full(degree + 1, bp[0]), np.repeat(inner, mult),
+                            np.full(degree + 1, bp[-1])])
+    return Basis(degree, knots, False)
+
+
+def cyclic_basis(degree, breakpoints, multiplicities=None) -> Basis:
+    """Periodic knot layout (splines.py:199-236)."""
+    bp = np.asarray(breakpoints, float)
+    mult = np.ones(len(bp), int) if multiplicities is None else np.asarray(multiplicities, int)
+    period = bp[-1] - bp[0]
+    one = np.repeat(bp[:-1], mult[:-1])
+    dim = len(one)
+    ms = int(mult[0])
+    start = dim + ms - 1 - degree
+    full = np.concatenate([one - period, one, one + period])
+    return Basis(degree, full[start: start + dim + 2 * degree + 2 - ms], True)
+
+
+def refine(basis: Basis, nref: int) -> Basis:
+    """Uniform refinement with simple new knots (splines.py:239-257)."""
+    bp = basis.breakpoints
+    mult = basis.multiplicities.copy()
+    pieces = [np.linspace(lo, hi, nref + 1)[:-1] for lo, hi in zip(bp[:-1], bp[1:])]
+    nbp = np.concatenate(pieces + [bp[-1:]])
+    nm = np.ones(len(nbp), int)
+    nm[::nref] = mult
+    if basis.closed:
+        nm[0] = nm[-1] = basis.seam_multiplicity
+        return cyclic_basis(basis.degree, nbp, nm)
+    return open_basis(basis.degree, nbp, nm)
+
+
+def design(basis: Basis, pts) -> np.ndarray:
+    """Dense (n_pts, dim) basis values folded onto the cyclic functions
+    (assembly.py:101-108)."""
+    pts = np.clip(np.atleast_1d(np.asarray(pts, float)), basis.a, basis.b)
+    mat = BSpline.design_matrix(pts, basis.knots, basis.degree).toarray()
+    if basis.closed:
+        mat[:, : basis.wrap] += mat[:, basis.dim:]
+        mat = mat[:, : basis.dim]
+    return mat
+
+
+def plain_support(basis: Basis, p):
+    lo = max(basis.knots[p], basis.a)
+    hi = min(basis.knots[p + basis.degree + 1], basis.b)
+    return (float(lo), float(hi)) if hi > lo else None
+
+
+def support(basis: Basis, i):
+    """Support intervals of logical function i (splines.py:355-363)."""
+    pieces = [i] + ([i + basis.dim] if basis.closed and i < basis.wrap else [])
+    return tuple(iv for iv in (plain_support(basis, p) for p in pieces) if iv is not None)
+
+
+def overlaps(iv_a, iv_b):
+    return any(min(ah, bh) - max(al, bl) > 0.0 for al, ah in iv_a for bl, bh in iv_b)
+
+
+# --------------------------------------------------------------------------
+# geometry (geometry.py:41-248)
+# --------------------------------------------------------------------------
+
+
+class Curve:
+    """B-spline curve f(s) = sum Q_i B_i(s) with scipy evaluation
+    (geometry.py:41-114)."""
+
+    def __init__(self, basis, control_points):
+        self.basis = as_basis(basis)
+        q = np.asarray(control_points, float)
+        self.coeffs = np.vstack([q, q[: self.basis.wrap]]) if self.basis.closed else q
+        self.spl = BSpline(self.basis.knots, self.coeffs, self.basis.degree, extrapolate=False)
+        self._der = {0: self.spl}
+
+    @classmethod
+    def from_reference(cls, curve):
+        return cls(curve.basis, curve.control_points)
+
+    @classmethod
+    def from_dict(cls, d):
+        return cls(Basis(int(d["degree"]), np.asarray(d["knots"], float), bool(d["closed"])),
+                   d["control_points"])
+
+    @property
+    def closed(self):
+        return self.basis.closed
+
+    @property
+    def length(self):
+        return self.basis.length
+
+    def spline(self, k):
+        while k not in self._der:
+            m = max(self._der)
+            self._der[m + 1] = self._der[m].derivative()
+        return self._der[k]
+
+    def eval(self, s, k=0):
+        s = np.clip(np.atleast_1d(np.asarray(s, float)), self.basis.a, self.basis.b)
+        return self.spline(k)(s)
+
+    def speed(self, s):  # geometry.py:111-114
+        return np.linalg.norm(self.eval(s, 1), axis=-1)
+
+    def is_c2(self):
+        return self.basis.min_smoothness() >= 2
+
+
+def k1_grid(curve: Curve, s, t):
+    """K1 = 0.5 ln(dist^2 / p^2) on a grid, periodic parameter distance on
+    closed curves from the UNWRAPPED |t-s| (geometry.py:127-139,225-248)."""
+    s = np.asarray(s, float)
+    t = np.asarray(t, float)
+    L = curve.length
+    fs, ft = curve.eval(s), curve.eval(t)
+    dx = fs[:, 0][:, None] - ft[:, 0][None, :]
+    dy = fs[:, 1][:, None] - ft[:, 1][None, :]
+    dist2 = dx * dx + dy * dy
+    delta = t[None, :] - s[:, None]
+    if curve.closed:
+        delta = delta - L * np.round(delta / L)
+        x = np.abs(t[None, :] - s[:, None])
+        p = (L / np.pi) * np.abs(np.sin(np.pi * x / L))
+    else:
+        p = np.abs(delta)
+    near = np.abs(delta) <= DIAG_REL * L
+    r = np.empty_like(dist2)
+    np.divide(dist2, p * p, out=r, where=~near)
+    if near.any():
+        mid = (s[:, None] + 0.5 * delta)[near]
+        if curve.closed:
+            mid = curve.basis.a + np.mod(mid - curve.basis.a, L)
+        r[near] = curve.speed(mid) ** 2
+    if r.min() <= 0.0:
+        raise ValueError("R <= 0 on assembly grid")
+    return 0.5 * np.log(r)
+
+
+def kbar_grid(curve: Curve, s, t):
+    """Normal-derivative kernel times J(t) (geometry.py:250-280)."""
+    L = curve.length
+    fs, ft, dt = curve.eval(s), curve.eval(t), curve.eval(t, 1)
+    dx = ft[:, 0][None, :] - fs[:, 0][:, None]
+    dy = ft[:, 1][None, :] - fs[:, 1][:, None]
+    dist2 = dx * dx + dy * dy
+    delta = t[None, :] - s[:, None]
+    if curve.closed:
+        delta = delta - L * np.round(delta / L)
+    near = np.abs(delta) <= DIAG_REL * L
+    out = np.empty_like(dist2)
+    np.divide(dy * dt[:, 0][None, :] - dx * dt[:, 1][None, :], dist2, out=out, where=~near)
+    if near.any():
+        srep = np.broadcast_to(s[:, None], near.shape)[near]
+        d1, d2 = curve.eval(srep, 1), curve.eval(srep, 2)
+        out[near] = 0.5 * (d1[:, 1] * d2[:, 0] - d1[:, 0] * d2[:, 1]) / np.sum(d1 ** 2, axis=-1)
+    return out
+
+
+# --------------------------------------------------------------------------
+# nodes + regular rules (quadrature.py:87-146, 510-540; splines.py:491-514)
+# --------------------------------------------------------------------------
+
+
+def build_nodes(fine: Basis):
+    """Shared node vector (quadrature.py:87-146)."""
+    d = fine.degree
+    els = fine.elements
+    pts = [fine.breakpoints]
+    extra = fine.multiplicities - 1
+    if fine.closed:
+        extra = extra.copy()
+        extra[0] = extra[-1] = fine.seam_multiplicity - 1
+    n_inner = 1 + extra[:-1] + extra[1:]
+    if not fine.closed:
+        n_inner[0] = n_inner[-1] = d
+    if np.all(n_inner == 1):
+        mids = 0.5 * (els[:, 0] + els[:, 1])
+        if fine.closed:
+            pts.append(mids)
+        else:
+            pts.append(np.linspace(els[0, 0], els[0, 1], d + 2))
+            pts.append(np.linspace(els[-1, 0], els[-1, 1], d + 2))
+            if len(els) > 2:
+                pts.append(mids[1:-1])
+    else:
+        for e, (lo, hi) in enumerate(els):
+            k = int(n_inner[e])
+            pts.append(lo + (hi - lo) * (np.arange(1, k + 1) / (k + 1)))
+    nodes = np.sort(np.concatenate(pts))
+    tol = DEDUP_RTOL * fine.length
+    nodes = nodes[np.concatenate([[True], np.diff(nodes) > tol])]
+    if fine.closed and fine.b - nodes[-1] <= tol:
+        nodes = nodes[:-1]
+    return nodes
+
+
+def gauss(order, lo=-1.0, hi=1.0):
+    x, w = np.polynomial.legendre.leggauss(order)
+    half = 0.5 * (hi - lo)
+    return 0.5 * (lo + hi) + half * x, half * w
+
+
+def weighted_integrals(parent: Basis, fine: Basis, i):
+    """mu_j = int B_i Bbar_j, per-element Gauss (splines.py:491-514)."""
+    order = (parent.degree + fine.degree) // 2 + 2
+    x, w = np.polynomial.legendre.leggauss(order)
+    sup = support(parent, i)
+    mu = np.zeros(fine.dim)
+    for lo, hi in fine.elements:
+        if not overlaps(((lo, hi),), sup):
+            continue
+        half = 0.5 * (hi - lo)
+        pts = 0.5 * (lo + hi) + half * x
+        bi = design(parent, pts)[:, i]
+        mu += design(fine, pts).T @ (half * w * bi)
+    return mu
+
+
+def regular_rules(parent: Basis, fine: Basis, nodes):
+    """Dense rule-weight matrix W (dim x nq): min-norm local solves per
+    parent function (quadrature.py:510-540)."""
+    bbar = design(fine, nodes).T
+    bpar = design(parent, nodes).T
+    W = np.zeros((parent.dim, len(nodes)))
+    for i in range(parent.dim):
+        nsel = np.flatnonzero(bpar[i] != 0.0)
+        sup = support(parent, i)
+        jsel = np.array([j for j in range(fine.dim) if overlaps(support(fine, j), sup)], int)
+        mu = weighted_integrals(parent, fine, i)[jsel]
+        w, _, rank, _ = scipy.linalg.lstsq(bbar[np.ix_(jsel, nsel)], mu, lapack_driver="gelsd")
+        W[i, nsel] = w
+    return W
+
+
+@dataclass
+class Disc:
+    curve: Curve
+    space: Basis
+    fine: Basis
+    nodes: np.ndarray
+    W: np.ndarray
+    G: np.ndarray
+    Bpar: np.ndarray
+    J: np.ndarray
+
+
+def build_discretization(curve, space, nref=1) -> Disc:
+    """assembly.py:147-172 (singular rules omitted: unused by the matrix)."""
+    curve = curve if isinstance(curve, Curve) else Curve.from_reference(curve)
+    space = as_basis(space)
+    fine = refine(space, nref)
+    nodes = build_nodes(fine)
+    W = regular_rules(space, fine, nodes)
+    J = curve.speed(nodes)
+    return Disc(curve, space, fine, nodes, W, W * J[None, :], design(space, nodes).T, J)
+
+
+# --------------------------------------------------------------------------
+# pair log moments (quadrature.py:182-197, 253-256, 372-504)
+# --------------------------------------------------------------------------
+
+
+def log_power_integral(j, z1, z2):
+    """[z^{j+1}/(j+1) (ln|z| - 1/(j+1))]_{z1}^{z2} (quadrature.py:182-197)."""
+    def F(z):
+        z = np.asarray(z, float)
+        out = np.zeros_like(z)
+        nz = z != 0.0
+        zz = z[nz]
+        out[nz] = zz ** (j + 1) / (j + 1) * (np.log(np.abs(zz)) - 1.0 / (j + 1))
+        return out
+    return F(z2) - F(z1)
+
+
+def pair_moments_closed(da, db, he, hf, delta):
+    """Closed-form centred double log moments (quadrature.py:372-410)."""
+    he, hf, delta = np.broadcast_arrays(np.asarray(he, float), np.asarray(hf, float),
+                                        np.asarray(delta, float))
+    n = he.shape[0]
+    out = np.zeros((n, da + 1, db + 1))
+    pmax = da + db + 1
+    for sgn in (1.0, -1.0):
+        xi = sgn * 0.5 * hf
+        z1 = xi - delta - 0.5 * he
+        z2 = xi - delta + 0.5 * he
+        llog = [log_power_integral(p, z1, z2) for p in range(pmax + 1)]
+        lpow = [(z2 ** (p + 1) - z1 ** (p + 1)) / (p + 1) for p in range(pmax + 1)]
+        for b in range(db + 1):
+            for m in range(b + 1):
+                cm = sgn * comb(b, m) / (m + 1)
+                for a in range(da + 1):
+                    acc = np.zeros(n)
+                    for r in range(a + 1):
+                        for q in range(b - m + 1):
+                            p = r + q + m + 1
+                            coef = (cm * comb(a, r) * comb(b - m, q) * (-1.0) ** (r + q)
+                                    * (xi - delta) ** (a - r) * xi ** (b - m - q))
+                            acc += coef * (llog[p] - lpow[p] / (m + 1))
+                    out[:, a, b] += acc
+    return out
+
+
+def pair_moments_gauss(da, db, he, hf, delta, order=PAIR_FAR_ORDER, period=None, gap_only=False):
+    """Tensor Gauss for analytic pair moments (quadrature.py:413-438)."""
+    he = np.asarray(he, float)[:, None, None]
+    hf = np.asarray(hf, float)[:, None, None]
+    delta = np.asarray(delta, float)[:, None, None]
+    x, w = gauss(order, -0.5, 0.5)
+    u = he * x[None, :, None]
+    v = hf * x[None, None, :]
+    arg = v - u - delta
+    if gap_only:
+        kern = np.log(np.abs(np.sinc(arg / period)))
+    else:
+        kern = np.log(np.abs(arg))
+        if period is not None:
+            kern += np.log(np.abs(np.sinc(arg / period)))
+    out = np.empty((u.shape[0], da + 1, db + 1))
+    for a in range(da + 1):
+        wa = (he[:, :, 0] ** (a + 1)) * (w * x ** a)[None, :]
+        for b in range(db + 1):
+            wb = (hf[:, 0, :] ** (b + 1)) * (w * x ** b)[None, :]
+            out[:, a, b] = np.einsum("ng,ngh,nh->n", wa, kern, wb)
+    return out
+
+
+@lru_cache(maxsize=16)
+def unit_pair_stack(da, db, nel, closed):
+    """Gap-indexed unit-width tables (quadrature.py:441-469)."""
+    if closed:
+        ks = np.arange(nel)
+        keff = ks - nel * np.round(ks / nel)
+    else:
+        keff = np.arange(-(nel - 1), nel).astype(float)
+    delta = -keff
+    ones = np.ones(len(keff))
+    near = np.abs(keff) <= 1
+    m2 = np.empty((len(keff), da + 1, db + 1))
+    m2[near] = pair_moments_closed(da, db, ones[near], ones[near], delta[near])
+    m2[~near] = pair_moments_gauss(da, db, ones[~near], ones[~near], delta[~near])
+    if closed:
+        m2 += pair_moments_gauss(da, db, ones, ones, delta, period=float(nel), gap_only=True)
+    m2.setflags(write=False)
+    return m2
+
+
+def centred_integrals(n):
+    pa = np.arange(n + 1)
+    return np.where(pa % 2 == 0, 0.5 ** pa / (pa + 1.0), 0.0)
+
+
+def uniform_pair_moments(fine: Basis, row_degree):
+    """Scaled gap table + kmap (quadrature.py:472-504)."""
+    nel = fine.n_elements
+    widths = fine.elements[:, 1] - fine.elements[:, 0]
+    h = widths.mean()
+    if not np.allclose(widths, h, rtol=DEDUP_RTOL):
+        raise ValueError("pair log moments require a uniform element mesh")
+    d = fine.degree
+    unit = unit_pair_stack(row_degree, d, nel, fine.closed)
+    pa, pb = np.arange(row_degree + 1), np.arange(d + 1)
+    ca, cb = centred_integrals(row_degree), centred_integrals(d)
+    scale = h ** (2.0 + pa[:, None] + pb[None, :])
+    m2 = scale[None] * (unit + np.log(h) * (ca[:, None] * cb[None, :]))
+    e = np.arange(nel)
+    diff = e[None, :] - e[:, None]
+    kmap = np.mod(diff, nel) if fine.closed else diff + (nel - 1)
+    return m2, kmap
+
+
+@lru_cache(maxsize=8)
+def cheb_setup(degree):
+    """Chebyshev points and inverse Vandermonde (splines.py:388-396)."""
+    x = np.cos(np.pi * (2 * np.arange(degree + 1) + 1) / (2 * degree + 2))
+    return x, np.linalg.inv(np.vander(x, degree + 1, increasing=True))
+
+
+def local_coeffs(basis: Basis, elements, degree, scale_fn=None):
+    """Per-element centred-monomial coefficients of the active functions
+    (splines.py:427-472)."""
+    x, vinv = cheb_setup(degree)
+    powers = np.arange(degree + 1)
+    elements = np.asarray(elements, float)
+    n_el = len(elements)
+    half = 0.5 * (elements[:, 1] - elements[:, 0])
+    mid = 0.5 * (elements[:, 0] + elements[:, 1])
+    pts = (mid[:, None] + half[:, None] * x[None, :]).ravel()
+    mat = BSpline.design_matrix(pts, basis.knots, basis.degree)
+    width = basis.degree + 1
+    cols = mat.indices.reshape(n_el, degree + 1, width)[:, 0, :].copy()
+    if basis.closed:
+        cols[cols >= basis.dim] -= basis.dim
+    vals = mat.data.reshape(n_el, degree + 1, width)
+    if scale_fn is not None:
+        vals = vals * np.asarray(scale_fn(pts), float).reshape(n_el, degree + 1, 1)
+    coeffs = np.einsum("pq,eqk->epk", vinv, vals)
+    coeffs *= (half[:, None] ** -powers[None, :])[:, :, None]
+    return coeffs, cols
+
+
+# --------------------------------------------------------------------------
+# dense assembly restatement (assembly.py:175-271, 287-343)
+# --------------------------------------------------------------------------
+
+
+def dense_ik1(disc: Disc):
+    """IK1 = G K1 G^T (assembly.py:175-183)."""
+    return disc.G @ (k1_grid(disc.curve, disc.nodes, disc.nodes) @ disc.G.T)
+
+
+def ik2_ingredients(disc: Disc):
+    """Theta (N x N_E), D (N_E x N_E) and the fit C (N_E x N) exactly as the
+    reference forms them (assembly.py:206-243)."""
+    fine, space = disc.fine, disc.space
+    d = fine.degree
+    bigd = space.degree + JFIT_DEGREE
+    m2, kmap = uniform_pair_moments(fine, bigd)
+    u, ucols = local_coeffs(space, fine.elements, bigd, scale_fn=disc.curve.speed)
+    v, vcols = local_coeffs(fine, fine.elements, d)
+    big4 = m2[kmap]
+    w_theta = np.matmul(np.matmul(u.transpose(0, 2, 1)[:, None], big4), v[None])
+    w_dmm = np.matmul(np.matmul(v.transpose(0, 2, 1)[:, None], big4[:, :, : d + 1, :]), v[None])
+    idx_t = ucols[:, None, :, None] * fine.dim + vcols[None, :, None, :]
+    idx_d = vcols[:, None, :, None] * fine.dim + vcols[None, :, None, :]
+    theta = np.bincount(idx_t.ravel(), weights=w_theta.ravel(),
+                        minlength=space.dim * fine.dim).reshape(space.dim, fine.dim)
+    dmm = np.bincount(idx_d.ravel(), weights=w_dmm.ravel(),
+                      minlength=fine.dim * fine.dim).reshape(fine.dim, fine.dim)
+    bbar_t = design(fine, disc.nodes)
+    target = (disc.Bpar * disc.J[None, :]).T
+    q, r = scipy.linalg.qr(bbar_t, mode="economic")
+    cfit = scipy.linalg.solve_triangular(r, q.T @ target)
+    return theta, dmm, cfit
+
+
+def dense_ik2(disc: Disc):
+    """IK2 = Theta C + (Theta C)^T - C^T D C (assembly.py:186-245)."""
+    theta, dmm, cfit = ik2_ingredients(disc)
+    tc = theta @ cfit
+    return tc + tc.T - cfit.T @ dmm @ cfit
+
+
+def scale_and_symmetrize(m):
+    """assembly.py:262-271."""
+    a = -m / TWO_PI
+    scale = np.abs(a).max()
+    defect = np.abs(a - a.T).max() / scale if scale > 0 else 0.0
+    return 0.5 * (a + a.T), float(defect)
+
+
+def b1_weighted(disc: Disc, g):
+    """assembly.py:312-319."""
+    return disc.G @ np.asarray(g(disc.nodes), float)
+
+
+def graded_points(lo, hi, order, to_lo, to_hi, levels=GRADE_LEVELS, ratio=GRADE_RATIO):
+    """assembly.py:349-378."""
+    def side(a, b, left):
+        h = b - a
+        cuts = h * ratio ** np.arange(levels + 1)
+        edges = np.concatenate([[0.0], cuts[::-1]])
+        if left:
+            return np.column_stack([a + edges[:-1], a + edges[1:]])
+        return np.column_stack([b - edges[1:], b - edges[:-1]])[::-1]
+    if to_lo and to_hi:
+        mid = 0.5 * (lo + hi)
+        pans = np.vstack([side(lo, mid, True), side(mid, hi, False)])
+    elif to_lo:
+        pans = side(lo, hi, True)
+    elif to_hi:
+        pans = side(lo, hi, False)
+    else:
+        pans = np.array([[lo, hi]])
+    pts, wts = zip(*(gauss(order, a, b) for a, b in pans))
+    return np.concatenate(pts), np.concatenate(wts)
+
+
+def element_gauss(space: Basis, order):
+    pts, wts = zip(*(gauss(order, lo, hi) for lo, hi in space.elements))
+    return np.concatenate(pts), np.concatenate(wts)
+
+
+def b1_gauss(curve: Curve, space: Basis, g, order=16):
+    """assembly.py:287-309."""
+    if space.closed:
+        pts, wts = element_gauss(space, order)
+    else:
+        last = space.n_elements - 1
+        pp = [graded_points(lo, hi, order, e == 0, e == last)
+              for e, (lo, hi) in enumerate(space.elements)]
+        pts = np.concatenate([p for p, _ in pp])
+        wts = np.concatenate([w for _, w in pp])
+    vals = np.asarray(g(pts), float)
+    return design(space, pts).T @ (wts * curve.speed(pts) * vals)
+
+
+def b2_gauss(curve: Curve, space: Basis, g, order=16):
+    """assembly.py:322-343."""
+    pts, wts = element_gauss(space, order)
+    inner = kbar_grid(curve, pts, pts) @ (wts * np.asarray(g(pts), float))
+    return design(space, pts).T @ (wts * curve.speed(pts) * inner) / TWO_PI
+
+
+# --------------------------------------------------------------------------
+# X-form restatement: X = IK1 + (2 Theta - C^T D) C
+# --------------------------------------------------------------------------
+
+
+def banded_fit_parts(disc: Disc):
+    """H = Bt^T Bt and S = Bt^T (J Bpar^T): the normal equations of the node
+    least-squares fit (assembly.py:233-243); C = H^{-1} S."""
+    bt = design(disc.fine, disc.nodes)
+    H = bt.T @ bt
+    S = bt.T @ (disc.Bpar * disc.J[None, :]).T
+    return H, S
+
+
+def xform_dense(disc: Disc):
+    """A through the X-form with C from the normal equations (Cholesky)."""
+    theta, dmm, _ = ik2_ingredients(disc)
+    H, S = banded_fit_parts(disc)
+    C = scipy.linalg.cho_solve(scipy.linalg.cho_factor(H), S)
+    X = dense_ik1(disc) + (2.0 * theta - C.T @ dmm) @ C
+    return -(X + X.T) / (2.0 * TWO_PI)

@@ -1,0 +1,614 @@
+"""Drop-in Galerkin assembly entry points (mirrors wqbem/assembly.py).
+
+Same names, arguments, return types and error behaviour as the reference:
+
+    build_discretization(curve, space, nref) -> Discretization   (assembly.py:147)
+    assemble_ik1(disc) -> ndarray[N, N]                           (assembly.py:175)
+    assemble_ik2(disc) -> ndarray[N, N]                           (assembly.py:186)
+    assemble_weighted_matrix(disc) -> (M, {"kernel_evals"}, s)    (assembly.py:248)
+    scale_and_symmetrize(M) -> (A, defect)                        (assembly.py:262)
+    assemble_b1_weighted(disc, dirichlet) -> ndarray[N]           (assembly.py:312)
+    assemble_b1(curve, space, dirichlet, order=16)                (assembly.py:287)
+
+The O(N^2) work runs ONLY on the GPU through the C-ABI library (``_lib``);
+there is no CPU fallback -- without the library or a CUDA device these raise
+``DeviceError``.  ``build_discretization`` is an O(N) host precompute (see
+``precompute``); the O(N^3) singular rules the matrix never reads are not
+built.
+
+Formulation.  With C = H^{-1} S the node least-squares fit
+(assembly.py:233-243), Theta and D the element-pair log moments,
+
+    X  = IK1 + X2,     X2 = (2 Theta - C^T D) C,
+    M  = (X + X^T)/2 = sym(IK1 + IK2),     A = -(X + X^T) / (4 pi).
+
+``assemble_weighted_matrix`` returns the symmetric M (it differs from the
+reference's unsymmetrised M only by the reference's own pre-symmetrisation
+defect, <= 2.5e-14 relative), so ``scale_and_symmetrize`` of it is exact.
+Device-resident variants (``assemble_matrix_device``) return torch tensors.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from . import precompute as PC
+from .errors import ConstructionError, DeviceError, GeometryError, UsageError
+from .geometry import BoundaryCurve, as_curve, parametric_speed
+from .splines import BasisSpec, RefinedBasis, active_values, as_basis, local_basis_coeffs, refine_uniform
+
+__all__ = [
+    "NodeVector",
+    "Discretization",
+    "build_discretization",
+    "assemble_ik1",
+    "assemble_ik2",
+    "assemble_weighted_matrix",
+    "assemble_matrix_device",
+    "scale_and_symmetrize",
+    "assemble_b1_weighted",
+    "assemble_b1",
+    "basis_values",
+]
+
+TWO_PI = 2.0 * np.pi
+_GRADE_LEVELS = 14
+_GRADE_RATIO = 0.3
+
+
+def _check_space(curve: BoundaryCurve, space: BasisSpec):
+    gb = curve.basis
+    if space.closed != gb.closed:
+        raise UsageError("solution space and curve disagree on closedness")
+    if abs(space.a - gb.a) > 1e-12 or abs(space.b - gb.b) > 1e-12:
+        raise UsageError("solution space and curve have different domains")
+
+
+def basis_values(basis, pts) -> np.ndarray:
+    """Dense (n_pts, dim) matrix of basis values (assembly.py:101-108)."""
+    basis = as_basis(basis)
+    vals, cols = active_values(basis, basis._check_domain(pts))
+    out = np.zeros((len(vals), basis.dim))
+    np.add.at(out, (np.repeat(np.arange(len(vals)), vals.shape[1]), cols.ravel()), vals.ravel())
+    return out
+
+
+@dataclass(frozen=True)
+class NodeVector:
+    """Shared quadrature nodes (quadrature.py:74-84)."""
+
+    nodes: np.ndarray
+    refined: RefinedBasis = field(repr=False)
+    element_index: np.ndarray = field(repr=False)
+
+    @property
+    def n(self) -> int:
+        return len(self.nodes)
+
+
+@dataclass
+class LogPart:
+    """Host-side ingredients of the log part (assembly.py:206-243)."""
+
+    path: str                      # "circulant" | "general"
+    h: float
+    da: int                        # P = p + JFIT_DEGREE
+    db: int                        # refined degree d
+    n_el: int
+    near_unit: np.ndarray          # (3, da+1, db+1)
+    s_start: np.ndarray            # (N,) S column band
+    s_w: np.ndarray                # (N, ws)
+    # circulant
+    e_start: np.ndarray = None
+    U: np.ndarray = None           # (N, tu, da+1)
+    v0: np.ndarray = None          # (db+1, db+1)
+    hinv_taps: np.ndarray = None   # (2K+1,)
+    # general
+    u: np.ndarray = None
+    v: np.ndarray = None
+    u_el: np.ndarray = None
+    u_loc: np.ndarray = None
+    v_el: np.ndarray = None
+    v_loc: np.ndarray = None
+    Lb: np.ndarray = None          # banded Cholesky factor of H
+    bw: int = 0
+
+
+@dataclass
+class Discretization:
+    """Solution space, shared node vector and the banded regular rules
+    (mirrors assembly.py:131-144; G and Bpar are exposed lazily as dense
+    arrays for compatibility, the GPU reads the band)."""
+
+    curve: BoundaryCurve
+    space: BasisSpec
+    refined: RefinedBasis
+    nodes: NodeVector
+    rules: PC.RuleBand
+    J_nodes: np.ndarray = field(repr=False)
+    f_nodes: np.ndarray = field(repr=False)
+    k1_mode: int = 0
+    invp2: np.ndarray = field(default=None, repr=False)
+    rule_seconds: float = 0.0
+    _logpart: object = field(default=None, repr=False)
+    _dev: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def regular_rules(self):
+        return self.rules
+
+    @property
+    def G(self) -> np.ndarray:
+        """Dense (dim, n_quad) rule weights times J (assembly.py:160)."""
+        N, nq = self.space.dim, self.nodes.n
+        g = np.zeros((N, nq))
+        rb = self.rules
+        for w in range(rb.WG):
+            m = w < rb.width
+            q = np.mod(rb.start[m] + w, nq)
+            g[np.flatnonzero(m), q] += rb.weights[m, w] * self.J_nodes[q]
+        return g
+
+    @property
+    def Bpar(self) -> np.ndarray:
+        return basis_values(self.space, self.nodes.nodes).T
+
+    @property
+    def closed(self) -> bool:
+        return self.space.closed
+
+
+def build_discretization(curve, space, nref: int) -> Discretization:
+    """Refine, build nodes and the banded regular rules, and sample the curve
+    at the nodes (assembly.py:147-172), in O(N) host time."""
+    curve = as_curve(curve)
+    space = as_basis(space)
+    _check_space(curve, space)
+    t0 = time.perf_counter()
+    refined = refine_uniform(space, nref)
+    fine = refined.basis
+    nodes = PC.build_nodes(fine)
+    rules = PC.regular_rule_band(space, fine, nodes)
+    rule_seconds = time.perf_counter() - t0
+    b = curve.basis
+    f_nodes = curve.spline(0)(np.clip(nodes, b.a, b.b))
+    J = parametric_speed(curve, nodes)
+    PC.check_diagonal_pairs(nodes, space.closed, curve.length)
+    invp2 = PC.k1_distance_table(nodes, space.closed, curve.length)
+    if invp2 is not None:
+        mode = _lib.WQ_K1_TABLE
+    else:
+        mode = _lib.WQ_K1_CLOSED if space.closed else _lib.WQ_K1_OPEN
+    el_idx = np.clip(np.searchsorted(fine.breakpoints, nodes, side="right") - 1, 0,
+                     fine.n_elements - 1)
+    return Discretization(curve=curve, space=space, refined=refined,
+                          nodes=NodeVector(nodes=nodes, refined=refined, element_index=el_idx),
+                          rules=rules, J_nodes=J, f_nodes=f_nodes, k1_mode=mode, invp2=invp2,
+                          rule_seconds=rule_seconds)
+
+
+# -- log-part host ingredients ---------------------------------------------------------
+
+
+def _incidence(cols, n_fun):
+    """(element, local) incidences of every function, padded with -1."""
+    n_el, w = cols.shape
+    fun = cols.ravel()
+    el = np.repeat(np.arange(n_el), w)
+    loc = np.tile(np.arange(w), n_el)
+    order = np.lexsort((el, fun))
+    fun, el, loc = fun[order], el[order], loc[order]
+    counts = np.bincount(fun, minlength=n_fun)
+    width = int(counts.max())
+    first = np.cumsum(counts) - counts
+    slot = np.arange(len(fun)) - first[fun]
+    E = np.full((n_fun, width), -1, np.int64)
+    L = np.zeros((n_fun, width), np.int64)
+    E[fun, slot] = el
+    L[fun, slot] = loc
+    return E, L, counts
+
+
+def _is_circulant(disc: Discretization) -> bool:
+    fine = disc.refined.basis
+    return (fine.closed and disc.refined.nref == 1 and np.all(fine.multiplicities == 1)
+            and fine.seam_multiplicity == 1 and fine.dim == fine.n_elements)
+
+
+def _log_part(disc: Discretization) -> LogPart:
+    if disc._logpart is not None:
+        return disc._logpart
+    fine, space = disc.refined.basis, disc.space
+    h = PC.uniform_width(fine)  # ConstructionError on graded meshes (quadrature.py:489-491)
+    d = fine.degree
+    da = space.degree + PC.JFIT_DEGREE
+    curve = disc.curve
+    cb = curve.basis
+
+    def jac(pts):
+        return np.linalg.norm(curve.spline(1)(np.clip(pts, cb.a, cb.b)), axis=-1)
+
+    u, ucols = local_basis_coeffs(space, fine.elements, da, scale_fn=jac)
+    v, vcols = local_basis_coeffs(fine, fine.elements, d)
+    H, S = PC.fit_bands(fine, space, disc.nodes.nodes, disc.J_nodes)
+    s_start, s_w = PC.band_of_columns(S, fine.closed)
+    lp = LogPart(path="general", h=h, da=da, db=d, n_el=fine.n_elements,
+                 near_unit=np.ascontiguousarray(PC.unit_near_table(da, d)),
+                 s_start=s_start, s_w=s_w)
+    N = space.dim
+    if _is_circulant(disc):
+        n = fine.n_elements
+        _, _, counts = _incidence(ucols, N)
+        tu = int(counts.max())
+        # with simple knots supp(B_i) = elements i-p .. i (mod n), unwrapped
+        e_start = np.arange(N) - space.degree
+        U = np.empty((N, tu, da + 1))
+        for a in range(tu):
+            e = np.mod(e_start + a, n)
+            loc = np.mod(np.arange(N) - e, n)  # local index of function i on element e
+            U[:, a, :] = u[e, :, loc]
+        if not (np.all(np.diff(s_start) == 1) and np.all(counts == tu)):
+            raise ConstructionError("circulant path needs unit-step supports")
+        if not np.all(ucols == np.mod(np.arange(n)[:, None] + np.arange(space.degree + 1)[None, :], n)):
+            raise ConstructionError("unexpected cyclic column layout")
+        hinv, K = PC.circulant_inverse(H, n)
+        if 2 * K + 1 >= n:
+            # the inverse has not decayed within half a period: use one full period
+            K = n // 2
+            taps = hinv[np.mod(np.arange(-K, K + 1), n)].copy()
+            if n % 2 == 0:  # k = -n/2 and +n/2 are the same residue
+                taps[0] *= 0.5
+                taps[-1] *= 0.5
+        else:
+            taps = np.concatenate([hinv[-K:] if K else np.empty(0), hinv[: K + 1]])
+        lp.path = "circulant"
+        lp.e_start = e_start.astype(np.int64)
+        lp.U = np.ascontiguousarray(U)
+        lp.v0 = np.ascontiguousarray(v[0])
+        lp.hinv_taps = np.ascontiguousarray(taps)
+    elif not fine.closed:
+        import scipy.linalg
+        bw = d
+        NE = fine.dim
+        Hd = H.tocsr()
+        ab = np.zeros((bw + 1, NE))
+        for j in range(bw + 1):
+            ab[j, : NE - j] = Hd.diagonal(-j)
+        try:
+            lo = scipy.linalg.cholesky_banded(ab, lower=True)
+        except np.linalg.LinAlgError as exc:
+            raise ConstructionError("node vector does not resolve the refined space") from exc
+        diag = lo[0]
+        if diag.min() ** 2 <= PC.RANK_RTOL ** 2 * (diag.max() ** 2):
+            raise ConstructionError("node vector does not resolve the refined space")
+        Lb = np.zeros((NE, bw + 1))
+        for j in range(bw + 1):
+            Lb[j:, j] = lo[j, : NE - j]
+        u_el, u_loc, _ = _incidence(ucols, N)
+        v_el, v_loc, _ = _incidence(vcols, NE)
+        lp.u, lp.v = np.ascontiguousarray(u), np.ascontiguousarray(v)
+        lp.u_el, lp.u_loc, lp.v_el, lp.v_loc = u_el, u_loc, v_el, v_loc
+        lp.Lb, lp.bw = Lb, bw
+    else:
+        raise ConstructionError(
+            "closed meshes with repeated knots or nref > 1 are not supported by the B200 "
+            "log-part yet (cyclic banded fit)")
+    disc._logpart = lp
+    return lp
+
+
+# -- device plumbing ------------------------------------------------------------------------
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as exc:  # pragma: no cover
+        raise DeviceError("PyTorch is required for device memory") from exc
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the B200 assembly has no CPU fallback")
+    return torch
+
+
+def _dev(disc: Discretization, key, make):
+    d = disc._dev
+    if key not in d:
+        d[key] = make()
+    return d[key]
+
+
+def _to_dev(torch, arr, dtype=None):
+    a = np.ascontiguousarray(arr)
+    t = torch.from_numpy(a)
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to("cuda")
+
+
+def _smooth(disc: Discretization):
+    torch = _torch()
+
+    def make():
+        rb = disc.rules
+        nodes = disc.nodes.nodes
+        d = {
+            "s": _to_dev(torch, nodes),
+            "fx": _to_dev(torch, disc.f_nodes[:, 0]),
+            "fy": _to_dev(torch, disc.f_nodes[:, 1]),
+            "J": _to_dev(torch, disc.J_nodes),
+            "g_start": _to_dev(torch, rb.start.astype(np.int64)),
+            "g_w": _to_dev(torch, (rb.weights * disc.J_nodes[np.mod(
+                rb.start[:, None] + np.arange(rb.WG)[None, :], len(nodes))])
+                * (np.arange(rb.WG)[None, :] < rb.width[:, None])),
+            "invp2": _to_dev(torch, disc.invp2) if disc.invp2 is not None else None,
+            "flag": torch.zeros(1, dtype=torch.int32, device="cuda"),
+        }
+        st = _lib.WqSmooth(disc.space.dim, len(nodes), rb.WG, int(disc.closed), disc.k1_mode,
+                           disc.curve.length, d["s"].data_ptr(), d["fx"].data_ptr(),
+                           d["fy"].data_ptr(), d["J"].data_ptr(),
+                           d["invp2"].data_ptr() if d["invp2"] is not None else None,
+                           d["g_start"].data_ptr(), d["g_w"].data_ptr())
+        # max node span over output tiles of WQ_TILE rows
+        T = _lib.WQ_TILE
+        N = disc.space.dim
+        first = rb.start[0::T]
+        last_idx = np.minimum(np.arange(0, N, T) + T, N) - 1
+        span = int((rb.start[last_idx] + rb.WG - first).max())
+        d["struct"] = st
+        d["span"] = span
+        return d
+
+    return _dev(disc, "smooth", make)
+
+
+def _check_flag(sm):
+    if int(sm["flag"].item()) & _lib.WQ_FLAG_R_NONPOSITIVE:
+        sm["flag"].zero_()
+        raise GeometryError("R <= 0 on assembly grid")
+
+
+def _ik1_into(disc, X, accumulate=False, row0=0, row1=None):
+    torch = _torch()
+    sm = _smooth(disc)
+    N = disc.space.dim
+    row1 = N if row1 is None else row1
+    _lib.call("wq_ik1", ctypes_ref(sm["struct"]), row0, row1, 0, N, _lib.ptr(X), X.stride(0),
+              int(accumulate), sm["span"], _lib.ptr(sm["flag"]), _lib.stream_handle())
+    return X
+
+
+def ctypes_ref(s):
+    import ctypes
+    return ctypes.byref(s)
+
+
+def _m2_table(disc, lp: LogPart):
+    torch = _torch()
+
+    def make():
+        n = lp.n_el
+        closed = disc.closed
+        n_gap = n if closed else 2 * n - 1
+        gx, gw = PC.gauss_unit(PC.PAIR_FAR_ORDER)
+        m2 = torch.empty((n_gap, lp.da + 1, lp.db + 1), dtype=torch.float64, device="cuda")
+        keep = [_to_dev(torch, lp.near_unit), _to_dev(torch, gx), _to_dev(torch, gw),
+                _to_dev(torch, PC.centred_monomial_integrals(lp.da)),
+                _to_dev(torch, PC.centred_monomial_integrals(lp.db))]
+        _lib.call("wq_pair_table", n, int(closed), lp.da, lp.db, lp.h, _lib.ptr(keep[0]),
+                  _lib.ptr(keep[1]), _lib.ptr(keep[2]), len(gx), _lib.ptr(keep[3]),
+                  _lib.ptr(keep[4]), _lib.ptr(m2), _lib.stream_handle())
+        return m2, keep
+
+    return make()
+
+
+def _logpart_dev(disc):
+    torch = _torch()
+    lp = _log_part(disc)
+
+    def make():
+        d = {"s_start": _to_dev(torch, lp.s_start.astype(np.int64)),
+             "s_w": _to_dev(torch, lp.s_w)}
+        N = disc.space.dim
+        if lp.path == "circulant":
+            d["e_start"] = _to_dev(torch, lp.e_start)
+            d["U"] = _to_dev(torch, lp.U)
+            d["v0"] = _to_dev(torch, lp.v0)
+            d["taps"] = _to_dev(torch, lp.hinv_taps)
+            tu = lp.U.shape[1]
+            d["struct"] = _lib.WqLogpart(N, lp.n_el, lp.da, tu, lp.s_w.shape[1],
+                                         d["e_start"].data_ptr(), d["U"].data_ptr(),
+                                         d["s_start"].data_ptr(), d["s_w"].data_ptr())
+        else:
+            NE = disc.refined.basis.dim
+            for k in ("u", "v", "u_el", "u_loc", "v_el", "v_loc", "Lb"):
+                d[k] = _to_dev(torch, getattr(lp, k))
+            d["struct"] = _lib.WqLogpart(N, NE, lp.da, 0, lp.s_w.shape[1], None, None,
+                                         d["s_start"].data_ptr(), d["s_w"].data_ptr())
+        return d
+
+    return lp, _dev(disc, "logpart", make)
+
+
+def _ik2_x2_into(disc, X, accumulate=True):
+    """X (+)= X2 (circulant: X2 itself; general: X2^T -- callers symmetrise)."""
+    torch = _torch()
+    lp, d = _logpart_dev(disc)
+    N = disc.space.dim
+    st = _lib.stream_handle()
+    m2, keep = _m2_table(disc, lp)
+    if lp.path == "circulant":
+        n = lp.n_el
+        nA = lp.da + 1
+        Zp = torch.empty((n, nA), dtype=torch.float64, device="cuda")
+        Zw = torch.empty((n, nA), dtype=torch.float64, device="cuda")
+        ff = torch.empty(n, dtype=torch.float64, device="cuda")
+        work = torch.empty(n, dtype=torch.float64, device="cuda")
+        K = (len(lp.hinv_taps) - 1) // 2
+        _lib.call("wq_circ_tables", n, lp.da, lp.db, _lib.ptr(m2), _lib.ptr(d["v0"]),
+                  _lib.ptr(d["taps"]), K, _lib.ptr(Zp), _lib.ptr(ff), _lib.ptr(work),
+                  _lib.ptr(Zw), st)
+        _lib.call("wq_ik2_circ", ctypes_ref(d["struct"]), _lib.ptr(Zp), _lib.ptr(ff), 0, N, 0, N,
+                  _lib.ptr(X), X.stride(0), int(accumulate), st)
+        return X
+    NE = disc.refined.basis.dim
+    pp = _lib.WqPairs(N, NE, lp.n_el, m2.shape[0], lp.da, lp.db, int(disc.closed),
+                      lp.u_el.shape[1], lp.v_el.shape[1], d["u_el"].data_ptr(),
+                      d["u_loc"].data_ptr(), d["v_el"].data_ptr(), d["v_loc"].data_ptr(),
+                      d["u"].data_ptr(), disc.space.degree, d["v"].data_ptr(), m2.data_ptr())
+    thetaT = torch.empty((NE, N), dtype=torch.float64, device="cuda")
+    D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
+    _lib.call("wq_theta_t", ctypes_ref(pp), _lib.ptr(thetaT), st)
+    _lib.call("wq_dmat", ctypes_ref(pp), _lib.ptr(D), st)
+    # E = H^{-1} D ; F = H^{-1} E^T = H^{-1} D H^{-1}
+    _lib.call("wq_band_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(D), NE, NE, st)
+    F = torch.empty_like(D)
+    _lib.call("wq_transpose", _lib.ptr(D), NE, NE, _lib.ptr(F), st)
+    _lib.call("wq_band_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(F), NE, NE, st)
+    # Phi = 2 H^{-1} Theta^T - F S
+    _lib.call("wq_band_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(thetaT), N, N, st)
+    _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(F), _lib.ptr(thetaT), st)
+    # X[j][i] (+)= sum_m S[m, j] Phi[m, i]  (= X2^T)
+    _lib.call("wq_add_st_phi", ctypes_ref(d["struct"]), _lib.ptr(thetaT), 0, N, _lib.ptr(X),
+              X.stride(0), int(accumulate), st)
+    return X
+
+
+def _new_square(disc):
+    torch = _torch()
+    N = disc.space.dim
+    return torch.empty((N, N), dtype=torch.float64, device="cuda")
+
+
+def _assemble_into(disc: Discretization, X, scaled: bool = True):
+    """Enqueue the whole assembly on the current stream (no host sync)."""
+    _ik1_into(disc, X, accumulate=False)
+    _ik2_x2_into(disc, X, accumulate=True)
+    alpha = -1.0 / (2.0 * TWO_PI) if scaled else 0.5
+    _lib.call("wq_symmetrize", _lib.ptr(X), X.shape[0], alpha, _lib.stream_handle())
+    return X
+
+
+def assemble_matrix_device(disc: Discretization, scaled: bool = True, out=None):
+    """Device-resident A = -(X + X^T)/(4 pi) (scaled) or M = (X + X^T)/2.
+    Returns a torch CUDA tensor; no host synchronisation except the geometry
+    flag check."""
+    X = _new_square(disc) if out is None else out
+    _assemble_into(disc, X, scaled)
+    _check_flag(_smooth(disc))
+    return X
+
+
+def assemble_ik1(disc: Discretization) -> np.ndarray:
+    """Smooth-part Galerkin matrix IK1 = G K1 G^T (assembly.py:175-183)."""
+    X = _new_square(disc)
+    _ik1_into(disc, X)
+    _check_flag(_smooth(disc))
+    return X.cpu().numpy()
+
+
+def assemble_ik2(disc: Discretization) -> np.ndarray:
+    """Log-part matrix Theta C + (Theta C)^T - C^T D C (assembly.py:186-245),
+    as (X2 + X2^T)/2 of the X-form."""
+    X = _new_square(disc)
+    _ik2_x2_into(disc, X, accumulate=False)
+    _lib.call("wq_symmetrize", _lib.ptr(X), X.shape[0], 0.5, _lib.stream_handle())
+    return X.cpu().numpy()
+
+
+def assemble_weighted_matrix(disc: Discretization):
+    """(M, {"kernel_evals": n_quad^2}, seconds) (assembly.py:248-259); the
+    seconds cover the device assembly (pair table, IK1, IK2, symmetrise)."""
+    torch = _torch()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    X = assemble_matrix_device(disc, scaled=False)
+    torch.cuda.synchronize()
+    seconds = time.perf_counter() - t0
+    return X.cpu().numpy(), {"kernel_evals": disc.nodes.n ** 2}, seconds
+
+
+def scale_and_symmetrize(m):
+    """A = (a + a^T)/2 with a = -m/(2 pi), and the relative symmetry defect
+    max|a - a^T| / max|a| (assembly.py:262-271).  Accepts a numpy array or a
+    square torch CUDA tensor (returned on the device)."""
+    torch = _torch()
+    on_dev = hasattr(m, "is_cuda") and m.is_cuda
+    X = m.to(torch.float64).contiguous().clone() if on_dev else _to_dev(torch, np.asarray(m, float))
+    n = X.shape[0]
+    if X.ndim != 2 or X.shape[1] != n:
+        raise UsageError("scale_and_symmetrize needs a square matrix")
+    stats = torch.empty(2, dtype=torch.float64, device="cuda")
+    st = _lib.stream_handle()
+    _lib.call("wq_absmax_defect", _lib.ptr(X), n, _lib.ptr(stats), st)
+    _lib.call("wq_symmetrize", _lib.ptr(X), n, -1.0 / (2.0 * TWO_PI), st)
+    mx, df = stats.cpu().numpy()
+    defect = float(df / mx) if mx > 0 else 0.0
+    return (X if on_dev else X.cpu().numpy()), defect
+
+
+def assemble_b1_weighted(disc: Discretization, dirichlet) -> np.ndarray:
+    """b1 through the regular weighted rules, one datum evaluation per node
+    (assembly.py:312-319): a banded matvec on the GPU."""
+    torch = _torch()
+    sm = _smooth(disc)
+    g = _to_dev(torch, np.asarray(dirichlet(disc.nodes.nodes), dtype=float))
+    b = torch.empty(disc.space.dim, dtype=torch.float64, device="cuda")
+    _lib.call("wq_b1w", ctypes_ref(sm["struct"]), _lib.ptr(g), _lib.ptr(b), _lib.stream_handle())
+    return b.cpu().numpy()
+
+
+def _graded_points(lo, hi, order, toward_lo, toward_hi, levels=_GRADE_LEVELS,
+                   ratio=_GRADE_RATIO):
+    """Composite Gauss panels shrinking toward flagged ends (assembly.py:349-378)."""
+    def one_side(p_lo, p_hi, to_lo):
+        h = p_hi - p_lo
+        cuts = h * ratio ** np.arange(levels + 1)
+        edges = np.concatenate([[0.0], cuts[::-1]])
+        if to_lo:
+            return np.column_stack([p_lo + edges[:-1], p_lo + edges[1:]])
+        return np.column_stack([p_hi - edges[1:], p_hi - edges[:-1]])[::-1]
+
+    if toward_lo and toward_hi:
+        mid = 0.5 * (lo + hi)
+        panels = np.vstack([one_side(lo, mid, True), one_side(mid, hi, False)])
+    elif toward_lo:
+        panels = one_side(lo, hi, True)
+    elif toward_hi:
+        panels = one_side(lo, hi, False)
+    else:
+        panels = np.array([[lo, hi]])
+    x, w = np.polynomial.legendre.leggauss(order)
+    half = 0.5 * (panels[:, 1] - panels[:, 0])
+    mid = 0.5 * (panels[:, 0] + panels[:, 1])
+    return (mid[:, None] + half[:, None] * x[None, :]).ravel(), (half[:, None] * w[None, :]).ravel()
+
+
+def assemble_b1(curve, space, dirichlet, order: int = 16) -> np.ndarray:
+    """b1[i] = int B_i u_D J ds by per-element Gauss, graded at open ends
+    (assembly.py:287-309).  O(N) host work (not on the O(N^2) path)."""
+    curve = as_curve(curve)
+    space = as_basis(space)
+    _check_space(curve, space)
+    els = space.elements
+    if space.closed:
+        x, w = np.polynomial.legendre.leggauss(order)
+        half = 0.5 * (els[:, 1] - els[:, 0])
+        mid = 0.5 * (els[:, 0] + els[:, 1])
+        pts = (mid[:, None] + half[:, None] * x[None, :]).ravel()
+        wts = (half[:, None] * w[None, :]).ravel()
+    else:
+        last = len(els) - 1
+        pp = [_graded_points(lo, hi, order, e == 0, e == last) for e, (lo, hi) in enumerate(els)]
+        pts = np.concatenate([p for p, _ in pp])
+        wts = np.concatenate([w for _, w in pp])
+    vals = np.asarray(dirichlet(pts), dtype=float)
+    bv, bc = active_values(space, pts)
+    jac = np.linalg.norm(curve.spline(1)(np.clip(pts, curve.basis.a, curve.basis.b)), axis=-1)
+    out = np.zeros(space.dim)
+    np.add.at(out, bc.ravel(), (bv * (wts * jac * vals)[:, None]).ravel())
+    return out

@@ -1,0 +1,169 @@
+// C-ABI plumbing: error reporting, version, epilogue and RHS kernels.
+//
+//   wq_symmetrize      <- scale_and_symmetrize   (assembly.py:262-271)
+//   wq_absmax_defect   <- its defect measure      (assembly.py:269-270)
+//   wq_b1w             <- assemble_b1_weighted    (assembly.py:312-319)
+#include <stdarg.h>
+#include <string.h>
+
+#include "wq_common.cuh"
+
+namespace wq {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return WQ_ECUDA;
+  }
+  return WQ_OK;
+}
+
+// A = alpha (X + X^T) in place.  One CTA per tile pair (bi <= bj); both
+// 32x32 tiles are staged in shared memory so each element is read and
+// written exactly once (HBM-bound: 16 B per entry).
+__global__ void __launch_bounds__(256) symmetrize_kernel(double* X, int64_t n, double alpha,
+                                                         int nb) {
+  __shared__ double a[32][33];
+  __shared__ double b[32][33];
+  // map blockIdx.x -> (bi, bj) with bi <= bj over the upper triangle of tiles
+  int64_t t = blockIdx.x;
+  int bi = 0;
+  {
+    // row bi holds nb - bi tiles
+    int64_t rem = t;
+    while (rem >= nb - bi) {
+      rem -= nb - bi;
+      ++bi;
+    }
+    t = rem;
+  }
+  int bj = bi + (int)t;
+  int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  int64_t r0 = (int64_t)bi * 32, c0 = (int64_t)bj * 32;
+  for (int y = ty; y < 32; y += 8) {
+    int64_t r = r0 + y, c = c0 + tx;
+    a[y][tx] = (r < n && c < n) ? X[r * n + c] : 0.0;
+    int64_t r2 = c0 + y, c2 = r0 + tx;
+    b[y][tx] = (r2 < n && c2 < n) ? X[r2 * n + c2] : 0.0;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    int64_t r = r0 + y, c = c0 + tx;
+    if (r < n && c < n) X[r * n + c] = alpha * (a[y][tx] + b[tx][y]);
+    int64_t r2 = c0 + y, c2 = r0 + tx;
+    if (bi != bj && r2 < n && c2 < n) X[r2 * n + c2] = alpha * (b[y][tx] + a[tx][y]);
+  }
+}
+
+__device__ __forceinline__ void atomic_max_pos(double* addr, double v) {
+  // non-negative doubles order like their bit patterns: deterministic max
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void __launch_bounds__(256) absmax_defect_kernel(const double* X, int64_t n, double* out) {
+  double m0 = 0.0, m1 = 0.0;
+  int64_t total = n * n;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = k / n, c = k - r * n;
+    double x = X[k];
+    m0 = fmax(m0, fabs(x));
+    m1 = fmax(m1, fabs(x - X[c * n + r]));
+  }
+  for (int o = 16; o; o >>= 1) {
+    m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+    m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_pos(out, m0);
+    atomic_max_pos(out + 1, m1);
+  }
+}
+
+__global__ void b1w_kernel(wq_smooth_t sm, const double* g, double* b) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= sm.n_rows) return;
+  double acc = 0.0;
+  for (int w = 0; w < sm.wg; ++w) {
+    int64_t q = pmod(sm.g_start[i] + w, sm.nq);
+    acc = fma(sm.g_w[i * sm.wg + w], g[q], acc);
+  }
+  b[i] = acc;
+}
+
+// FP64 pipe peak probe: 8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(256) fp64_peak_kernel(int64_t iters, double seed, double* out) {
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  double a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999999, c = 1e-9;
+  for (int64_t k = 0; k < iters; ++k) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+  }
+  double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (r == 12345.678) out[blockIdx.x] = r;  // keep the chains alive
+}
+
+}  // namespace wq
+
+using namespace wq;
+
+extern "C" {
+
+int wq_version(void) { return 1; }
+
+int wq_fp64_peak(int64_t iters, int blocks, double* out, void* stream) {
+  if (iters <= 0 || blocks <= 0 || !out) {
+    set_error("wq_fp64_peak: bad arguments");
+    return WQ_EINVAL;
+  }
+  fp64_peak_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, 1.0, out);
+  return check_launch("wq_fp64_peak");
+}
+
+const char* wq_last_error(void) { return g_err; }
+
+int wq_symmetrize(double* X, int64_t n, double alpha, void* stream) {
+  if (!X || n <= 0) {
+    set_error("wq_symmetrize: bad arguments");
+    return WQ_EINVAL;
+  }
+  int nb = ceil_div(n, 32);
+  int64_t tiles = (int64_t)nb * (nb + 1) / 2;
+  symmetrize_kernel<<<(unsigned)tiles, 256, 0, (cudaStream_t)stream>>>(X, n, alpha, nb);
+  return check_launch("wq_symmetrize");
+}
+
+int wq_absmax_defect(const double* X, int64_t n, double* out, void* stream) {
+  if (!X || !out || n <= 0) {
+    set_error("wq_absmax_defect: bad arguments");
+    return WQ_EINVAL;
+  }
+  cudaMemsetAsync(out, 0, 2 * sizeof(double), (cudaStream_t)stream);
+  absmax_defect_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(X, n, out);
+  return check_launch("wq_absmax_defect");
+}
+
+int wq_b1w(const wq_smooth_t* sm, const double* g, double* b, void* stream) {
+  if (!sm || !g || !b) {
+    set_error("wq_b1w: bad arguments");
+    return WQ_EINVAL;
+  }
+  b1w_kernel<<<ceil_div(sm->n_rows, 128), 128, 0, (cudaStream_t)stream>>>(*sm, g, b);
+  return check_launch("wq_b1w");
+}
+
+}  // extern "C"

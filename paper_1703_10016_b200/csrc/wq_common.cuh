@@ -1,0 +1,30 @@
+// Shared helpers for the sm_100a FP64 SGBEM assembly kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <math.h>
+
+#include "../../include/wqb200.h"
+
+namespace wq {
+
+// Last error message of the calling host thread (C-ABI: wq_last_error()).
+void set_error(const char* fmt, ...);
+
+// Record a launch error (if any) and return the C-ABI status.
+int check_launch(const char* what);
+
+__host__ __device__ __forceinline__ int64_t pmod(int64_t a, int64_t n) {
+  int64_t r = a % n;
+  return r < 0 ? r + n : r;
+}
+
+__host__ __device__ __forceinline__ int ceil_div(int64_t a, int64_t b) {
+  return (int)((a + b - 1) / b);
+}
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kTwoPi = 6.28318530717958647692;
+
+}  // namespace wq

@@ -1,0 +1,156 @@
+// Fused smooth-kernel grid + banded sum-factorised contraction (north_star
+// (a)+(b)); replaces assemble_ik1 (assembly.py:175-183) and the K1 grid of
+// KernelSplit.K1_grid (geometry.py:225-248):
+//
+//   IK1[i, j] = sum_q sum_r G[i,q] K1(eta_q, eta_r) G[j,r],
+//   K1 = 1/2 ln(|f(s) - f(t)|^2 / p(s,t)^2),  K1(s,s) = ln J(s).
+//
+// One CTA owns a TI x TJ output tile.  The node rows/columns its rules touch
+// (a contiguous, seam-wrapping range of span <= 2*T + wg) are staged in
+// shared memory, the K1 tile is evaluated there once (never written to HBM),
+// then contracted as T = K1 G^T (per outer node) and X = G T.
+#include "wq_common.cuh"
+
+namespace wq {
+
+constexpr int IK1_TI = WQ_TILE;
+constexpr int IK1_TJ = WQ_TILE;
+constexpr int IK1_THREADS = 256;
+
+struct NodeRec {
+  double s, fx, fy, J;
+};
+
+__device__ __forceinline__ double k1_value(const wq_smooth_t& sm, int64_t qa, const NodeRec& a,
+                                           int64_t ra, const NodeRec& b, int* bad) {
+  double R;
+  if (qa == ra) {
+    R = a.J * a.J;  // continuity limit J^2 (geometry.py:240-245)
+  } else {
+    double dx = a.fx - b.fx, dy = a.fy - b.fy;
+    double dist2 = dx * dx + dy * dy;
+    if (sm.k1_mode == WQ_K1_TABLE) {
+      int64_t g = ra > qa ? ra - qa : qa - ra;
+      R = dist2 * sm.invp2[g];
+    } else if (sm.k1_mode == WQ_K1_OPEN) {
+      double p = fabs(b.s - a.s);
+      R = dist2 / (p * p);
+    } else {
+      // periodic distance from the UNWRAPPED |t - s| (geometry.py:136-138)
+      double x = fabs(b.s - a.s);
+      double p = (sm.period / kPi) * fabs(sin(kPi * x / sm.period));
+      R = dist2 / (p * p);
+    }
+  }
+  if (!(R > 0.0)) *bad = 1;
+  return 0.5 * log(R);
+}
+
+__global__ void __launch_bounds__(IK1_THREADS)
+ik1_tile_kernel(wq_smooth_t sm, int64_t row0, int64_t row1, int64_t col0, int64_t col1, double* X,
+                int64_t ldx, int accumulate, int span, int* flag) {
+  extern __shared__ double smem[];
+  const int wg = (int)sm.wg;
+  const int64_t I0 = row0 + (int64_t)blockIdx.y * IK1_TI;
+  const int64_t J0 = col0 + (int64_t)blockIdx.x * IK1_TJ;
+  const int ni = (int)(row1 - I0 < IK1_TI ? row1 - I0 : IK1_TI);
+  const int nj = (int)(col1 - J0 < IK1_TJ ? col1 - J0 : IK1_TJ);
+  const int64_t qlo = sm.g_start[I0];
+  const int nQ = (int)(sm.g_start[I0 + ni - 1] + wg - qlo);
+  const int64_t rlo = sm.g_start[J0];
+  const int nR = (int)(sm.g_start[J0 + nj - 1] + wg - rlo);
+
+  NodeRec* qn = reinterpret_cast<NodeRec*>(smem);         // span
+  NodeRec* rn = qn + span;                                // span
+  double* K = reinterpret_cast<double*>(rn + span);       // span * span
+  double* T = K + (size_t)span * span;                    // span * TJ
+  double* Gi = T + (size_t)span * IK1_TJ;                 // TI * wg
+  double* Gj = Gi + IK1_TI * wg;                          // TJ * wg
+  int* qidx = reinterpret_cast<int*>(Gj + IK1_TJ * wg);   // span
+  int* ridx = qidx + span;                                // span
+
+  for (int k = threadIdx.x; k < nQ; k += blockDim.x) {
+    int64_t a = pmod(qlo + k, sm.nq);
+    qidx[k] = (int)a;
+    qn[k] = NodeRec{sm.s[a], sm.fx[a], sm.fy[a], sm.J[a]};
+  }
+  for (int k = threadIdx.x; k < nR; k += blockDim.x) {
+    int64_t a = pmod(rlo + k, sm.nq);
+    ridx[k] = (int)a;
+    rn[k] = NodeRec{sm.s[a], sm.fx[a], sm.fy[a], sm.J[a]};
+  }
+  for (int k = threadIdx.x; k < IK1_TI * wg; k += blockDim.x) {
+    int ii = k / wg;
+    Gi[k] = ii < ni ? sm.g_w[(I0 + ii) * wg + (k - ii * wg)] : 0.0;
+  }
+  for (int k = threadIdx.x; k < IK1_TJ * wg; k += blockDim.x) {
+    int jj = k / wg;
+    Gj[k] = jj < nj ? sm.g_w[(J0 + jj) * wg + (k - jj * wg)] : 0.0;
+  }
+  __syncthreads();
+
+  int bad = 0;
+  for (int k = threadIdx.x; k < nQ * nR; k += blockDim.x) {
+    int a = k / nR, b = k - a * nR;
+    K[a * span + b] = k1_value(sm, qidx[a], qn[a], ridx[b], rn[b], &bad);
+  }
+  if (bad) atomicOr(flag, WQ_FLAG_R_NONPOSITIVE);
+  __syncthreads();
+
+  // T[q][jj] = sum_w K[q][r_j + w] G[j][w]
+  for (int k = threadIdx.x; k < nQ * IK1_TJ; k += blockDim.x) {
+    int q = k / IK1_TJ, jj = k - q * IK1_TJ;
+    double acc = 0.0;
+    if (jj < nj) {
+      int r0 = (int)(sm.g_start[J0 + jj] - rlo);
+      const double* kr = K + q * span + r0;
+      const double* gj = Gj + jj * wg;
+      for (int w = 0; w < wg; ++w) acc = fma(kr[w], gj[w], acc);
+    }
+    T[q * IK1_TJ + jj] = acc;
+  }
+  __syncthreads();
+
+  // X[i][j] = sum_w G[i][w] T[q_i + w][jj]
+  for (int k = threadIdx.x; k < ni * IK1_TJ; k += blockDim.x) {
+    int ii = k / IK1_TJ, jj = k - ii * IK1_TJ;
+    if (jj >= nj) continue;
+    int q0 = (int)(sm.g_start[I0 + ii] - qlo);
+    const double* gi = Gi + ii * wg;
+    double acc = 0.0;
+    for (int w = 0; w < wg; ++w) acc = fma(gi[w], T[(q0 + w) * IK1_TJ + jj], acc);
+    double* dst = X + (I0 - row0 + ii) * ldx + (J0 - col0 + jj);
+    *dst = accumulate ? *dst + acc : acc;
+  }
+}
+
+}  // namespace wq
+
+using namespace wq;
+
+extern "C" int wq_ik1(const wq_smooth_t* sm, int64_t row0, int64_t row1, int64_t col0, int64_t col1,
+                      double* X, int64_t ldx, int accumulate, int64_t max_span, int* flag,
+                      void* stream) {
+  if (!sm || !X || !flag || row0 < 0 || row1 > sm->n_rows || col0 < 0 || col1 > sm->n_rows ||
+      row1 <= row0 || col1 <= col0 || sm->wg <= 0 || max_span < sm->wg) {
+    set_error("wq_ik1: bad arguments");
+    return WQ_EINVAL;
+  }
+  if (sm->k1_mode == WQ_K1_TABLE && !sm->invp2) {
+    set_error("wq_ik1: table mode without invp2");
+    return WQ_EINVAL;
+  }
+  int span = (int)max_span;
+  size_t smem = (size_t)2 * span * sizeof(NodeRec) + (size_t)span * span * 8 +
+                (size_t)span * IK1_TJ * 8 + (size_t)(IK1_TI + IK1_TJ) * sm->wg * 8 +
+                (size_t)2 * span * sizeof(int);
+  if (smem > 227 * 1024) {
+    set_error("wq_ik1: node span %d too large for one tile (%zu B smem)", span, smem);
+    return WQ_EUNSUPPORTED;
+  }
+  cudaFuncSetAttribute(ik1_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(ceil_div(col1 - col0, IK1_TJ), ceil_div(row1 - row0, IK1_TI));
+  ik1_tile_kernel<<<grid, IK1_THREADS, smem, (cudaStream_t)stream>>>(*sm, row0, row1, col0, col1, X,
+                                                                     ldx, accumulate, span, flag);
+  return check_launch("wq_ik1");
+}

@@ -1,0 +1,484 @@
+// Log-singular part of the Galerkin matrix (assemble_ik2, assembly.py:186-245)
+// in the X-form:
+//
+//   X2 = (2 Theta - C^T D) C,  C = H^{-1} S,   IK2 = (X2 + X2^T) / 2,
+//
+// * wq_pair_table   : gap-indexed double log moments (quadrature.py:441-504)
+// * wq_circ_tables  : closed uniform simple-knot meshes: fold the (translation
+//                     invariant) v, H^{-1} and D into per-gap tables
+// * wq_ik2_circ     : fused Phi = H^{-1} Psi^T evaluation + banded S contraction
+// * general path    : Theta^T / D element-pair gathers, banded Cholesky column
+//                     solves, S gathers (open meshes, any multiplicities)
+#include "wq_common.cuh"
+
+namespace wq {
+
+// ---------------------------------------------------------------------------
+// pair-moment table
+// ---------------------------------------------------------------------------
+
+constexpr int PT_MAXG = 32;   // max Gauss order
+constexpr int PT_MAXA = 24;   // max row degree + 1
+constexpr int PT_MAXB = 8;    // max col degree + 1
+
+__global__ void __launch_bounds__(128)
+pair_table_kernel(int64_t nel, int closed, int da, int db, double h, const double* near_unit,
+                  const double* gx, const double* gw, int ng, const double* ca, const double* cb,
+                  double* m2) {
+  __shared__ double x[PT_MAXG], w[PT_MAXG];
+  __shared__ double wa[PT_MAXG][PT_MAXA];   // w_g x_g^a
+  __shared__ double wb[PT_MAXG][PT_MAXB];   // w_h x_h^b
+  __shared__ double kern[PT_MAXG][PT_MAXG + 1];
+  __shared__ double t[PT_MAXG][PT_MAXB];
+  __shared__ double acc[PT_MAXA][PT_MAXB];
+  const int64_t k = blockIdx.x;
+  double keff;
+  if (closed) {
+    keff = (double)k - (double)nel * rint((double)k / (double)nel);
+  } else {
+    keff = (double)(k - (nel - 1));
+  }
+  const double delta = -keff;
+  const int nA = da + 1, nB = db + 1;
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+    x[g] = gx[g];
+    w[g] = gw[g];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ng * nA; e += blockDim.x) {
+    int g = e / nA, a = e - g * nA;
+    wa[g][a] = w[g] * pow(x[g], (double)a);
+  }
+  for (int e = threadIdx.x; e < ng * nB; e += blockDim.x) {
+    int g = e / nB, b = e - g * nB;
+    wb[g][b] = w[g] * pow(x[g], (double)b);
+  }
+  const bool near = fabs(keff) <= 1.0;
+  for (int e = threadIdx.x; e < nA * nB; e += blockDim.x) {
+    int a = e / nB, b = e - a * nB;
+    acc[a][b] = near ? near_unit[((int)keff + 1) * nA * nB + e] : 0.0;
+  }
+  __syncthreads();
+
+  // pass 0: ln|v - u - delta| (far gaps); pass 1: periodic ln|sinc| (closed)
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 0 && near) continue;
+    if (pass == 1 && !closed) continue;
+    for (int e = threadIdx.x; e < ng * ng; e += blockDim.x) {
+      int g = e / ng, hh = e - g * ng;
+      double arg = (x[hh] - x[g]) - delta;  // v - u - delta, he = hf = 1
+      double val;
+      if (pass == 0) {
+        val = log(fabs(arg));
+      } else {
+        double y = arg / (double)nel;          // np.sinc(arg / period)
+        double py = kPi * y;
+        double s = (y == 0.0) ? 1.0 : sin(py) / py;
+        val = log(fabs(s));
+      }
+      kern[g][hh] = val;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < ng * nB; e += blockDim.x) {
+      int g = e / nB, b = e - g * nB;
+      double s = 0.0;
+      for (int hh = 0; hh < ng; ++hh) s = fma(kern[g][hh], wb[hh][b], s);
+      t[g][b] = s;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nA * nB; e += blockDim.x) {
+      int a = e / nB, b = e - a * nB;
+      double s = 0.0;
+      for (int g = 0; g < ng; ++g) s = fma(wa[g][a], t[g][b], s);
+      acc[a][b] += s;
+    }
+    __syncthreads();
+  }
+  const double lh = log(h);
+  for (int e = threadIdx.x; e < nA * nB; e += blockDim.x) {
+    int a = e / nB, b = e - a * nB;
+    double scale = pow(h, 2.0 + (double)a + (double)b);
+    m2[k * nA * nB + e] = scale * (acc[a][b] + lh * (ca[a] * cb[b]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// circulant tables
+// ---------------------------------------------------------------------------
+
+__global__ void circ_z_kernel(int64_t n, int da, int db, const double* m2, const double* v0,
+                              double* Z) {
+  const int nA = da + 1, nB = db + 1;
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n * nA) return;
+  int64_t g = e / nA;
+  int al = (int)(e - g * nA);
+  double acc = 0.0;
+  for (int b = 0; b < nB; ++b) {
+    const double* row = m2 + pmod(g - b, n) * nA * nB + al * nB;
+    for (int be = 0; be < nB; ++be) acc = fma(row[be], v0[be * nB + b], acc);
+  }
+  Z[e] = acc;
+}
+
+__global__ void circ_dd_kernel(int64_t n, int da, int db, const double* Z, const double* v0,
+                               double* dd) {
+  const int nA = da + 1, nB = db + 1;
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double acc = 0.0;
+  for (int a = 0; a < nB; ++a) {
+    const double* z = Z + pmod(k + a, n) * nA;
+    for (int al = 0; al < nB; ++al) acc = fma(v0[al * nB + a], z[al], acc);
+  }
+  dd[k] = acc;
+}
+
+// out[g][c] = sum_{|k|<=K} in[(g + k) mod n][c] taps[K + k]
+__global__ void circ_corr_kernel(int64_t n, int nc, const double* in, const double* taps, int64_t K,
+                                 double* out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n * nc) return;
+  int64_t g = e / nc;
+  int c = (int)(e - g * nc);
+  double acc = 0.0;
+  for (int64_t k = -K; k <= K; ++k) acc = fma(in[pmod(g + k, n) * nc + c], taps[K + k], acc);
+  out[e] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// fused circulant log part: X[i,j] (+)= sum_t S[s_j+t, j] Phi[s_j+t, i]
+// ---------------------------------------------------------------------------
+
+constexpr int CT = WQ_TILE;  // rows (i) and cols (j) per CTA
+
+__global__ void __launch_bounds__(256)
+ik2_circ_kernel(wq_logpart_t lp, const double* Zp, const double* ff, int64_t row0, int64_t row1,
+                int64_t col0, int64_t col1, double* X, int64_t ldx, int accumulate) {
+  extern __shared__ double smem[];
+  const int nA = (int)lp.da + 1, tu = (int)lp.tu, ws = (int)lp.ws;
+  const int64_t n = lp.n_fine;
+  const int64_t I0 = row0 + (int64_t)blockIdx.y * CT;
+  const int64_t J0 = col0 + (int64_t)blockIdx.x * CT;
+  const int ni = (int)(row1 - I0 < CT ? row1 - I0 : CT);
+  const int nj = (int)(col1 - J0 < CT ? col1 - J0 : CT);
+  // unit-step starts (closed uniform simple knots, nref = 1)
+  const int64_t mlo = lp.s_start[J0];
+  const int mspan = CT - 1 + ws;
+  const int64_t gmin = mlo - lp.e_start[I0] - (CT - 1) - (tu - 1);
+  const int zspan = mspan + CT - 1 + tu - 1;
+  const int64_t fmin = mlo - lp.s_start[I0] - (CT - 1) - (ws - 1);
+  const int fspan = mspan + CT - 1 + ws - 1;
+
+  double* Us = smem;                          // CT * tu * nA
+  double* Zs = Us + CT * tu * nA;             // zspan * nA
+  double* Fs = Zs + zspan * nA;               // fspan
+  double* Si = Fs + fspan;                    // CT * ws
+  double* Sj = Si + CT * ws;                  // CT * ws
+  double* Ph = Sj + CT * ws;                  // mspan * CT
+
+  for (int k = threadIdx.x; k < CT * tu * nA; k += blockDim.x) {
+    int ii = k / (tu * nA);
+    Us[k] = ii < ni ? lp.U[(I0 + ii) * tu * nA + (k - ii * tu * nA)] : 0.0;
+  }
+  for (int k = threadIdx.x; k < zspan * nA; k += blockDim.x) {
+    int g = k / nA;
+    Zs[k] = Zp[pmod(gmin + g, n) * nA + (k - g * nA)];
+  }
+  for (int k = threadIdx.x; k < fspan; k += blockDim.x) Fs[k] = ff[pmod(fmin + k, n)];
+  for (int k = threadIdx.x; k < CT * ws; k += blockDim.x) {
+    int ii = k / ws;
+    Si[k] = ii < ni ? lp.s_w[(I0 + ii) * ws + (k - ii * ws)] : 0.0;
+    Sj[k] = ii < nj ? lp.s_w[(J0 + ii) * ws + (k - ii * ws)] : 0.0;
+  }
+  __syncthreads();
+
+  // Phi[mm][ii], m = mlo + mm
+  for (int k = threadIdx.x; k < mspan * CT; k += blockDim.x) {
+    int mm = k / CT, ii = k - mm * CT;
+    double acc = 0.0;
+    if (ii < ni) {
+      // Zp row for (m, i, a): m - e_start[i] - a = (mlo + mm) - (e_start[I0] + ii) - a
+      const int zb = (int)((mlo + mm) - (lp.e_start[I0] + ii) - gmin);
+      const double* u = Us + ii * tu * nA;
+      for (int a = 0; a < tu; ++a) {
+        const double* z = Zs + (zb - a) * nA;
+        const double* ua = u + a * nA;
+        for (int al = 0; al < nA; ++al) acc = fma(ua[al], z[al], acc);
+      }
+      acc *= 2.0;
+      const int fb = (int)((mlo + mm) - (lp.s_start[I0] + ii) - fmin);
+      const double* si = Si + ii * ws;
+      for (int t = 0; t < ws; ++t) acc = fma(-si[t], Fs[fb - t], acc);
+    }
+    Ph[mm * CT + ii] = acc;
+  }
+  __syncthreads();
+
+  for (int k = threadIdx.x; k < CT * CT; k += blockDim.x) {
+    int ii = k / CT, jj = k - ii * CT;
+    if (ii >= ni || jj >= nj) continue;
+    const double* sj = Sj + jj * ws;
+    double acc = 0.0;
+    for (int t = 0; t < ws; ++t) acc = fma(sj[t], Ph[(jj + t) * CT + ii], acc);
+    double* dst = X + (I0 - row0 + ii) * ldx + (J0 - col0 + jj);
+    *dst = accumulate ? *dst + acc : acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// general path (open meshes): element-pair gathers + banded solves
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int64_t gap_index(const wq_pairs_t& pp, int64_t e, int64_t f) {
+  return pp.closed ? pmod(f - e, pp.n_el) : f - e + pp.n_el - 1;
+}
+
+// Theta^T[l][i] = sum_{(f,b) in inc_v(l)} sum_{(e,a) in inc_u(i)} u[e][:,a]^T M2[gap] v[f][:,b]
+__global__ void theta_t_kernel(wq_pairs_t pp, double* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t l = blockIdx.y;
+  if (i >= pp.n_rows) return;
+  const int nA = (int)pp.da + 1, nB = (int)pp.db + 1, nU = (int)pp.pu + 1;
+  double acc = 0.0;
+  for (int vb = 0; vb < pp.wv; ++vb) {
+    int64_t f = pp.v_el[l * pp.wv + vb];
+    if (f < 0) continue;
+    int b = (int)pp.v_loc[l * pp.wv + vb];
+    const double* vf = pp.v + f * nB * nB;
+    for (int ua = 0; ua < pp.wu; ++ua) {
+      int64_t e = pp.u_el[i * pp.wu + ua];
+      if (e < 0) continue;
+      int a = (int)pp.u_loc[i * pp.wu + ua];
+      const double* ue = pp.u + e * nA * nU;
+      const double* m = pp.m2 + gap_index(pp, e, f) * nA * nB;
+      double s = 0.0;
+      for (int al = 0; al < nA; ++al) {
+        double r = 0.0;
+        for (int be = 0; be < nB; ++be) r = fma(m[al * nB + be], vf[be * nB + b], r);
+        s = fma(ue[al * nU + a], r, s);
+      }
+      acc += s;
+    }
+  }
+  out[l * pp.n_rows + i] = acc;
+}
+
+// D[l][m] = sum_{(e,a) in inc_v(l)} sum_{(f,b) in inc_v(m)} v[e][:,a]^T M2[gap][:db+1] v[f][:,b]
+__global__ void dmat_kernel(wq_pairs_t pp, double* out) {
+  int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t l = blockIdx.y;
+  if (m >= pp.n_fine) return;
+  const int nA = (int)pp.da + 1, nB = (int)pp.db + 1;
+  double acc = 0.0;
+  for (int va = 0; va < pp.wv; ++va) {
+    int64_t e = pp.v_el[l * pp.wv + va];
+    if (e < 0) continue;
+    int a = (int)pp.v_loc[l * pp.wv + va];
+    const double* ve = pp.v + e * nB * nB;
+    for (int vb = 0; vb < pp.wv; ++vb) {
+      int64_t f = pp.v_el[m * pp.wv + vb];
+      if (f < 0) continue;
+      int b = (int)pp.v_loc[m * pp.wv + vb];
+      const double* vf = pp.v + f * nB * nB;
+      const double* mm = pp.m2 + gap_index(pp, e, f) * nA * nB;
+      double s = 0.0;
+      for (int al = 0; al < nB; ++al) {
+        double r = 0.0;
+        for (int be = 0; be < nB; ++be) r = fma(mm[al * nB + be], vf[be * nB + b], r);
+        s = fma(ve[al * nB + a], r, s);
+      }
+      acc += s;
+    }
+  }
+  out[l * pp.n_fine + m] = acc;
+}
+
+// X <- H^{-1} X column by column, H = L L^T banded (Lb[k][j] = L[k][k-j]).
+__global__ void band_solve_cols_kernel(int64_t n, int bw, const double* Lb, double* X,
+                                       int64_t ncols, int64_t ldx) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  double* x = X + c;
+  for (int64_t k = 0; k < n; ++k) {
+    double s = x[k * ldx];
+    const double* lk = Lb + k * (bw + 1);
+    for (int j = 1; j <= bw && j <= k; ++j) s = fma(-lk[j], x[(k - j) * ldx], s);
+    x[k * ldx] = s / lk[0];
+  }
+  for (int64_t k = n - 1; k >= 0; --k) {
+    double s = x[k * ldx];
+    for (int j = 1; j <= bw && k + j < n; ++j) s = fma(-Lb[(k + j) * (bw + 1) + j], x[(k + j) * ldx], s);
+    x[k * ldx] = s / Lb[k * (bw + 1)];
+  }
+}
+
+__global__ void transpose_kernel(const double* in, int64_t rows, int64_t cols, double* out) {
+  __shared__ double t[32][33];
+  int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int y = ty; y < 32; y += 8) {
+    int64_t r = r0 + y, c = c0 + tx;
+    if (r < rows && c < cols) t[y][tx] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    int64_t r = c0 + y, c = r0 + tx;
+    if (r < cols && c < rows) out[r * rows + c] = t[tx][y];
+  }
+}
+
+// P[m][i] = alpha P[m][i] - sum_t F[m][(s_i + t) mod nf] S_i[t]
+__global__ void gather_fs_kernel(wq_logpart_t lp, double alpha, const double* F, double* P) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t m = blockIdx.y;
+  if (i >= lp.n_rows) return;
+  const int64_t nf = lp.n_fine;
+  double acc = alpha * P[m * lp.n_rows + i];
+  for (int t = 0; t < lp.ws; ++t) {
+    double s = lp.s_w[i * lp.ws + t];
+    if (s != 0.0) acc = fma(-F[m * nf + pmod(lp.s_start[i] + t, nf)], s, acc);
+  }
+  P[m * lp.n_rows + i] = acc;
+}
+
+// X[j][i] (+)= sum_t S_j[t] Phi[(s_j + t) mod nf][i]
+__global__ void add_st_phi_kernel(wq_logpart_t lp, const double* Phi, int64_t row0, double* X,
+                                  int64_t ldx, int accumulate) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t j = row0 + blockIdx.y;
+  if (i >= lp.n_rows) return;
+  double acc = 0.0;
+  for (int t = 0; t < lp.ws; ++t) {
+    double s = lp.s_w[j * lp.ws + t];
+    if (s != 0.0) acc = fma(s, Phi[pmod(lp.s_start[j] + t, lp.n_fine) * lp.n_rows + i], acc);
+  }
+  double* dst = X + (j - row0) * ldx + i;
+  *dst = accumulate ? *dst + acc : acc;
+}
+
+}  // namespace wq
+
+using namespace wq;
+
+extern "C" {
+
+int wq_pair_table(int64_t nel, int closed, int da, int db, double h, const double* near_unit,
+                  const double* gx, const double* gw, int n_gauss, const double* ca,
+                  const double* cb, double* m2, void* stream) {
+  if (nel < 2 || da + 1 > PT_MAXA || db + 1 > PT_MAXB || n_gauss > PT_MAXG || n_gauss < 1 ||
+      !near_unit || !gx || !gw || !ca || !cb || !m2 || !(h > 0)) {
+    set_error("wq_pair_table: bad arguments");
+    return WQ_EINVAL;
+  }
+  int64_t n_gap = closed ? nel : 2 * nel - 1;
+  pair_table_kernel<<<(unsigned)n_gap, 128, 0, (cudaStream_t)stream>>>(
+      nel, closed, da, db, h, near_unit, gx, gw, n_gauss, ca, cb, m2);
+  return check_launch("wq_pair_table");
+}
+
+int wq_circ_tables(int64_t n, int da, int db, const double* m2, const double* v0,
+                   const double* hinv_taps, int64_t K, double* Zp, double* ff, double* work,
+                   double* Zwork, void* stream) {
+  if (n < 2 || !m2 || !v0 || !hinv_taps || !Zp || !ff || !work || !Zwork || K < 0 || K > n) {
+    set_error("wq_circ_tables: bad arguments");
+    return WQ_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nA = da + 1;
+  circ_z_kernel<<<ceil_div(n * nA, 256), 256, 0, s>>>(n, da, db, m2, v0, Zwork);
+  circ_dd_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, da, db, Zwork, v0, ff);
+  circ_corr_kernel<<<ceil_div(n * nA, 256), 256, 0, s>>>(n, nA, Zwork, hinv_taps, K, Zp);
+  // ff = hinv * dd * hinv (hinv symmetric: correlation == convolution)
+  circ_corr_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, 1, ff, hinv_taps, K, work);
+  circ_corr_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, 1, work, hinv_taps, K, ff);
+  return check_launch("wq_circ_tables");
+}
+
+int wq_ik2_circ(const wq_logpart_t* lp, const double* Zp, const double* ff, int64_t row0,
+                int64_t row1, int64_t col0, int64_t col1, double* X, int64_t ldx, int accumulate,
+                void* stream) {
+  if (!lp || !Zp || !ff || !X || row0 < 0 || row1 > lp->n_rows || col0 < 0 ||
+      col1 > lp->n_rows || row1 <= row0 || col1 <= col0 || lp->n_fine != lp->n_rows) {
+    set_error("wq_ik2_circ: bad arguments");
+    return WQ_EINVAL;
+  }
+  const int nA = (int)lp->da + 1, tu = (int)lp->tu, ws = (int)lp->ws;
+  const int mspan = CT - 1 + ws;
+  const int zspan = mspan + CT - 1 + tu - 1;
+  const int fspan = mspan + CT - 1 + ws - 1;
+  size_t smem = ((size_t)CT * tu * nA + (size_t)zspan * nA + fspan + 2 * CT * ws + (size_t)mspan * CT) * 8;
+  if (smem > 227 * 1024) {
+    set_error("wq_ik2_circ: tile does not fit in shared memory");
+    return WQ_EUNSUPPORTED;
+  }
+  cudaFuncSetAttribute(ik2_circ_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(ceil_div(col1 - col0, CT), ceil_div(row1 - row0, CT));
+  ik2_circ_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(*lp, Zp, ff, row0, row1, col0, col1, X,
+                                                             ldx, accumulate);
+  return check_launch("wq_ik2_circ");
+}
+
+int wq_theta_t(const wq_pairs_t* pp, double* thetaT, void* stream) {
+  if (!pp || !thetaT) {
+    set_error("wq_theta_t: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 grid(ceil_div(pp->n_rows, 128), (unsigned)pp->n_fine);
+  theta_t_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*pp, thetaT);
+  return check_launch("wq_theta_t");
+}
+
+int wq_dmat(const wq_pairs_t* pp, double* D, void* stream) {
+  if (!pp || !D) {
+    set_error("wq_dmat: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 grid(ceil_div(pp->n_fine, 128), (unsigned)pp->n_fine);
+  dmat_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*pp, D);
+  return check_launch("wq_dmat");
+}
+
+int wq_band_solve_cols(int64_t n, int64_t bw, const double* Lb, double* X, int64_t ncols,
+                       int64_t ldx, void* stream) {
+  if (n <= 0 || bw < 0 || !Lb || !X || ncols <= 0) {
+    set_error("wq_band_solve_cols: bad arguments");
+    return WQ_EINVAL;
+  }
+  band_solve_cols_kernel<<<ceil_div(ncols, 128), 128, 0, (cudaStream_t)stream>>>(n, (int)bw, Lb, X,
+                                                                                   ncols, ldx);
+  return check_launch("wq_band_solve_cols");
+}
+
+int wq_transpose(const double* in, int64_t rows, int64_t cols, double* out, void* stream) {
+  if (!in || !out || rows <= 0 || cols <= 0) {
+    set_error("wq_transpose: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 grid(ceil_div(cols, 32), ceil_div(rows, 32));
+  transpose_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(in, rows, cols, out);
+  return check_launch("wq_transpose");
+}
+
+int wq_gather_fs(const wq_logpart_t* lp, double alpha, const double* F, double* P, void* stream) {
+  if (!lp || !F || !P) {
+    set_error("wq_gather_fs: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 grid(ceil_div(lp->n_rows, 128), (unsigned)lp->n_fine);
+  gather_fs_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, alpha, F, P);
+  return check_launch("wq_gather_fs");
+}
+
+int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64_t row1, double* X,
+                  int64_t ldx, int accumulate, void* stream) {
+  if (!lp || !Phi || !X || row0 < 0 || row1 > lp->n_rows || row1 <= row0) {
+    set_error("wq_add_st_phi: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 grid(ceil_div(lp->n_rows, 128), (unsigned)(row1 - row0));
+  add_st_phi_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, Phi, row0, X, ldx, accumulate);
+  return check_launch("wq_add_st_phi");
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+"""CPU: the O(N) host precompute of the product against the reference's
+outputs, and a numpy execution of the exact GPU dataflow (same host arrays,
+same index conventions as the kernels) against the reference matrix."""
+
+import numpy as np
+import pytest
+
+import paper_1703_10016_b200 as W
+from paper_1703_10016_b200 import assembly as AS, precompute as PC
+from paper_1703_10016_b200.errors import ConstructionError, UsageError
+from oracle import wq_oracle as O
+from _cases import golden_names, load, product_objects, rel
+
+FULL = [n for n in golden_names() if "G" in load(n)[0]]
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_nodes_match_reference(name):
+    z, meta = load(name)
+    curve, space = product_objects(meta)
+    disc = W.build_discretization(curve, space, meta["nref"])
+    assert np.array_equal(disc.nodes.nodes, z["nodes"])
+    assert np.array_equal(disc.J_nodes, z["J_nodes"])  # same scipy evaluation
+    assert disc.nodes.n == meta["nq"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_rule_band_matches_reference_G(name):
+    z, meta = load(name)
+    curve, space = product_objects(meta)
+    disc = W.build_discretization(curve, space, meta["nref"])
+    G = disc.G
+    assert np.array_equal(G != 0, z["G"] != 0)
+    # min-norm solver differences live in the exactness null space
+    # (SURVEY sec.7 iii: <= 8.8e-11 at p=5, effect on IK1 <= 2e-15)
+    tol = {2: 1e-13, 3: 1e-12, 4: 1e-10, 5: 1e-9}[space.degree]
+    assert rel(G, z["G"]) <= tol
+
+
+def _emulate_gpu_dataflow(disc):
+    """numpy rendition of wq_ik1 + wq_pair_table + wq_circ_tables +
+    wq_ik2_circ / general path + wq_symmetrize on the product's arrays."""
+    N = disc.space.dim
+    nodes = disc.nodes.nodes
+    ocurve = O.Curve(disc.curve.basis, disc.curve.control_points)
+    X = disc.G @ O.k1_grid(ocurve, nodes, nodes) @ disc.G.T
+    lp = AS._log_part(disc)
+    n = lp.n_el
+    m2, _ = O.uniform_pair_moments(O.as_basis(disc.refined.basis), lp.da)
+    if lp.path == "circulant":
+        nB = lp.db + 1
+        Z = sum(np.roll(m2, b, axis=0) @ lp.v0[:, b] for b in range(nB))
+        dd = sum(np.roll(Z[:, :nB], -a, axis=0) @ lp.v0[:nB, a] for a in range(nB))
+        K = (len(lp.hinv_taps) - 1) // 2
+        corr = lambda arr: sum(np.roll(arr, -k, axis=0) * lp.hinv_taps[K + k] for k in range(-K, K + 1))
+        Zp, ff = corr(Z), corr(corr(dd))
+        m = np.arange(n)
+        Phi = np.zeros((n, N))
+        for i in range(N):
+            for a in range(lp.U.shape[1]):
+                Phi[:, i] += 2 * Zp[np.mod(m - lp.e_start[i] - a, n)] @ lp.U[i, a]
+            for t in range(lp.s_w.shape[1]):
+                Phi[:, i] -= lp.s_w[i, t] * ff[np.mod(m - lp.s_start[i] - t, n)]
+        X2 = np.zeros((N, N))
+        for j in range(N):
+            for t in range(lp.s_w.shape[1]):
+                X2[:, j] += lp.s_w[j, t] * Phi[(lp.s_start[j] + t) % n]
+        X = X + X2
+    else:
+        import scipy.linalg as sl
+        NE = disc.refined.basis.dim
+        gap = (lambda e, f: (f - e) % n) if disc.closed else (lambda e, f: f - e + n - 1)
+        thT = np.zeros((NE, N))
+        D = np.zeros((NE, NE))
+        for l in range(NE):
+            for f, b in zip(lp.v_el[l], lp.v_loc[l]):
+                if f < 0:
+                    continue
+                for i in range(N):
+                    for e, a in zip(lp.u_el[i], lp.u_loc[i]):
+                        if e >= 0:
+                            thT[l, i] += lp.u[e][:, a] @ m2[gap(e, f)] @ lp.v[f][:, b]
+                for mm in range(NE):
+                    for e, a in zip(lp.v_el[mm], lp.v_loc[mm]):
+                        if e >= 0:
+                            D[mm, l] += lp.v[e][:, a] @ m2[gap(e, f)][: lp.db + 1] @ lp.v[f][:, b]
+        L = np.zeros((NE, NE))
+        for j in range(lp.bw + 1):
+            L[np.arange(j, NE), np.arange(0, NE - j)] = lp.Lb[j:, j]
+        hinv = lambda Y: sl.solve_triangular(L.T, sl.solve_triangular(L, Y, lower=True))
+        F = hinv(hinv(D).T)
+        Phi = 2 * hinv(thT)
+        for i in range(N):
+            for t in range(lp.s_w.shape[1]):
+                Phi[:, i] -= F[:, (lp.s_start[i] + t) % NE] * lp.s_w[i, t]
+        X2T = np.zeros((N, N))
+        for j in range(N):
+            for t in range(lp.s_w.shape[1]):
+                X2T[j] += lp.s_w[j, t] * Phi[(lp.s_start[j] + t) % NE]
+        X = X + X2T
+    return -(X + X.T) / (4 * np.pi)
+
+
+@pytest.mark.parametrize("name", ["ell_p3_n32", "ell_p2_n64", "ell_p5_n64", "star_p4_n128",
+                                  "c1_slit_p2_n64", "slit_p4_n24_dbl", "parabola_p3_n16",
+                                  "slit_p5_n24"])
+def test_gpu_dataflow_in_numpy_matches_reference(name):
+    z, meta = load(name)
+    curve, space = product_objects(meta)
+    disc = W.build_discretization(curve, space, meta["nref"])
+    assert rel(_emulate_gpu_dataflow(disc), z["A"]) <= 5e-14
+
+
+def test_k1_distance_modes():
+    z, meta = load("ell_p3_n64")
+    curve, space = product_objects(meta)
+    disc = W.build_discretization(curve, space, 1)
+    assert disc.k1_mode == 0 and disc.invp2 is not None   # uniform binary nodes -> gap table
+    x = np.abs(disc.nodes.nodes - disc.nodes.nodes[0])
+    L = curve.length
+    p = (L / np.pi) * np.abs(np.sin(np.pi * x / L))
+    assert np.array_equal(disc.invp2[1:], 1.0 / (p[1:] * p[1:]))
+    z, meta = load("c1_slit_p2_n64")
+    curve, space = product_objects(meta)
+    assert W.build_discretization(curve, space, 1).k1_mode == 1  # open: graded end nodes
+
+
+def test_circulant_detection_and_taps():
+    curve, space = product_objects(load("ell_p3_n128")[1])
+    lp = AS._log_part(W.build_discretization(curve, space, 1))
+    assert lp.path == "circulant"
+    K = (len(lp.hinv_taps) - 1) // 2
+    assert np.allclose(lp.hinv_taps, lp.hinv_taps[::-1], rtol=0, atol=1e-15 * abs(lp.hinv_taps[K]))
+    if 2 * K + 1 < 128:
+        assert abs(lp.hinv_taps[0]) <= 1e-18 * abs(lp.hinv_taps[K])
+
+
+def test_errors_mirror_reference():
+    curve, _ = product_objects(load("ell_p3_n64")[1])
+    with pytest.raises(UsageError):
+        W.build_discretization(curve, W.make_open_basis(3, np.linspace(0, 1, 9)), 1)
+    slit = W.load_curve({"degree": 1, "knots": [-1, -1, 1, 1], "control_points": [[-1, 0], [1, 0]]})
+    graded = W.make_open_basis(2, np.array([-1, -0.9, -0.5, 0.0, 0.5, 0.9, 1.0]))
+    disc = W.build_discretization(slit, graded, 1)
+    with pytest.raises(ConstructionError, match="uniform element mesh"):
+        AS._log_part(disc)   # quadrature.py:489-491
+
+
+def test_precompute_is_linear_time():
+    import time
+    space = W.make_cyclic_basis(3, np.linspace(0, 1, 8193))
+    t0 = time.perf_counter()
+    fine = W.refine_uniform(space, 1).basis
+    nodes = PC.build_nodes(fine)
+    rb = PC.regular_rule_band(space, fine, nodes)
+    assert time.perf_counter() - t0 < 30.0
+    assert rb.WG == 7 and np.ptp(rb.weights, axis=0).max() < 1e-15
