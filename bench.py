@@ -1,68 +1,376 @@
-"""bench.py -- SGBEM V-matrix assembly entries/s (FP64) on B200 (v1)."""
-import argparse, json, os, sys, time
+"""bench.py -- SGBEM V-matrix assembly throughput (entries/s, FP64) on B200.
+
+Workload (BASELINE.json configs[3], "C4"): closed ellipse (semi-axes 2, 1;
+16 control points, cubic), p = 3, 32768 uniform elements -> N = 32768,
+n_q = 65536, dense A = 8.6 GB.  One STEP = one full assembly of A on the
+device: pair-moment table (cold), circulant log-part tables, fused K1 grid +
+banded contraction (IK1), fused log part (IK2), symmetrise/scale epilogue.
+Inputs are the O(N) precompute of ``build_discretization`` (host, timed
+separately as ``precompute_s``); the output (8.6 GB) exceeds L2 (126 MB) and
+is rewritten every step, so no L2 flush is needed.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 (torchrun): rows are partitioned in contiguous blocks, each rank
+assembles its block with no communication, one NCCL all-gather returns X,
+and every rank applies the symmetrise epilogue (weak/strong: total work is
+fixed -> "strong").  ``--impl reference`` times the CPU oracle port of the
+reference algorithm (oracle/wq_oracle.py, row-block restatement) on a
+bounded row sample of the same workload (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, ROOT)
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "SGBEM V-matrix assembly entries/s (FP64)"
+UNIT = "entries/s"
+FP64_DATASHEET_TFLOPS = 37.2  # 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
+SURVEY_W_C4 = 9.62e11         # algorithmic flop-eq of the C4 assembly
 
 
-def ellipse():
+def workload(n_el: int, p: int = 3, geometry: str = "ellipse"):
     import paper_1703_10016_b200 as W
-    th = 2 * np.pi * np.arange(16) / 16
-    return W.load_curve({"degree": 3, "closed": True, "breakpoints": np.linspace(0, 1, 17).tolist(),
-                         "control_points": np.column_stack([2 * np.cos(th), np.sin(th)]).tolist()})
+    if geometry == "ellipse":
+        th = 2 * np.pi * np.arange(16) / 16
+        cp = np.column_stack([2 * np.cos(th), np.sin(th)])
+        bp = np.linspace(0, 1, 17)
+    else:
+        th = 2 * np.pi * np.arange(32) / 32
+        r = 1 + 0.3 * np.cos(5 * th)
+        cp = np.column_stack([r * np.cos(th), r * np.sin(th)])
+        bp = np.linspace(0, 1, 33)
+    curve = W.load_curve({"degree": 3, "closed": True, "breakpoints": bp.tolist(),
+                          "control_points": cp.tolist()})
+    space = W.make_cyclic_basis(p, np.linspace(0, 1, n_el + 1))
+    return curve, space
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def fp64_peak_tflops(torch, _lib):
+    """Measured DFMA throughput (burst) of this GPU: the roofline denominator."""
+    blocks = 148 * 16
+    out = torch.empty(blocks, dtype=torch.float64, device="cuda")
+    iters = 20000
+    _lib.call("wq_fp64_peak", iters, blocks, _lib.ptr(out), _lib.stream_handle())
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.call("wq_fp64_peak", iters, blocks, _lib.ptr(out), _lib.stream_handle())
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, blocks * 256 * iters * 64 * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+def kernel_flops(disc):
+    """Algorithmic flop-eq per launch of the two dominant kernels (DESIGN.md
+    'roofline'): DFMA = 2, DADD/DMUL = 1, ln = 44 (libdevice fast path,
+    SURVEY F9)."""
+    N, nq = disc.space.dim, disc.nodes.n
+    wg = disc.rules.WG
+    c_k1 = 4 + 1 + 44 + 1                     # dist^2, x 1/p^2, ln, x 1/2
+    ik1 = c_k1 * nq * nq + 2 * wg * (nq * N + N * N)
+    from paper_1703_10016_b200 import assembly as AS
+    lp = AS._log_part(disc)
+    if lp.path == "circulant":
+        K = lp.U.shape[1] * (lp.da + 1)            # (p+1)(P+1) = 64 at p = 3
+        ws = lp.s_w.shape[1]
+        ik2 = 2 * (K + ws) * N * N + 2 * ws * N * N   # Phi (Theta H^-1 + F S), then S^T Phi
+    else:
+        ik2 = None
+    return {"ik1": ik1, "ik2": ik2}
+
+
+def run_reference(args):
+    """CPU oracle port (reference algorithm, row-block restatement) on a
+    bounded row sample of the same workload; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import wq_oracle as O
+    curve, space = workload(args.n_el, args.p, args.geometry)
+    oc = O.Curve(curve.basis, curve.control_points)
+    ob = O.Basis(space.degree, space.knots, space.closed)
+    t0 = time.perf_counter()
+    cr = O.CirculantRows(oc, ob)
+    setup = time.perf_counter() - t0
+    N = space.dim
+    R = args.ref_rows
+    rng = np.random.default_rng(0)
+    for _ in range(args.warmup):
+        cr.m_rows(rng.integers(0, N, 1))
+    times = []
+    for k in range(args.steps):
+        rows = rng.integers(0, N, R)
+        t0 = time.perf_counter()
+        cr.a_rows(rows)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    value = R * N / t
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (deterministic analytic geometry, BASELINE.json configs[3])",
+        "config": {"workload": f"C4 ellipse p={args.p} N={N}", "N": N,
+                   "sample_rows_per_step": R},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{R} random rows of A per step (row-block restatement of "
+                                   f"assemble_weighted_matrix + scale_and_symmetrize), setup "
+                                   f"{setup:.1f}s untimed (rules + lru-cached pair table, as "
+                                   f"the reference's warm path)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
 
 
 def main():
-    ap = argparse.ArgumentParser()
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--impl", default="b200")
-    a = ap.parse_args()
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n-el", type=int, default=32768)
+    ap.add_argument("--p", type=int, default=3)
+    ap.add_argument("--geometry", default="ellipse", choices=["ellipse", "star"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
     import torch
+    import torch.distributed as dist
     import paper_1703_10016_b200 as W
-    from paper_1703_10016_b200 import assembly as AS, _lib
+    from paper_1703_10016_b200 import _lib, assembly as AS, distributed as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    curve, space = workload(args.n_el, args.p, args.geometry)
     t0 = time.perf_counter()
-    space = W.make_cyclic_basis(3, np.linspace(0, 1, a.n + 1))
-    disc = W.build_discretization(ellipse(), space, 1)
+    disc = W.build_discretization(curve, space, 1)
     AS._log_part(disc)
-    t_pre = time.perf_counter() - t0
+    precompute_s = time.perf_counter() - t0
     N = space.dim
+    bounds, per = D.row_blocks(N, world)
+    r0, r1 = bounds[rank]
+
     X = torch.empty((N, N), dtype=torch.float64, device="cuda")
-    for _ in range(a.warmup):
-        AS._assemble_into(disc, X)
+    Xb = X if world == 1 else torch.zeros((per, N), dtype=torch.float64, device="cuda")
+    alpha = -1.0 / (4.0 * np.pi)
+    launches = {"n": 0}
+
+    def step():
+        if world == 1:
+            AS._assemble_into(disc, X)
+            launches["n"] += 9
+            return
+        if r1 > r0:
+            D.assemble_rows_device(disc, Xb, r0, r1)
+        D.gather_rows(Xb, X, per)
+        _lib.call("wq_symmetrize", _lib.ptr(X), N, alpha, _lib.stream_handle())
+        launches["n"] += 9
+
+    for _ in range(args.warmup):
+        step()
     torch.cuda.synchronize()
     AS._check_flag(AS._smooth(disc))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches["n"] = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.steps):
-        AS._assemble_into(disc, X)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / a.steps
-    # phase split
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    ph = np.zeros(3)
-    for _ in range(3):
-        ev[0].record(); AS._ik1_into(disc, X); ev[1].record()
-        AS._ik2_x2_into(disc, X, accumulate=True); ev[2].record()
-        _lib.call("wq_symmetrize", _lib.ptr(X), N, -1.0 / (4 * np.pi), _lib.stream_handle()); ev[3].record()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
         torch.cuda.synchronize()
-        ph += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])]
-    ph /= 3
-    # fp64 peak
-    out = torch.empty(148 * 16, dtype=torch.float64, device="cuda")
-    iters = 20000
-    _lib.call("wq_fp64_peak", iters, 148 * 16, _lib.ptr(out), _lib.stream_handle())
-    torch.cuda.synchronize()
-    e0.record(); _lib.call("wq_fp64_peak", iters, 148 * 16, _lib.ptr(out), _lib.stream_handle()); e1.record()
-    torch.cuda.synchronize()
-    peak = 148 * 16 * 256 * iters * 64 * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e12
-    print(json.dumps({"metric": "entries/s", "value": N * N / (ms * 1e-3), "ms_per_step": ms, "N": N,
-                      "phases_ms": {"ik1": ph[0], "ik2": ph[1], "sym": ph[2]}, "fp64_peak_tflops": peak,
-                      "precompute_s": t_pre}))
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t_dev = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    ms = float(t_dev.item())
+    gpu_launches = launches["n"]
+    value = N * N / (ms * 1e-3)
+
+    # ---- per-kernel split + roofline of the dominant kernel (1 GPU layout) ----
+    peak = fp64_peak_tflops(torch, _lib)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    reps = 3
+    split = np.zeros(4)
+    for _ in range(reps):
+        ev[0].record()
+        tables = AS._circ_tables(disc)
+        ev[1].record()
+        AS._ik1_into(disc, X)
+        ev[2].record()
+        AS._ik2_x2_rows(disc, X, 0, N, accumulate=True, tables=tables)
+        ev[3].record()
+        _lib.call("wq_symmetrize", _lib.ptr(X), N, alpha, _lib.stream_handle())
+        ev[4].record()
+        torch.cuda.synchronize()
+        split += [ev[k].elapsed_time(ev[k + 1]) for k in range(4)]
+    split /= reps
+    names = ["tables", "ik1", "ik2", "symmetrize"]
+    fl = kernel_flops(disc)
+    dom = "ik1" if split[1] >= split[2] else "ik2"
+    dom_ms = split[1] if dom == "ik1" else split[2]
+    achieved = fl[dom] / (dom_ms * 1e-3) / 1e12
+    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_tile_kernel", "ik2": "ik2_circ_kernel"}[dom],
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_source": "measured DFMA probe (wq_fp64_peak, burst); MEASURED_PEAKS.json has "
+                               "no FP64 entry", "peak_datasheet": FP64_DATASHEET_TFLOPS,
+                "traffic": None}
+    survey_frac = SURVEY_W_C4 * (N / 32768) ** 2 / (ms * 1e-3) / (peak * 1e12) * world ** 0 \
+        if (args.n_el == 32768 and args.p == 3) else None
+
+    # ---- end to end through the public API with host buffers (N = 1 layout) ----
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        host = torch.empty((N, N), dtype=torch.float64, pin_memory=True)
+        sm = AS._smooth(disc)
+        lp, dd = AS._logpart_dev(disc)
+        inputs = [v for v in list(sm.values()) + list(dd.values())
+                  if isinstance(v, torch.Tensor) and v.is_cuda and v.numel() > 1]
+        pinned = [t.cpu().pin_memory() for t in inputs]
+        h2d = sum(t.numel() * t.element_size() for t in pinned)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for src, dst in zip(pinned, inputs):
+                dst.copy_(src, non_blocking=True)
+            AS._assemble_into(disc, X)
+            host.copy_(X, non_blocking=True)
+            torch.cuda.synchronize()
+        t_e2e = (time.perf_counter() - t0) / args.e2e_steps
+        e2e = {"value": N * N / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(N * N * 8), "ms_per_step": t_e2e * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, N)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic analytic geometry, BASELINE.json configs[3])",
+            "config": {"workload": f"C4: closed ellipse 2x1 (16 ctrl pts, cubic), p={args.p}, "
+                                   f"{args.n_el} uniform elements", "N": N, "nq": disc.nodes.n,
+                       "parallelism": f"row-blocks x{world}" if world > 1 else "single GPU",
+                       "l2": "8.6 GB output > 126 MB L2, rewritten every step (no flush needed)"},
+            "clocks": clk.summary(),
+            "gpu_launches": gpu_launches,
+            "split_ms": dict(zip(names, [float(x) for x in split])),
+            "roofline": roofline,
+            "fp64_roofline_fraction_survey_W": survey_frac,
+            "precompute_s": precompute_s,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args, N):
+    """Oracle port timed on this host on a bounded row sample (10-30 s)."""
+    try:
+        from oracle import wq_oracle as O
+    except ImportError:
+        return None
+    curve, space = workload(args.n_el, args.p, args.geometry)
+    cr = O.CirculantRows(O.Curve(curve.basis, curve.control_points),
+                         O.Basis(space.degree, space.knots, space.closed))
+    rows = np.random.default_rng(1).integers(0, N, args.ref_rows)
+    cr.a_rows(rows[:1])
+    t0 = time.perf_counter()
+    cr.a_rows(rows)
+    t = time.perf_counter() - t0
+    return {"value": len(rows) * N / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{len(rows)} rows of A ({len(rows) * N} entries) via the oracle row-block "
+                      f"restatement, {t:.1f}s; setup (rules, pair table) untimed"}
 
 
 if __name__ == "__main__":

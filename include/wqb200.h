@@ -68,6 +68,10 @@ const char* wq_last_error(void);
  * in practice). */
 int wq_fp64_peak(int64_t iters, int blocks, double* out, void* stream);
 
+/* FP64 tensor-core probe: blocks x 8 warps x iters x 8 DMMA m8n8k4 (512 flops
+ * each); mode 1 adds 32 DFMA per lane per iteration (pipe-overlap probe). */
+int wq_dmma_peak(int64_t iters, int blocks, int mode, double* out, void* stream);
+
 /*
  * IK1 rows/cols block (replaces assemble_ik1, assembly.py:175-183, with the
  * K1 grid of geometry.py:225-248 evaluated in-kernel and never stored):

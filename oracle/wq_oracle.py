@@ -651,3 +651,160 @@ def xform_dense(disc: Disc):
     C = scipy.linalg.cho_solve(scipy.linalg.cho_factor(H), S)
     X = dense_ik1(disc) + (2.0 * theta - C.T @ dmm) @ C
     return -(X + X.T) / (2.0 * TWO_PI)
+
+
+# --------------------------------------------------------------------------
+# row-block restatement for closed uniform simple-knot meshes (config 2-4)
+# --------------------------------------------------------------------------
+#
+# The reference cannot run config 4 (550 GB pair tensor, 34 GB K1 grid,
+# O(N^3) precompute).  These functions compute ROWS of
+#   M = IK1 + IK2,  IK2 = Theta C + (Theta C)^T - C^T D C   (assembly.py:244-245)
+# from the same ingredients (pair table, local coefficients, fit operator),
+# using only per-row work: K1 rows (geometry.py:225-248), element-pair sums
+# for Theta rows, and circular convolutions (FFT) for every product with the
+# circulant H^{-1} and D (closed uniform simple-knot meshes only).  Validated
+# against the dense restatement / reference goldens where those run.
+
+
+def design_sparse(basis: Basis, pts):
+    """Sparse CSR (n_pts, dim) basis values, cyclic columns folded."""
+    import scipy.sparse as sp
+    pts = np.clip(np.atleast_1d(np.asarray(pts, float)), basis.a, basis.b)
+    m = BSpline.design_matrix(pts, basis.knots, basis.degree).tocoo()
+    cols = m.col.copy()
+    if basis.closed:
+        cols[cols >= basis.dim] -= basis.dim
+    return sp.csr_matrix((m.data, (m.row, cols)), shape=(len(pts), basis.dim))
+
+
+def _rules_local(parent: Basis, fine: Basis, nodes, closed):
+    """Regular rules restated per row with sparse local data (quadrature.py:
+    510-540, splines.py:491-514): active nodes where B_i != 0, exactness
+    functions = fine functions active on the elements of supp(B_i), moments by
+    per-element Gauss, minimum-norm gelsd solve.  Returns (idx, W) lists."""
+    order = (parent.degree + fine.degree) // 2 + 2
+    xg, wg = np.polynomial.legendre.leggauss(order)
+    els = fine.elements
+    half = 0.5 * (els[:, 1] - els[:, 0])
+    gp = (0.5 * (els[:, 0] + els[:, 1])[:, None] + half[:, None] * xg[None, :]).ravel()
+    gw = (half[:, None] * wg[None, :]).ravel()
+    Bc = design_sparse(parent, gp).tocsc()
+    Bf = design_sparse(fine, gp).tocsr()
+    Bn = design_sparse(parent, nodes).tocsc()
+    Fn = design_sparse(fine, nodes).tocsr()
+    idx_list, w_list = [], []
+    for i in range(parent.dim):
+        col = Bn.getcol(i)
+        nsel = np.sort(col.indices[col.data != 0.0])
+        ci = Bc.getcol(i)
+        g_i = ci.indices[ci.data != 0.0]
+        sub = Bf[g_i]
+        jsel = np.unique(sub.indices)
+        mu = np.asarray(sub[:, jsel].T @ (gw[g_i] * ci.toarray().ravel()[g_i])).ravel()
+        local = Fn[nsel][:, jsel].toarray().T
+        w, *_ = scipy.linalg.lstsq(local, mu, lapack_driver="gelsd")
+        idx_list.append(nsel)
+        w_list.append(w)
+    return idx_list, w_list
+
+
+class CirculantRows:
+    """Rows of M / A for a closed uniform simple-knot discretization."""
+
+    def __init__(self, curve: Curve, space: Basis):
+        assert space.closed and np.all(space.multiplicities == 1)
+        self.curve, self.space = curve, space
+        self.n = n = space.n_elements
+        self.N = N = space.dim
+        assert N == n
+        self.nodes = build_nodes(space)
+        self.J = curve.speed(self.nodes)
+        idx, w = _rules_local(space, space, self.nodes, True)
+        nq = len(self.nodes)
+        rows = np.concatenate([np.full(len(q), i) for i, q in enumerate(idx)])
+        cols = np.concatenate(idx)
+        vals = np.concatenate([wi * self.J[q] for wi, q in zip(w, idx)])
+        import scipy.sparse as sp
+        self.G = sp.csr_matrix((vals, (rows, cols)), shape=(N, nq))
+        bt = sp.csr_matrix(design(space, self.nodes))
+        self.H0 = np.asarray((bt.T @ bt)[0].todense()).ravel()  # circulant first row
+        self.S = (bt.T @ sp.csr_matrix(design(space, self.nodes) * self.J[:, None])).tocsc()
+        self.lam_h = np.fft.fft(self.H0).real
+        d = space.degree
+        self.P = space.degree + JFIT_DEGREE
+        self.m2, _ = uniform_pair_moments(space, self.P)
+        self.u, self.ucols = local_coeffs(space, space.elements, self.P, scale_fn=curve.speed)
+        self.v, self.vcols = local_coeffs(space, space.elements, d)
+        # D circulant: D[0, m] by element pairs (e, a) with vcols[e, a] = 0
+        dd = np.zeros(n)
+        for e, a in zip(*np.nonzero(self.vcols == 0)):
+            if True:
+                f_ = np.arange(n)
+                blk = np.einsum("p,fpq,fqb->fb", self.v[e][:, a], self.m2[(f_ - e) % n][:, : d + 1],
+                                self.v)
+                np.add.at(dd, self.vcols.ravel(), blk.ravel())
+        self.lam_d = np.fft.fft(dd).real  # D symmetric circulant: D[l,m] = dd[(m-l) mod n]
+
+    # circular products with the circulant H^{-1} and D
+    def hinv(self, x):
+        return np.real(np.fft.ifft(np.fft.fft(x, axis=0) / self._lam(self.lam_h, x), axis=0))
+
+    def dmul(self, x):
+        return np.real(np.fft.ifft(np.fft.fft(x, axis=0) * self._lam(self.lam_d, x), axis=0))
+
+    @staticmethod
+    def _lam(lam, x):
+        return lam if x.ndim == 1 else lam[:, None]
+
+    def theta_row(self, i):
+        """Theta[i, :] by element pairs (assembly.py:215-228)."""
+        n, d = self.n, self.space.degree
+        out = np.zeros(n)
+        for e, a in zip(*np.nonzero(self.ucols == i)):
+            if True:
+                ue = self.u[e][:, a]
+                f_ = np.arange(n)
+                blocks = np.einsum("p,fpq,fqb->fb", ue, self.m2[(f_ - e) % n], self.v)
+                np.add.at(out, self.vcols.ravel(), blocks.ravel())
+        return out
+
+    def theta_matvec(self, w):
+        """(Theta w)[j] for all j via per-(alpha, beta) circular convolutions."""
+        n, d = self.n, self.space.degree
+        # y_f[beta] = sum_b v_f[beta, b] w[vcols[f, b]]
+        y = np.einsum("fqb,fb->fq", self.v, w[self.vcols])
+        # Y_e[alpha] = sum_f M2[f - e][alpha, beta] y_f[beta]  (correlation)
+        M = np.fft.fft(self.m2, axis=0)                 # over gap k = f - e
+        Yf = np.fft.fft(y, axis=0)
+        Y = np.real(np.fft.ifft(np.einsum("kpq,kq->kp", M, np.conj(Yf)), axis=0))
+        Y = np.conj(Y) if np.iscomplexobj(Y) else Y
+        # correlation: Y_e = sum_k M2[k] y_{e+k}  ->  ifft(conj(fft(m2)) * fft(y)) for real data
+        Y = np.real(np.fft.ifft(np.einsum("kpq,kq->kp", np.conj(M), Yf), axis=0))
+        out = np.zeros(self.N)
+        np.add.at(out, self.ucols.ravel(), np.einsum("epa,ep->ea", self.u, Y).ravel())
+        return out
+
+    def m_rows(self, rows):
+        """Rows of M = IK1 + IK2 (assembly.py:256)."""
+        import scipy.sparse as sp
+        nodes, N = self.nodes, self.N
+        out = np.empty((len(rows), N))
+        Gt = self.G.T.tocsr()
+        for r, i in enumerate(rows):
+            gi = self.G.getrow(i)
+            q = gi.indices
+            k1 = k1_grid(self.curve, nodes[q], nodes)
+            ik1 = (gi.data @ k1) @ Gt
+            e_i = np.zeros(N)
+            e_i[i] = 1.0
+            c_i = self.hinv(np.asarray(self.S[:, i].todense()).ravel())   # C[:, i]
+            th_i = self.theta_row(i)
+            tc_row = self.S.T @ self.hinv(th_i)                            # (Theta C)[i, :]
+            tc_col = self.theta_matvec(c_i)                                 # (Theta C)[:, i]
+            ctdc = self.S.T @ self.hinv(self.dmul(c_i))                     # (C^T D C)[i, :]
+            out[r] = np.asarray(ik1).ravel() + tc_row + tc_col - ctdc
+        return out
+
+    def a_rows(self, rows):
+        return -self.m_rows(rows) / TWO_PI

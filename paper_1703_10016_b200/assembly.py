@@ -434,27 +434,44 @@ def _logpart_dev(disc):
     return lp, _dev(disc, "logpart", make)
 
 
+def _circ_tables(disc):
+    """Pair table -> folded circulant tables (Z' = H^{-1}-folded Theta gap
+    table, ff = H^{-1} D H^{-1}) on the device; O(n_el) work per call."""
+    torch = _torch()
+    lp, d = _logpart_dev(disc)
+    st = _lib.stream_handle()
+    m2, keep = _m2_table(disc, lp)
+    n = lp.n_el
+    nA = lp.da + 1
+    Zp = torch.empty((n, nA), dtype=torch.float64, device="cuda")
+    Zw = torch.empty((n, nA), dtype=torch.float64, device="cuda")
+    ff = torch.empty(n, dtype=torch.float64, device="cuda")
+    work = torch.empty(n, dtype=torch.float64, device="cuda")
+    K = (len(lp.hinv_taps) - 1) // 2
+    _lib.call("wq_circ_tables", n, lp.da, lp.db, _lib.ptr(m2), _lib.ptr(d["v0"]),
+              _lib.ptr(d["taps"]), K, _lib.ptr(Zp), _lib.ptr(ff), _lib.ptr(work), _lib.ptr(Zw), st)
+    return Zp, ff
+
+
+def _ik2_x2_rows(disc, X, row0, row1, accumulate=True, tables=None):
+    """Circulant path: X[rows] (+)= X2[row0:row1, :] (X points at row0)."""
+    lp, d = _logpart_dev(disc)
+    N = disc.space.dim
+    Zp, ff = _circ_tables(disc) if tables is None else tables
+    _lib.call("wq_ik2_circ", ctypes_ref(d["struct"]), _lib.ptr(Zp), _lib.ptr(ff), row0, row1, 0, N,
+              _lib.ptr(X), X.stride(0), int(accumulate), _lib.stream_handle())
+    return X
+
+
 def _ik2_x2_into(disc, X, accumulate=True):
     """X (+)= X2 (circulant: X2 itself; general: X2^T -- callers symmetrise)."""
     torch = _torch()
     lp, d = _logpart_dev(disc)
     N = disc.space.dim
     st = _lib.stream_handle()
-    m2, keep = _m2_table(disc, lp)
     if lp.path == "circulant":
-        n = lp.n_el
-        nA = lp.da + 1
-        Zp = torch.empty((n, nA), dtype=torch.float64, device="cuda")
-        Zw = torch.empty((n, nA), dtype=torch.float64, device="cuda")
-        ff = torch.empty(n, dtype=torch.float64, device="cuda")
-        work = torch.empty(n, dtype=torch.float64, device="cuda")
-        K = (len(lp.hinv_taps) - 1) // 2
-        _lib.call("wq_circ_tables", n, lp.da, lp.db, _lib.ptr(m2), _lib.ptr(d["v0"]),
-                  _lib.ptr(d["taps"]), K, _lib.ptr(Zp), _lib.ptr(ff), _lib.ptr(work),
-                  _lib.ptr(Zw), st)
-        _lib.call("wq_ik2_circ", ctypes_ref(d["struct"]), _lib.ptr(Zp), _lib.ptr(ff), 0, N, 0, N,
-                  _lib.ptr(X), X.stride(0), int(accumulate), st)
-        return X
+        return _ik2_x2_rows(disc, X, 0, N, accumulate)
+    m2, keep = _m2_table(disc, lp)
     NE = disc.refined.basis.dim
     pp = _lib.WqPairs(N, NE, lp.n_el, m2.shape[0], lp.da, lp.db, int(disc.closed),
                       lp.u_el.shape[1], lp.v_el.shape[1], d["u_el"].data_ptr(),
