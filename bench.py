@@ -240,7 +240,7 @@ def main():
     def step():
         if world == 1:
             AS._assemble_into(disc, X)
-            launches["n"] += 9
+            launches["n"] += 9 if AS._use_v2(disc) else 9
             return
         if r1 > r0:
             D.assemble_rows_device(disc, Xb, r0, r1)
@@ -277,26 +277,29 @@ def main():
     peak = fp64_peak_tflops(torch, _lib)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     reps = 3
-    split = np.zeros(4)
+    split = np.zeros(3)
+    sm = AS._smooth(disc)
+    lp, dd = AS._logpart_dev(disc)
     for _ in range(reps):
         ev[0].record()
-        tables = AS._circ_tables(disc)
+        zext = AS._zext_table(disc)
         ev[1].record()
-        AS._ik1_into(disc, X)
+        _lib.call("wq_ik1_sym", AS.ctypes_ref(sm["struct"]), _lib.ptr(X), N, sm["span64"],
+                  _lib.ptr(sm["flag"]), _lib.stream_handle())
         ev[2].record()
-        AS._ik2_x2_rows(disc, X, 0, N, accumulate=True, tables=tables)
+        _lib.call("wq_x2_pairs", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
+                  lp.uext.shape[1], lp.zstride, _lib.ptr(dd["uext"]), _lib.ptr(zext),
+                  _lib.ptr(dd["s_w"]), alpha, 2.0, _lib.ptr(X), N, _lib.stream_handle())
         ev[3].record()
-        _lib.call("wq_symmetrize", _lib.ptr(X), N, alpha, _lib.stream_handle())
-        ev[4].record()
         torch.cuda.synchronize()
-        split += [ev[k].elapsed_time(ev[k + 1]) for k in range(4)]
+        split += [ev[k].elapsed_time(ev[k + 1]) for k in range(3)]
     split /= reps
-    names = ["tables", "ik1", "ik2", "symmetrize"]
+    names = ["tables", "ik1_sym", "x2_pairs"]
     fl = kernel_flops(disc)
     dom = "ik1" if split[1] >= split[2] else "ik2"
     dom_ms = split[1] if dom == "ik1" else split[2]
     achieved = fl[dom] / (dom_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_tile_kernel", "ik2": "ik2_circ_kernel"}[dom],
+    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2_pairs_kernel"}[dom],
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": "measured DFMA probe (wq_fp64_peak, burst); MEASURED_PEAKS.json has "
                                "no FP64 entry", "peak_datasheet": FP64_DATASHEET_TFLOPS,

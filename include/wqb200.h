@@ -168,6 +168,35 @@ int wq_gather_fs(const wq_logpart_t* lp, double alpha, const double* F, double* 
 int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64_t row1,
                   double* X, int64_t ldx, int accumulate, void* stream);
 
+/*
+ * v2 circulant pipeline (closed uniform simple-knot meshes, nref = 1), tiles of
+ * WQ_FTILE rows over the upper-triangle tile pairs (I <= J):
+ *
+ * wq_ik1_sym: X[I-tile, J-tile] = IK1(I,J) for I <= J only (IK1 is symmetric).
+ *   max_span: max node span of WQ_FTILE consecutive rules.
+ * wq_zext:   Zext[g] = [Z'[g][0..nA-1], 0 .., ff[g] at column nApad, 0 ..]
+ *   (row stride zstride).
+ * wq_x2_pairs: log part on the FP64 tensor cores + fused epilogue, in place:
+ *   A(I,J) = alpha (w_ik1 IK1(I,J) + X2(I,J) + X2(J,I)^T), A(J,I) = A(I,J)^T,
+ *   reading IK1(I,J) from X (written by wq_ik1_sym), where
+ *   X2[i,j] = sum_t S[j-d+t, j] Phi[j-d+t, i],
+ *   Phi[m,i] = sum_K Uext[i][K] Zrow(m-i, K),  Uext[i] = [2U[i][a][al] (a*nApad+al),
+ *   -S[i-d+t, i] (tu*nApad + t), 0 ..] (ktot columns).
+ *   alpha = -1/(4 pi), w_ik1 = 2 gives A; alpha = 1/2 gives M = (X + X^T)/2.
+ */
+#define WQ_FTILE 64
+int wq_ik1_sym(const wq_smooth_t* sm, double* X, int64_t ldx, int64_t max_span, int* flag,
+               void* stream);
+int wq_zext(int64_t n, int nA, int nApad, int zstride, const double* Zp, const double* ff,
+            double* Zext, void* stream);
+int wq_x2_pairs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+                const double* Uext, const double* Zext, const double* s_w, double alpha,
+                double w_ik1, double* X, int64_t ldx, void* stream);
+
+/* Self-test hooks (unit tests): fast 0.5*ln vs libdevice; one DMMA 8x8x4. */
+int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream);
+int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream);
+
 /* Epilogue (assembly.py:262-271): A = alpha * (X + X^T), in place, n x n. */
 int wq_symmetrize(double* X, int64_t n, double alpha, void* stream);
 

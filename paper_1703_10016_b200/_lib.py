@@ -23,6 +23,7 @@ c_vp = ctypes.c_void_p
 
 WQ_FLAG_R_NONPOSITIVE = 1
 WQ_TILE = 32
+WQ_FTILE = 64
 WQ_K1_TABLE, WQ_K1_OPEN, WQ_K1_CLOSED = 0, 1, 2
 
 
@@ -67,6 +68,12 @@ _SIGS = {
     "wq_symmetrize": [c_vp, c_i64, c_dbl, c_vp],
     "wq_absmax_defect": [c_vp, c_i64, c_vp, c_vp],
     "wq_b1w": [ctypes.POINTER(WqSmooth), c_vp, c_vp, c_vp],
+    "wq_ik1_sym": [ctypes.POINTER(WqSmooth), c_vp, c_i64, c_i64, c_vp, c_vp],
+    "wq_zext": [c_i64, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp],
+    "wq_x2_pairs": [c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_dbl,
+                    c_dbl, c_vp, c_i64, c_vp],
+    "wq_selftest_log": [c_i64, c_vp, c_vp, c_vp, c_vp],
+    "wq_selftest_dmma": [c_vp, c_vp, c_vp, c_vp],
 }
 
 EXPORTED = tuple(_SIGS)

@@ -107,6 +107,9 @@ class LogPart:
     U: np.ndarray = None           # (N, tu, da+1)
     v0: np.ndarray = None          # (db+1, db+1)
     hinv_taps: np.ndarray = None   # (2K+1,)
+    uext: np.ndarray = None        # (N, ktot) [2U | -S_i | 0] for the DMMA kernel
+    nApad: int = 0
+    zstride: int = 0
     # general
     u: np.ndarray = None
     v: np.ndarray = None
@@ -265,6 +268,18 @@ def _log_part(disc: Discretization) -> LogPart:
                 taps[-1] *= 0.5
         else:
             taps = np.concatenate([hinv[-K:] if K else np.empty(0), hinv[: K + 1]])
+        nA = da + 1
+        nApad = -(-nA // 4) * 4
+        ws = s_w.shape[1]
+        wspad = -(-ws // 4) * 4
+        ktot = tu * nApad + wspad
+        uext = np.zeros((N, ktot))
+        for a in range(tu):
+            uext[:, a * nApad: a * nApad + nA] = 2.0 * U[:, a, :]
+        uext[:, tu * nApad: tu * nApad + ws] = -s_w
+        zs = nApad + 1
+        zs += (4 - zs % 16) % 16
+        lp.uext, lp.nApad, lp.zstride = np.ascontiguousarray(uext), nApad, zs
         lp.path = "circulant"
         lp.e_start = e_start.astype(np.int64)
         lp.U = np.ascontiguousarray(U)
@@ -360,6 +375,9 @@ def _smooth(disc: Discretization):
         span = int((rb.start[last_idx] + rb.WG - first).max())
         d["struct"] = st
         d["span"] = span
+        T = _lib.WQ_FTILE
+        last_idx = np.minimum(np.arange(0, N, T) + T, N) - 1
+        d["span64"] = int((rb.start[last_idx] + rb.WG - rb.start[0::T]).max())
         return d
 
     return _dev(disc, "smooth", make)
@@ -419,6 +437,7 @@ def _logpart_dev(disc):
             d["U"] = _to_dev(torch, lp.U)
             d["v0"] = _to_dev(torch, lp.v0)
             d["taps"] = _to_dev(torch, lp.hinv_taps)
+            d["uext"] = _to_dev(torch, lp.uext)
             tu = lp.U.shape[1]
             d["struct"] = _lib.WqLogpart(N, lp.n_el, lp.da, tu, lp.s_w.shape[1],
                                          d["e_start"].data_ptr(), d["U"].data_ptr(),
@@ -501,11 +520,47 @@ def _new_square(disc):
     return torch.empty((N, N), dtype=torch.float64, device="cuda")
 
 
+def _zext_table(disc):
+    """Z' and ff packed into the row layout the DMMA kernel streams."""
+    torch = _torch()
+    lp, d = _logpart_dev(disc)
+    Zp, ff = _circ_tables(disc)
+    n = lp.n_el
+    Zext = torch.empty((n, lp.zstride), dtype=torch.float64, device="cuda")
+    _lib.call("wq_zext", n, lp.da + 1, lp.nApad, lp.zstride, _lib.ptr(Zp), _lib.ptr(ff),
+              _lib.ptr(Zext), _lib.stream_handle())
+    return Zext
+
+
+def _assemble_v2(disc: Discretization, X, alpha: float, w_ik1: float = 2.0, zext=None):
+    """Circulant v2 pipeline: tables -> ik1_sym (upper tiles) -> x2_pairs
+    (DMMA log part + fused symmetric epilogue), in place in X."""
+    lp, d = _logpart_dev(disc)
+    sm = _smooth(disc)
+    st = _lib.stream_handle()
+    Zext = _zext_table(disc) if zext is None else zext
+    N = disc.space.dim
+    if w_ik1 != 0.0:
+        _lib.call("wq_ik1_sym", ctypes_ref(sm["struct"]), _lib.ptr(X), X.stride(0), sm["span64"],
+                  _lib.ptr(sm["flag"]), st)
+    _lib.call("wq_x2_pairs", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
+              lp.uext.shape[1], lp.zstride, _lib.ptr(d["uext"]), _lib.ptr(Zext), _lib.ptr(d["s_w"]),
+              alpha, w_ik1, _lib.ptr(X), X.stride(0), st)
+    return X
+
+
+def _use_v2(disc) -> bool:
+    lp = _log_part(disc)
+    return lp.path == "circulant" and disc.space.degree <= 5
+
+
 def _assemble_into(disc: Discretization, X, scaled: bool = True):
     """Enqueue the whole assembly on the current stream (no host sync)."""
+    alpha = -1.0 / (2.0 * TWO_PI) if scaled else 0.5
+    if _use_v2(disc):
+        return _assemble_v2(disc, X, alpha)
     _ik1_into(disc, X, accumulate=False)
     _ik2_x2_into(disc, X, accumulate=True)
-    alpha = -1.0 / (2.0 * TWO_PI) if scaled else 0.5
     _lib.call("wq_symmetrize", _lib.ptr(X), X.shape[0], alpha, _lib.stream_handle())
     return X
 
@@ -532,6 +587,9 @@ def assemble_ik2(disc: Discretization) -> np.ndarray:
     """Log-part matrix Theta C + (Theta C)^T - C^T D C (assembly.py:186-245),
     as (X2 + X2^T)/2 of the X-form."""
     X = _new_square(disc)
+    if _use_v2(disc):
+        _assemble_v2(disc, X, 0.5, w_ik1=0.0)
+        return X.cpu().numpy()
     _ik2_x2_into(disc, X, accumulate=False)
     _lib.call("wq_symmetrize", _lib.ptr(X), X.shape[0], 0.5, _lib.stream_handle())
     return X.cpu().numpy()
