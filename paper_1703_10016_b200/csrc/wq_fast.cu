@@ -402,10 +402,14 @@ x2_pairs_kernel(X2Params P, const double* __restrict__ Uext, const double* __res
 #pragma unroll
     for (int e = 0; e < 2; ++e) Tst[i_l * TSTRIDE + 8 * jb + 2 * c + e] = vals[jb][e];
   __syncthreads();
-  // coalesced writes of A(I,J) and A(J,I) = A(I,J)^T
+  // coalesced writes of A(I,J) and A(J,I) = A(I,J)^T; diagonal tiles are
+  // mirrored from their upper triangle so A is exactly symmetric
   for (int k = tid; k < FT * FT; k += FTHREADS) {
     const int a = k >> 6, b = k & 63;
-    if (a < ni && b < nj) X[(I0 + a) * ldx + J0 + b] = Tst[a * TSTRIDE + b];
+    if (a < ni && b < nj) {
+      const double v = (bi == bj && a > b) ? Tst[b * TSTRIDE + a] : Tst[a * TSTRIDE + b];
+      X[(I0 + a) * ldx + J0 + b] = v;
+    }
   }
   if (bi != bj) {
     for (int k = tid; k < FT * FT; k += FTHREADS) {

@@ -141,8 +141,14 @@ __global__ void circ_corr_kernel(int64_t n, int nc, const double* in, const doub
   if (e >= n * nc) return;
   int64_t g = e / nc;
   int c = (int)(e - g * nc);
+  // start index (g - K) mod n, then step with a conditional wrap (no divisions)
+  int64_t idx = g - K;
+  while (idx < 0) idx += n;
   double acc = 0.0;
-  for (int64_t k = -K; k <= K; ++k) acc = fma(in[pmod(g + k, n) * nc + c], taps[K + k], acc);
+  for (int64_t k = 0; k <= 2 * K; ++k) {
+    acc = fma(in[idx * nc + c], taps[k], acc);
+    if (++idx == n) idx = 0;
+  }
   out[e] = acc;
 }
 

@@ -1,6 +1,6 @@
 """FP64 pipe probes: DFMA, DMMA, DMMA+DFMA (prints TFLOP/s)."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1703_10016_b200 import _lib
 
