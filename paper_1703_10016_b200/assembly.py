@@ -550,8 +550,14 @@ def _assemble_v2(disc: Discretization, X, alpha: float, w_ik1: float = 2.0, zext
 
 
 def _use_v2(disc) -> bool:
+    """The v2/v3 tile kernels need the circulant log part and the closed
+    uniform rule layout (rule i on nodes 2(i-p)+1 .. 2(i-p)+2p+1)."""
     lp = _log_part(disc)
-    return lp.path == "circulant" and disc.space.degree <= 5
+    rb = disc.rules
+    p = disc.space.degree
+    return (lp.path == "circulant" and 2 <= p <= 5 and rb.WG == 2 * p + 1
+            and np.all(rb.width == rb.WG) and np.all(np.diff(rb.start) == 2)
+            and disc.nodes.n == 2 * disc.space.dim)
 
 
 def _assemble_into(disc: Discretization, X, scaled: bool = True):
