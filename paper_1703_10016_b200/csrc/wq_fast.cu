@@ -159,7 +159,7 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, double* X, int64_t ldx, int* flag) {
   __shared__ double qx[NQ], qy[NQ], qJ[NQ], qs[NQ];
   __shared__ double rx[NQ], ry[NQ], rs[NQ];
   __shared__ int qa[NQ], ra[NQ];
-  __shared__ double Gi[FT][8], Gj[FT][8];
+  __shared__ double Gi[FT][WG], Gj[FT][WG];
   extern __shared__ double T1[];  // [FT][NQP]: T1[j][q] = sum_w K1[q][2j + w] G_j[w]
 
   const int64_t N = sm.n_rows, nq = sm.nq;
@@ -188,10 +188,10 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, double* X, int64_t ldx, int* flag) {
       ra[k] = (int)b;
       rx[k] = sm.fx[b]; ry[k] = sm.fy[b]; rs[k] = sm.s[b];
     }
-    for (int k = tid; k < FT * 8; k += IK1_THREADS) {
-      const int ii = k >> 3, w = k & 7;
-      Gi[ii][w] = (ii < ni && w < WG) ? sm.g_w[(I0 + ii) * WG + w] : 0.0;
-      Gj[ii][w] = (ii < nj && w < WG) ? sm.g_w[(J0 + ii) * WG + w] : 0.0;
+    for (int k = tid; k < FT * WG; k += IK1_THREADS) {
+      const int ii = k / WG, w = k - ii * WG;
+      Gi[ii][w] = ii < ni ? sm.g_w[(I0 + ii) * WG + w] : 0.0;
+      Gj[ii][w] = ii < nj ? sm.g_w[(J0 + ii) * WG + w] : 0.0;
     }
     for (int k = tid; k < 3 * LOGTAB; k += IK1_THREADS) tab[k] = g_logtab[k];
   }
