@@ -236,17 +236,19 @@ def main():
     Xb = X if world == 1 else torch.zeros((per, N), dtype=torch.float64, device="cuda")
     alpha = -1.0 / (4.0 * np.pi)
     launches = {"n": 0}
+    # our kernels per step: pair table, 5 circulant-table kernels, zext, ik1, x2 (+ symmetrise N>1)
+    per_step = 9 if world == 1 else (10 if r1 > r0 else 8)
 
     def step():
         if world == 1:
             AS._assemble_into(disc, X)
-            launches["n"] += 9 if AS._use_v2(disc) else 9
-            return
-        if r1 > r0:
-            D.assemble_rows_device(disc, Xb, r0, r1)
-        D.gather_rows(Xb, X, per)
-        _lib.call("wq_symmetrize", _lib.ptr(X), N, alpha, _lib.stream_handle())
-        launches["n"] += 9
+        else:
+            zext = AS._zext_table(disc)
+            if r1 > r0:
+                D.assemble_rows_device(disc, Xb, r0, r1, zext=zext)
+            D.gather_rows(Xb, X, per)
+            _lib.call("wq_symmetrize", _lib.ptr(X), N, alpha, _lib.stream_handle())
+        launches["n"] += per_step
 
     for _ in range(args.warmup):
         step()

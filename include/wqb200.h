@@ -193,6 +193,21 @@ int wq_x2_pairs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstri
                 const double* Uext, const double* Zext, const double* s_w, double alpha,
                 double w_ik1, double* X, int64_t ldx, void* stream);
 
+/*
+ * Row-block variants for multi-GPU sharding: tile rows
+ * [tile_row0, tile_row1) (units of WQ_FTILE rows), all columns, no symmetry
+ * exploitation; Xrows points at global row tile_row0 * WQ_FTILE.
+ *   wq_ik1_rows: Xrows = IK1[rows, :]
+ *   wq_x2_rows:  Xrows = alpha (w_ik1 Xrows + X2[rows, :])   (unsymmetrised X)
+ * After an all-gather of X, wq_symmetrize(X, N, -1/(4 pi)) gives A.
+ */
+int wq_ik1_rows(const wq_smooth_t* sm, int64_t tile_row0, int64_t tile_row1, double* Xrows,
+                int64_t ldx, int* flag, void* stream);
+int wq_x2_rows(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+               const double* Uext, const double* Zext, const double* s_w, double alpha,
+               double w_ik1, int64_t tile_row0, int64_t tile_row1, double* Xrows, int64_t ldx,
+               void* stream);
+
 /* Self-test hooks (unit tests): fast 0.5*ln vs libdevice; one DMMA 8x8x4. */
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream);
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream);

@@ -36,18 +36,15 @@ __global__ void __launch_bounds__(256) symmetrize_kernel(double* X, int64_t n, d
   __shared__ double a[32][33];
   __shared__ double b[32][33];
   // map blockIdx.x -> (bi, bj) with bi <= bj over the upper triangle of tiles
-  int64_t t = blockIdx.x;
-  int bi = 0;
-  {
-    // row bi holds nb - bi tiles
-    int64_t rem = t;
-    while (rem >= nb - bi) {
-      rem -= nb - bi;
-      ++bi;
-    }
-    t = rem;
-  }
-  int bj = bi + (int)t;
+  // (row bi holds nb - bi tiles; start(b) = b nb - b (b - 1) / 2)
+  const int64_t t = blockIdx.x;
+  const double B = 2.0 * nb + 1.0;
+  int bi = (int)floor((B - sqrt(B * B - 8.0 * (double)t)) * 0.5);
+  if (bi < 0) bi = 0;
+  if (bi > nb - 1) bi = nb - 1;
+  while (bi > 0 && (int64_t)bi * nb - (int64_t)bi * (bi - 1) / 2 > t) --bi;
+  while (bi + 1 < nb && (int64_t)(bi + 1) * nb - (int64_t)(bi + 1) * bi / 2 <= t) ++bi;
+  const int bj = bi + (int)(t - ((int64_t)bi * nb - (int64_t)bi * (bi - 1) / 2));
   int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   int64_t r0 = (int64_t)bi * 32, c0 = (int64_t)bj * 32;
   for (int y = ty; y < 32; y += 8) {

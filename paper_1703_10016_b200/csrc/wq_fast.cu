@@ -150,9 +150,21 @@ __device__ __forceinline__ double k1_half_ln(double qx, double qy, int qa, doubl
   return half_ln(R, tab);
 }
 
+// Tile mapping: sym (tile_row0 < 0): upper-triangle pairs of an nb x nb tile grid;
+// rect: tile rows tile_row0 .. + gridDim.x / nbj, all nbj tile columns, output rows
+// offset by tile_row0 * FT (a rank's row block).
+__device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int& bi, int& bj) {
+  if (tile_row0 < 0) {
+    tri_index(blockIdx.x, nb, bi, bj);
+  } else {
+    bi = tile_row0 + (int)(blockIdx.x / nb);
+    bj = (int)(blockIdx.x % nb);
+  }
+}
+
 template <int P, int MODE>
 __global__ void __launch_bounds__(IK1_THREADS, 2)
-ik1_sym_kernel(wq_smooth_t sm, int nb, double* X, int64_t ldx, int* flag) {
+ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, double* X, int64_t ldx, int* flag) {
   using C = Ik1Cfg<P, MODE>;
   constexpr int WG = C::WG, NQ = C::NQ, NQP = C::NQP, HJ = C::HJ;
   __shared__ double tab[3 * LOGTAB];
@@ -164,7 +176,8 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, double* X, int64_t ldx, int* flag) {
 
   const int64_t N = sm.n_rows, nq = sm.nq;
   int bi, bj;
-  tri_index(blockIdx.x, nb, bi, bj);
+  tile_of_block(nb, tile_row0, bi, bj);
+  const int64_t row_off = tile_row0 < 0 ? 0 : (int64_t)tile_row0 * FT;
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
   const int nj = (int)min((int64_t)FT, N - J0);
@@ -248,7 +261,7 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, double* X, int64_t ldx, int* flag) {
       double acc = 0.0;
 #pragma unroll
       for (int w = 0; w < WG; ++w) acc = fma(Gi[i][w], win[w], acc);
-      if (i < ni && j < nj) X[(I0 + i) * ldx + J0 + j] = acc;
+      if (i < ni && j < nj) X[(I0 - row_off + i) * ldx + J0 + j] = acc;
 #pragma unroll
       for (int w = 0; w < WG - 2; ++w) win[w] = win[w + 2];
     }
@@ -361,7 +374,7 @@ template <int P>
 __global__ void __launch_bounds__(X2_THREADS, 2)
 x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
                 const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
-                int nb) {
+                int nb, int tile_row0) {
   using C = X2Cfg<P>;
   extern __shared__ double smem[];
   double* Zsm = smem;                              // ZROWS * ZSTRIDE
@@ -370,19 +383,22 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   double* Ssm = Tst + FT * TSTRIDE;                // FT * 16
   const int64_t n = N;
   int bi, bj;
-  tri_index(blockIdx.x, nb, bi, bj);
+  tile_of_block(nb, tile_row0, bi, bj);
+  const bool rect = tile_row0 >= 0;
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
   const int nj = (int)min((int64_t)FT, N - J0);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, c = lane & 3;
+  // rect mode: X points at the rank's row block (row tile_row0 * FT)
+  const int64_t row_off = rect ? (int64_t)tile_row0 * FT : 0;
 
   // IK1(I,J) tile -> Tst (asynchronous)
   if (w_ik1 != 0.0) {
     for (int k = tid; k < FT * FT; k += X2_THREADS) {
       const int a = k >> 6, b = k & 63;
-      if (a < ni && b < nj) cp_async8(Tst + a * TSTRIDE + b, X + (I0 + a) * ldx + J0 + b);
+      if (a < ni && b < nj) cp_async8(Tst + a * TSTRIDE + b, X + (I0 - row_off + a) * ldx + J0 + b);
       else Tst[a * TSTRIDE + b] = 0.0;
     }
   } else {
@@ -391,7 +407,8 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   for (int k = tid; k < FT * PSTRIDE; k += X2_THREADS) Phs[k] = 0.0;
 
   double acc[8][2];
-  for (int orient = 0; orient < 2; ++orient) {
+  const int norient = rect ? 1 : 2;
+  for (int orient = 0; orient < norient; ++orient) {
     // 0: Phi rows = I, m over J-range, contraction with S_J -> X2(I,J)
     // 1: Phi rows = J, m over I-range, contraction with S_I -> X2(J,I)
     const int64_t R0 = orient == 0 ? I0 : J0;
@@ -431,6 +448,14 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
     }
   }
   __syncthreads();
+  if (rect) {
+    // unsymmetrised row block: X(I,J) = alpha (w IK1 + X2(I,J))
+    for (int k = tid; k < FT * FT; k += X2_THREADS) {
+      const int a = k >> 6, b = k & 63;
+      if (a < ni && b < nj) X[(I0 - row_off + a) * ldx + J0 + b] = alpha * Tst[a * TSTRIDE + b];
+    }
+    return;
+  }
   // acc holds X2(J,I): lane (j = 8warp + r, i = 8ib + 2c + e).  A(J,I)[j][i] =
   // alpha (Tst[i][j] + X2(J,I)[j][i]) -> staged in Phs as [j][i]
 #pragma unroll
@@ -491,7 +516,8 @@ __global__ void selftest_dmma_kernel(const double* A, const double* B, double* C
 }
 
 template <int P, int MODE>
-static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, cudaStream_t st) {
+static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, cudaStream_t st,
+                      int tile_row0, int tile_row1) {
   using C = Ik1Cfg<P, MODE>;
   if (sm->wg != C::WG) {
     set_error("wq_ik1_sym: rule band width %lld != 2p+1", (long long)sm->wg);
@@ -500,22 +526,26 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
   const size_t smem = (size_t)FT * C::NQP * 8;
   cudaFuncSetAttribute(ik1_sym_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(sm->n_rows, FT);
-  const int64_t pairs = (int64_t)nb * (nb + 1) / 2;
-  ik1_sym_kernel<P, MODE><<<(unsigned)pairs, IK1_THREADS, smem, st>>>(*sm, nb, X, ldx, flag);
+  const int64_t blocks = tile_row0 < 0 ? (int64_t)nb * (nb + 1) / 2
+                                       : (int64_t)(tile_row1 - tile_row0) * nb;
+  ik1_sym_kernel<P, MODE><<<(unsigned)blocks, IK1_THREADS, smem, st>>>(*sm, nb, tile_row0, X, ldx,
+                                                                        flag);
   return check_launch("wq_ik1_sym");
 }
 
 template <int P>
 static int launch_x2(int64_t N, const double* Uext, const double* Zext, const double* s_w,
-                     double alpha, double w_ik1, double* X, int64_t ldx, cudaStream_t st) {
+                     double alpha, double w_ik1, double* X, int64_t ldx, cudaStream_t st,
+                     int tile_row0, int tile_row1) {
   using C = X2Cfg<P>;
   const size_t smem = ((size_t)C::ZROWS * C::ZSTRIDE + (size_t)FT * PSTRIDE + (size_t)FT * TSTRIDE +
                        (size_t)FT * 16) * 8;
   cudaFuncSetAttribute(x2_pairs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(N, FT);
-  const int64_t pairs = (int64_t)nb * (nb + 1) / 2;
-  x2_pairs_kernel<P><<<(unsigned)pairs, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
-                                                                ldx, nb);
+  const int64_t blocks = tile_row0 < 0 ? (int64_t)nb * (nb + 1) / 2
+                                       : (int64_t)(tile_row1 - tile_row0) * nb;
+  x2_pairs_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
+                                                                 ldx, nb, tile_row0);
   return check_launch("wq_x2_pairs");
 }
 
@@ -525,9 +555,8 @@ using namespace wq;
 
 extern "C" {
 
-int wq_ik1_sym(const wq_smooth_t* sm, double* X, int64_t ldx, int64_t max_span, int* flag,
-               void* stream) {
-  (void)max_span;
+static int ik1_dispatch(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, void* stream,
+                        int tile_row0, int tile_row1) {
   if (!sm || !X || !flag || sm->n_rows <= 0 || !sm->closed) {
     set_error("wq_ik1_sym: bad arguments (closed uniform meshes only)");
     return WQ_EINVAL;
@@ -541,15 +570,36 @@ int wq_ik1_sym(const wq_smooth_t* sm, double* X, int64_t ldx, int64_t max_span, 
   cudaStream_t st = (cudaStream_t)stream;
   const int p = (int)(sm->wg - 1) / 2;
   const bool tab = sm->k1_mode == WQ_K1_TABLE;
+#define WQ_IK1_CASE(PP)                                                                          \
+  case PP:                                                                                       \
+    return tab ? launch_ik1<PP, WQ_K1_TABLE>(sm, X, ldx, flag, st, tile_row0, tile_row1)         \
+               : launch_ik1<PP, WQ_K1_CLOSED>(sm, X, ldx, flag, st, tile_row0, tile_row1);
   switch (p) {
-    case 2: return tab ? launch_ik1<2, WQ_K1_TABLE>(sm, X, ldx, flag, st) : launch_ik1<2, WQ_K1_CLOSED>(sm, X, ldx, flag, st);
-    case 3: return tab ? launch_ik1<3, WQ_K1_TABLE>(sm, X, ldx, flag, st) : launch_ik1<3, WQ_K1_CLOSED>(sm, X, ldx, flag, st);
-    case 4: return tab ? launch_ik1<4, WQ_K1_TABLE>(sm, X, ldx, flag, st) : launch_ik1<4, WQ_K1_CLOSED>(sm, X, ldx, flag, st);
-    case 5: return tab ? launch_ik1<5, WQ_K1_TABLE>(sm, X, ldx, flag, st) : launch_ik1<5, WQ_K1_CLOSED>(sm, X, ldx, flag, st);
+    WQ_IK1_CASE(2)
+    WQ_IK1_CASE(3)
+    WQ_IK1_CASE(4)
+    WQ_IK1_CASE(5)
     default:
       set_error("wq_ik1_sym: degree %d unsupported (2..5)", p);
       return WQ_EUNSUPPORTED;
   }
+#undef WQ_IK1_CASE
+}
+
+int wq_ik1_sym(const wq_smooth_t* sm, double* X, int64_t ldx, int64_t max_span, int* flag,
+               void* stream) {
+  (void)max_span;
+  return ik1_dispatch(sm, X, ldx, flag, stream, -1, -1);
+}
+
+int wq_ik1_rows(const wq_smooth_t* sm, int64_t tile_row0, int64_t tile_row1, double* Xrows,
+                int64_t ldx, int* flag, void* stream) {
+  if (!sm || tile_row0 < 0 || tile_row1 <= tile_row0 ||
+      tile_row1 > ceil_div(sm->n_rows, FT)) {
+    set_error("wq_ik1_rows: bad tile rows");
+    return WQ_EINVAL;
+  }
+  return ik1_dispatch(sm, Xrows, ldx, flag, stream, (int)tile_row0, (int)tile_row1);
 }
 
 int wq_zext(int64_t n, int nA, int nApad, int zstride, const double* Zp, const double* ff,
@@ -563,9 +613,10 @@ int wq_zext(int64_t n, int nA, int nApad, int zstride, const double* Zp, const d
   return check_launch("wq_zext");
 }
 
-int wq_x2_pairs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
-                const double* Uext, const double* Zext, const double* s_w, double alpha,
-                double w_ik1, double* X, int64_t ldx, void* stream) {
+static int x2_dispatch(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+                       const double* Uext, const double* Zext, const double* s_w, double alpha,
+                       double w_ik1, double* X, int64_t ldx, void* stream, int tile_row0,
+                       int tile_row1) {
   if (N <= 0 || !Uext || !Zext || !s_w || !X) {
     set_error("wq_x2_pairs: bad arguments");
     return WQ_EINVAL;
@@ -578,7 +629,7 @@ int wq_x2_pairs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstri
       set_error("wq_x2_pairs: layout mismatch for p=%d", PP);                                  \
       return WQ_EINVAL;                                                                        \
     }                                                                                          \
-    return launch_x2<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, st);
+    return launch_x2<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, st, tile_row0, tile_row1);
   switch (p) {
     WQ_X2_CASE(2)
     WQ_X2_CASE(3)
@@ -589,6 +640,25 @@ int wq_x2_pairs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstri
       return WQ_EUNSUPPORTED;
   }
 #undef WQ_X2_CASE
+}
+
+int wq_x2_pairs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+                const double* Uext, const double* Zext, const double* s_w, double alpha,
+                double w_ik1, double* X, int64_t ldx, void* stream) {
+  return x2_dispatch(N, p, nA, nApad, ws, ktot, zstride, Uext, Zext, s_w, alpha, w_ik1, X, ldx,
+                     stream, -1, -1);
+}
+
+int wq_x2_rows(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+               const double* Uext, const double* Zext, const double* s_w, double alpha,
+               double w_ik1, int64_t tile_row0, int64_t tile_row1, double* Xrows, int64_t ldx,
+               void* stream) {
+  if (tile_row0 < 0 || tile_row1 <= tile_row0 || tile_row1 > ceil_div(N, FT)) {
+    set_error("wq_x2_rows: bad tile rows");
+    return WQ_EINVAL;
+  }
+  return x2_dispatch(N, p, nA, nApad, ws, ktot, zstride, Uext, Zext, s_w, alpha, w_ik1, Xrows, ldx,
+                     stream, (int)tile_row0, (int)tile_row1);
 }
 
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream) {

@@ -13,10 +13,10 @@ from __future__ import annotations
 import numpy as np
 
 
-def row_blocks(n: int, world: int, align: int = 32):
-    """Contiguous [r0, r1) per rank, sizes multiples of ``align`` except the
-    last, covering 0..n exactly (equal-size blocks -> all_gather needs
-    equal shards, so shards are padded to the max block)."""
+def row_blocks(n: int, world: int, align: int = 64):
+    """Contiguous [r0, r1) per rank covering 0..n, block starts aligned to
+    ``align`` rows (the kernels' tile height) and equal padded height ``per``
+    (all_gather needs equal shards)."""
     per = -(-n // world)
     per = -(-per // align) * align
     bounds = []
@@ -46,15 +46,47 @@ def gather_rows(local_block, full, per, group=None):
     return full
 
 
-def assemble_rows_device(disc, X_block, row0: int, row1: int):
-    """Rows [row0, row1) of X = IK1 + X2 into X_block (shape (row1-row0, N)),
-    circulant path (closed uniform simple-knot meshes)."""
+def assemble_rows_device(disc, X_block, row0: int, row1: int, zext=None):
+    """Rows [row0, row1) of the unsymmetrised X = IK1 + X2 into X_block
+    (leading dimension N), circulant path (closed uniform simple-knot meshes).
+    row0 must be a multiple of the 64-row tile; no communication."""
     from . import assembly as AS
     from . import _lib
 
+    if not AS._use_v2(disc):
+        raise NotImplementedError("row-block sharding needs the circulant (closed uniform) path")
+    T = _lib.WQ_FTILE
+    if row0 % T:
+        raise ValueError("row blocks must start on a 64-row tile boundary")
+    t0, t1 = row0 // T, -(-row1 // T)
     lp, d = AS._logpart_dev(disc)
-    if lp.path != "circulant":
-        raise NotImplementedError("row-block sharding needs the circulant log-part path")
-    AS._ik1_into(disc, X_block, accumulate=False, row0=row0, row1=row1)
-    AS._ik2_x2_rows(disc, X_block, row0, row1, accumulate=True)
+    sm = AS._smooth(disc)
+    st = _lib.stream_handle()
+    Zext = AS._zext_table(disc) if zext is None else zext
+    N = disc.space.dim
+    _lib.call("wq_ik1_rows", AS.ctypes_ref(sm["struct"]), t0, t1, _lib.ptr(X_block),
+              X_block.stride(0), _lib.ptr(sm["flag"]), st)
+    _lib.call("wq_x2_rows", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
+              lp.uext.shape[1], lp.zstride, _lib.ptr(d["uext"]), _lib.ptr(Zext), _lib.ptr(d["s_w"]),
+              1.0, 1.0, t0, t1, _lib.ptr(X_block), X_block.stride(0), st)
     return X_block
+
+
+def assemble_distributed(disc, X, group=None):
+    """A = -(X + X^T)/(4 pi) on every rank: local row block, one all-gather,
+    local symmetrise epilogue.  X: (N, N) CUDA tensor on this rank."""
+    import torch
+    import torch.distributed as dist
+    from . import _lib
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    N = disc.space.dim
+    bounds, per = row_blocks(N, world)
+    r0, r1 = bounds[rank]
+    Xb = torch.zeros((per, N), dtype=torch.float64, device=X.device)
+    if r1 > r0:
+        assemble_rows_device(disc, Xb, r0, r1)
+    gather_rows(Xb, X, per, group)
+    _lib.call("wq_symmetrize", _lib.ptr(X), N, -1.0 / (4.0 * np.pi), _lib.stream_handle())
+    return X
