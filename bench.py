@@ -139,7 +139,9 @@ def kernel_flops(disc):
     N, nq = disc.space.dim, disc.nodes.n
     wg = disc.rules.WG
     c_k1 = 4 + 1 + 44 + 1                     # dist^2, x 1/p^2, ln, x 1/2
-    ik1 = c_k1 * nq * nq + 2 * wg * (nq * N + N * N)
+    nb = -(-N // 64)
+    sym = (nb + 1) / (2.0 * nb)                # ik1_sym computes the upper-triangle tiles only
+    ik1 = (c_k1 * nq * nq + 2 * wg * (nq * N + N * N)) * sym
     from paper_1703_10016_b200 import assembly as AS
     lp = AS._log_part(disc)
     if lp.path == "circulant":
@@ -306,7 +308,8 @@ def main():
                 "peak_source": "measured DFMA probe (wq_fp64_peak, burst); MEASURED_PEAKS.json has "
                                "no FP64 entry", "peak_datasheet": FP64_DATASHEET_TFLOPS,
                 "traffic": None}
-    survey_frac = SURVEY_W_C4 * (N / 32768) ** 2 / (ms * 1e-3) / (peak * 1e12) * world ** 0 \
+    # fixed W for C4, x (N+1)/(2N) when the symmetry of A is exploited
+    survey_frac = SURVEY_W_C4 * (N + 1) / (2.0 * N) / (ms * 1e-3) / (peak * 1e12 * world) \
         if (args.n_el == 32768 and args.p == 3) else None
 
     # ---- end to end through the public API with host buffers (N = 1 layout) ----
