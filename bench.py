@@ -74,7 +74,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -153,6 +153,21 @@ def kernel_flops(disc):
     return {"ik1": ik1, "ik2": ik2}
 
 
+def committed_traffic(dom):
+    """dram read+write bytes per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/r*_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return None
+    try:
+        data = json.load(open(files[-1]))
+        key = {"ik1": "ik1_sym_kernel", "ik2": "x2_pairs_kernel"}[dom]
+        return data[key]["total"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def run_reference(args):
     """CPU oracle port (reference algorithm, row-block restatement) on a
     bounded row sample of the same workload; rank 0 only."""
@@ -200,8 +215,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n-el", type=int, default=32768)
     ap.add_argument("--p", type=int, default=3)
@@ -262,6 +277,7 @@ def main():
     launches["n"] = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        time.sleep(0.3)  # let nvidia-smi start sampling before the timed region
         e0.record()
         for _ in range(args.steps):
             step()
@@ -307,7 +323,7 @@ def main():
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": "measured DFMA probe (wq_fp64_peak, burst); MEASURED_PEAKS.json has "
                                "no FP64 entry", "peak_datasheet": FP64_DATASHEET_TFLOPS,
-                "traffic": None}
+                "traffic": committed_traffic(dom), "traffic_unit": "bytes per launch (ncu, profiles/)"}
     # fixed W for C4, x (N+1)/(2N) when the symmetry of A is exploited
     survey_frac = SURVEY_W_C4 * (N + 1) / (2.0 * N) / (ms * 1e-3) / (peak * 1e12 * world) \
         if (args.n_el == 32768 and args.p == 3) else None
