@@ -107,6 +107,16 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
 }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+// 8-byte copy, zero-filled when !valid (src is not read then)
+__device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gsrc, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(n));
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // ---------------------------------------------------------------------------
@@ -214,8 +224,13 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, double* X, int64_t ldx, in
   int bad = 0;
   const double* __restrict__ invp2 = sm.invp2;
   const double period = sm.period;
-  if (tid < 2 * NQ) {
-    const int q = tid >> 1, h = tid & 1;
+  // (q, half) items: half 0 on threads 0..143, half 1 on 144..287, so a warp
+  // (but one) shares its column j: G_j and r-node loads are broadcasts
+  constexpr int HALF_THREADS = IK1_THREADS / 2;
+  static_assert(NQ <= HALF_THREADS, "tile too tall for the (q, half) mapping");
+  const int h = tid >= HALF_THREADS ? 1 : 0;
+  const int q = tid - h * HALF_THREADS;
+  if (q < NQ) {
     const double mx = qx[q], my = qy[q], mJ = qJ[q], ms = qs[q];
     const int ma = qa[q];
     const int jb = h * HJ;
@@ -351,7 +366,7 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64
 
 // out[a][b] = sum_m Phs[a][m] S_b[m - b + d]; warp owns row block `warp`
 template <int P>
-__device__ __forceinline__ void s_contract(const double* Phs, const double* Ssm, double (&acc)[8][2]) {
+__device__ __forceinline__ void s_contract(const double* Phs, const double* Bfr, double (&acc)[8][2]) {
   using C = X2Cfg<P>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane >> 2, c = lane & 3;
@@ -361,10 +376,8 @@ __device__ __forceinline__ void s_contract(const double* Phs, const double* Ssm,
   for (int jb = 0; jb < 8; ++jb) {
 #pragma unroll
     for (int s = 0; s < C::KS / 4; ++s) {
-      const int mm = 4 * s + c;
-      const double a = Phs[(8 * warp + r) * PSTRIDE + 8 * jb + mm];
-      const int t = mm - r;
-      const double b = (t >= 0 && t <= 2 * C::D) ? Ssm[(8 * jb + r) * 16 + t] : 0.0;
+      const double a = Phs[(8 * warp + r) * PSTRIDE + 8 * jb + 4 * s + c];
+      const double b = Bfr[(jb * (C::KS / 4) + s) * 32 + lane];
       dmma(acc[jb][0], acc[jb][1], a, b);
     }
   }
@@ -380,7 +393,8 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   double* Zsm = smem;                              // ZROWS * ZSTRIDE
   double* Phs = Zsm + C::ZROWS * C::ZSTRIDE;       // FT * PSTRIDE (also output staging)
   double* Tst = Phs + FT * PSTRIDE;                // FT * TSTRIDE: w IK1 + X2(I,J)
-  double* Ssm = Tst + FT * TSTRIDE;                // FT * 16
+  double* Ssm = Tst + FT * TSTRIDE;                // FT * 16 (S band rows)
+  double* Bfr = Ssm + FT * 16;                     // 8 * KS/4 * 32 (fragment order)
   const int64_t n = N;
   int bi, bj;
   tile_of_block(nb, tile_row0, bi, bj);
@@ -423,19 +437,26 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
       const int row = k / (C::ZSTRIDE / 2), cc = 2 * (k - row * (C::ZSTRIDE / 2));
       int64_t g = g0 + row;
       if (g >= n) g %= n;
-      const double* src = Zext + g * C::ZSTRIDE + cc;
-      cp_async8(Zsm + row * C::ZSTRIDE + cc, src);
-      cp_async8(Zsm + row * C::ZSTRIDE + cc + 1, src + 1);
+      cp_async16(Zsm + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
     }
     for (int k = tid; k < FT * 16; k += X2_THREADS) {
       const int row = k >> 4, t = k & 15;
-      Ssm[k] = (row < nc && t < C::WS) ? sw[(C0 + row) * C::WS + t] : 0.0;
+      const bool ok = row < nc && t < C::WS;
+      cp_async8_zfill(Ssm + k, sw + (ok ? (C0 + row) * C::WS + t : 0), ok);
     }
     cp_async_wait_all();
     __syncthreads();
+    // S band in B-fragment order: Bfr[jb][s][lane] = S_{8jb+r}[4s+c-r] (0 outside the band)
+    for (int k = tid; k < 8 * (C::KS / 4) * 32; k += X2_THREADS) {
+      const int ln = k & 31, s = (k >> 5) % (C::KS / 4), jb = (k >> 5) / (C::KS / 4);
+      const int rr = ln >> 2, cc = ln & 3;
+      const int t = 4 * s + cc - rr;
+      Bfr[k] = (t >= 0 && t <= 2 * C::D) ? Ssm[(8 * jb + rr) * 16 + t] : 0.0;
+    }
+    __syncthreads();
     phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin);
     __syncthreads();
-    s_contract<P>(Phs, Ssm, acc);
+    s_contract<P>(Phs, Bfr, acc);
     if (orient == 0) {
       // Tst[i][j] = w IK1 + X2(I,J); lane holds (i = 8warp + r, j = 8jb + 2c + e)
 #pragma unroll
@@ -539,7 +560,7 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
                      int tile_row0, int tile_row1) {
   using C = X2Cfg<P>;
   const size_t smem = ((size_t)C::ZROWS * C::ZSTRIDE + (size_t)FT * PSTRIDE + (size_t)FT * TSTRIDE +
-                       (size_t)FT * 16) * 8;
+                       (size_t)FT * 16 + (size_t)8 * (C::KS / 4) * 32) * 8;
   cudaFuncSetAttribute(x2_pairs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(N, FT);
   const int64_t blocks = tile_row0 < 0 ? (int64_t)nb * (nb + 1) / 2
