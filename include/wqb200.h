@@ -221,6 +221,14 @@ int wq_absmax_defect(const double* X, int64_t n, double* out, void* stream);
 /* Weighted RHS (assembly.py:312-319): b[i] = sum_w G[i, w] g[(g_start[i]+w) mod nq]. */
 int wq_b1w(const wq_smooth_t* sm, const double* g, double* b, void* stream);
 
+/*
+ * Double-layer RHS inner integral (assemble_b2, assembly.py:322-343; Kbar_points,
+ * geometry.py:250-280): inner[s] = sum_t Kbar(s,t) wg[t] over M = 16 n_el per-element
+ * Gauss points; f, f' at the points, kdiag = C^2 curvature limit on s == t.
+ */
+int wq_b2_inner(int64_t M, const double* fx, const double* fy, const double* tx, const double* ty,
+                const double* wg, const double* kdiag, double* inner, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

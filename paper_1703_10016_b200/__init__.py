@@ -24,6 +24,7 @@ from .assembly import (
     NodeVector,
     assemble_b1,
     assemble_b1_weighted,
+    assemble_b2,
     assemble_ik1,
     assemble_ik2,
     assemble_matrix_device,

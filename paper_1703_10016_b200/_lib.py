@@ -75,6 +75,7 @@ _SIGS = {
     "wq_ik1_rows": [ctypes.POINTER(WqSmooth), c_i64, c_i64, c_vp, c_i64, c_vp, c_vp],
     "wq_x2_rows": [c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                    c_i64, c_i64, c_vp, c_i64, c_vp],
+    "wq_b2_inner": [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "wq_selftest_log": [c_i64, c_vp, c_vp, c_vp, c_vp],
     "wq_selftest_dmma": [c_vp, c_vp, c_vp, c_vp],
 }

@@ -52,6 +52,7 @@ __all__ = [
     "scale_and_symmetrize",
     "assemble_b1_weighted",
     "assemble_b1",
+    "assemble_b2",
     "basis_values",
 ]
 
@@ -693,3 +694,39 @@ def assemble_b1(curve, space, dirichlet, order: int = 16) -> np.ndarray:
     out = np.zeros(space.dim)
     np.add.at(out, bc.ravel(), (bv * (wts * jac * vals)[:, None]).ravel())
     return out
+
+
+def assemble_b2(curve, space, dirichlet, order: int = 16) -> np.ndarray:
+    """b2[i] = 1/(2 pi) int B_i J [int Kbar(s,t) u_D(t) dt] ds by per-element
+    Gauss on both integrals (assembly.py:322-343).  The (M x M) Kbar grid,
+    M = order * n_el, is evaluated on the GPU (wq_b2_inner) and never stored;
+    the diagonal uses the C^2 curvature limit (geometry.py:269-279)."""
+    torch = _torch()
+    curve = as_curve(curve)
+    space = as_basis(space)
+    _check_space(curve, space)
+    if not curve.is_c2():
+        raise GeometryError("double-layer right-hand side needs a C^2 curve")
+    els = space.elements
+    x, w = np.polynomial.legendre.leggauss(order)
+    half = 0.5 * (els[:, 1] - els[:, 0])
+    mid = 0.5 * (els[:, 0] + els[:, 1])
+    pts = (mid[:, None] + half[:, None] * x[None, :]).ravel()
+    wts = (half[:, None] * w[None, :]).ravel()
+    b = curve.basis
+    cp = np.clip(pts, b.a, b.b)
+    f = curve.spline(0)(cp)
+    d1 = curve.spline(1)(cp)
+    d2 = curve.spline(2)(cp)
+    kdiag = 0.5 * (d1[:, 1] * d2[:, 0] - d1[:, 0] * d2[:, 1]) / np.sum(d1 ** 2, axis=-1)
+    wg = wts * np.asarray(dirichlet(pts), dtype=float)
+    dev = [_to_dev(torch, a) for a in (f[:, 0], f[:, 1], d1[:, 0], d1[:, 1], wg, kdiag)]
+    inner = torch.empty(len(pts), dtype=torch.float64, device="cuda")
+    _lib.call("wq_b2_inner", len(pts), *[_lib.ptr(t) for t in dev], _lib.ptr(inner),
+              _lib.stream_handle())
+    inner = inner.cpu().numpy()
+    jac = np.linalg.norm(d1, axis=-1)
+    bv, bc = active_values(space, pts)
+    out = np.zeros(space.dim)
+    np.add.at(out, bc.ravel(), (bv * (wts * jac * inner)[:, None]).ravel())
+    return out / TWO_PI
