@@ -158,6 +158,13 @@ int wq_dmat(const wq_pairs_t* pp, double* D, void* stream);
 int wq_band_solve_cols(int64_t n, int64_t bw, const double* Lb, double* X, int64_t ncols,
                        int64_t ldx, void* stream);
 
+/* Cyclic (seam-coupled) banded SPD solve on every column: X <- H^{-1} X with the
+ * arrow Cholesky factor: Lb (m x (bw+1), m = n - bw) of the leading band, L21
+ * (bw x m, row-major) = A21 L11^{-T}, L22 (bw x bw, row-major lower) of the Schur
+ * complement.  bw <= 16. */
+int wq_cyc_solve_cols(int64_t n, int64_t bw, const double* Lb, const double* L21,
+                      const double* L22, double* X, int64_t ncols, int64_t ldx, void* stream);
+
 /* out = in^T for an (rows x cols) matrix. */
 int wq_transpose(const double* in, int64_t rows, int64_t cols, double* out, void* stream);
 

@@ -118,8 +118,10 @@ class LogPart:
     u_loc: np.ndarray = None
     v_el: np.ndarray = None
     v_loc: np.ndarray = None
-    Lb: np.ndarray = None          # banded Cholesky factor of H
+    Lb: np.ndarray = None          # banded Cholesky factor of H (leading block if cyclic)
     bw: int = 0
+    L21: np.ndarray = None         # cyclic meshes: seam coupling rows of the arrow factor
+    L22: np.ndarray = None
 
 
 @dataclass
@@ -286,33 +288,12 @@ def _log_part(disc: Discretization) -> LogPart:
         lp.U = np.ascontiguousarray(U)
         lp.v0 = np.ascontiguousarray(v[0])
         lp.hinv_taps = np.ascontiguousarray(taps)
-    elif not fine.closed:
-        import scipy.linalg
-        bw = d
-        NE = fine.dim
-        Hd = H.tocsr()
-        ab = np.zeros((bw + 1, NE))
-        for j in range(bw + 1):
-            ab[j, : NE - j] = Hd.diagonal(-j)
-        try:
-            lo = scipy.linalg.cholesky_banded(ab, lower=True)
-        except np.linalg.LinAlgError as exc:
-            raise ConstructionError("node vector does not resolve the refined space") from exc
-        diag = lo[0]
-        if diag.min() ** 2 <= PC.RANK_RTOL ** 2 * (diag.max() ** 2):
-            raise ConstructionError("node vector does not resolve the refined space")
-        Lb = np.zeros((NE, bw + 1))
-        for j in range(bw + 1):
-            Lb[j:, j] = lo[j, : NE - j]
+    else:
+        lp.Lb, lp.bw, lp.L21, lp.L22 = PC.fit_cholesky(H, d, fine.closed)
         u_el, u_loc, _ = _incidence(ucols, N)
-        v_el, v_loc, _ = _incidence(vcols, NE)
+        v_el, v_loc, _ = _incidence(vcols, fine.dim)
         lp.u, lp.v = np.ascontiguousarray(u), np.ascontiguousarray(v)
         lp.u_el, lp.u_loc, lp.v_el, lp.v_loc = u_el, u_loc, v_el, v_loc
-        lp.Lb, lp.bw = Lb, bw
-    else:
-        raise ConstructionError(
-            "closed meshes with repeated knots or nref > 1 are not supported by the B200 "
-            "log-part yet (cyclic banded fit)")
     disc._logpart = lp
     return lp
 
@@ -445,8 +426,9 @@ def _logpart_dev(disc):
                                          d["s_start"].data_ptr(), d["s_w"].data_ptr())
         else:
             NE = disc.refined.basis.dim
-            for k in ("u", "v", "u_el", "u_loc", "v_el", "v_loc", "Lb"):
-                d[k] = _to_dev(torch, getattr(lp, k))
+            for k in ("u", "v", "u_el", "u_loc", "v_el", "v_loc", "Lb", "L21", "L22"):
+                if getattr(lp, k) is not None:
+                    d[k] = _to_dev(torch, getattr(lp, k))
             d["struct"] = _lib.WqLogpart(N, NE, lp.da, 0, lp.s_w.shape[1], None, None,
                                          d["s_start"].data_ptr(), d["s_w"].data_ptr())
         return d
@@ -501,13 +483,21 @@ def _ik2_x2_into(disc, X, accumulate=True):
     D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
     _lib.call("wq_theta_t", ctypes_ref(pp), _lib.ptr(thetaT), st)
     _lib.call("wq_dmat", ctypes_ref(pp), _lib.ptr(D), st)
+    def hsolve(Y, ncols):
+        if lp.L21 is None:
+            _lib.call("wq_band_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(Y), ncols,
+                      Y.stride(0), st)
+        else:
+            _lib.call("wq_cyc_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(d["L21"]),
+                      _lib.ptr(d["L22"]), _lib.ptr(Y), ncols, Y.stride(0), st)
+
     # E = H^{-1} D ; F = H^{-1} E^T = H^{-1} D H^{-1}
-    _lib.call("wq_band_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(D), NE, NE, st)
+    hsolve(D, NE)
     F = torch.empty_like(D)
     _lib.call("wq_transpose", _lib.ptr(D), NE, NE, _lib.ptr(F), st)
-    _lib.call("wq_band_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(F), NE, NE, st)
+    hsolve(F, NE)
     # Phi = 2 H^{-1} Theta^T - F S
-    _lib.call("wq_band_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(thetaT), N, N, st)
+    hsolve(thetaT, N)
     _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(F), _lib.ptr(thetaT), st)
     # X[j][i] (+)= sum_m S[m, j] Phi[m, i]  (= X2^T)
     _lib.call("wq_add_st_phi", ctypes_ref(d["struct"]), _lib.ptr(thetaT), 0, N, _lib.ptr(X),

@@ -319,6 +319,48 @@ __global__ void band_solve_cols_kernel(int64_t n, int bw, const double* Lb, doub
   }
 }
 
+// Cyclic banded SPD solve, X <- H^{-1} X per column, with the arrow-shaped
+// Cholesky factor of the seam-coupled band: H = [[A11, A21^T], [A21, A22]],
+// A11 (m x m, m = n - bw) banded = L11 L11^T (Lb), L21 = A21 L11^{-T} (bw x m,
+// dense), A22 - L21 L21^T = L22 L22^T (bw x bw, lower, row-major).
+__global__ void cyc_solve_cols_kernel(int64_t n, int bw, const double* Lb, const double* L21,
+                                      const double* L22, double* X, int64_t ncols, int64_t ldx) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  double* x = X + c;
+  const int64_t m = n - bw;
+  for (int64_t k = 0; k < m; ++k) {  // y1 = L11^{-1} x1
+    double s = x[k * ldx];
+    const double* lk = Lb + k * (bw + 1);
+    for (int j = 1; j <= bw && j <= k; ++j) s = fma(-lk[j], x[(k - j) * ldx], s);
+    x[k * ldx] = s / lk[0];
+  }
+  double y2[16];
+  for (int k = 0; k < bw; ++k) {  // y2 = L22^{-1} (x2 - L21 y1)
+    double s = x[(m + k) * ldx];
+    const double* l = L21 + (int64_t)k * m;
+    for (int64_t j = 0; j < m; ++j) s = fma(-l[j], x[j * ldx], s);
+    for (int j = 0; j < k; ++j) s = fma(-L22[k * bw + j], y2[j], s);
+    y2[k] = s / L22[k * bw + k];
+  }
+  for (int k = bw - 1; k >= 0; --k) {  // z2 = L22^{-T} y2
+    double s = y2[k];
+    for (int j = k + 1; j < bw; ++j) s = fma(-L22[j * bw + k], y2[j], s);
+    y2[k] = s / L22[k * bw + k];
+    x[(m + k) * ldx] = y2[k];
+  }
+  for (int64_t j = 0; j < m; ++j) {  // y1 -= L21^T z2
+    double s = x[j * ldx];
+    for (int k = 0; k < bw; ++k) s = fma(-L21[(int64_t)k * m + j], y2[k], s);
+    x[j * ldx] = s;
+  }
+  for (int64_t k = m - 1; k >= 0; --k) {  // z1 = L11^{-T} (...)
+    double s = x[k * ldx];
+    for (int j = 1; j <= bw && k + j < m; ++j) s = fma(-Lb[(k + j) * (bw + 1) + j], x[(k + j) * ldx], s);
+    x[k * ldx] = s / Lb[k * (bw + 1)];
+  }
+}
+
 __global__ void transpose_kernel(const double* in, int64_t rows, int64_t cols, double* out) {
   __shared__ double t[32][33];
   int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
@@ -454,6 +496,17 @@ int wq_band_solve_cols(int64_t n, int64_t bw, const double* Lb, double* X, int64
   band_solve_cols_kernel<<<ceil_div(ncols, 128), 128, 0, (cudaStream_t)stream>>>(n, (int)bw, Lb, X,
                                                                                    ncols, ldx);
   return check_launch("wq_band_solve_cols");
+}
+
+int wq_cyc_solve_cols(int64_t n, int64_t bw, const double* Lb, const double* L21,
+                      const double* L22, double* X, int64_t ncols, int64_t ldx, void* stream) {
+  if (n <= 0 || bw < 1 || bw > 16 || bw >= n || !Lb || !L21 || !L22 || !X || ncols <= 0) {
+    set_error("wq_cyc_solve_cols: bad arguments");
+    return WQ_EINVAL;
+  }
+  cyc_solve_cols_kernel<<<ceil_div(ncols, 128), 128, 0, (cudaStream_t)stream>>>(n, (int)bw, Lb, L21,
+                                                                                  L22, X, ncols, ldx);
+  return check_launch("wq_cyc_solve_cols");
 }
 
 int wq_transpose(const double* in, int64_t rows, int64_t cols, double* out, void* stream) {

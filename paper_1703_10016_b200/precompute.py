@@ -441,3 +441,46 @@ def circulant_inverse(H, nfine):
     hinv[: K + 1] = taps[: K + 1]
     hinv[nfine - K:] = taps[1: K + 1][::-1]
     return hinv, K
+
+
+def fit_cholesky(H, bw: int, closed: bool):
+    """Cholesky factor of the fit normal matrix H (N_E x N_E, half-bandwidth
+    bw).  Open meshes: plain banded factor.  Closed meshes: H couples across
+    the seam, so the factor is arrow-shaped: the leading m = N_E - bw block is
+    banded (Lb), the last bw rows are dense (L21 = A21 L11^{-T}) plus a small
+    dense Schur factor L22.  Returns (Lb, bw, L21, L22) with Lb[k, j] = L[k, k-j].
+    Raises ConstructionError when H is not numerically SPD (the reference's
+    rank check, assembly.py:238-242 / quadrature.py:136-140)."""
+    import scipy.linalg
+
+    H = H.tocsr()
+    n = H.shape[0]
+    m = n - bw if closed else n
+    if closed and m <= bw:
+        raise ConstructionError("closed mesh too small for the cyclic banded fit")
+    ab = np.zeros((bw + 1, m))
+    for j in range(bw + 1):
+        ab[j, : m - j] = H[:m, :m].diagonal(-j)
+    try:
+        lo = scipy.linalg.cholesky_banded(ab, lower=True)
+    except np.linalg.LinAlgError as exc:
+        raise ConstructionError("node vector does not resolve the refined space") from exc
+    Lb = np.zeros((m, bw + 1))
+    for j in range(bw + 1):
+        Lb[j:, j] = lo[j, : m - j]
+    L21 = L22 = None
+    diag = lo[0]
+    if closed:
+        A21 = H[m:, :m].toarray()
+        L21 = scipy.linalg.solve_banded((bw, 0), lo, A21.T).T
+        Sch = H[m:, m:].toarray() - L21 @ L21.T
+        try:
+            L22 = np.linalg.cholesky(Sch)
+        except np.linalg.LinAlgError as exc:
+            raise ConstructionError("node vector does not resolve the refined space") from exc
+        diag = np.concatenate([diag, np.diag(L22)])
+        L21 = np.ascontiguousarray(L21)
+        L22 = np.ascontiguousarray(L22)
+    if diag.min() ** 2 <= RANK_RTOL ** 2 * diag.max() ** 2:
+        raise ConstructionError("node vector does not resolve the refined space")
+    return Lb, bw, L21, L22

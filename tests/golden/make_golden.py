@@ -179,6 +179,15 @@ def main(which=None):
             continue
         run_case(name, curve, space, g, gname, b2)
 
+    # refined exactness space (nref = 2): closed -> general (non-circulant) path, open too
+    for name, curve, space, g, gname in (
+            ("ell_p3_n32_nref2", ell, make_cyclic_basis(3, np.linspace(0, 1, 33)), g_ell,
+             "exp(x)cos(y)"),
+            ("slit_p2_n16_nref2", slit, make_open_basis(2, np.linspace(-1, 1, 17)), sq, "x^2")):
+        if which and not any(w in name for w in which):
+            continue
+        run_case(name, curve, space, g, gname, False, nref=2)
+
     if not which or "components" in which:
         # component pins: pair-moment tables and local polynomial coefficients
         comp = {}

@@ -85,8 +85,12 @@ def _emulate_gpu_dataflow(disc):
                         if e >= 0:
                             D[mm, l] += lp.v[e][:, a] @ m2[gap(e, f)][: lp.db + 1] @ lp.v[f][:, b]
         L = np.zeros((NE, NE))
+        m = lp.Lb.shape[0]
         for j in range(lp.bw + 1):
-            L[np.arange(j, NE), np.arange(0, NE - j)] = lp.Lb[j:, j]
+            L[np.arange(j, m), np.arange(0, m - j)] = lp.Lb[j:, j]
+        if lp.L21 is not None:   # closed mesh: arrow-shaped factor
+            L[m:, :m] = lp.L21
+            L[m:, m:] = lp.L22
         hinv = lambda Y: sl.solve_triangular(L.T, sl.solve_triangular(L, Y, lower=True))
         F = hinv(hinv(D).T)
         Phi = 2 * hinv(thT)
@@ -103,7 +107,8 @@ def _emulate_gpu_dataflow(disc):
 
 @pytest.mark.parametrize("name", ["ell_p3_n32", "ell_p2_n64", "ell_p5_n64", "star_p4_n128",
                                   "c1_slit_p2_n64", "slit_p4_n24_dbl", "parabola_p3_n16",
-                                  "slit_p5_n24"])
+                                  "slit_p5_n24", "closed_smooth_p3_n24", "ell_p3_n32_nref2",
+                                  "slit_p2_n16_nref2"])
 def test_gpu_dataflow_in_numpy_matches_reference(name):
     z, meta = load(name)
     curve, space = product_objects(meta)
