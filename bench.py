@@ -254,7 +254,11 @@ def main():
     alpha = -1.0 / (4.0 * np.pi)
     launches = {"n": 0}
     # our kernels per step: pair table, 5 circulant-table kernels, zext, ik1, x2 (+ symmetrise N>1)
-    per_step = 9 if world == 1 else (10 if r1 > r0 else 8)
+    if world == 1:
+        nch = len(AS.pair_chunks(N, 16 if N >= 4096 else 1))
+        per_step = 7 + (2 * nch if nch > 1 else 2)   # tables (7) + ik1/x2 chunks
+    else:
+        per_step = 10 if r1 > r0 else 8
 
     def step():
         if world == 1:

@@ -215,6 +215,19 @@ int wq_x2_rows(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
                double w_ik1, int64_t tile_row0, int64_t tile_row1, double* Xrows, int64_t ldx,
                void* stream);
 
+/*
+ * Pair-range variants of the symmetric pipeline: upper-triangle tile pairs
+ * [pair0, pair1) in row-major triangular order (row bi holds nb - bi pairs,
+ * nb = ceil(N / WQ_FTILE)).  x2 pairs of a range read IK1 of the same range,
+ * so consecutive ranges can be pipelined on two streams.
+ */
+int wq_ik1_pairs(const wq_smooth_t* sm, int64_t pair0, int64_t pair1, double* X, int64_t ldx,
+                 int* flag, void* stream);
+int wq_x2_pairs_range(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+                      const double* Uext, const double* Zext, const double* s_w, double alpha,
+                      double w_ik1, int64_t pair0, int64_t pair1, double* X, int64_t ldx,
+                      void* stream);
+
 /* Self-test hooks (unit tests): fast 0.5*ln vs libdevice; one DMMA 8x8x4. */
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream);
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream);

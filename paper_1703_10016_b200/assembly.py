@@ -320,6 +320,8 @@ def _dev(disc: Discretization, key, make):
 
 def _to_dev(torch, arr, dtype=None):
     a = np.ascontiguousarray(arr)
+    if not a.flags.writeable:
+        a = a.copy()
     t = torch.from_numpy(a)
     if dtype is not None:
         t = t.to(dtype)
@@ -523,20 +525,66 @@ def _zext_table(disc):
     return Zext
 
 
-def _assemble_v2(disc: Discretization, X, alpha: float, w_ik1: float = 2.0, zext=None):
-    """Circulant v2 pipeline: tables -> ik1_sym (upper tiles) -> x2_pairs
-    (DMMA log part + fused symmetric epilogue), in place in X."""
+_AUX_STREAMS = {}
+
+
+def _aux_stream(torch):
+    dev = torch.cuda.current_device()
+    if dev not in _AUX_STREAMS:
+        _AUX_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    return _AUX_STREAMS[dev]
+
+
+def pair_chunks(N: int, chunks: int):
+    """Split the upper-triangle tile pairs (64-row tiles) into contiguous
+    ranges of about equal size."""
+    nb = -(-N // _lib.WQ_FTILE)
+    total = nb * (nb + 1) // 2
+    chunks = max(1, min(chunks, total))
+    edges = np.linspace(0, total, chunks + 1).round().astype(np.int64)
+    return [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:]) if b > a]
+
+
+def _assemble_v2(disc: Discretization, X, alpha: float, w_ik1: float = 2.0, zext=None,
+                 chunks: int = None):
+    """Circulant pipeline in place in X: tables -> ik1_sym (upper tiles of IK1)
+    -> x2_pairs (DMMA log part + fused symmetric epilogue).  The tile pairs are
+    split into chunks; IK1 chunks run on an auxiliary stream and the x2 chunk k
+    waits only for IK1 chunk k, so the FP64 (ik1) and FP64-tensor (x2) kernels
+    of neighbouring chunks overlap on the SMs."""
+    torch = _torch()
     lp, d = _logpart_dev(disc)
     sm = _smooth(disc)
-    st = _lib.stream_handle()
+    main = torch.cuda.current_stream()
+    st = _lib.stream_handle(main)
     Zext = _zext_table(disc) if zext is None else zext
     N = disc.space.dim
-    if w_ik1 != 0.0:
+    x2args = (N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1], lp.uext.shape[1],
+              lp.zstride, _lib.ptr(d["uext"]), _lib.ptr(Zext), _lib.ptr(d["s_w"]), alpha, w_ik1)
+    if w_ik1 == 0.0:
+        _lib.call("wq_x2_pairs", *x2args, _lib.ptr(X), X.stride(0), st)
+        return X
+    if chunks is None:
+        chunks = 16 if N >= 4096 else 1
+    ranges = pair_chunks(N, chunks)
+    if len(ranges) == 1:
         _lib.call("wq_ik1_sym", ctypes_ref(sm["struct"]), _lib.ptr(X), X.stride(0), sm["span64"],
                   _lib.ptr(sm["flag"]), st)
-    _lib.call("wq_x2_pairs", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
-              lp.uext.shape[1], lp.zstride, _lib.ptr(d["uext"]), _lib.ptr(Zext), _lib.ptr(d["s_w"]),
-              alpha, w_ik1, _lib.ptr(X), X.stride(0), st)
+        _lib.call("wq_x2_pairs", *x2args, _lib.ptr(X), X.stride(0), st)
+        return X
+    aux = _aux_stream(torch)
+    aux.wait_stream(main)
+    ast = _lib.stream_handle(aux)
+    events = []
+    for a, b in ranges:
+        _lib.call("wq_ik1_pairs", ctypes_ref(sm["struct"]), a, b, _lib.ptr(X), X.stride(0),
+                  _lib.ptr(sm["flag"]), ast)
+        ev = torch.cuda.Event()
+        ev.record(aux)
+        events.append(ev)
+    for (a, b), ev in zip(ranges, events):
+        main.wait_event(ev)
+        _lib.call("wq_x2_pairs_range", *x2args, a, b, _lib.ptr(X), X.stride(0), st)
     return X
 
 

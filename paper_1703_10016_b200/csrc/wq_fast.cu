@@ -163,9 +163,9 @@ __device__ __forceinline__ double k1_half_ln(double qx, double qy, int qa, doubl
 // Tile mapping: sym (tile_row0 < 0): upper-triangle pairs of an nb x nb tile grid;
 // rect: tile rows tile_row0 .. + gridDim.x / nbj, all nbj tile columns, output rows
 // offset by tile_row0 * FT (a rank's row block).
-__device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int& bi, int& bj) {
+__device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int64_t pair0, int& bi, int& bj) {
   if (tile_row0 < 0) {
-    tri_index(blockIdx.x, nb, bi, bj);
+    tri_index(pair0 + blockIdx.x, nb, bi, bj);
   } else {
     bi = tile_row0 + (int)(blockIdx.x / nb);
     bj = (int)(blockIdx.x % nb);
@@ -174,7 +174,8 @@ __device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int& bi, in
 
 template <int P, int MODE>
 __global__ void __launch_bounds__(IK1_THREADS, 2)
-ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, double* X, int64_t ldx, int* flag) {
+ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, int64_t ldx,
+               int* flag) {
   using C = Ik1Cfg<P, MODE>;
   constexpr int WG = C::WG, NQ = C::NQ, NQP = C::NQP, HJ = C::HJ;
   __shared__ double tab[3 * LOGTAB];
@@ -186,7 +187,7 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, double* X, int64_t ldx, in
 
   const int64_t N = sm.n_rows, nq = sm.nq;
   int bi, bj;
-  tile_of_block(nb, tile_row0, bi, bj);
+  tile_of_block(nb, tile_row0, pair0, bi, bj);
   const int64_t row_off = tile_row0 < 0 ? 0 : (int64_t)tile_row0 * FT;
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
@@ -387,7 +388,7 @@ template <int P>
 __global__ void __launch_bounds__(X2_THREADS, 2)
 x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
                 const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
-                int nb, int tile_row0) {
+                int nb, int tile_row0, int64_t pair0) {
   using C = X2Cfg<P>;
   extern __shared__ double smem[];
   double* Zsm = smem;                              // ZROWS * ZSTRIDE
@@ -397,7 +398,7 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   double* Bfr = Ssm + FT * 16;                     // 8 * KS/4 * 32 (fragment order)
   const int64_t n = N;
   int bi, bj;
-  tile_of_block(nb, tile_row0, bi, bj);
+  tile_of_block(nb, tile_row0, pair0, bi, bj);
   const bool rect = tile_row0 >= 0;
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
@@ -538,7 +539,7 @@ __global__ void selftest_dmma_kernel(const double* A, const double* B, double* C
 
 template <int P, int MODE>
 static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, cudaStream_t st,
-                      int tile_row0, int tile_row1) {
+                      int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
   using C = Ik1Cfg<P, MODE>;
   if (sm->wg != C::WG) {
     set_error("wq_ik1_sym: rule band width %lld != 2p+1", (long long)sm->wg);
@@ -547,26 +548,32 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
   const size_t smem = (size_t)FT * C::NQP * 8;
   cudaFuncSetAttribute(ik1_sym_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(sm->n_rows, FT);
-  const int64_t blocks = tile_row0 < 0 ? (int64_t)nb * (nb + 1) / 2
-                                       : (int64_t)(tile_row1 - tile_row0) * nb;
-  ik1_sym_kernel<P, MODE><<<(unsigned)blocks, IK1_THREADS, smem, st>>>(*sm, nb, tile_row0, X, ldx,
-                                                                        flag);
+  const int64_t all = (int64_t)nb * (nb + 1) / 2;
+  if (pair1 < 0 || pair1 > all) pair1 = all;
+  if (pair0 < 0) pair0 = 0;
+  const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
+  if (blocks <= 0) return WQ_OK;
+  ik1_sym_kernel<P, MODE><<<(unsigned)blocks, IK1_THREADS, smem, st>>>(*sm, nb, tile_row0, pair0, X,
+                                                                        ldx, flag);
   return check_launch("wq_ik1_sym");
 }
 
 template <int P>
 static int launch_x2(int64_t N, const double* Uext, const double* Zext, const double* s_w,
                      double alpha, double w_ik1, double* X, int64_t ldx, cudaStream_t st,
-                     int tile_row0, int tile_row1) {
+                     int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
   using C = X2Cfg<P>;
   const size_t smem = ((size_t)C::ZROWS * C::ZSTRIDE + (size_t)FT * PSTRIDE + (size_t)FT * TSTRIDE +
                        (size_t)FT * 16 + (size_t)8 * (C::KS / 4) * 32) * 8;
   cudaFuncSetAttribute(x2_pairs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(N, FT);
-  const int64_t blocks = tile_row0 < 0 ? (int64_t)nb * (nb + 1) / 2
-                                       : (int64_t)(tile_row1 - tile_row0) * nb;
+  const int64_t all = (int64_t)nb * (nb + 1) / 2;
+  if (pair1 < 0 || pair1 > all) pair1 = all;
+  if (pair0 < 0) pair0 = 0;
+  const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
+  if (blocks <= 0) return WQ_OK;
   x2_pairs_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
-                                                                 ldx, nb, tile_row0);
+                                                                 ldx, nb, tile_row0, pair0);
   return check_launch("wq_x2_pairs");
 }
 
@@ -577,7 +584,7 @@ using namespace wq;
 extern "C" {
 
 static int ik1_dispatch(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, void* stream,
-                        int tile_row0, int tile_row1) {
+                        int tile_row0, int tile_row1, int64_t pair0 = -1, int64_t pair1 = -1) {
   if (!sm || !X || !flag || sm->n_rows <= 0 || !sm->closed) {
     set_error("wq_ik1_sym: bad arguments (closed uniform meshes only)");
     return WQ_EINVAL;
@@ -593,8 +600,8 @@ static int ik1_dispatch(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag
   const bool tab = sm->k1_mode == WQ_K1_TABLE;
 #define WQ_IK1_CASE(PP)                                                                          \
   case PP:                                                                                       \
-    return tab ? launch_ik1<PP, WQ_K1_TABLE>(sm, X, ldx, flag, st, tile_row0, tile_row1)         \
-               : launch_ik1<PP, WQ_K1_CLOSED>(sm, X, ldx, flag, st, tile_row0, tile_row1);
+    return tab ? launch_ik1<PP, WQ_K1_TABLE>(sm, X, ldx, flag, st, tile_row0, tile_row1, pair0, pair1) \
+               : launch_ik1<PP, WQ_K1_CLOSED>(sm, X, ldx, flag, st, tile_row0, tile_row1, pair0, pair1);
   switch (p) {
     WQ_IK1_CASE(2)
     WQ_IK1_CASE(3)
@@ -611,6 +618,11 @@ int wq_ik1_sym(const wq_smooth_t* sm, double* X, int64_t ldx, int64_t max_span, 
                void* stream) {
   (void)max_span;
   return ik1_dispatch(sm, X, ldx, flag, stream, -1, -1);
+}
+
+int wq_ik1_pairs(const wq_smooth_t* sm, int64_t pair0, int64_t pair1, double* X, int64_t ldx,
+                 int* flag, void* stream) {
+  return ik1_dispatch(sm, X, ldx, flag, stream, -1, -1, pair0, pair1);
 }
 
 int wq_ik1_rows(const wq_smooth_t* sm, int64_t tile_row0, int64_t tile_row1, double* Xrows,
@@ -637,7 +649,7 @@ int wq_zext(int64_t n, int nA, int nApad, int zstride, const double* Zp, const d
 static int x2_dispatch(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
                        const double* Uext, const double* Zext, const double* s_w, double alpha,
                        double w_ik1, double* X, int64_t ldx, void* stream, int tile_row0,
-                       int tile_row1) {
+                       int tile_row1, int64_t pair0 = -1, int64_t pair1 = -1) {
   if (N <= 0 || !Uext || !Zext || !s_w || !X) {
     set_error("wq_x2_pairs: bad arguments");
     return WQ_EINVAL;
@@ -650,7 +662,8 @@ static int x2_dispatch(int64_t N, int p, int nA, int nApad, int ws, int ktot, in
       set_error("wq_x2_pairs: layout mismatch for p=%d", PP);                                  \
       return WQ_EINVAL;                                                                        \
     }                                                                                          \
-    return launch_x2<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, st, tile_row0, tile_row1);
+    return launch_x2<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, st, tile_row0, tile_row1, \
+                         pair0, pair1);
   switch (p) {
     WQ_X2_CASE(2)
     WQ_X2_CASE(3)
@@ -668,6 +681,14 @@ int wq_x2_pairs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstri
                 double w_ik1, double* X, int64_t ldx, void* stream) {
   return x2_dispatch(N, p, nA, nApad, ws, ktot, zstride, Uext, Zext, s_w, alpha, w_ik1, X, ldx,
                      stream, -1, -1);
+}
+
+int wq_x2_pairs_range(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+                      const double* Uext, const double* Zext, const double* s_w, double alpha,
+                      double w_ik1, int64_t pair0, int64_t pair1, double* X, int64_t ldx,
+                      void* stream) {
+  return x2_dispatch(N, p, nA, nApad, ws, ktot, zstride, Uext, Zext, s_w, alpha, w_ik1, X, ldx,
+                     stream, -1, -1, pair0, pair1);
 }
 
 int wq_x2_rows(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
