@@ -255,8 +255,7 @@ def main():
     launches = {"n": 0}
     # our kernels per step: pair table, 5 circulant-table kernels, zext, ik1, x2 (+ symmetrise N>1)
     if world == 1:
-        nch = len(AS.pair_chunks(N, 16 if N >= 4096 else 1))
-        per_step = 7 + (2 * nch if nch > 1 else 2)   # tables (7) + ik1/x2 chunks
+        per_step = 9   # pair table, 5 circulant-table kernels, zext, ik1_sym, x2_runs
     else:
         per_step = 10 if r1 > r0 else 8
 
@@ -311,19 +310,21 @@ def main():
         _lib.call("wq_ik1_sym", AS.ctypes_ref(sm["struct"]), _lib.ptr(X), N, sm["span64"],
                   _lib.ptr(sm["flag"]), _lib.stream_handle())
         ev[2].record()
-        _lib.call("wq_x2_pairs", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
+        runs = AS._diag_runs(disc)
+        _lib.call("wq_x2_runs", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
                   lp.uext.shape[1], lp.zstride, _lib.ptr(dd["uext"]), _lib.ptr(zext),
-                  _lib.ptr(dd["s_w"]), alpha, 2.0, _lib.ptr(X), N, _lib.stream_handle())
+                  _lib.ptr(dd["s_w"]), alpha, 2.0, _lib.ptr(runs), runs.shape[0], _lib.ptr(X), N,
+                  _lib.stream_handle())
         ev[3].record()
         torch.cuda.synchronize()
         split += [ev[k].elapsed_time(ev[k + 1]) for k in range(3)]
     split /= reps
-    names = ["tables", "ik1_sym", "x2_pairs"]
+    names = ["tables", "ik1_sym", "x2_runs"]
     fl = kernel_flops(disc)
     dom = "ik1" if split[1] >= split[2] else "ik2"
     dom_ms = split[1] if dom == "ik1" else split[2]
     achieved = fl[dom] / (dom_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2_pairs_kernel"}[dom],
+    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2_runs_kernel"}[dom],
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": "measured DFMA probe (wq_fp64_peak, burst); MEASURED_PEAKS.json has "
                                "no FP64 entry", "peak_datasheet": FP64_DATASHEET_TFLOPS,

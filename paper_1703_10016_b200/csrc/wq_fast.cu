@@ -123,6 +123,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ik1_sym_kernel: closed uniform nodes, rule i on nodes 2(i-p)+1 .. 2(i-p)+2p+1
 // ---------------------------------------------------------------------------
 
+// optional per-CTA phase timestamps (clock64), set by wq_debug_x2_timing (tools only)
+__device__ long long* g_x2_dbg = nullptr;
+__device__ __forceinline__ void x2_mark(int slot) {
+  long long* d = g_x2_dbg;
+  if (d != nullptr && threadIdx.x == 0) d[(int64_t)blockIdx.x * 8 + slot] = clock64();
+}
+
 constexpr int IK1_THREADS = 288;  // 9 warps: 2*nQ (q, half) items
 
 template <int P, int MODE>
@@ -219,7 +226,9 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
     }
     for (int k = tid; k < 3 * LOGTAB; k += IK1_THREADS) tab[k] = g_logtab[k];
   }
+  x2_mark(0);
   __syncthreads();
+  x2_mark(1);
 
   // ---- phase 1: item (q, half): sliding window over r = 2j .. 2j+WG-1 ----
   int bad = 0;
@@ -259,7 +268,9 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
     }
   }
   if (bad) atomicOr(flag, WQ_FLAG_R_NONPOSITIVE);
+  x2_mark(2);
   __syncthreads();
+  x2_mark(3);
 
   // ---- phase 2: item (j, quarter c): IK1[i][j], i in 16c .. 16c+15 ----
   if (tid < 4 * FT) {
@@ -282,6 +293,7 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
       for (int w = 0; w < WG - 2; ++w) win[w] = win[w + 2];
     }
   }
+  x2_mark(4);
 }
 
 // ---------------------------------------------------------------------------
@@ -315,6 +327,7 @@ struct X2Cfg {
 };
 
 constexpr int X2_THREADS = 256;
+
 constexpr int PSTRIDE = 76;  // Phi smem row stride (== 12 mod 16), >= SPAN and 56 + KS
 constexpr int TSTRIDE = 65;  // transpose staging stride
 
@@ -409,6 +422,7 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   // rect mode: X points at the rank's row block (row tile_row0 * FT)
   const int64_t row_off = rect ? (int64_t)tile_row0 * FT : 0;
 
+  x2_mark(0);
   // IK1(I,J) tile -> Tst (asynchronous)
   if (w_ik1 != 0.0) {
     for (int k = tid; k < FT * FT; k += X2_THREADS) {
@@ -455,9 +469,12 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
       Bfr[k] = (t >= 0 && t <= 2 * C::D) ? Ssm[(8 * jb + rr) * 16 + t] : 0.0;
     }
     __syncthreads();
+    x2_mark(1 + 3 * orient);
     phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin);
     __syncthreads();
+    x2_mark(2 + 3 * orient);
     s_contract<P>(Phs, Bfr, acc);
+    x2_mark(3 + 3 * orient);
     if (orient == 0) {
       // Tst[i][j] = w IK1 + X2(I,J); lane holds (i = 8warp + r, j = 8jb + 2c + e)
 #pragma unroll
@@ -502,6 +519,164 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
       const double v = (bi == bj && b > a) ? Phs[a * TSTRIDE + b] : Phs[b * TSTRIDE + a];
       X[(I0 + a) * ldx + J0 + b] = v;
     }
+  }
+  x2_mark(7);
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// ---------------------------------------------------------------------------
+// x2_runs_kernel: one CTA walks a run of tile pairs (I, I + delta) along one
+// diagonal.  Both skewed Z' windows depend only on delta, so they are staged
+// once per run and stay resident; the next pair's IK1 tile and S bands are
+// prefetched with cp.async while the current pair runs on the DMMA pipe.
+// Per pair: Phi (both orientations) + banded S contraction + fused epilogue,
+// identical arithmetic to x2_pairs_kernel (bit-identical results).
+// ---------------------------------------------------------------------------
+
+constexpr int RUN_SROW = 8;  // padded S band row (WS <= 8 doubles for p <= 3; 16 otherwise)
+
+template <int P>
+struct RunCfg {
+  static constexpr int SROW = (2 * P + 1) <= 8 ? 8 : 16;
+};
+
+template <int P>
+__global__ void __launch_bounds__(X2_THREADS, 1)
+x2_runs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
+               const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
+               int nb, const int* __restrict__ runs) {
+  using C = X2Cfg<P>;
+  constexpr int SROW = RunCfg<P>::SROW;
+  constexpr int ZW = C::ZROWS * C::ZSTRIDE;
+  constexpr int NKS = C::KS / 4;
+  extern __shared__ double smem[];
+  double* Zsm0 = smem;                          // orientation 0 window
+  double* Zsm1 = Zsm0 + ZW;                     // orientation 1 window
+  double* Phs = Zsm1 + ZW;                      // FT * PSTRIDE (also output staging)
+  double* Tbuf = Phs + FT * PSTRIDE;            // 2 x FT * TSTRIDE (w IK1 + X2(I,J))
+  double* Sbuf = Tbuf + 2 * FT * TSTRIDE;       // 2 bufs x 2 (I, J) x FT * SROW
+  double* Bfr = Sbuf + 4 * FT * SROW;           // 8 * NKS * 32
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int r = lane >> 2, c = lane & 3;
+  const int delta = runs[3 * blockIdx.x], i_start = runs[3 * blockIdx.x + 1];
+  const int len = runs[3 * blockIdx.x + 2];
+  const int64_t n = N;
+
+  x2_mark(0);
+  // resident skewed windows: orientation 0 (rows I, m over J) and 1 (rows J, m over I)
+  for (int o = 0; o < 2; ++o) {
+    const int64_t dd = (o == 0 ? 1 : -1) * (int64_t)delta * FT;
+    const int64_t gmin = dd - C::D - 63 + P - C::AMAX;
+    int64_t g0 = gmin % n;
+    if (g0 < 0) g0 += n;
+    double* Z = o == 0 ? Zsm0 : Zsm1;
+    for (int k = tid; k < C::ZROWS * (C::ZSTRIDE / 2); k += X2_THREADS) {
+      const int row = k / (C::ZSTRIDE / 2), cc = 2 * (k - row * (C::ZSTRIDE / 2));
+      int64_t g = g0 + row;
+      if (g >= n) g %= n;
+      cp_async16(Z + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
+    }
+  }
+  // Phs pad columns must be finite (they multiply zero B entries)
+  for (int k = tid; k < FT * (PSTRIDE - C::SPAN); k += X2_THREADS) {
+    const int row = k / (PSTRIDE - C::SPAN), col = C::SPAN + k % (PSTRIDE - C::SPAN);
+    Phs[row * PSTRIDE + col] = 0.0;
+  }
+
+  auto prefetch = [&](int t, int buf) {
+    const int bi = i_start + t, bj = bi + delta;
+    const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
+    const int ni = (int)min((int64_t)FT, N - I0), nj = (int)min((int64_t)FT, N - J0);
+    double* T = Tbuf + buf * FT * TSTRIDE;
+    if (w_ik1 != 0.0) {
+      for (int k = tid; k < FT * FT; k += X2_THREADS) {
+        const int a = k >> 6, b = k & 63;
+        const bool ok = a < ni && b < nj;
+        cp_async8_zfill(T + a * TSTRIDE + b, X + (ok ? (I0 + a) * ldx + J0 + b : 0), ok);
+      }
+    } else {
+      for (int k = tid; k < FT * FT; k += X2_THREADS) T[(k >> 6) * TSTRIDE + (k & 63)] = 0.0;
+    }
+    double* S = Sbuf + buf * 2 * FT * SROW;
+    for (int k = tid; k < 2 * FT * SROW; k += X2_THREADS) {
+      const int side = k / (FT * SROW), rem = k - side * FT * SROW;
+      const int row = rem / SROW, tt = rem - row * SROW;
+      const int64_t base = side == 0 ? I0 : J0;
+      const int nr = side == 0 ? ni : nj;
+      const bool ok = row < nr && tt < C::WS;
+      cp_async8_zfill(S + k, sw + (ok ? (base + row) * C::WS + tt : 0), ok);
+    }
+    cp_async_commit();
+  };
+
+  prefetch(0, 0);
+  for (int t = 0; t < len; ++t) {
+    const int buf = t & 1;
+    const int bi = i_start + t, bj = bi + delta;
+    const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
+    const int ni = (int)min((int64_t)FT, N - I0), nj = (int)min((int64_t)FT, N - J0);
+    double* Tst = Tbuf + buf * FT * TSTRIDE;
+    const double* S = Sbuf + buf * 2 * FT * SROW;
+    cp_async_wait_group0();
+    __syncthreads();
+    if (t + 1 < len) prefetch(t + 1, buf ^ 1);
+    x2_mark(1);
+    double acc[8][2];
+    for (int orient = 0; orient < 2; ++orient) {
+      const int64_t R0 = orient == 0 ? I0 : J0;
+      const int64_t C0 = orient == 0 ? J0 : I0;
+      const int64_t M0 = C0 - C::D;
+      const int64_t gmin = M0 - (R0 + 63) + P - C::AMAX;
+      // S band of the contraction side in fragment order (side 1 = J for orient 0)
+      const double* Sside = S + (orient == 0 ? 1 : 0) * FT * SROW;
+      for (int k = tid; k < 8 * NKS * 32; k += X2_THREADS) {
+        const int ln = k & 31, s = (k >> 5) % NKS, jb = (k >> 5) / NKS;
+        const int rr = ln >> 2, cc = ln & 3;
+        const int tt = 4 * s + cc - rr;
+        Bfr[k] = (tt >= 0 && tt <= 2 * C::D) ? Sside[(8 * jb + rr) * SROW + tt] : 0.0;
+      }
+      phi_block<P>(Uext, N, orient == 0 ? Zsm0 : Zsm1, Phs, M0, R0, gmin);
+      __syncthreads();
+      s_contract<P>(Phs, Bfr, acc);
+      if (orient == 0) {
+#pragma unroll
+        for (int jb = 0; jb < 8; ++jb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double* tp = Tst + (8 * warp + r) * TSTRIDE + 8 * jb + 2 * c + e;
+            *tp = fma(w_ik1, *tp, acc[jb][e]);
+          }
+        __syncthreads();  // Phs / Bfr reuse by orientation 1
+      }
+    }
+    __syncthreads();
+    x2_mark(2);
+#pragma unroll
+    for (int ib = 0; ib < 8; ++ib)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jl = 8 * warp + r, il = 8 * ib + 2 * c + e;
+        Phs[jl * TSTRIDE + il] = alpha * (Tst[il * TSTRIDE + jl] + acc[ib][e]);
+      }
+    __syncthreads();
+    if (bi != bj) {
+      for (int k = tid; k < FT * FT; k += X2_THREADS) {
+        const int a = k >> 6, b = k & 63;
+        if (a < nj && b < ni) X[(J0 + a) * ldx + I0 + b] = Phs[a * TSTRIDE + b];
+      }
+    }
+    for (int k = tid; k < FT * FT; k += X2_THREADS) {
+      const int a = k >> 6, b = k & 63;
+      if (a < ni && b < nj) {
+        const double v = (bi == bj && b > a) ? Phs[a * TSTRIDE + b] : Phs[b * TSTRIDE + a];
+        X[(I0 + a) * ldx + J0 + b] = v;
+      }
+    }
+    __syncthreads();  // Phs reuse by the next pair
+    x2_mark(3);
   }
 }
 
@@ -575,6 +750,25 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
   x2_pairs_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
                                                                  ldx, nb, tile_row0, pair0);
   return check_launch("wq_x2_pairs");
+}
+
+template <int P>
+static int launch_x2_runs(int64_t N, const double* Uext, const double* Zext, const double* s_w,
+                          double alpha, double w_ik1, double* X, int64_t ldx, const int* runs,
+                          int n_runs, cudaStream_t st) {
+  using C = X2Cfg<P>;
+  const size_t smem = ((size_t)2 * C::ZROWS * C::ZSTRIDE + (size_t)FT * PSTRIDE +
+                       (size_t)2 * FT * TSTRIDE + (size_t)4 * FT * RunCfg<P>::SROW +
+                       (size_t)8 * (C::KS / 4) * 32) * 8;
+  if (smem > 227 * 1024) {
+    set_error("wq_x2_runs: %zu B shared memory needed", smem);
+    return WQ_EUNSUPPORTED;
+  }
+  cudaFuncSetAttribute(x2_runs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nb = ceil_div(N, FT);
+  x2_runs_kernel<P><<<(unsigned)n_runs, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
+                                                                ldx, nb, runs);
+  return check_launch("wq_x2_runs");
 }
 
 }  // namespace wq
@@ -703,11 +897,49 @@ int wq_x2_rows(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
                      stream, (int)tile_row0, (int)tile_row1);
 }
 
+int wq_x2_runs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+               const double* Uext, const double* Zext, const double* s_w, double alpha,
+               double w_ik1, const int* runs, int64_t n_runs, double* X, int64_t ldx,
+               void* stream) {
+  if (N <= 0 || !Uext || !Zext || !s_w || !X || !runs || n_runs <= 0) {
+    set_error("wq_x2_runs: bad arguments");
+    return WQ_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+#define WQ_XR_CASE(PP)                                                                         \
+  case PP:                                                                                     \
+    if (nA != X2Cfg<PP>::NA || nApad != X2Cfg<PP>::NAPAD || ws != X2Cfg<PP>::WS ||              \
+        ktot != X2Cfg<PP>::KTOT || zstride != X2Cfg<PP>::ZSTRIDE) {                             \
+      set_error("wq_x2_runs: layout mismatch for p=%d", PP);                                   \
+      return WQ_EINVAL;                                                                        \
+    }                                                                                          \
+    return launch_x2_runs<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, runs, (int)n_runs, st);
+  switch (p) {
+    WQ_XR_CASE(2)
+    WQ_XR_CASE(3)
+    WQ_XR_CASE(4)
+    WQ_XR_CASE(5)
+    default:
+      set_error("wq_x2_runs: degree %d unsupported (2..5)", p);
+      return WQ_EUNSUPPORTED;
+  }
+#undef WQ_XR_CASE
+}
+
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream) {
   int rc = ensure_logtab();
   if (rc) return rc;
   selftest_log_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x, out_fast, out_ref);
   return check_launch("wq_selftest_log");
+}
+
+int wq_debug_x2_timing(long long* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(g_x2_dbg, &buf, sizeof(buf));
+  if (e != cudaSuccess) {
+    set_error("wq_debug_x2_timing: %s", cudaGetErrorString(e));
+    return WQ_ECUDA;
+  }
+  return WQ_OK;
 }
 
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream) {
