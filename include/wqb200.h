@@ -243,6 +243,10 @@ int wq_x2_runs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
 /* Self-test hooks (unit tests): fast 0.5*ln vs libdevice; one DMMA 8x8x4. */
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream);
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream);
+/* Throughput probe of 0.5*ln (tools): mode 0 table ln, 1 without I2F, 2 libdevice. */
+int wq_probe_log(int64_t iters, int blocks, int mode, double* out, void* stream);
+/* Tuning knob: column passes of the ik1 tile kernel (1: 2 CTAs/SM, 2: 3 CTAs/SM). */
+int wq_set_ik1_passes(int npass);
 /* Profiling hook: per-CTA phase clock64 stamps of wq_x2_pairs (8 per CTA) into
  * buf (device memory), or NULL to disable. */
 int wq_debug_x2_timing(long long* buf);

@@ -85,6 +85,8 @@ _SIGS = {
     "wq_selftest_log": [c_i64, c_vp, c_vp, c_vp, c_vp],
     "wq_selftest_dmma": [c_vp, c_vp, c_vp, c_vp],
     "wq_debug_x2_timing": [c_vp],
+    "wq_set_ik1_passes": [c_int],
+    "wq_probe_log": [c_i64, c_int, c_int, c_vp, c_vp],
 }
 
 EXPORTED = tuple(_SIGS)

@@ -542,6 +542,7 @@ def _diag_runs(disc):
 
 
 _AUX_STREAMS = {}
+_USE_RUNS = False   # x2_runs (1 CTA/SM, resident windows) measured slower than x2_pairs (2 CTA/SM)
 
 
 def _aux_stream(torch):
@@ -586,9 +587,12 @@ def _assemble_v2(disc: Discretization, X, alpha: float, w_ik1: float = 2.0, zext
     if len(ranges) == 1:
         _lib.call("wq_ik1_sym", ctypes_ref(sm["struct"]), _lib.ptr(X), X.stride(0), sm["span64"],
                   _lib.ptr(sm["flag"]), st)
-        runs = _diag_runs(disc)
-        _lib.call("wq_x2_runs", *x2args, _lib.ptr(runs), runs.shape[0], _lib.ptr(X), X.stride(0),
-                  st)
+        if _USE_RUNS and disc.space.degree <= 4:
+            runs = _diag_runs(disc)
+            _lib.call("wq_x2_runs", *x2args, _lib.ptr(runs), runs.shape[0], _lib.ptr(X),
+                      X.stride(0), st)
+        else:
+            _lib.call("wq_x2_pairs", *x2args, _lib.ptr(X), X.stride(0), st)
         return X
     aux = _aux_stream(torch)
     aux.wait_stream(main)

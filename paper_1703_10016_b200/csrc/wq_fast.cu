@@ -23,6 +23,8 @@
 // Both kernels are deterministic (no atomics on values).
 #include <math.h>
 
+#include <algorithm>
+
 #include "wq_common.cuh"
 
 namespace wq {
@@ -30,36 +32,48 @@ namespace wq {
 constexpr int FT = 64;  // tile rows/cols
 
 // ---------------------------------------------------------------------------
-// 0.5*ln(x), x > 0 normal: x = 2^e m, m in [1,2); c_j = 1/mid_j on 16
-// mantissa bins (a 16-double table spans the 32 banks once: lookups never
-// conflict); r = m c_j - 1 with one FMA rounding (|r| < 2^-6); ln(1+r) by its
-// degree-9 series (truncation < 1.1e-19); -ln c_j as a double-double.
+// 0.5*ln(x), x > 0 normal: x = 2^e m, m in [1,2); c_j = 1/mid_j on 1024
+// mantissa bins (24 KB table in shared memory: the kernel arguments of
+// neighbouring lanes are close, so lookups are mostly broadcasts); r = m c_j - 1
+// with one FMA rounding (|r| < 2^-11); ln(1+r) by its degree-5 series
+// (truncation < 3e-21); -ln c_j as a double-double.
 // ---------------------------------------------------------------------------
 
-constexpr int LOGTAB = 16;
-__device__ double g_logtab[3 * LOGTAB];  // c_j | 0.5*(-ln c_j)_hi | 0.5*(-ln c_j)_lo
+constexpr int LOGBITS = 10;              // 1024-entry table (read through L1)
+constexpr int LOGTAB = 1 << LOGBITS;
+__device__ double g_logtab[3 * LOGTAB];
+__device__ double g_logtab16[3 * 16];  // 16-entry table: spans the 32 banks once (smem)  // c_j | 0.5*(-ln c_j)_hi | 0.5*(-ln c_j)_lo
 static bool g_logtab_ready[64];
 
-int ensure_logtab() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && g_logtab_ready[dev]) return WQ_OK;
-  double tab[3 * LOGTAB];
-  for (int j = 0; j < LOGTAB; ++j) {
-    long double mid = 1.0L + (j + 0.5L) / LOGTAB;
+static int upload_logtab(const void* sym, int bins) {
+  double* tab = new double[3 * bins];
+  for (int j = 0; j < bins; ++j) {
+    long double mid = 1.0L + (j + 0.5L) / bins;
     double c = (double)(1.0L / mid);
     long double nl = -logl((long double)c);
     double hi = (double)nl;
     double lo = (double)(nl - (long double)hi);
     tab[j] = c;
-    tab[LOGTAB + j] = 0.5 * hi;
-    tab[2 * LOGTAB + j] = 0.5 * lo;
+    tab[bins + j] = 0.5 * hi;
+    tab[2 * bins + j] = 0.5 * lo;
   }
-  cudaError_t e = cudaMemcpyToSymbol(g_logtab, tab, sizeof(tab));
+  cudaError_t e = cudaMemcpyToSymbol(sym, tab, sizeof(double) * 3 * bins);
+  delete[] tab;
   if (e != cudaSuccess) {
     set_error("log table upload: %s", cudaGetErrorString(e));
     return WQ_ECUDA;
   }
+  return WQ_OK;
+}
+
+int ensure_logtab() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && g_logtab_ready[dev]) return WQ_OK;
+  int rc = upload_logtab(g_logtab, LOGTAB);
+  if (rc) return rc;
+  rc = upload_logtab(g_logtab16, 16);
+  if (rc) return rc;
   if (dev >= 0 && dev < 64) g_logtab_ready[dev] = true;
   return WQ_OK;
 }
@@ -72,11 +86,38 @@ __device__ __forceinline__ double half_ln(double x, const double* __restrict__ t
   const int hi = __double2hiint(x);
   const int lo = __double2loint(x);
   const int e = (hi >> 20) - 1023;
-  const int j = (hi >> 16) & (LOGTAB - 1);
+  const int j = (hi >> (20 - LOGBITS)) & (LOGTAB - 1);
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-  const double r = fma(m, tab[j], -1.0);
-  // 0.5 ln(1+r) = 0.5 r + r^2 q(r),  q = 0.5 * sum_{k=2..9} (-1)^(k+1) r^(k-2) / k
-  double q = fma(r, 0.5 / 9.0, -0.5 / 8.0);
+  const double r = fma(m, tab[j], -1.0);  // |r| < 2^-(LOGBITS+1)
+  // 0.5 ln(1+r) = 0.5 r + r^2 q(r), q = 0.5 sum_{k>=2} (-1)^(k+1) r^(k-2) / k, truncated
+  // at the degree where r^(deg+1)/(deg+1) < 1.2e-19 (degree 9 for 16 bins, 5 for 1024)
+  double q;
+  if constexpr (LOGBITS >= 10) {
+    q = fma(r, 0.5 / 5.0, -0.5 / 4.0);
+  } else {
+    q = fma(r, 0.5 / 9.0, -0.5 / 8.0);
+    q = fma(r, q, 0.5 / 7.0);
+    q = fma(r, q, -0.5 / 6.0);
+    q = fma(r, q, 0.5 / 5.0);
+    q = fma(r, q, -0.5 / 4.0);
+  }
+  q = fma(r, q, 0.5 / 3.0);
+  q = fma(r, q, -0.25);
+  const double r2 = r * r;
+  const double de = (double)e;
+  const double t_hi = fma(de, HLN2_A, tab[LOGTAB + j]);
+  const double t_lo = fma(de, HLN2_B, tab[2 * LOGTAB + j]);
+  return t_hi + fma(r, 0.5, fma(r2, q, t_lo));
+}
+
+__device__ __forceinline__ double half_ln16(double x, const double* __restrict__ tab) {
+  const int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  const int e = (hi >> 20) - 1023;
+  const int j = (hi >> 16) & 15;
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+  const double r = fma(m, tab[j], -1.0);  // |r| < 2^-5
+  double q = fma(r, 0.5 / 9.0, -0.5 / 8.0);  // degree 9: truncation < 1.1e-19
   q = fma(r, q, 0.5 / 7.0);
   q = fma(r, q, -0.5 / 6.0);
   q = fma(r, q, 0.5 / 5.0);
@@ -85,8 +126,8 @@ __device__ __forceinline__ double half_ln(double x, const double* __restrict__ t
   q = fma(r, q, -0.25);
   const double r2 = r * r;
   const double de = (double)e;
-  const double t_hi = fma(de, HLN2_A, tab[LOGTAB + j]);
-  const double t_lo = fma(de, HLN2_B, tab[2 * LOGTAB + j]);
+  const double t_hi = fma(de, HLN2_A, tab[16 + j]);
+  const double t_lo = fma(de, HLN2_B, tab[32 + j]);
   return t_hi + fma(r, 0.5, fma(r2, q, t_lo));
 }
 
@@ -140,7 +181,7 @@ struct Ik1Cfg {
   static constexpr int HJ = FT / 2;              // columns per half
 };
 
-template <int MODE>
+template <int MODE, int TAB>
 __device__ __forceinline__ double k1_half_ln(double qx, double qy, int qa, double qJ, double qs,
                                              double rx, double ry, int ra, double rs,
                                              const double* __restrict__ invp2, double period,
@@ -160,11 +201,12 @@ __device__ __forceinline__ double k1_half_ln(double qx, double qy, int qa, doubl
       R = d2 / (p * p);
     }
   }
-  if (!(R > 0.0) || !(R < 1e300)) {
-    bad = 1;
-    R = 1.0;
-  }
-  return half_ln(R, tab);
+  // R must be a positive finite normal double (geometry.py:246-247): test the
+  // high word on the integer pipe; a failing pair raises GeometryError on the
+  // host, so its (garbage) logarithm is never used
+  const unsigned rh = (unsigned)__double2hiint(R);
+  bad |= (rh - 0x00100000u) >= 0x7fe00000u;
+  return TAB == 0 ? half_ln16(R, tab) : half_ln(R, tab);
 }
 
 // Tile mapping: sym (tile_row0 < 0): upper-triangle pairs of an nb x nb tile grid;
@@ -179,13 +221,17 @@ __device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int64_t pai
   }
 }
 
-template <int P, int MODE>
+// NPASS column passes per tile: 1 pass keeps T1 for all 64 columns (68 KB smem,
+// 2 CTAs/SM); 2 passes halve T1 (3 CTAs/SM) at +8% halo kernel evaluations.
+// NOTE: one CTA per upper-triangle tile pair (non-persistent): measured faster
+// than persistent / multi-pass / multi-stream variants on B200.
+template <int P, int MODE, int TAB>
 __global__ void __launch_bounds__(IK1_THREADS, 2)
 ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, int64_t ldx,
                int* flag) {
   using C = Ik1Cfg<P, MODE>;
   constexpr int WG = C::WG, NQ = C::NQ, NQP = C::NQP, HJ = C::HJ;
-  __shared__ double tab[3 * LOGTAB];
+  __shared__ double stab[3 * 16];
   __shared__ double qx[NQ], qy[NQ], qJ[NQ], qs[NQ];
   __shared__ double rx[NQ], ry[NQ], rs[NQ];
   __shared__ int qa[NQ], ra[NQ];
@@ -224,7 +270,8 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
       Gi[ii][w] = ii < ni ? sm.g_w[(I0 + ii) * WG + w] : 0.0;
       Gj[ii][w] = ii < nj ? sm.g_w[(J0 + ii) * WG + w] : 0.0;
     }
-    for (int k = tid; k < 3 * LOGTAB; k += IK1_THREADS) tab[k] = g_logtab[k];
+    if (TAB == 0)
+      for (int k = tid; k < 3 * 16; k += IK1_THREADS) stab[k] = g_logtab16[k];
   }
   x2_mark(0);
   __syncthreads();
@@ -232,6 +279,7 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
 
   // ---- phase 1: item (q, half): sliding window over r = 2j .. 2j+WG-1 ----
   int bad = 0;
+  const double* __restrict__ tab = TAB == 0 ? stab : g_logtab;
   const double* __restrict__ invp2 = sm.invp2;
   const double period = sm.period;
   // (q, half) items: half 0 on threads 0..143, half 1 on 144..287, so a warp
@@ -248,16 +296,16 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
 #pragma unroll
     for (int w = 0; w < WG - 2; ++w) {
       const int r = 2 * jb + w;
-      win[w] = k1_half_ln<MODE>(mx, my, ma, mJ, ms, rx[r], ry[r], ra[r], rs[r], invp2, period, tab,
+      win[w] = k1_half_ln<MODE, TAB>(mx, my, ma, mJ, ms, rx[r], ry[r], ra[r], rs[r], invp2, period, tab,
                                 bad);
     }
 #pragma unroll 4
     for (int jj = 0; jj < HJ; ++jj) {
       const int j = jb + jj;
       const int r = 2 * j + WG - 2;
-      win[WG - 2] = k1_half_ln<MODE>(mx, my, ma, mJ, ms, rx[r], ry[r], ra[r], rs[r], invp2, period,
+      win[WG - 2] = k1_half_ln<MODE, TAB>(mx, my, ma, mJ, ms, rx[r], ry[r], ra[r], rs[r], invp2, period,
                                      tab, bad);
-      win[WG - 1] = k1_half_ln<MODE>(mx, my, ma, mJ, ms, rx[r + 1], ry[r + 1], ra[r + 1], rs[r + 1],
+      win[WG - 1] = k1_half_ln<MODE, TAB>(mx, my, ma, mJ, ms, rx[r + 1], ry[r + 1], ra[r + 1], rs[r + 1],
                                      invp2, period, tab, bad);
       double acc = 0.0;
 #pragma unroll
@@ -323,7 +371,7 @@ struct X2Cfg {
   static constexpr int NKB = (SPAN + 7 + 7) / 8;       // 8-row k blocks per row group
   static constexpr int ZROWS = 56 + 8 * NKB + AMAX;
   static constexpr int KS = ((8 + 2 * D) + 3) / 4 * 4;  // S-contraction K
-  static constexpr int PF = 6;                          // B-fragment prefetch depth
+  static constexpr int PF = 12;                         // B-fragment prefetch depth
 };
 
 constexpr int X2_THREADS = 256;
@@ -351,8 +399,9 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64
 #pragma unroll
   for (int s = 0; s < C::PF; ++s) bq[s] = valid ? __ldg(urow + 4 * s) : 0.0;
   const int zbase = (int)(kb0 + r + P - gmin);
-#pragma unroll
-  for (int s = 0; s < C::NSTEPS; ++s) {
+  // A fragments of k-step s: Zsm[(zbase + 8 kb - off(s)) * ZSTRIDE + col(s)], kb = 0..NKB-1;
+  // software-pipelined one k-step ahead so the DMMAs never wait on their LDS
+  auto zptr = [&](int s) -> const double* {
     int off, col;
     if (s < C::SZ) {
       off = (4 * s) / C::NAPAD;
@@ -361,11 +410,26 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64
       off = 4 * (s - C::SZ) + c;
       col = C::NAPAD;
     }
+    return Zsm + (zbase - off) * C::ZSTRIDE + col;
+  };
+  double afr[2][C::NKB];
+  {
+    const double* z = zptr(0);
+#pragma unroll
+    for (int kb = 0; kb < C::NKB; ++kb) afr[0][kb] = z[kb * 8 * C::ZSTRIDE];
+  }
+#pragma unroll
+  for (int s = 0; s < C::NSTEPS; ++s) {
+    const int cur = s & 1;
+    if (s + 1 < C::NSTEPS) {
+      const double* z = zptr(s + 1);
+#pragma unroll
+      for (int kb = 0; kb < C::NKB; ++kb) afr[cur ^ 1][kb] = z[kb * 8 * C::ZSTRIDE];
+    }
     const double b = bq[s % C::PF];
     if (s + C::PF < C::NSTEPS) bq[s % C::PF] = valid ? __ldg(urow + 4 * (s + C::PF)) : 0.0;
-    const double* z = Zsm + (zbase - off) * C::ZSTRIDE + col;
 #pragma unroll
-    for (int kb = 0; kb < C::NKB; ++kb) dmma(acc[kb][0], acc[kb][1], z[kb * 8 * C::ZSTRIDE], b);
+    for (int kb = 0; kb < C::NKB; ++kb) dmma(acc[kb][0], acc[kb][1], afr[cur][kb], b);
   }
 #pragma unroll
   for (int kb = 0; kb < C::NKB; ++kb) {
@@ -693,6 +757,48 @@ __global__ void zext_kernel(int64_t n, int nA, int nApad, int zstride, const dou
   Zext[e] = v;
 }
 
+// throughput probe of the kernel-evaluation building blocks (tools only):
+// mode 0: half_ln; 1: half_ln with the exponent conversion replaced by a DADD
+// trick; 2: libdevice 0.5*log; 3: full K1 (dist^2, x 1/p^2, half_ln)
+__device__ __forceinline__ double half_ln_noi2f(double x, const double* __restrict__ tab) {
+  const int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  const int j = (hi >> (20 - LOGBITS)) & (LOGTAB - 1);
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+  const double r = fma(m, tab[j], -1.0);
+  double q = fma(r, 0.5 / 5.0, -0.5 / 4.0);
+  q = fma(r, q, 0.5 / 3.0);
+  q = fma(r, q, -0.25);
+  const double r2 = r * r;
+  // exponent as a double: 2^52 + biased exponent, minus (2^52 + 1023)
+  const double de = __hiloint2double(0x43300000, (hi >> 20) & 0x7ff) - 4503599627371519.0;
+  const double t_hi = fma(de, HLN2_A, tab[LOGTAB + j]);
+  const double t_lo = fma(de, HLN2_B, tab[2 * LOGTAB + j]);
+  return t_hi + fma(r, 0.5, fma(r2, q, t_lo));
+}
+
+__global__ void __launch_bounds__(256) probe_log_kernel(int64_t iters, int mode, double* out) {
+  __shared__ double tab[3 * LOGTAB];
+  for (int k = threadIdx.x; k < 3 * LOGTAB; k += blockDim.x) tab[k] = g_logtab[k];
+  __syncthreads();
+  double x0 = 1.5 + threadIdx.x * 1e-3, x1 = x0 + 0.25, x2 = x0 + 0.5, x3 = x0 + 0.75;
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  for (int64_t it = 0; it < iters; ++it) {
+    if (mode == 0) {
+      a0 += half_ln(x0, tab); a1 += half_ln(x1, tab); a2 += half_ln(x2, tab); a3 += half_ln(x3, tab);
+    } else if (mode == 1) {
+      a0 += half_ln_noi2f(x0, tab); a1 += half_ln_noi2f(x1, tab);
+      a2 += half_ln_noi2f(x2, tab); a3 += half_ln_noi2f(x3, tab);
+    } else {
+      a0 += 0.5 * log(x0); a1 += 0.5 * log(x1); a2 += 0.5 * log(x2); a3 += 0.5 * log(x3);
+    }
+    x0 = fma(x0, 1.0000001, 1e-9); x1 = fma(x1, 1.0000001, 1e-9);
+    x2 = fma(x2, 1.0000001, 1e-9); x3 = fma(x3, 1.0000001, 1e-9);
+  }
+  double r = a0 + a1 + a2 + a3;
+  if (r == 12345.678) out[blockIdx.x] = r;
+}
+
 // self-test hooks: fast ln vs libdevice, and a DMMA fragment-layout check
 __global__ void selftest_log_kernel(int64_t n, const double* x, double* out_fast, double* out_ref) {
   __shared__ double tab[3 * LOGTAB];
@@ -712,6 +818,8 @@ __global__ void selftest_dmma_kernel(const double* A, const double* B, double* C
   C[r * 8 + 2 * c + 1] = c1;
 }
 
+static int g_ik1_tab = 0;  // 0: 16-entry smem ln table, 1: 1024-entry table via L1
+
 template <int P, int MODE>
 static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, cudaStream_t st,
                       int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
@@ -721,15 +829,15 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
     return WQ_EINVAL;
   }
   const size_t smem = (size_t)FT * C::NQP * 8;
-  cudaFuncSetAttribute(ik1_sym_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = g_ik1_tab == 1 ? ik1_sym_kernel<P, MODE, 1> : ik1_sym_kernel<P, MODE, 0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(sm->n_rows, FT);
   const int64_t all = (int64_t)nb * (nb + 1) / 2;
   if (pair1 < 0 || pair1 > all) pair1 = all;
   if (pair0 < 0) pair0 = 0;
   const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
   if (blocks <= 0) return WQ_OK;
-  ik1_sym_kernel<P, MODE><<<(unsigned)blocks, IK1_THREADS, smem, st>>>(*sm, nb, tile_row0, pair0, X,
-                                                                        ldx, flag);
+  kern<<<(unsigned)blocks, IK1_THREADS, smem, st>>>(*sm, nb, tile_row0, pair0, X, ldx, flag);
   return check_launch("wq_ik1_sym");
 }
 
@@ -931,6 +1039,22 @@ int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_re
   if (rc) return rc;
   selftest_log_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x, out_fast, out_ref);
   return check_launch("wq_selftest_log");
+}
+
+int wq_probe_log(int64_t iters, int blocks, int mode, double* out, void* stream) {
+  int rc = ensure_logtab();
+  if (rc) return rc;
+  probe_log_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, mode, out);
+  return check_launch("wq_probe_log");
+}
+
+int wq_set_ik1_passes(int mode) {
+  if (mode < 1 || mode > 2) {
+    set_error("wq_set_ik1_passes: 1 (16-entry smem ln table) or 2 (1024-entry, L1)");
+    return WQ_EINVAL;
+  }
+  g_ik1_tab = mode - 1;
+  return WQ_OK;
 }
 
 int wq_debug_x2_timing(long long* buf) {
