@@ -225,23 +225,40 @@ __device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int64_t pai
 // 2 CTAs/SM); 2 passes halve T1 (3 CTAs/SM) at +8% halo kernel evaluations.
 // NOTE: one CTA per upper-triangle tile pair (non-persistent): measured faster
 // than persistent / multi-pass / multi-stream variants on B200.
-template <int P, int MODE, int TAB>
-__global__ void __launch_bounds__(IK1_THREADS, 2)
-ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, int64_t ldx,
-               int* flag) {
+// shared-memory footprint (doubles) of one ik1 tile: T1 | node data | rules | table | indices
+template <int P, int MODE>
+struct Ik1Smem {
   using C = Ik1Cfg<P, MODE>;
+  static constexpr int T1 = FT * C::NQP;
+  static constexpr int NODE = 7 * C::NQ;
+  static constexpr int RULE = 2 * FT * C::WG;
+  static constexpr int TAB = 3 * 16;
+  static constexpr int IDX = C::NQ + 1;  // 2 NQ ints
+  static constexpr int TOTAL = T1 + NODE + RULE + TAB + IDX;
+};
+
+// One upper-triangle 64 x 64 tile (bi, bj) of IK1 (all 288 threads of the CTA).
+template <int P, int MODE, int TAB>
+__device__ __forceinline__ void ik1_tile(const wq_smooth_t& sm, int bi, int bj, int64_t row_off,
+                                         double* X, int64_t ldx, int& bad, double* dsm) {
+  using C = Ik1Cfg<P, MODE>;
+  using L = Ik1Smem<P, MODE>;
   constexpr int WG = C::WG, NQ = C::NQ, NQP = C::NQP, HJ = C::HJ;
-  __shared__ double stab[3 * 16];
-  __shared__ double qx[NQ], qy[NQ], qJ[NQ], qs[NQ];
-  __shared__ double rx[NQ], ry[NQ], rs[NQ];
-  __shared__ int qa[NQ], ra[NQ];
-  __shared__ double Gi[FT][WG], Gj[FT][WG];
-  extern __shared__ double T1[];  // [FT][NQP]: T1[j][q] = sum_w K1[q][2j + w] G_j[w]
+  double* T1 = dsm;                        // [FT][NQP]: T1[j][q] = sum_w K1[q][2j + w] G_j[w]
+  double* qx = T1 + L::T1;
+  double* qy = qx + NQ;
+  double* qJ = qy + NQ;
+  double* qs = qJ + NQ;
+  double* rx = qs + NQ;
+  double* ry = rx + NQ;
+  double* rs = ry + NQ;
+  double (*Gi)[WG] = reinterpret_cast<double (*)[WG]>(rs + NQ);
+  double (*Gj)[WG] = reinterpret_cast<double (*)[WG]>(rs + NQ + FT * WG);
+  double* stab = rs + NQ + 2 * FT * WG;
+  int* qa = reinterpret_cast<int*>(stab + 3 * 16);
+  int* ra = qa + NQ;
 
   const int64_t N = sm.n_rows, nq = sm.nq;
-  int bi, bj;
-  tile_of_block(nb, tile_row0, pair0, bi, bj);
-  const int64_t row_off = tile_row0 < 0 ? 0 : (int64_t)tile_row0 * FT;
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
   const int nj = (int)min((int64_t)FT, N - J0);
@@ -278,7 +295,6 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
   x2_mark(1);
 
   // ---- phase 1: item (q, half): sliding window over r = 2j .. 2j+WG-1 ----
-  int bad = 0;
   const double* __restrict__ tab = TAB == 0 ? stab : g_logtab;
   const double* __restrict__ invp2 = sm.invp2;
   const double period = sm.period;
@@ -315,7 +331,6 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
       for (int w = 0; w < WG - 2; ++w) win[w] = win[w + 2];
     }
   }
-  if (bad) atomicOr(flag, WQ_FLAG_R_NONPOSITIVE);
   x2_mark(2);
   __syncthreads();
   x2_mark(3);
@@ -342,6 +357,19 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
     }
   }
   x2_mark(4);
+}
+
+template <int P, int MODE, int TAB>
+__global__ void __launch_bounds__(IK1_THREADS, 2)
+ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, int64_t ldx,
+               int* flag) {
+  extern __shared__ double dsm[];
+  int bi, bj;
+  tile_of_block(nb, tile_row0, pair0, bi, bj);
+  const int64_t row_off = tile_row0 < 0 ? 0 : (int64_t)tile_row0 * FT;
+  int bad = 0;
+  ik1_tile<P, MODE, TAB>(sm, bi, bj, row_off, X, ldx, bad, dsm);
+  if (bad) atomicOr(flag, WQ_FLAG_R_NONPOSITIVE);
 }
 
 // ---------------------------------------------------------------------------
@@ -384,9 +412,9 @@ constexpr int TSTRIDE = 65;  // transpose staging stride
 template <int P>
 __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64_t N,
                                           const double* Zsm, double* Phs, int64_t M0, int64_t R0,
-                                          int64_t gmin) {
+                                          int64_t gmin, int warp) {
   using C = X2Cfg<P>;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
   const int64_t kb0 = M0 - (R0 + 8 * warp + 7);
   double acc[C::NKB][2];
@@ -444,9 +472,10 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64
 
 // out[a][b] = sum_m Phs[a][m] S_b[m - b + d]; warp owns row block `warp`
 template <int P>
-__device__ __forceinline__ void s_contract(const double* Phs, const double* Bfr, double (&acc)[8][2]) {
+__device__ __forceinline__ void s_contract(const double* Phs, const double* Bfr, double (&acc)[8][2],
+                                           int warp) {
   using C = X2Cfg<P>;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
 #pragma unroll
   for (int jb = 0; jb < 8; ++jb) acc[jb][0] = acc[jb][1] = 0.0;
@@ -462,42 +491,54 @@ __device__ __forceinline__ void s_contract(const double* Phs, const double* Bfr,
 }
 
 template <int P>
-__global__ void __launch_bounds__(X2_THREADS, 2)
-x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
-                const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
-                int nb, int tile_row0, int64_t pair0) {
+struct X2Smem {
   using C = X2Cfg<P>;
-  extern __shared__ double smem[];
+  static constexpr int TOTAL = C::ZROWS * C::ZSTRIDE + FT * PSTRIDE + FT * TSTRIDE + FT * 16 +
+                               8 * (C::KS / 4) * 32;
+};
+
+// One tile pair (bi, bj) of the log part + fused symmetric epilogue (or, rect,
+// the unsymmetrised row block).  Threads >= X2_THREADS of a larger CTA only
+// take part in the barriers.
+template <int P>
+__device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Uext,
+                                        const double* __restrict__ Zext,
+                                        const double* __restrict__ sw, double alpha, double w_ik1,
+                                        double* X, int64_t ldx, int bi, int bj, bool rect,
+                                        int64_t row_off, double* smem) {
+  using C = X2Cfg<P>;
   double* Zsm = smem;                              // ZROWS * ZSTRIDE
   double* Phs = Zsm + C::ZROWS * C::ZSTRIDE;       // FT * PSTRIDE (also output staging)
   double* Tst = Phs + FT * PSTRIDE;                // FT * TSTRIDE: w IK1 + X2(I,J)
   double* Ssm = Tst + FT * TSTRIDE;                // FT * 16 (S band rows)
   double* Bfr = Ssm + FT * 16;                     // 8 * KS/4 * 32 (fragment order)
   const int64_t n = N;
-  int bi, bj;
-  tile_of_block(nb, tile_row0, pair0, bi, bj);
-  const bool rect = tile_row0 >= 0;
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
   const int nj = (int)min((int64_t)FT, N - J0);
   const int tid = threadIdx.x;
+  const bool act = tid < X2_THREADS;
   const int lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, c = lane & 3;
-  // rect mode: X points at the rank's row block (row tile_row0 * FT)
-  const int64_t row_off = rect ? (int64_t)tile_row0 * FT : 0;
 
   x2_mark(0);
   // IK1(I,J) tile -> Tst (asynchronous)
-  if (w_ik1 != 0.0) {
-    for (int k = tid; k < FT * FT; k += X2_THREADS) {
-      const int a = k >> 6, b = k & 63;
-      if (a < ni && b < nj) cp_async8(Tst + a * TSTRIDE + b, X + (I0 - row_off + a) * ldx + J0 + b);
-      else Tst[a * TSTRIDE + b] = 0.0;
+  if (act) {
+    if (w_ik1 != 0.0) {
+      for (int k = tid; k < FT * FT; k += X2_THREADS) {
+        const int a = k >> 6, b = k & 63;
+        if (a < ni && b < nj) cp_async8(Tst + a * TSTRIDE + b, X + (I0 - row_off + a) * ldx + J0 + b);
+        else Tst[a * TSTRIDE + b] = 0.0;
+      }
+    } else {
+      for (int k = tid; k < FT * TSTRIDE; k += X2_THREADS) Tst[k] = 0.0;
     }
-  } else {
-    for (int k = tid; k < FT * TSTRIDE; k += X2_THREADS) Tst[k] = 0.0;
+    // Phs pad columns must be finite (they multiply zero B entries)
+    for (int k = tid; k < FT * (PSTRIDE - C::SPAN); k += X2_THREADS) {
+      const int row = k / (PSTRIDE - C::SPAN), col = C::SPAN + k % (PSTRIDE - C::SPAN);
+      Phs[row * PSTRIDE + col] = 0.0;
+    }
   }
-  for (int k = tid; k < FT * PSTRIDE; k += X2_THREADS) Phs[k] = 0.0;
 
   double acc[8][2];
   const int norient = rect ? 1 : 2;
@@ -512,13 +553,13 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
     if (orient == 1) __syncthreads();  // Zsm / Phs / Ssm reuse
     int64_t g0 = gmin % n;
     if (g0 < 0) g0 += n;
-    for (int k = tid; k < C::ZROWS * (C::ZSTRIDE / 2); k += X2_THREADS) {
+    for (int k = tid; act && k < C::ZROWS * (C::ZSTRIDE / 2); k += X2_THREADS) {
       const int row = k / (C::ZSTRIDE / 2), cc = 2 * (k - row * (C::ZSTRIDE / 2));
       int64_t g = g0 + row;
       if (g >= n) g %= n;
       cp_async16(Zsm + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
     }
-    for (int k = tid; k < FT * 16; k += X2_THREADS) {
+    for (int k = tid; act && k < FT * 16; k += X2_THREADS) {
       const int row = k >> 4, t = k & 15;
       const bool ok = row < nc && t < C::WS;
       cp_async8_zfill(Ssm + k, sw + (ok ? (C0 + row) * C::WS + t : 0), ok);
@@ -526,7 +567,7 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
     cp_async_wait_all();
     __syncthreads();
     // S band in B-fragment order: Bfr[jb][s][lane] = S_{8jb+r}[4s+c-r] (0 outside the band)
-    for (int k = tid; k < 8 * (C::KS / 4) * 32; k += X2_THREADS) {
+    for (int k = tid; act && k < 8 * (C::KS / 4) * 32; k += X2_THREADS) {
       const int ln = k & 31, s = (k >> 5) % (C::KS / 4), jb = (k >> 5) / (C::KS / 4);
       const int rr = ln >> 2, cc = ln & 3;
       const int t = 4 * s + cc - rr;
@@ -534,12 +575,12 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
     }
     __syncthreads();
     x2_mark(1 + 3 * orient);
-    phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin);
+    if (act) phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
     __syncthreads();
     x2_mark(2 + 3 * orient);
-    s_contract<P>(Phs, Bfr, acc);
+    if (act) s_contract<P>(Phs, Bfr, acc, warp);
     x2_mark(3 + 3 * orient);
-    if (orient == 0) {
+    if (orient == 0 && act) {
       // Tst[i][j] = w IK1 + X2(I,J); lane holds (i = 8warp + r, j = 8jb + 2c + e)
 #pragma unroll
       for (int jb = 0; jb < 8; ++jb)
@@ -553,7 +594,7 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   __syncthreads();
   if (rect) {
     // unsymmetrised row block: X(I,J) = alpha (w IK1 + X2(I,J))
-    for (int k = tid; k < FT * FT; k += X2_THREADS) {
+    for (int k = tid; act && k < FT * FT; k += X2_THREADS) {
       const int a = k >> 6, b = k & 63;
       if (a < ni && b < nj) X[(I0 - row_off + a) * ldx + J0 + b] = alpha * Tst[a * TSTRIDE + b];
     }
@@ -561,23 +602,25 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   }
   // acc holds X2(J,I): lane (j = 8warp + r, i = 8ib + 2c + e).  A(J,I)[j][i] =
   // alpha (Tst[i][j] + X2(J,I)[j][i]) -> staged in Phs as [j][i]
+  if (act) {
 #pragma unroll
-  for (int ib = 0; ib < 8; ++ib)
+    for (int ib = 0; ib < 8; ++ib)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int jl = 8 * warp + r, il = 8 * ib + 2 * c + e;
-      Phs[jl * TSTRIDE + il] = alpha * (Tst[il * TSTRIDE + jl] + acc[ib][e]);
-    }
+      for (int e = 0; e < 2; ++e) {
+        const int jl = 8 * warp + r, il = 8 * ib + 2 * c + e;
+        Phs[jl * TSTRIDE + il] = alpha * (Tst[il * TSTRIDE + jl] + acc[ib][e]);
+      }
+  }
   __syncthreads();
   // A(J,I) rows (coalesced), A(I,J) = transpose; diagonal tiles mirror their
   // lower-staged triangle so A is exactly symmetric
   if (bi != bj) {
-    for (int k = tid; k < FT * FT; k += X2_THREADS) {
+    for (int k = tid; act && k < FT * FT; k += X2_THREADS) {
       const int a = k >> 6, b = k & 63;  // row J0 + a, col I0 + b
       if (a < nj && b < ni) X[(J0 + a) * ldx + I0 + b] = Phs[a * TSTRIDE + b];
     }
   }
-  for (int k = tid; k < FT * FT; k += X2_THREADS) {
+  for (int k = tid; act && k < FT * FT; k += X2_THREADS) {
     const int a = k >> 6, b = k & 63;  // row I0 + a, col J0 + b
     if (a < ni && b < nj) {
       const double v = (bi == bj && b > a) ? Phs[a * TSTRIDE + b] : Phs[b * TSTRIDE + a];
@@ -589,6 +632,81 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int P>
+__global__ void __launch_bounds__(X2_THREADS, 2)
+x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
+                const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
+                int nb, int tile_row0, int64_t pair0) {
+  extern __shared__ double smem[];
+  int bi, bj;
+  tile_of_block(nb, tile_row0, pair0, bi, bj);
+  const bool rect = tile_row0 >= 0;
+  x2_tile<P>(N, Uext, Zext, sw, alpha, w_ik1, X, ldx, bi, bj, rect,
+             rect ? (int64_t)tile_row0 * FT : 0, smem);
+}
+
+// ---------------------------------------------------------------------------
+// Fused single launch: IK1 tiles (FP64 DFMA, issue-bound) and log-part tile
+// pairs (DMMA) as interleaved CTAs, so both kinds share every SM.  Block
+// order: ik1(0..L-1), then x2(k) / ik1(k+L) alternating, then the remaining
+// x2.  x2(k) needs IK1(k): it waits for ready[k] == epoch, published by
+// ik1(k) after its tile is globally visible.  CTAs are dispatched in blockIdx
+// order and ik1 CTAs never wait, so every awaited producer is already
+// resident or finished; the wait is bounded (trap instead of a hang).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int P, int MODE, int TAB>
+__global__ void __launch_bounds__(IK1_THREADS, 2)
+fused_pairs_kernel(wq_smooth_t sm, const double* __restrict__ Uext,
+                   const double* __restrict__ Zext, const double* __restrict__ sw, double alpha,
+                   double w_ik1, double* X, int64_t ldx, int nb, int64_t n_pairs, int64_t lead,
+                   int* ready, int epoch, int* flag) {
+  extern __shared__ double dsm[];
+  const int64_t b = blockIdx.x;
+  const int64_t m = n_pairs - lead;
+  bool is_x2;
+  int64_t t;
+  if (b < lead) {
+    is_x2 = false;
+    t = b;
+  } else {
+    const int64_t j = b - lead;
+    if (j < 2 * m) {
+      is_x2 = (j & 1) == 0;
+      t = is_x2 ? (j >> 1) : lead + (j >> 1);
+    } else {
+      is_x2 = true;
+      t = m + (j - 2 * m);
+    }
+  }
+  int bi, bj;
+  tri_index(t, nb, bi, bj);
+  if (!is_x2) {
+    int bad = 0;
+    ik1_tile<P, MODE, TAB>(sm, bi, bj, 0, X, ldx, bad, dsm);
+    if (bad) atomicOr(flag, WQ_FLAG_R_NONPOSITIVE);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicExch(ready + t, epoch);
+  } else {
+    if (threadIdx.x == 0) {
+      unsigned spins = 0;
+      while (ld_acquire(ready + t) != epoch) {
+        __nanosleep(200);
+        if (++spins > (1u << 27)) __trap();
+      }
+    }
+    __syncthreads();
+    x2_tile<P>(sm.n_rows, Uext, Zext, sw, alpha, w_ik1, X, ldx, bi, bj, false, 0, dsm);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // x2_runs_kernel: one CTA walks a run of tile pairs (I, I + delta) along one
@@ -702,9 +820,9 @@ x2_runs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restr
         const int tt = 4 * s + cc - rr;
         Bfr[k] = (tt >= 0 && tt <= 2 * C::D) ? Sside[(8 * jb + rr) * SROW + tt] : 0.0;
       }
-      phi_block<P>(Uext, N, orient == 0 ? Zsm0 : Zsm1, Phs, M0, R0, gmin);
+      phi_block<P>(Uext, N, orient == 0 ? Zsm0 : Zsm1, Phs, M0, R0, gmin, warp);
       __syncthreads();
-      s_contract<P>(Phs, Bfr, acc);
+      s_contract<P>(Phs, Bfr, acc, warp);
       if (orient == 0) {
 #pragma unroll
         for (int jb = 0; jb < 8; ++jb)
@@ -742,6 +860,207 @@ x2_runs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restr
     __syncthreads();  // Phs reuse by the next pair
     x2_mark(3);
   }
+}
+
+// ---------------------------------------------------------------------------
+// x2_runs16_kernel: diagonal runs with 16 warps -- warps 0-7 compute orientation
+// 0 (X2(I,J)) while warps 8-15 compute orientation 1 (X2(J,I)) of the same tile
+// pair, each with its own Phi buffer, so the DMMA pipe sees 16 warps; both
+// skewed windows stay resident for the whole run; the next pair's IK1 tile and
+// S bands are prefetched with cp.async.  Bit-identical to x2_pairs_kernel.
+// p <= 3 (223 KB shared memory, 1 CTA/SM).
+// ---------------------------------------------------------------------------
+
+constexpr int X2R16_THREADS = 512;
+
+template <int P>
+__global__ void __launch_bounds__(X2R16_THREADS, 1)
+x2_runs16_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
+                 const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
+                 int nb, const int* __restrict__ runs) {
+  using C = X2Cfg<P>;
+  constexpr int SROW = 8;
+  static_assert(C::WS <= SROW, "x2_runs16 needs 2p+1 <= 8");
+  constexpr int ZW = C::ZROWS * C::ZSTRIDE;
+  constexpr int NKS = C::KS / 4;
+  constexpr int BFR = 8 * NKS * 32;
+  extern __shared__ double smem[];
+  double* Zsm = smem;                            // 2 x ZW: orientation windows
+  double* Phs = Zsm + 2 * ZW;                    // 2 x FT * PSTRIDE
+  double* Tbuf = Phs + 2 * FT * PSTRIDE;         // 2 x FT * TSTRIDE (IK1 tile -> w IK1 + X2(I,J))
+  double* Sbuf = Tbuf + 2 * FT * TSTRIDE;        // 2 bufs x 2 sides (I, J) x FT * SROW
+  double* Bfr = Sbuf + 4 * FT * SROW;            // 2 x BFR
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, gw = tid >> 5;
+  const int grp = gw >> 3, warp = gw & 7;        // orientation group, warp within group
+  const int gtid = tid & 255;
+  const int r = lane >> 2, c = lane & 3;
+  const int delta = runs[3 * blockIdx.x], i_start = runs[3 * blockIdx.x + 1];
+  const int len = runs[3 * blockIdx.x + 2];
+  const int64_t n = N;
+
+  x2_mark(0);
+  {
+    // resident windows (group g stages window g)
+    const int64_t dd = (grp == 0 ? 1 : -1) * (int64_t)delta * FT;
+    const int64_t gmin = dd - C::D - 63 + P - C::AMAX;
+    int64_t g0 = gmin % n;
+    if (g0 < 0) g0 += n;
+    double* Z = Zsm + grp * ZW;
+    for (int k = gtid; k < C::ZROWS * (C::ZSTRIDE / 2); k += 256) {
+      const int row = k / (C::ZSTRIDE / 2), cc = 2 * (k - row * (C::ZSTRIDE / 2));
+      int64_t g = g0 + row;
+      if (g >= n) g %= n;
+      cp_async16(Z + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
+    }
+    double* Pg = Phs + grp * FT * PSTRIDE;
+    for (int k = gtid; k < FT * (PSTRIDE - C::SPAN); k += 256) {
+      const int row = k / (PSTRIDE - C::SPAN), col = C::SPAN + k % (PSTRIDE - C::SPAN);
+      Pg[row * PSTRIDE + col] = 0.0;
+    }
+  }
+
+  auto prefetch = [&](int t, int buf) {
+    const int pbi = i_start + t, pbj = pbi + delta;
+    const int64_t pI0 = (int64_t)pbi * FT, pJ0 = (int64_t)pbj * FT;
+    const int pni = (int)min((int64_t)FT, N - pI0), pnj = (int)min((int64_t)FT, N - pJ0);
+    double* T = Tbuf + buf * FT * TSTRIDE;
+    if (w_ik1 != 0.0) {
+      for (int k = tid; k < FT * FT; k += X2R16_THREADS) {
+        const int a = k >> 6, b = k & 63;
+        const bool ok = a < pni && b < pnj;
+        cp_async8_zfill(T + a * TSTRIDE + b, X + (ok ? (pI0 + a) * ldx + pJ0 + b : 0), ok);
+      }
+    } else {
+      for (int k = tid; k < FT * FT; k += X2R16_THREADS) T[(k >> 6) * TSTRIDE + (k & 63)] = 0.0;
+    }
+    double* S = Sbuf + buf * 2 * FT * SROW;
+    for (int k = tid; k < 2 * FT * SROW; k += X2R16_THREADS) {
+      const int side = k / (FT * SROW), rem = k - side * FT * SROW;
+      const int row = rem / SROW, tt = rem - row * SROW;
+      const int64_t base = side == 0 ? pI0 : pJ0;
+      const int nr = side == 0 ? pni : pnj;
+      const bool ok = row < nr && tt < C::WS;
+      cp_async8_zfill(S + k, sw + (ok ? (base + row) * C::WS + tt : 0), ok);
+    }
+    cp_async_commit();
+  };
+
+  prefetch(0, 0);
+  for (int t = 0; t < len; ++t) {
+    const int buf = t & 1;
+    const int bi = i_start + t, bj = bi + delta;
+    const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
+    const int ni = (int)min((int64_t)FT, N - I0), nj = (int)min((int64_t)FT, N - J0);
+    double* Tst = Tbuf + buf * FT * TSTRIDE;
+    const double* S = Sbuf + buf * 2 * FT * SROW;
+    cp_async_wait_group0();
+    __syncthreads();
+    if (t + 1 < len) prefetch(t + 1, buf ^ 1);
+    // this group's orientation: 0 -> rows I, m over J, S_J ; 1 -> rows J, m over I, S_I
+    const int64_t R0 = grp == 0 ? I0 : J0;
+    const int64_t C0 = grp == 0 ? J0 : I0;
+    const int64_t M0 = C0 - C::D;
+    const int64_t gmin = M0 - (R0 + 63) + P - C::AMAX;
+    double* Pg = Phs + grp * FT * PSTRIDE;
+    double* Bg = Bfr + grp * BFR;
+    {
+      const double* Sside = S + (grp == 0 ? 1 : 0) * FT * SROW;
+      for (int k = gtid; k < BFR; k += 256) {
+        const int ln = k & 31, s = (k >> 5) % NKS, jb = (k >> 5) / NKS;
+        const int rr = ln >> 2, cc = ln & 3;
+        const int tt = 4 * s + cc - rr;
+        Bg[k] = (tt >= 0 && tt <= 2 * C::D) ? Sside[(8 * jb + rr) * SROW + tt] : 0.0;
+      }
+    }
+    x2_mark(1);
+    phi_block<P>(Uext, N, Zsm + grp * ZW, Pg, M0, R0, gmin, warp);
+    __syncthreads();
+    double acc[8][2];
+    s_contract<P>(Pg, Bg, acc, warp);
+    if (grp == 0) {
+      // Tst[i][j] = w IK1 + X2(I,J); lane holds (i = 8warp + r, j = 8jb + 2c + e)
+#pragma unroll
+      for (int jb = 0; jb < 8; ++jb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double* tp = Tst + (8 * warp + r) * TSTRIDE + 8 * jb + 2 * c + e;
+          *tp = fma(w_ik1, *tp, acc[jb][e]);
+        }
+    }
+    __syncthreads();
+    x2_mark(2);
+    double* Ost = Phs + FT * PSTRIDE;  // group 1's Phi buffer, free now: output staging [j][i]
+    if (grp == 1) {
+#pragma unroll
+      for (int ib = 0; ib < 8; ++ib)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int jl = 8 * warp + r, il = 8 * ib + 2 * c + e;
+          Ost[jl * TSTRIDE + il] = alpha * (Tst[il * TSTRIDE + jl] + acc[ib][e]);
+        }
+    }
+    __syncthreads();
+    if (bi != bj) {
+      for (int k = tid; k < FT * FT; k += X2R16_THREADS) {
+        const int a = k >> 6, b = k & 63;
+        if (a < nj && b < ni) X[(J0 + a) * ldx + I0 + b] = Ost[a * TSTRIDE + b];
+      }
+    }
+    for (int k = tid; k < FT * FT; k += X2R16_THREADS) {
+      const int a = k >> 6, b = k & 63;
+      if (a < ni && b < nj) {
+        const double v = (bi == bj && b > a) ? Ost[a * TSTRIDE + b] : Ost[b * TSTRIDE + a];
+        X[(I0 + a) * ldx + J0 + b] = v;
+      }
+    }
+    x2_mark(3);
+  }
+}
+
+// DMMA loop probe (tools only): the phi_block inner loop on resident shared
+// data, mode 0 as in the kernel, 1 without the B (Uext) loads, 2 without the
+// A (Zsm) loads, 3 neither.
+template <int MODE>
+__global__ void __launch_bounds__(256) probe_phi_kernel(int iters, const double* __restrict__ Uext,
+                                                        double* out) {
+  using C = X2Cfg<3>;
+  __shared__ double Zsm[C::ZROWS * C::ZSTRIDE];
+  for (int k = threadIdx.x; k < C::ZROWS * C::ZSTRIDE; k += 256) Zsm[k] = 1e-3 * (k % 17);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = lane >> 2, c = lane & 3;
+  double acc[C::NKB][2];
+#pragma unroll
+  for (int kb = 0; kb < C::NKB; ++kb) acc[kb][0] = acc[kb][1] = 0.0;
+  const double* urow = Uext + (blockIdx.x * 64 + 8 * warp + r) * C::KTOT + c;
+  const int zbase = 56 - 8 * warp + r + C::AMAX;
+  for (int it = 0; it < iters; ++it) {
+    double bq[C::PF];
+#pragma unroll
+    for (int s = 0; s < C::PF; ++s) bq[s] = MODE & 1 ? 0.5 : __ldg(urow + 4 * s);
+#pragma unroll
+    for (int s = 0; s < C::NSTEPS; ++s) {
+      int off, col;
+      if (s < C::SZ) {
+        off = (4 * s) / C::NAPAD;
+        col = (4 * s - off * C::NAPAD) + c;
+      } else {
+        off = 4 * (s - C::SZ) + c;
+        col = C::NAPAD;
+      }
+      const double b = bq[s % C::PF];
+      if (!(MODE & 1) && s + C::PF < C::NSTEPS) bq[s % C::PF] = __ldg(urow + 4 * (s + C::PF));
+      const double* z = Zsm + (zbase - off) * C::ZSTRIDE + col;
+#pragma unroll
+      for (int kb = 0; kb < C::NKB; ++kb)
+        dmma(acc[kb][0], acc[kb][1], MODE & 2 ? 0.25 : z[kb * 8 * C::ZSTRIDE], b);
+    }
+  }
+  double t = 0;
+#pragma unroll
+  for (int kb = 0; kb < C::NKB; ++kb) t += acc[kb][0] + acc[kb][1];
+  if (t == 12345.678) out[blockIdx.x] = t;
 }
 
 // Zext[g] = [Z'[g][0..nA-1], 0.., ff[g] at column nApad, 0..]
@@ -828,7 +1147,7 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
     set_error("wq_ik1_sym: rule band width %lld != 2p+1", (long long)sm->wg);
     return WQ_EINVAL;
   }
-  const size_t smem = (size_t)FT * C::NQP * 8;
+  const size_t smem = (size_t)Ik1Smem<P, MODE>::TOTAL * 8;
   auto kern = g_ik1_tab == 1 ? ik1_sym_kernel<P, MODE, 1> : ik1_sym_kernel<P, MODE, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(sm->n_rows, FT);
@@ -861,6 +1180,25 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
 }
 
 template <int P>
+static int launch_x2_runs16(int64_t N, const double* Uext, const double* Zext, const double* s_w,
+                            double alpha, double w_ik1, double* X, int64_t ldx, const int* runs,
+                            int n_runs, cudaStream_t st) {
+  using C = X2Cfg<P>;
+  const size_t smem = ((size_t)2 * C::ZROWS * C::ZSTRIDE + (size_t)2 * FT * PSTRIDE +
+                       (size_t)2 * FT * TSTRIDE + (size_t)4 * FT * 8 +
+                       (size_t)2 * 8 * (C::KS / 4) * 32) * 8;
+  if (smem > 227 * 1024) {
+    set_error("wq_x2_runs: %zu B shared memory needed", smem);
+    return WQ_EUNSUPPORTED;
+  }
+  cudaFuncSetAttribute(x2_runs16_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nb = ceil_div(N, FT);
+  x2_runs16_kernel<P><<<(unsigned)n_runs, X2R16_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha,
+                                                                      w_ik1, X, ldx, nb, runs);
+  return check_launch("wq_x2_runs");
+}
+
+template <int P>
 static int launch_x2_runs(int64_t N, const double* Uext, const double* Zext, const double* s_w,
                           double alpha, double w_ik1, double* X, int64_t ldx, const int* runs,
                           int n_runs, cudaStream_t st) {
@@ -877,6 +1215,41 @@ static int launch_x2_runs(int64_t N, const double* Uext, const double* Zext, con
   x2_runs_kernel<P><<<(unsigned)n_runs, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
                                                                 ldx, nb, runs);
   return check_launch("wq_x2_runs");
+}
+
+template <int P, int MODE>
+static int launch_fused(const wq_smooth_t* sm, const double* Uext, const double* Zext,
+                        const double* s_w, double alpha, double w_ik1, double* X, int64_t ldx,
+                        int* ready, int epoch, int64_t lead, int* flag, cudaStream_t st) {
+  using C = Ik1Cfg<P, MODE>;
+  if (sm->wg != C::WG) {
+    set_error("wq_assemble_fused: rule band width %lld != 2p+1", (long long)sm->wg);
+    return WQ_EINVAL;
+  }
+  const size_t smem = (size_t)std::max(Ik1Smem<P, MODE>::TOTAL, X2Smem<P>::TOTAL) * 8;
+  if (smem > 227 * 1024) {
+    set_error("wq_assemble_fused: %zu B shared memory needed", smem);
+    return WQ_EUNSUPPORTED;
+  }
+  auto kern = g_ik1_tab == 1 ? fused_pairs_kernel<P, MODE, 1> : fused_pairs_kernel<P, MODE, 0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nb = ceil_div(sm->n_rows, FT);
+  const int64_t pairs = (int64_t)nb * (nb + 1) / 2;
+  if (lead < 1) lead = 1;
+  if (lead > pairs) lead = pairs;
+  kern<<<(unsigned)(2 * pairs), IK1_THREADS, smem, st>>>(*sm, Uext, Zext, s_w, alpha, w_ik1, X, ldx,
+                                                          nb, pairs, lead, ready, epoch, flag);
+  return check_launch("wq_assemble_fused");
+}
+
+template <int P>
+static int launch_x2_runs_any(int64_t N, const double* Uext, const double* Zext, const double* s_w,
+                              double alpha, double w_ik1, double* X, int64_t ldx, const int* runs,
+                              int n_runs, cudaStream_t st) {
+  if constexpr (P <= 3)
+    return launch_x2_runs16<P>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, runs, n_runs, st);
+  else
+    return launch_x2_runs<P>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, runs, n_runs, st);
 }
 
 }  // namespace wq
@@ -1021,7 +1394,7 @@ int wq_x2_runs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
       set_error("wq_x2_runs: layout mismatch for p=%d", PP);                                   \
       return WQ_EINVAL;                                                                        \
     }                                                                                          \
-    return launch_x2_runs<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, runs, (int)n_runs, st);
+    return launch_x2_runs_any<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, runs, (int)n_runs, st);
   switch (p) {
     WQ_XR_CASE(2)
     WQ_XR_CASE(3)
@@ -1032,6 +1405,45 @@ int wq_x2_runs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
       return WQ_EUNSUPPORTED;
   }
 #undef WQ_XR_CASE
+}
+
+int wq_assemble_fused(const wq_smooth_t* sm, int p, int nA, int nApad, int ws, int ktot, int zstride,
+                      const double* Uext, const double* Zext, const double* s_w, double alpha,
+                      double w_ik1, int* ready, int epoch, int64_t lead, double* X, int64_t ldx,
+                      int* flag, void* stream) {
+  if (!sm || !Uext || !Zext || !s_w || !ready || !X || !flag || !sm->closed || epoch == 0) {
+    set_error("wq_assemble_fused: bad arguments");
+    return WQ_EINVAL;
+  }
+  if (sm->k1_mode == WQ_K1_TABLE && !sm->invp2) {
+    set_error("wq_assemble_fused: table mode without invp2");
+    return WQ_EINVAL;
+  }
+  int rc = ensure_logtab();
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool tab = sm->k1_mode == WQ_K1_TABLE;
+#define WQ_FU_CASE(PP)                                                                         \
+  case PP:                                                                                     \
+    if (nA != X2Cfg<PP>::NA || nApad != X2Cfg<PP>::NAPAD || ws != X2Cfg<PP>::WS ||              \
+        ktot != X2Cfg<PP>::KTOT || zstride != X2Cfg<PP>::ZSTRIDE) {                             \
+      set_error("wq_assemble_fused: layout mismatch for p=%d", PP);                            \
+      return WQ_EINVAL;                                                                        \
+    }                                                                                          \
+    return tab ? launch_fused<PP, WQ_K1_TABLE>(sm, Uext, Zext, s_w, alpha, w_ik1, X, ldx, ready,\
+                                               epoch, lead, flag, st)                          \
+               : launch_fused<PP, WQ_K1_CLOSED>(sm, Uext, Zext, s_w, alpha, w_ik1, X, ldx,      \
+                                                ready, epoch, lead, flag, st);
+  switch (p) {
+    WQ_FU_CASE(2)
+    WQ_FU_CASE(3)
+    WQ_FU_CASE(4)
+    WQ_FU_CASE(5)
+    default:
+      set_error("wq_assemble_fused: degree %d unsupported (2..5)", p);
+      return WQ_EUNSUPPORTED;
+  }
+#undef WQ_FU_CASE
 }
 
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream) {
@@ -1046,6 +1458,17 @@ int wq_probe_log(int64_t iters, int blocks, int mode, double* out, void* stream)
   if (rc) return rc;
   probe_log_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, mode, out);
   return check_launch("wq_probe_log");
+}
+
+int wq_probe_phi(int iters, int blocks, int mode, const double* Uext, double* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (mode) {
+    case 0: probe_phi_kernel<0><<<blocks, 256, 0, st>>>(iters, Uext, out); break;
+    case 1: probe_phi_kernel<1><<<blocks, 256, 0, st>>>(iters, Uext, out); break;
+    case 2: probe_phi_kernel<2><<<blocks, 256, 0, st>>>(iters, Uext, out); break;
+    default: probe_phi_kernel<3><<<blocks, 256, 0, st>>>(iters, Uext, out); break;
+  }
+  return check_launch("wq_probe_phi");
 }
 
 int wq_set_ik1_passes(int mode) {
