@@ -58,6 +58,28 @@ def workload(n_el: int, p: int = 3, geometry: str = "ellipse"):
     return curve, space
 
 
+def workload_c5(n_el: int = 16384, p: int = 4, seed: int = 0, zone: float = 0.2,
+                ratio: float = 0.9, growth_elems: int = 60):
+    """BASELINE.json configs[4] ("C5"): open slit [-1, 1] x {0}, degree p,
+    n_el elements graded geometrically (ratio per element) toward both ends
+    over the outer `zone` fraction, growth from the end element capped at the
+    interior width after `growth_elems` elements (the literal 0.9^3277
+    underflows); every interior knot doubled with probability
+    0.25 from np.random.default_rng(seed).random(n_el - 1) (4030 doubles ->
+    N = 20418 at the defaults)."""
+    import paper_1703_10016_b200 as W
+    ng = int(round(zone * n_el))
+    w = np.ones(n_el)
+    fac = ratio ** np.maximum(0, growth_elems - np.arange(ng))
+    w[:ng] = fac
+    w[n_el - ng:] = fac[::-1]
+    bp = np.concatenate([[0.0], np.cumsum(w)])
+    bp = -1.0 + 2.0 * bp / bp[-1]
+    mult = np.where(np.random.default_rng(seed).random(n_el - 1) < 0.25, 2, 1)
+    curve = W.load_curve({"degree": 1, "knots": [-1, -1, 1, 1], "control_points": [[-1, 0], [1, 0]]})
+    return curve, W.make_open_basis(p, bp, mult)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -255,7 +277,7 @@ def main():
     launches = {"n": 0}
     # our kernels per step: pair table, 5 circulant-table kernels, zext, ik1, x2 (+ symmetrise N>1)
     if world == 1:
-        per_step = 9   # pair table, 5 circulant-table kernels, zext, ik1_sym, x2_runs
+        per_step = 9   # pair table, 5 circulant-table kernels, zext, ik1_sym, x2_pairs
     else:
         per_step = 10 if r1 > r0 else 8
 
@@ -310,21 +332,20 @@ def main():
         _lib.call("wq_ik1_sym", AS.ctypes_ref(sm["struct"]), _lib.ptr(X), N, sm["span64"],
                   _lib.ptr(sm["flag"]), _lib.stream_handle())
         ev[2].record()
-        runs = AS._diag_runs(disc)
-        _lib.call("wq_x2_runs", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
+        # the production log-part kernel (assembly._assemble_v2)
+        _lib.call("wq_x2_pairs", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
                   lp.uext.shape[1], lp.zstride, _lib.ptr(dd["uext"]), _lib.ptr(zext),
-                  _lib.ptr(dd["s_w"]), alpha, 2.0, _lib.ptr(runs), runs.shape[0], _lib.ptr(X), N,
-                  _lib.stream_handle())
+                  _lib.ptr(dd["s_w"]), alpha, 2.0, _lib.ptr(X), N, _lib.stream_handle())
         ev[3].record()
         torch.cuda.synchronize()
         split += [ev[k].elapsed_time(ev[k + 1]) for k in range(3)]
     split /= reps
-    names = ["tables", "ik1_sym", "x2_runs"]
+    names = ["tables", "ik1_sym", "x2_pairs"]
     fl = kernel_flops(disc)
     dom = "ik1" if split[1] >= split[2] else "ik2"
     dom_ms = split[1] if dom == "ik1" else split[2]
     achieved = fl[dom] / (dom_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2_runs_kernel"}[dom],
+    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2_pairs_kernel"}[dom],
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": "measured DFMA probe (wq_fp64_peak, burst); MEASURED_PEAKS.json has "
                                "no FP64 entry", "peak_datasheet": FP64_DATASHEET_TFLOPS,

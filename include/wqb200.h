@@ -57,6 +57,9 @@ typedef struct {
   const double* invp2;     /* (nq) 1/p^2 per index gap (WQ_K1_TABLE) or NULL   */
   const int64_t* g_start;  /* (N) unwrapped first node of row i (monotone)    */
   const double* g_w;       /* (N, wg) G[i, (g_start[i]+w) mod nq]             */
+  int64_t near_k;          /* 0, or K: distinct node pairs closer than eps_diag */
+  const double* near_j2;   /* (nq, K): J(mid)^2 of pair (q, q+k+1 mod nq), 0 if */
+                           /* not near (geometry.py:237-245); else NULL       */
 } wq_smooth_t;
 
 /* Version / identification. */
@@ -282,6 +285,52 @@ int wq_b1w(const wq_smooth_t* sm, const double* g, double* b, void* stream);
  */
 int wq_b2_inner(int64_t M, const double* fx, const double* fy, const double* tx, const double* ty,
                 const double* wg, const double* kdiag, double* inner, void* stream);
+
+/*
+ * Non-uniform meshes (graded / any multiplicity; BASELINE config 5).  Replaces
+ * the gap-indexed pair table of _pair_log_moments (quadrature.py:441-504), which
+ * raises ConstructionError on graded meshes (quadrature.py:489-491), and the
+ * Theta / D accumulation of _log_part (assembly.py:206-236), per element pair.
+ *
+ * wq_gen_pair_blocks: for outer elements e in [e0, e1) and every inner element f,
+ *   wt[e-e0][f] = U_e^T M(e,f) V_f  ((pu+1) x (db+1); pu must equal db)
+ *   wd[e-e0][f] = V_e^T M(e,f) V_f  ((db+1) x (db+1))
+ * elh/elm: element widths / midpoints; u (n_el, da+1, pu+1), v (n_el, db+1, db+1)
+ * centred-monomial coefficients (splines.py:427-472; u times the fitted J);
+ * near (touching / overlapping) pairs of e are f = near_lo[e] + k (mod n_el),
+ * k < near_cnt[e] <= max_near: equal widths take near_unit (3 x (da+1) x (db+1),
+ * the closed-form unit entries at dl = -1, 0, 1, quadrature.py:372-410, 458),
+ * unequal widths a Duffy split with the packed rules `touch` (x16 w16 x30 w30
+ * Gauss-Legendre on (0,1), xl14 wl14 for the weight -ln x); all other pairs
+ * tensor Gauss (quadrature.py:413-438) with gx/gw = orders 30 | 16 | 12 on
+ * (-1/2, 1/2), concatenated (30 below two larger widths of separation, 16
+ * below eight, 12 beyond).
+ * ca/cb: centred monomial integrals c_a (da+1), c_b (db+1).  closed != 0 adds the
+ * periodic gap term (quadrature.py:459-468) for period `period`.
+ */
+int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int pu, int closed,
+                       double period, const double* elh, const double* elm, const double* u,
+                       const double* v, const int64_t* near_lo, const int64_t* near_cnt,
+                       int max_near, const double* near_unit, const double* touch,
+                       const double* gx, const double* gw, const double* ca,
+                       const double* cb, double* wt, double* wd, void* stream);
+
+/* thetaT[l][i] += sum over the chunk's incidences of i (u_el/u_loc, width wu) and
+ * all incidences of l (v_el/v_loc, width wv, -1 padded) of wt blocks; i in [i0, i1). */
+int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1,
+                        int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
+                        const int64_t* u_el, const int64_t* u_loc, const int64_t* v_el,
+                        const int64_t* v_loc, const double* wt, double* thetaT, void* stream);
+
+/* D[l][m] += chunk contributions of wd blocks, l in [l0, l1), all m. */
+int wq_gen_gather_d(int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1, int64_t l0, int64_t l1,
+                    int wv, int nB, const int64_t* v_el, const int64_t* v_loc, const double* wd,
+                    double* D, void* stream);
+
+/* wq_band_solve_cols with the last bw (<= 8) solution values kept in registers:
+ * one load and one store per row and column (large n). */
+int wq_band_solve_win(int64_t n, int64_t bw, const double* Lb, double* X, int64_t ncols,
+                      int64_t ldx, void* stream);
 
 #ifdef __cplusplus
 }

@@ -808,3 +808,164 @@ class CirculantRows:
 
     def a_rows(self, rows):
         return -self.m_rows(rows) / TWO_PI
+
+
+# --------------------------------------------------------------------------
+# generalised log part for NON-UNIFORM meshes (config 5)
+# --------------------------------------------------------------------------
+#
+# The reference raises ConstructionError on graded meshes (quadrature.py:
+# 489-491).  Its uniform recipe (unit-width gap stack + analytic h-scaling,
+# quadrature.py:441-504) generalises per element pair: scale by h_e so the pair
+# becomes (1, rho = h_f/h_e, delta/h_e), evaluate there (closed form
+# quadrature.py:372-410 when the elements are near, 30x30 Gauss
+# quadrature.py:413-438 otherwise) and apply
+#   M = h_e^(a+b+2) (M'(1, rho, delta') + ln h_e c_a(1) c_b(rho)).
+# "Near" means touching or overlapping: separation <= 1e-9 of the larger
+# width.  On uniform meshes that is the reference's |gap| <= 1 split
+# (quadrature.py:458) and reproduces its numbers (tests/test_oracle.py).  The
+# SURVEY 8(c) suggestion of a wider closed-form zone was measured and rejected:
+# at any positive separation the closed form loses 1e-3..1e+11 of the
+# natural slot scale h_e^(a+1) h_f^(b+1) in the high slots (a >= 8), while
+# 30x30 Gauss is at 1e-15 from separation 0.05 max(h_e, h_f) on
+# (tests/test_oracle.py::test_gauss_beats_closed_form_off_contact).
+
+NEAR_TOUCH = 1e-9
+
+
+def centred_integrals_scaled(n, rho):
+    """C_b(rho) = int_{-rho/2}^{rho/2} v^b dv for b = 0..n (rho broadcast)."""
+    rho = np.asarray(rho, float)
+    pb = np.arange(n + 1)
+    c = centred_integrals(n)
+    return rho[..., None] ** (pb + 1.0) * c
+
+
+def pair_moments_touching(da, db, rho, dl, n=24, levels=16, ratio=0.15):
+    """Unit-normalised moments of a touching pair of unequal widths (outer
+    width 1, inner rho, offset dl = +-(1 + rho)/2): tensor Gauss on panels
+    graded geometrically toward the shared corner, where ln|v - u - dl| is
+    singular.  The reference's closed form (quadrature.py:372-410) is only
+    used by it at rho = 1; measured here it loses 1e-2..1e+2 of the natural
+    slot scale in the high slots at rho != 1, this rule ~1e-15
+    (tests/test_oracle.py)."""
+    x, w = np.polynomial.legendre.leggauss(n)
+
+    def panels(a, b, toward_a):
+        L = b - a
+        inner = [a + L * ratio ** k for k in range(levels, 0, -1)] if toward_a else \
+            [b - L * ratio ** k for k in range(1, levels + 1)]
+        e = np.array(sorted([a, b] + inner))
+        lo, hi = e[:-1, None], e[1:, None]
+        return (0.5 * (lo + hi) + 0.5 * (hi - lo) * x).ravel(), (0.5 * (hi - lo) * w).ravel()
+
+    U, WU = panels(-0.5, 0.5, dl > 0)
+    V, WV = panels(-rho / 2, rho / 2, dl < 0)
+    K = np.log(np.abs(V[None, :] - U[:, None] - dl))
+    A = WU[:, None] * U[:, None] ** np.arange(da + 1)[None, :]
+    B = WV[:, None] * V[:, None] ** np.arange(db + 1)[None, :]
+    return A.T @ K @ B
+
+
+def pair_moments_general(da, db, he, hf, delta, closed_period=None):
+    """Centred double log moments for arbitrary element pairs; he, hf, delta
+    arrays (delta = outer centre minus inner centre, as quadrature.py:382)."""
+    he, hf, delta = np.broadcast_arrays(np.asarray(he, float), np.asarray(hf, float),
+                                        np.asarray(delta, float))
+    rho = hf / he
+    dl = delta / he
+    # equal widths at (rounding-)integer offsets: use the exact integer, as the
+    # reference's gap-indexed unit table does (quadrature.py:452-456)
+    same = np.abs(rho - 1.0) < 1e-12
+    rho = np.where(same, 1.0, rho)
+    snap = same & (np.abs(dl - np.rint(dl)) < 1e-9)
+    dl = np.where(snap, np.rint(dl), dl)
+    sep = np.abs(delta) - 0.5 * (he + hf)
+    near = sep <= NEAR_TOUCH * np.maximum(he, hf)
+    m = np.empty((len(he), da + 1, db + 1))
+    ones = np.ones(len(he))
+    # equal widths: the reference's closed form (its |gap| <= 1 entries);
+    # touching pairs of unequal widths: graded composite Gauss (see below)
+    cl = near & (rho == 1.0)
+    if cl.any():
+        m[cl] = pair_moments_closed(da, db, ones[cl], rho[cl], dl[cl])
+    for k in np.flatnonzero(near & (rho != 1.0)):   # exact contact geometry (rounding aside)
+        m[k] = pair_moments_touching(da, db, rho[k], np.copysign(0.5 * (1.0 + rho[k]), dl[k]))
+    if (~near).any():
+        m[~near] = pair_moments_gauss(da, db, ones[~near], rho[~near], dl[~near])
+    if closed_period is not None:
+        m += pair_moments_gauss(da, db, ones, rho, dl, period=(closed_period / he)[:, None, None],
+                                gap_only=True)
+    pa, pb = np.arange(da + 1), np.arange(db + 1)
+    scale = he[:, None, None] ** (2.0 + pa[None, :, None] + pb[None, None, :])
+    ca = centred_integrals(da)
+    cb = centred_integrals_scaled(db, rho)  # (n, db+1)
+    return scale * (m + np.log(he)[:, None, None] * ca[None, :, None] * cb[:, None, :])
+
+
+def ik2_ingredients_general(disc: Disc, chunk=None):
+    """Theta, D and the fit C as in ik2_ingredients, with per-pair moments
+    (any element widths); outer elements processed in chunks."""
+    fine, space = disc.fine, disc.space
+    d = fine.degree
+    bigd = space.degree + JFIT_DEGREE
+    els = fine.elements
+    ne = len(els)
+    h = els[:, 1] - els[:, 0]
+    mid = 0.5 * (els[:, 0] + els[:, 1])
+    u, ucols = local_coeffs(space, els, bigd, scale_fn=disc.curve.speed)
+    v, vcols = local_coeffs(fine, els, d)
+    theta = np.zeros(space.dim * fine.dim)
+    dmm = np.zeros(fine.dim * fine.dim)
+    chunk = chunk or max(1, 4096 // ne)
+    for e0 in range(0, ne, chunk):
+        es = np.arange(e0, min(ne, e0 + chunk))
+        e_idx = np.repeat(es, ne)
+        f_idx = np.tile(np.arange(ne), len(es))
+        delta = mid[e_idx] - mid[f_idx]
+        if fine.closed:
+            L = fine.length
+            delta = delta - L * np.round(delta / L)
+        m2 = pair_moments_general(bigd, d, h[e_idx], h[f_idx], delta,
+                                  closed_period=fine.length if fine.closed else None)
+        m2 = m2.reshape(len(es), ne, bigd + 1, d + 1)
+        w_theta = np.matmul(np.matmul(u[es].transpose(0, 2, 1)[:, None], m2), v[None])
+        w_dmm = np.matmul(np.matmul(v[es].transpose(0, 2, 1)[:, None], m2[:, :, : d + 1, :]),
+                          v[None])
+        idx_t = ucols[es][:, None, :, None] * fine.dim + vcols[None, :, None, :]
+        idx_d = vcols[es][:, None, :, None] * fine.dim + vcols[None, :, None, :]
+        theta += np.bincount(idx_t.ravel(), weights=w_theta.ravel(), minlength=theta.size)
+        dmm += np.bincount(idx_d.ravel(), weights=w_dmm.ravel(), minlength=dmm.size)
+    theta = theta.reshape(space.dim, fine.dim)
+    dmm = dmm.reshape(fine.dim, fine.dim)
+    bbar_t = design(fine, disc.nodes)
+    target = (disc.Bpar * disc.J[None, :]).T
+    q, r = scipy.linalg.qr(bbar_t, mode="economic")
+    cfit = scipy.linalg.solve_triangular(r, q.T @ target)
+    return theta, dmm, cfit
+
+
+def dense_ik2_general(disc: Disc):
+    theta, dmm, cfit = ik2_ingredients_general(disc)
+    tc = theta @ cfit
+    return tc + tc.T - cfit.T @ dmm @ cfit
+
+
+def config5_space(n_el=16384, degree=4, seed=0, zone=0.2, ratio=0.9, growth_elems=60):
+    """Config 5 mesh (BASELINE.json configs[4]) under a well-posed reading of
+    its grading: the outer `zone` fraction of elements on each side is graded
+    geometrically with `ratio` per element toward the endpoint, the growth
+    from the end element capped at the interior width after `growth_elems`
+    elements (0.9^3277 underflows the literal reading); every
+    interior knot doubled with probability 0.25 drawn from
+    np.random.default_rng(seed).random(n_el - 1)."""
+    ng = int(round(zone * n_el))
+    w = np.ones(n_el)
+    k = np.arange(ng)
+    fac = ratio ** np.maximum(0, growth_elems - k)   # end element: ratio^growth_elems
+    w[:ng] = fac
+    w[n_el - ng:] = fac[::-1]
+    bp = np.concatenate([[0.0], np.cumsum(w)])
+    bp = -1.0 + 2.0 * bp / bp[-1]
+    mult = np.where(np.random.default_rng(seed).random(n_el - 1) < 0.25, 2, 1)
+    return open_basis(degree, bp, mult)

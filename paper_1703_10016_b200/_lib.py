@@ -30,7 +30,8 @@ WQ_K1_TABLE, WQ_K1_OPEN, WQ_K1_CLOSED = 0, 1, 2
 class WqSmooth(ctypes.Structure):
     _fields_ = [("n_rows", c_i64), ("nq", c_i64), ("wg", c_i64), ("closed", c_i64),
                 ("k1_mode", c_i64), ("period", c_dbl), ("s", c_vp), ("fx", c_vp), ("fy", c_vp),
-                ("J", c_vp), ("invp2", c_vp), ("g_start", c_vp), ("g_w", c_vp)]
+                ("J", c_vp), ("invp2", c_vp), ("g_start", c_vp), ("g_w", c_vp),
+                ("near_k", c_i64), ("near_j2", c_vp)]
 
 
 class WqLogpart(ctypes.Structure):
@@ -90,6 +91,14 @@ _SIGS = {
     "wq_set_ik1_passes": [c_int],
     "wq_probe_log": [c_i64, c_int, c_int, c_vp, c_vp],
     "wq_probe_phi": [c_int, c_int, c_int, c_vp, c_vp, c_vp],
+    "wq_gen_pair_blocks": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_vp,
+                           c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                           c_vp, c_vp, c_vp],
+    "wq_gen_gather_theta": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_int,
+                            c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+    "wq_gen_gather_d": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,
+                        c_vp, c_vp],
+    "wq_band_solve_win": [c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp],
 }
 
 EXPORTED = tuple(_SIGS)

@@ -122,6 +122,14 @@ class LogPart:
     bw: int = 0
     L21: np.ndarray = None         # cyclic meshes: seam coupling rows of the arrow factor
     L22: np.ndarray = None
+    # graded (non-uniform) meshes: per-pair blocks instead of the gap table
+    graded: bool = False
+    elh: np.ndarray = None         # (n_el,) widths
+    elm: np.ndarray = None         # (n_el,) midpoints
+    near_lo: np.ndarray = None     # (n_el,) first near inner element (cyclic)
+    near_cnt: np.ndarray = None    # (n_el,) number of near inner elements
+    ucols: np.ndarray = None
+    vcols: np.ndarray = None
 
 
 @dataclass
@@ -139,6 +147,8 @@ class Discretization:
     f_nodes: np.ndarray = field(repr=False)
     k1_mode: int = 0
     invp2: np.ndarray = field(default=None, repr=False)
+    near_k: int = 0                # distinct node pairs within eps_diag (geometry.py:237-245)
+    near_j2: np.ndarray = field(default=None, repr=False)
     rule_seconds: float = 0.0
     _logpart: object = field(default=None, repr=False)
     _dev: dict = field(default_factory=dict, repr=False)
@@ -183,8 +193,9 @@ def build_discretization(curve, space, nref: int) -> Discretization:
     b = curve.basis
     f_nodes = curve.spline(0)(np.clip(nodes, b.a, b.b))
     J = parametric_speed(curve, nodes)
-    PC.check_diagonal_pairs(nodes, space.closed, curve.length)
-    invp2 = PC.k1_distance_table(nodes, space.closed, curve.length)
+    near_k, near_j2 = PC.near_diagonal_pairs(nodes, space.closed, b.a, curve.length,
+                                             lambda s: parametric_speed(curve, s))
+    invp2 = PC.k1_distance_table(nodes, space.closed, curve.length) if near_k == 0 else None
     if invp2 is not None:
         mode = _lib.WQ_K1_TABLE
     else:
@@ -194,7 +205,7 @@ def build_discretization(curve, space, nref: int) -> Discretization:
     return Discretization(curve=curve, space=space, refined=refined,
                           nodes=NodeVector(nodes=nodes, refined=refined, element_index=el_idx),
                           rules=rules, J_nodes=J, f_nodes=f_nodes, k1_mode=mode, invp2=invp2,
-                          rule_seconds=rule_seconds)
+                          near_k=near_k, near_j2=near_j2, rule_seconds=rule_seconds)
 
 
 # -- log-part host ingredients ---------------------------------------------------------
@@ -225,11 +236,19 @@ def _is_circulant(disc: Discretization) -> bool:
             and fine.seam_multiplicity == 1 and fine.dim == fine.n_elements)
 
 
+# route uniform meshes through the per-pair (graded-mesh) kernels too; tests use
+# it to pin those kernels against the reference's uniform-mesh outputs
+_FORCE_PER_PAIR = False
+
+
 def _log_part(disc: Discretization) -> LogPart:
     if disc._logpart is not None:
         return disc._logpart
     fine, space = disc.refined.basis, disc.space
-    h = PC.uniform_width(fine)  # ConstructionError on graded meshes (quadrature.py:489-491)
+    # the reference raises ConstructionError on graded meshes (quadrature.py:489-491);
+    # here they take the per-pair route
+    graded = _FORCE_PER_PAIR or not PC.is_uniform_mesh(fine)
+    h = None if graded else PC.uniform_width(fine)
     d = fine.degree
     da = space.degree + PC.JFIT_DEGREE
     curve = disc.curve
@@ -246,7 +265,7 @@ def _log_part(disc: Discretization) -> LogPart:
                  near_unit=np.ascontiguousarray(PC.unit_near_table(da, d)),
                  s_start=s_start, s_w=s_w)
     N = space.dim
-    if _is_circulant(disc):
+    if not graded and _is_circulant(disc):
         n = fine.n_elements
         _, _, counts = _incidence(ucols, N)
         tu = int(counts.max())
@@ -294,6 +313,10 @@ def _log_part(disc: Discretization) -> LogPart:
         v_el, v_loc, _ = _incidence(vcols, fine.dim)
         lp.u, lp.v = np.ascontiguousarray(u), np.ascontiguousarray(v)
         lp.u_el, lp.u_loc, lp.v_el, lp.v_loc = u_el, u_loc, v_el, v_loc
+        if graded:
+            lp.graded = True
+            lp.elh, lp.elm, lp.near_lo, lp.near_cnt = PC.element_pair_geometry(fine)
+            lp.ucols, lp.vcols = np.asarray(ucols), np.asarray(vcols)
     disc._logpart = lp
     return lp
 
@@ -344,13 +367,15 @@ def _smooth(disc: Discretization):
                 rb.start[:, None] + np.arange(rb.WG)[None, :], len(nodes))])
                 * (np.arange(rb.WG)[None, :] < rb.width[:, None])),
             "invp2": _to_dev(torch, disc.invp2) if disc.invp2 is not None else None,
+            "near_j2": _to_dev(torch, disc.near_j2) if disc.near_k else None,
             "flag": torch.zeros(1, dtype=torch.int32, device="cuda"),
         }
         st = _lib.WqSmooth(disc.space.dim, len(nodes), rb.WG, int(disc.closed), disc.k1_mode,
                            disc.curve.length, d["s"].data_ptr(), d["fx"].data_ptr(),
                            d["fy"].data_ptr(), d["J"].data_ptr(),
                            d["invp2"].data_ptr() if d["invp2"] is not None else None,
-                           d["g_start"].data_ptr(), d["g_w"].data_ptr())
+                           d["g_start"].data_ptr(), d["g_w"].data_ptr(), disc.near_k,
+                           d["near_j2"].data_ptr() if disc.near_k else None)
         # max node span over output tiles of WQ_TILE rows
         T = _lib.WQ_TILE
         N = disc.space.dim
@@ -428,9 +453,18 @@ def _logpart_dev(disc):
                                          d["s_start"].data_ptr(), d["s_w"].data_ptr())
         else:
             NE = disc.refined.basis.dim
-            for k in ("u", "v", "u_el", "u_loc", "v_el", "v_loc", "Lb", "L21", "L22"):
+            for k in ("u", "v", "u_el", "u_loc", "v_el", "v_loc", "Lb", "L21", "L22",
+                      "elh", "elm", "near_lo", "near_cnt"):
                 if getattr(lp, k) is not None:
                     d[k] = _to_dev(torch, getattr(lp, k))
+            if lp.graded:
+                tiers = [PC.gauss_unit(n) for n in PC.GEN_GAUSS_TIERS]
+                d["gx"] = _to_dev(torch, np.concatenate([t[0] for t in tiers]))
+                d["gw"] = _to_dev(torch, np.concatenate([t[1] for t in tiers]))
+                d["touch"] = _to_dev(torch, PC.touch_rules())
+                d["near_unit"] = _to_dev(torch, lp.near_unit)
+                d["ca"] = _to_dev(torch, PC.centred_monomial_integrals(lp.da))
+                d["cb"] = _to_dev(torch, PC.centred_monomial_integrals(lp.db))
             d["struct"] = _lib.WqLogpart(N, NE, lp.da, 0, lp.s_w.shape[1], None, None,
                                          d["s_start"].data_ptr(), d["s_w"].data_ptr())
         return d
@@ -475,18 +509,26 @@ def _ik2_x2_into(disc, X, accumulate=True):
     st = _lib.stream_handle()
     if lp.path == "circulant":
         return _ik2_x2_rows(disc, X, 0, N, accumulate)
-    m2, keep = _m2_table(disc, lp)
     NE = disc.refined.basis.dim
-    pp = _lib.WqPairs(N, NE, lp.n_el, m2.shape[0], lp.da, lp.db, int(disc.closed),
-                      lp.u_el.shape[1], lp.v_el.shape[1], d["u_el"].data_ptr(),
-                      d["u_loc"].data_ptr(), d["v_el"].data_ptr(), d["v_loc"].data_ptr(),
-                      d["u"].data_ptr(), disc.space.degree, d["v"].data_ptr(), m2.data_ptr())
-    thetaT = torch.empty((NE, N), dtype=torch.float64, device="cuda")
-    D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
-    _lib.call("wq_theta_t", ctypes_ref(pp), _lib.ptr(thetaT), st)
-    _lib.call("wq_dmat", ctypes_ref(pp), _lib.ptr(D), st)
+    if lp.graded:
+        thetaT, D = _graded_theta_d(disc, lp, d)
+    else:
+        m2, keep = _m2_table(disc, lp)
+        pp = _lib.WqPairs(N, NE, lp.n_el, m2.shape[0], lp.da, lp.db, int(disc.closed),
+                          lp.u_el.shape[1], lp.v_el.shape[1], d["u_el"].data_ptr(),
+                          d["u_loc"].data_ptr(), d["v_el"].data_ptr(), d["v_loc"].data_ptr(),
+                          d["u"].data_ptr(), disc.space.degree, d["v"].data_ptr(),
+                          m2.data_ptr())
+        thetaT = torch.empty((NE, N), dtype=torch.float64, device="cuda")
+        D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
+        _lib.call("wq_theta_t", ctypes_ref(pp), _lib.ptr(thetaT), st)
+        _lib.call("wq_dmat", ctypes_ref(pp), _lib.ptr(D), st)
+
     def hsolve(Y, ncols):
-        if lp.L21 is None:
+        if lp.L21 is None and lp.bw <= 8:
+            _lib.call("wq_band_solve_win", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(Y), ncols,
+                      Y.stride(0), st)
+        elif lp.L21 is None:
             _lib.call("wq_band_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(Y), ncols,
                       Y.stride(0), st)
         else:
@@ -505,6 +547,45 @@ def _ik2_x2_into(disc, X, accumulate=True):
     _lib.call("wq_add_st_phi", ctypes_ref(d["struct"]), _lib.ptr(thetaT), 0, N, _lib.ptr(X),
               X.stride(0), int(accumulate), st)
     return X
+
+
+# device bytes for one chunk of per-pair Theta / D blocks (graded meshes)
+_GEN_CHUNK_BYTES = 1 << 30
+
+
+def _graded_theta_d(disc, lp: LogPart, d):
+    """Theta^T (N_E x N) and D (N_E x N_E) of a graded mesh: per-pair blocks
+    for a chunk of outer elements, then deterministic gathers (replaces the
+    gap-table accumulation of assembly.py:206-236, which the reference only
+    supports on uniform meshes)."""
+    torch = _torch()
+    st = _lib.stream_handle()
+    N, NE, n = disc.space.dim, disc.refined.basis.dim, lp.n_el
+    nU, nB = lp.u.shape[2], lp.db + 1
+    per_e = n * (nU * nB + nB * nB) * 8
+    chunk = int(max(1, min(n, _GEN_CHUNK_BYTES // per_e)))
+    wt = torch.empty((chunk, n, nU, nB), dtype=torch.float64, device="cuda")
+    wd = torch.empty((chunk, n, nB, nB), dtype=torch.float64, device="cuda")
+    thetaT = torch.zeros((NE, N), dtype=torch.float64, device="cuda")
+    D = torch.zeros((NE, NE), dtype=torch.float64, device="cuda")
+    max_near = int(lp.near_cnt.max())
+    period = float(disc.refined.basis.length) if disc.closed else 0.0
+    wu, wv = lp.u_el.shape[1], lp.v_el.shape[1]
+    for e0 in range(0, n, chunk):
+        e1 = min(n, e0 + chunk)
+        _lib.call("wq_gen_pair_blocks", n, e0, e1, lp.da, lp.db, nU - 1, int(disc.closed), period,
+                  _lib.ptr(d["elh"]), _lib.ptr(d["elm"]), _lib.ptr(d["u"]), _lib.ptr(d["v"]),
+                  _lib.ptr(d["near_lo"]), _lib.ptr(d["near_cnt"]), max_near,
+                  _lib.ptr(d["near_unit"]), _lib.ptr(d["touch"]), _lib.ptr(d["gx"]),
+                  _lib.ptr(d["gw"]), _lib.ptr(d["ca"]), _lib.ptr(d["cb"]), _lib.ptr(wt),
+                  _lib.ptr(wd), st)
+        uc, vc = lp.ucols[e0:e1], lp.vcols[e0:e1]
+        _lib.call("wq_gen_gather_theta", N, NE, n, e0, e1, int(uc.min()), int(uc.max()) + 1, wu,
+                  wv, nU, nB, _lib.ptr(d["u_el"]), _lib.ptr(d["u_loc"]), _lib.ptr(d["v_el"]),
+                  _lib.ptr(d["v_loc"]), _lib.ptr(wt), _lib.ptr(thetaT), st)
+        _lib.call("wq_gen_gather_d", NE, n, e0, e1, int(vc.min()), int(vc.max()) + 1, wv, nB,
+                  _lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(wd), _lib.ptr(D), st)
+    return thetaT, D
 
 
 def _new_square(disc):
@@ -639,7 +720,7 @@ def _use_v2(disc) -> bool:
     lp = _log_part(disc)
     rb = disc.rules
     p = disc.space.degree
-    return (lp.path == "circulant" and 2 <= p <= 5 and rb.WG == 2 * p + 1
+    return (lp.path == "circulant" and disc.near_k == 0 and 2 <= p <= 5 and rb.WG == 2 * p + 1
             and np.all(rb.width == rb.WG) and np.all(np.diff(rb.start) == 2)
             and disc.nodes.n == 2 * disc.space.dim)
 

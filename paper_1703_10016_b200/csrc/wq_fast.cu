@@ -1264,6 +1264,10 @@ static int ik1_dispatch(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag
     set_error("wq_ik1_sym: bad arguments (closed uniform meshes only)");
     return WQ_EINVAL;
   }
+  if (sm->near_k > 0) {
+    set_error("wq_ik1_sym: near-diagonal node pairs need wq_ik1");
+    return WQ_EUNSUPPORTED;
+  }
   if (sm->k1_mode == WQ_K1_TABLE && !sm->invp2) {
     set_error("wq_ik1_sym: table mode without invp2");
     return WQ_EINVAL;
@@ -1411,7 +1415,8 @@ int wq_assemble_fused(const wq_smooth_t* sm, int p, int nA, int nApad, int ws, i
                       const double* Uext, const double* Zext, const double* s_w, double alpha,
                       double w_ik1, int* ready, int epoch, int64_t lead, double* X, int64_t ldx,
                       int* flag, void* stream) {
-  if (!sm || !Uext || !Zext || !s_w || !ready || !X || !flag || !sm->closed || epoch == 0) {
+  if (!sm || !Uext || !Zext || !s_w || !ready || !X || !flag || !sm->closed || epoch == 0 ||
+      sm->near_k > 0) {
     set_error("wq_assemble_fused: bad arguments");
     return WQ_EINVAL;
   }

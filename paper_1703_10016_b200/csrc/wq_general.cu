@@ -1,0 +1,546 @@
+// Non-uniform meshes (graded elements, any knot multiplicity; config 5):
+// element-pair Theta / D blocks computed per pair on the device, then gathered
+// into Theta^T (N_E x N) and D (N_E x N_E) for the general fit path.
+//
+// The reference supports only uniform meshes here (quadrature.py:489-491
+// raises).  Its unit-width recipe (quadrature.py:441-504) is generalised per
+// pair (restated in oracle/wq_oracle.py::pair_moments_general):
+//   near pairs (touching / overlapping, as the reference's |gap| <= 1 entries,
+//     quadrature.py:458; listed by the host): closed-form moments
+//     (quadrature.py:372-410) in width-normalised coordinates (h_e = 1,
+//     h_f = rho, delta' = delta / h_e), scaled by
+//     M = h_e^(a+b+2) (M' + ln h_e c_a C_b(rho)), then contracted;
+//   far pairs: tensor Gauss (quadrature.py:413-438) applied directly to the
+//     contracted integrand  int int U_e(x) log|y - x| V_f(y),  U_e / V_f the
+//     element polynomials of the coarse (times fitted J) and fine functions --
+//     algebraically the same as contracting the Gauss moments, with the order
+//     tiered by separation (30 below two widths, as the reference; 16 below
+//     eight; 12 beyond -- all converged to rounding for the degree <= 16 x 5
+//     polynomials involved).
+// Closed meshes add the periodic gap term log|sinc(r / L)| (quadrature.py:
+// 459-468) -- far pairs use log|L/pi sin(pi r / L)|, its exact sum with log|r|.
+// Every output is a fixed-order sum (deterministic; no atomics).
+#include "wq_common.cuh"
+
+namespace wq {
+
+constexpr int GMAXA = 24;   // max row polynomial degree + 1 (P + 1)
+constexpr int GMAXB = 8;    // max column degree + 1
+constexpr int GMAXP = GMAXA + GMAXB;
+constexpr int GT0 = 30, GT1 = 16, GT2 = 12;   // Gauss tiers
+constexpr int GTSUM = GT0 + GT1 + GT2;
+
+__constant__ double c_binom[GMAXP][GMAXP];
+static bool g_consts_ready[64];
+
+static int ensure_consts() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && g_consts_ready[dev]) return WQ_OK;
+  static double b[GMAXP][GMAXP];
+  for (int n = 0; n < GMAXP; ++n) {
+    b[n][0] = 1.0;
+    for (int k = 1; k <= n; ++k) b[n][k] = b[n - 1][k - 1] + (k <= n - 1 ? b[n - 1][k] : 0.0);
+  }
+  cudaError_t e = cudaMemcpyToSymbol(c_binom, b, sizeof(b));
+  if (e != cudaSuccess) {
+    set_error("constant upload: %s", cudaGetErrorString(e));
+    return WQ_ECUDA;
+  }
+  if (dev >= 0 && dev < 64) g_consts_ready[dev] = true;
+  return WQ_OK;
+}
+
+// [z^{j+1}/(j+1) (ln|z| - 1/(j+1))], limit 0 at z = 0 (quadrature.py:182-197)
+__device__ __forceinline__ double log_bracket(int j, double zp1, double lz, bool zero) {
+  return zero ? 0.0 : zp1 / (j + 1) * (lz - 1.0 / (j + 1));
+}
+
+// Closed-form unit-normalised moments (he = 1, hf = rho, delta = dl) added into
+// out[a * ldo + b] (quadrature.py:372-410, same summation structure).
+__device__ void pair_closed(int da, int db, double rho, double dl, double* out, int ldo) {
+  const int pmax = da + db + 1;
+  for (int s = 0; s < 2; ++s) {
+    const double sgn = s == 0 ? 1.0 : -1.0;
+    const double xi = sgn * 0.5 * rho;
+    const double z1 = xi - dl - 0.5, z2 = xi - dl + 0.5;
+    const bool z1z = z1 == 0.0, z2z = z2 == 0.0;
+    const double l1 = z1z ? 0.0 : log(fabs(z1)), l2 = z2z ? 0.0 : log(fabs(z2));
+    double llog[GMAXP + 1], lpow[GMAXP + 1];
+    double p1 = z1, p2 = z2;  // z^(p+1)
+    for (int p = 0; p <= pmax; ++p) {
+      llog[p] = log_bracket(p, p2, l2, z2z) - log_bracket(p, p1, l1, z1z);
+      lpow[p] = (p2 - p1) / (p + 1);
+      p1 *= z1;
+      p2 *= z2;
+    }
+    const double xd = xi - dl;
+    for (int b = 0; b <= db; ++b) {
+      for (int m = 0; m <= b; ++m) {
+        const double cm = sgn * c_binom[b][m] / (m + 1);
+        for (int a = 0; a <= da; ++a) {
+          double acc = 0.0;
+          for (int r = 0; r <= a; ++r) {
+            double t = 1.0;  // (xi - delta)^(a - r)
+            for (int k = 0; k < a - r; ++k) t *= xd;
+            for (int q = 0; q <= b - m; ++q) {
+              const int p = r + q + m + 1;
+              double u = 1.0;  // xi^(b - m - q)
+              for (int k = 0; k < b - m - q; ++k) u *= xi;
+              const double sign = ((r + q) & 1) ? -1.0 : 1.0;
+              const double coef = cm * c_binom[a][r] * c_binom[b - m][q] * sign * t * u;
+              acc += coef * (llog[p] - lpow[p] / (m + 1));
+            }
+          }
+          out[a * ldo + b] += acc;
+        }
+      }
+    }
+  }
+}
+
+struct GenArgs {
+  int64_t n_el, e0, e1;     // all elements; chunk [e0, e1)
+  int da, db, pu;           // P, d, coarse degree
+  int closed;
+  double period;
+  const double* elh;        // (n_el) widths
+  const double* elm;        // (n_el) midpoints
+  const double* u;          // (n_el, da+1, pu+1) coarse coefficients (times fitted J)
+  const double* v;          // (n_el, db+1, db+1) fine coefficients
+  const int64_t* near_lo;   // (n_el) near pairs of e: f = near_lo[e] + k (mod n_el),
+  const int64_t* near_cnt;  //        k < near_cnt[e]
+  const double* near_unit;  // (3, da+1, db+1) unit closed-form table, dl = -1, 0, +1 (host)
+  const double* touch;      // packed Duffy rules: x16 w16 x30 w30 on (0,1), xl14 wl14
+  const double* gx;         // tier Gauss nodes on (-1/2, 1/2), 30 | 16 | 12 concatenated
+  const double* gw;         // weights
+  const double* ca;         // (da+1) unit centred integrals
+  const double* cb;         // (db+1)
+  double* wt;               // (e1-e0, n_el, pu+1, db+1) Theta blocks
+  double* wd;               // (e1-e0, n_el, db+1, db+1) D blocks
+};
+
+__device__ __forceinline__ double wrap_delta(const GenArgs& A, double d) {
+  return A.closed ? d - A.period * rint(d / A.period) : d;
+}
+
+__device__ __forceinline__ bool is_near(const GenArgs& A, int64_t e, int64_t f) {
+  int64_t k = f - A.near_lo[e];
+  if (k < 0) k += A.n_el;
+  return k < A.near_cnt[e];
+}
+
+constexpr int FP_THREADS = 64;
+
+// One CTA per (64 inner elements f, one outer element e of the chunk); one
+// thread per pair.  NP = p + 1 = d + 1 columns on both sides (compile time, so
+// the 2 x NP^2 block accumulators stay in registers).  The outer element's
+// weighted polynomial values at every tier's nodes sit in shared memory.
+template <int NP>
+__global__ void __launch_bounds__(FP_THREADS)
+pair_far_kernel(GenArgs A) {
+  __shared__ double Ut[GTSUM][NP];   // h_e w_g U_e(h_e x_g)
+  __shared__ double Vt[GTSUM][NP];   // h_e w_g V_e(h_e x_g)
+  __shared__ double Xt[GTSUM];       // h_e x_g
+  __shared__ double Gx[GTSUM], Gw[GTSUM];
+  const int nA = A.da + 1;
+  const int64_t e = A.e0 + blockIdx.y;
+  const double he = A.elh[e];
+  for (int g = threadIdx.x; g < GTSUM; g += FP_THREADS) {
+    Gx[g] = A.gx[g];
+    Gw[g] = A.gw[g];
+    const double x = he * A.gx[g], w = he * A.gw[g];
+    Xt[g] = x;
+    const double* ue = A.u + e * nA * NP;
+    const double* ve = A.v + e * NP * NP;
+#pragma unroll
+    for (int ap = 0; ap < NP; ++ap) {
+      double s = 0.0;
+      for (int al = nA - 1; al >= 0; --al) s = fma(s, x, ue[al * NP + ap]);
+      Ut[g][ap] = w * s;
+      s = 0.0;
+#pragma unroll
+      for (int al = NP - 1; al >= 0; --al) s = fma(s, x, ve[al * NP + ap]);
+      Vt[g][ap] = w * s;
+    }
+  }
+  __syncthreads();
+  const int64_t f = (int64_t)blockIdx.x * FP_THREADS + threadIdx.x;
+  if (f >= A.n_el || is_near(A, e, f)) return;
+  const double hf = A.elh[f];
+  const double delta = wrap_delta(A, A.elm[e] - A.elm[f]);
+  const double sep = fabs(delta) - 0.5 * (he + hf);
+  const double hm = fmax(he, hf);
+  const int t0 = sep < 2.0 * hm ? 0 : (sep < 8.0 * hm ? GT0 : GT0 + GT1);
+  const int ng = sep < 2.0 * hm ? GT0 : (sep < 8.0 * hm ? GT1 : GT2);
+  double vf[NP][NP];
+#pragma unroll
+  for (int b = 0; b < NP; ++b)
+#pragma unroll
+    for (int bp = 0; bp < NP; ++bp) vf[b][bp] = A.v[(f * NP + b) * NP + bp];
+  double wT[NP][NP], wD[NP][NP];
+#pragma unroll
+  for (int a = 0; a < NP; ++a)
+#pragma unroll
+    for (int b = 0; b < NP; ++b) wT[a][b] = wD[a][b] = 0.0;
+  const bool closed = A.closed;
+  const double invL = closed ? 1.0 / A.period : 0.0;
+  const double lnLpi = closed ? log(A.period / kPi) : 0.0;
+  for (int h = 0; h < ng; ++h) {
+    const double y = hf * Gx[t0 + h], wy = hf * Gw[t0 + h];
+    double vy[NP];
+#pragma unroll
+    for (int bp = 0; bp < NP; ++bp) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = NP - 1; b >= 0; --b) s = fma(s, y, vf[b][bp]);
+      vy[bp] = wy * s;
+    }
+    const double base = y - delta;  // r = y - x - delta
+    double tU[NP], tV[NP];
+#pragma unroll
+    for (int a = 0; a < NP; ++a) tU[a] = tV[a] = 0.0;
+    for (int g = 0; g < ng; ++g) {
+      const double r = base - Xt[t0 + g];
+      const double k = closed ? log(fabs(sinpi(r * invL))) + lnLpi : log(fabs(r));
+#pragma unroll
+      for (int a = 0; a < NP; ++a) {
+        tU[a] = fma(Ut[t0 + g][a], k, tU[a]);
+        tV[a] = fma(Vt[t0 + g][a], k, tV[a]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NP; ++a)
+#pragma unroll
+      for (int bp = 0; bp < NP; ++bp) {
+        wT[a][bp] = fma(tU[a], vy[bp], wT[a][bp]);
+        wD[a][bp] = fma(tV[a], vy[bp], wD[a][bp]);
+      }
+  }
+  double* wt = A.wt + ((e - A.e0) * A.n_el + f) * NP * NP;
+  double* wd = A.wd + ((e - A.e0) * A.n_el + f) * NP * NP;
+#pragma unroll
+  for (int a = 0; a < NP; ++a)
+#pragma unroll
+    for (int bp = 0; bp < NP; ++bp) {
+      wt[a * NP + bp] = wT[a][bp];
+      wd[a * NP + bp] = wD[a][bp];
+    }
+}
+
+constexpr int TOUCH_XI = 16, TOUCH_ETA = 30, TOUCH_LOG = 14;
+
+// Touching pair of unequal widths (outer 1, inner rho, dl = sig (1 + rho)/2):
+// with t, y the distances from the shared corner, ln|v - u - dl| = ln(t + y);
+// the Duffy split y <= rho t (y = rho xi eta) / y >= rho t (t = xi eta, y = rho xi)
+// gives  rho xi [ln xi + g(eta)],  g = ln(1 + rho eta) | ln(rho + eta):
+// ln xi by the -ln-weighted rule, the rest by Gauss-Legendre (exact in xi for
+// the degree <= P + d + 1 polynomials; g analytic for rho in [1/8, 8]).
+__device__ void pair_touch(int da, int db, double rho, double sig, const double* R, double* out,
+                           int ldo) {
+  const double* x16 = R;
+  const double* w16 = R + TOUCH_XI;
+  const double* x30 = R + 2 * TOUCH_XI;
+  const double* w30 = x30 + TOUCH_ETA;
+  const double* xl = w30 + TOUCH_ETA;
+  const double* wl = xl + TOUCH_LOG;
+  for (int tri = 0; tri < 2; ++tri) {
+    for (int k = 0; k < TOUCH_ETA; ++k) {
+      const double eta = x30[k];
+      const double g = tri == 0 ? log1p(rho * eta) : log(rho + eta);
+      for (int j = 0; j < TOUCH_XI + TOUCH_LOG; ++j) {
+        const bool lg = j >= TOUCH_XI;
+        const double xi = lg ? xl[j - TOUCH_XI] : x16[j];
+        const double wx = lg ? -wl[j - TOUCH_XI] : w16[j] * g;
+        double u, v;
+        if (tri == 0) {
+          u = sig * (xi - 0.5);
+          v = -sig * rho * (xi * eta - 0.5);
+        } else {
+          u = sig * (xi * eta - 0.5);
+          v = -sig * rho * (xi - 0.5);
+        }
+        double ua = w30[k] * wx * rho * xi;
+        for (int a = 0; a <= da; ++a) {
+          double t = ua;
+          for (int b = 0; b <= db; ++b) {
+            out[a * ldo + b] += t;
+            t *= v;
+          }
+          ua *= u;
+        }
+      }
+    }
+  }
+}
+
+constexpr int NP_THREADS = 32;
+
+// Near pairs: one thread per (e, k < near_cnt[e]); moment matrix in shared memory.
+__global__ void __launch_bounds__(NP_THREADS)
+pair_near_kernel(GenArgs A, int max_near) {
+  extern __shared__ double sh[];
+  const int nA = A.da + 1, nB = A.db + 1, nU = A.pu + 1;
+  const int64_t e = A.e0 + blockIdx.y;
+  const int k = blockIdx.x * NP_THREADS + threadIdx.x;
+  if (k >= A.near_cnt[e] || k >= max_near) return;
+  int64_t f = A.near_lo[e] + k;
+  if (f >= A.n_el) f -= A.n_el;
+  double* M = sh + threadIdx.x * nA * nB;
+  for (int i = 0; i < nA * nB; ++i) M[i] = 0.0;
+  const double he = A.elh[e], hf = A.elh[f];
+  const double delta = wrap_delta(A, A.elm[e] - A.elm[f]);
+  double rho = hf / he, dl = delta / he;
+  if (fabs(rho - 1.0) < 1e-12) {  // exact integer gaps as the unit table (quadrature.py:452-456)
+    rho = 1.0;
+    if (fabs(dl - rint(dl)) < 1e-9) dl = rint(dl);
+  }
+  if (rho == 1.0 && (dl == -1.0 || dl == 0.0 || dl == 1.0)) {
+    // equal widths: the reference's closed-form unit entries, host-computed
+    const double* t = A.near_unit + (int)(1.0 - dl) * nA * nB;  // rows keff = -dl = -1, 0, 1
+    for (int i = 0; i < nA * nB; ++i) M[i] = t[i];
+  } else if (rho == 1.0) {
+    pair_closed(A.da, A.db, rho, dl, M, nB);
+  } else {
+    pair_touch(A.da, A.db, rho, dl > 0.0 ? 1.0 : -1.0, A.touch, M, nB);
+  }
+  if (A.closed) {  // periodic gap term, 30 x 30 Gauss (quadrature.py:459-468)
+    const double per = A.period / he;
+    for (int g = 0; g < GT0; ++g) {
+      double t[GMAXB];
+      for (int b = 0; b < nB; ++b) t[b] = 0.0;
+      for (int h = 0; h < GT0; ++h) {
+        const double xh = A.gx[h];
+        const double arg = (rho * xh - A.gx[g]) - dl;
+        const double yy = arg / per;
+        const double kv = yy == 0.0 ? 0.0 : log(fabs(sinpi(yy) / (kPi * yy)));
+        double wv = A.gw[h] * rho;
+        for (int b = 0; b < nB; ++b) {
+          t[b] = fma(kv, wv, t[b]);
+          wv *= rho * xh;
+        }
+      }
+      double wu = A.gw[g];
+      for (int a = 0; a < nA; ++a) {
+        for (int b = 0; b < nB; ++b) M[a * nB + b] = fma(wu, t[b], M[a * nB + b]);
+        wu *= A.gx[g];
+      }
+    }
+  }
+  const double lh = log(he);
+  double hea = he * he;
+  double rp = rho;
+  double cbr[GMAXB];
+  for (int b = 0; b < nB; ++b) {
+    cbr[b] = rp * A.cb[b];
+    rp *= rho;
+  }
+  for (int a = 0; a < nA; ++a) {
+    double s = hea;
+    for (int b = 0; b < nB; ++b) {
+      M[a * nB + b] = s * (M[a * nB + b] + lh * (A.ca[a] * cbr[b]));
+      s *= he;
+    }
+    hea *= he;
+  }
+  const double* ue = A.u + e * nA * nU;
+  const double* ve = A.v + e * nB * nB;
+  const double* vf = A.v + f * nB * nB;
+  double* wt = A.wt + ((e - A.e0) * A.n_el + f) * nU * nB;
+  double* wd = A.wd + ((e - A.e0) * A.n_el + f) * nB * nB;
+  for (int bp = 0; bp < nB; ++bp) {
+    double mv[GMAXA];
+    for (int al = 0; al < nA; ++al) {
+      double s = 0.0;
+      for (int be = 0; be < nB; ++be) s = fma(M[al * nB + be], vf[be * nB + bp], s);
+      mv[al] = s;
+    }
+    for (int ap = 0; ap < nU; ++ap) {
+      double s = 0.0;
+      for (int al = 0; al < nA; ++al) s = fma(ue[al * nU + ap], mv[al], s);
+      wt[ap * nB + bp] = s;
+    }
+    for (int ap = 0; ap < nB; ++ap) {
+      double s = 0.0;
+      for (int al = 0; al < nB; ++al) s = fma(ve[al * nB + ap], mv[al], s);
+      wd[ap * nB + bp] = s;
+    }
+  }
+}
+
+// Theta^T[l][i] += sum_{(e,a) in inc_u(i), e in chunk} sum_{(f,b) in inc_v(l)} WT[e][f][a][b]
+__global__ void gather_theta_kernel(int64_t n_rows, int64_t n_el, int64_t e0, int64_t e1,
+                                    int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
+                                    const int64_t* u_el, const int64_t* u_loc,
+                                    const int64_t* v_el, const int64_t* v_loc, const double* wt,
+                                    double* thetaT) {
+  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t l = blockIdx.y;
+  if (i >= i1) return;
+  double acc = 0.0;
+  for (int ua = 0; ua < wu; ++ua) {
+    const int64_t e = u_el[i * wu + ua];
+    if (e < e0 || e >= e1) continue;
+    const int a = (int)u_loc[i * wu + ua];
+    const double* blk = wt + (e - e0) * n_el * nU * nB + a * nB;
+    for (int vb = 0; vb < wv; ++vb) {
+      const int64_t f = v_el[l * wv + vb];
+      if (f < 0) continue;
+      acc += blk[f * nU * nB + v_loc[l * wv + vb]];
+    }
+  }
+  thetaT[l * n_rows + i] += acc;
+}
+
+// D[l][m] += sum_{(e,a) in inc_v(l), e in chunk} sum_{(f,b) in inc_v(m)} WD[e][f][a][b]
+__global__ void gather_d_kernel(int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1, int64_t l0,
+                                int64_t l1, int wv, int nB, const int64_t* v_el,
+                                const int64_t* v_loc, const double* wd, double* D) {
+  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t l = l0 + blockIdx.y;
+  if (m >= n_fine || l >= l1) return;
+  double acc = 0.0;
+  for (int va = 0; va < wv; ++va) {
+    const int64_t e = v_el[l * wv + va];
+    if (e < e0 || e >= e1) continue;
+    const int a = (int)v_loc[l * wv + va];
+    const double* blk = wd + (e - e0) * n_el * nB * nB + a * nB;
+    for (int vb = 0; vb < wv; ++vb) {
+      const int64_t f = v_el[m * wv + vb];
+      if (f < 0) continue;
+      acc += blk[f * nB * nB + v_loc[m * wv + vb]];
+    }
+  }
+  D[l * n_fine + m] += acc;
+}
+
+// Banded Cholesky solves X <- L^{-T} L^{-1} X per column with the last BW
+// values of the column in registers (one load + one store per row).
+template <int BW>
+__global__ void band_solve_win_kernel(int64_t n, const double* Lb, double* X, int64_t ncols,
+                                      int64_t ldx) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  double* x = X + c;
+  double w[BW];
+#pragma unroll
+  for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = y_{k-1-j}
+  for (int64_t k = 0; k < n; ++k) {
+    const double* lk = Lb + k * (BW + 1);
+    double s = x[k * ldx];
+#pragma unroll
+    for (int j = 1; j <= BW; ++j) s = fma(-lk[j], w[j - 1], s);  // zero window before row 0
+    s = s / lk[0];
+    x[k * ldx] = s;
+#pragma unroll
+    for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
+    w[0] = s;
+  }
+#pragma unroll
+  for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = z_{k+1+j}
+  for (int64_t k = n - 1; k >= 0; --k) {
+    double s = x[k * ldx];
+#pragma unroll
+    for (int j = 1; j <= BW; ++j)
+      if (k + j < n) s = fma(-Lb[(k + j) * (BW + 1) + j], w[j - 1], s);
+    s = s / Lb[k * (BW + 1)];
+    x[k * ldx] = s;
+#pragma unroll
+    for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
+    w[0] = s;
+  }
+}
+
+}  // namespace wq
+
+using namespace wq;
+
+extern "C" {
+
+int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int pu, int closed,
+                       double period, const double* elh, const double* elm, const double* u,
+                       const double* v, const int64_t* near_lo, const int64_t* near_cnt,
+                       int max_near, const double* near_unit, const double* touch,
+                       const double* gx, const double* gw, const double* ca, const double* cb, double* wt, double* wd,
+                       void* stream) {
+  if (n_el <= 0 || e0 < 0 || e1 > n_el || e1 <= e0 || da + 1 > GMAXA || db + 1 > GMAXB ||
+      db < 1 || pu != db || max_near < 0 || !near_unit || !touch || !gx || !gw || !elh || !elm || !u || !v || !near_lo || !near_cnt ||
+      !ca || !cb || !wt || !wd || (closed && !(period > 0))) {
+    set_error("wq_gen_pair_blocks: bad arguments");
+    return WQ_EINVAL;
+  }
+  int rc = ensure_consts();
+  if (rc) return rc;
+  GenArgs A{n_el, e0, e1, da, db, pu, closed, period, elh, elm, u, v, near_lo, near_cnt,
+            near_unit, touch, gx, gw, ca, cb, wt, wd};
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 g1(ceil_div(n_el, FP_THREADS), (unsigned)(e1 - e0));
+  switch (db + 1) {
+    case 2: pair_far_kernel<2><<<g1, FP_THREADS, 0, st>>>(A); break;
+    case 3: pair_far_kernel<3><<<g1, FP_THREADS, 0, st>>>(A); break;
+    case 4: pair_far_kernel<4><<<g1, FP_THREADS, 0, st>>>(A); break;
+    case 5: pair_far_kernel<5><<<g1, FP_THREADS, 0, st>>>(A); break;
+    case 6: pair_far_kernel<6><<<g1, FP_THREADS, 0, st>>>(A); break;
+    case 7: pair_far_kernel<7><<<g1, FP_THREADS, 0, st>>>(A); break;
+    default: pair_far_kernel<8><<<g1, FP_THREADS, 0, st>>>(A); break;
+  }
+  rc = check_launch("wq_gen_pair_blocks(far)");
+  if (rc || max_near == 0) return rc;
+  const size_t smem = (size_t)NP_THREADS * (da + 1) * (db + 1) * sizeof(double);
+  cudaFuncSetAttribute(pair_near_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 g2(ceil_div(max_near, NP_THREADS), (unsigned)(e1 - e0));
+  pair_near_kernel<<<g2, NP_THREADS, smem, st>>>(A, max_near);
+  return check_launch("wq_gen_pair_blocks(near)");
+}
+
+int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1,
+                        int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
+                        const int64_t* u_el, const int64_t* u_loc, const int64_t* v_el,
+                        const int64_t* v_loc, const double* wt, double* thetaT, void* stream) {
+  if (i1 <= i0 || i0 < 0 || i1 > n_rows || n_fine <= 0 || !u_el || !u_loc || !v_el || !v_loc ||
+      !wt || !thetaT) {
+    set_error("wq_gen_gather_theta: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 grid(ceil_div(i1 - i0, 64), (unsigned)n_fine);
+  gather_theta_kernel<<<grid, 64, 0, (cudaStream_t)stream>>>(n_rows, n_el, e0, e1, i0, i1, wu, wv,
+                                                            nU, nB, u_el, u_loc, v_el, v_loc, wt,
+                                                            thetaT);
+  return check_launch("wq_gen_gather_theta");
+}
+
+int wq_gen_gather_d(int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1, int64_t l0, int64_t l1,
+                    int wv, int nB, const int64_t* v_el, const int64_t* v_loc, const double* wd,
+                    double* D, void* stream) {
+  if (l1 <= l0 || l0 < 0 || l1 > n_fine || !v_el || !v_loc || !wd || !D) {
+    set_error("wq_gen_gather_d: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 grid(ceil_div(n_fine, 128), (unsigned)(l1 - l0));
+  gather_d_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(n_fine, n_el, e0, e1, l0, l1, wv, nB,
+                                                         v_el, v_loc, wd, D);
+  return check_launch("wq_gen_gather_d");
+}
+
+int wq_band_solve_win(int64_t n, int64_t bw, const double* Lb, double* X, int64_t ncols,
+                      int64_t ldx, void* stream) {
+  if (n <= 0 || bw < 1 || bw > 8 || !Lb || !X || ncols <= 0 || ldx < ncols) {
+    set_error("wq_band_solve_win: bad arguments");
+    return WQ_EINVAL;
+  }
+  const unsigned grid = ceil_div(ncols, 64);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (bw) {
+    case 1: band_solve_win_kernel<1><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 2: band_solve_win_kernel<2><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 3: band_solve_win_kernel<3><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 4: band_solve_win_kernel<4><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 5: band_solve_win_kernel<5><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 6: band_solve_win_kernel<6><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 7: band_solve_win_kernel<7><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    default: band_solve_win_kernel<8><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+  }
+  return check_launch("wq_band_solve_win");
+}
+
+}  // extern "C"

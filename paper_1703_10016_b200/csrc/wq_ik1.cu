@@ -21,11 +21,28 @@ struct NodeRec {
   double s, fx, fy, J;
 };
 
+// J(mid)^2 for a distinct node pair within eps_diag, from the host table
+__device__ __forceinline__ bool near_pair_j2(const wq_smooth_t& sm, int64_t qa, int64_t ra,
+                                             double* R) {
+  int64_t lo = qa < ra ? qa : ra, d = qa < ra ? ra - qa : qa - ra;
+  if (sm.closed && sm.nq - d < d) {  // seam pair: forward from the larger index
+    lo = qa < ra ? ra : qa;
+    d = sm.nq - d;
+  }
+  if (d > sm.near_k) return false;
+  const double v = sm.near_j2[lo * sm.near_k + (d - 1)];
+  if (!(v > 0.0)) return false;
+  *R = v;
+  return true;
+}
+
 __device__ __forceinline__ double k1_value(const wq_smooth_t& sm, int64_t qa, const NodeRec& a,
                                            int64_t ra, const NodeRec& b, int* bad) {
   double R;
   if (qa == ra) {
     R = a.J * a.J;  // continuity limit J^2 (geometry.py:240-245)
+  } else if (sm.near_k > 0 && near_pair_j2(sm, qa, ra, &R)) {
+    // distinct nodes within eps_diag: J^2 at the pair midpoint (geometry.py:237-245)
   } else {
     double dx = a.fx - b.fx, dy = a.fy - b.fy;
     double dist2 = dx * dx + dy * dy;

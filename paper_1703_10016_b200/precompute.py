@@ -225,6 +225,14 @@ def regular_rule_band(parent: BasisSpec, fine: BasisSpec, nodes: np.ndarray) -> 
         sel = np.flatnonzero((j_len == sj) & (n_len == sn))
         Am = local[sel][:, :sj, :sn]
         bm = mu[sel][:, :sj]
+        if sj > sn:   # more exactness functions than nodes: rank < len(jsel) (quadrature.py:528-531)
+            # padded / seam-wrapped ranges hold zero or repeated rows: count
+            # the distinct live exactness functions
+            lm = (Am != 0.0).any(axis=2) | (bm != 0.0)
+            for k in range(len(sel)):
+                if len(np.unique(jidx[sel[k], :sj][lm[k]])) > sn:
+                    raise ConstructionError(
+                        f"rank-deficient local collocation matrix for weight {int(sel[k])}")
         u_, s_, vt = np.linalg.svd(Am, full_matrices=False)
         if np.any(s_[:, -1] <= max(sj, sn) * np.finfo(float).eps * s_[:, 0]):
             raise ConstructionError("rank-deficient local collocation matrix for a weight")
@@ -273,15 +281,42 @@ def k1_distance_table(nodes, closed, length):
     return inv
 
 
-def check_diagonal_pairs(nodes, closed, length):
-    """The kernel treats only n1 == n2 as the eps_diag limit (geometry.py:
-    237-245); verify no distinct node pair is that close."""
+def near_diagonal_pairs(nodes, closed, a, length, speed):
+    """Distinct node pairs within eps_diag = DIAG_REL L of each other take the
+    continuity limit J(mid)^2 (geometry.py:237-245) instead of the divided
+    difference.  Returns (K, table) with table[q, k-1] = J(mid)^2 for the pair
+    (q, q+k mod nq) when near, else 0; K = 0 (table None) when no distinct
+    pair is near (uniform meshes).  ``speed`` evaluates J at parameters; a is
+    the start of the curve's parameter domain."""
     eps = DIAG_REL * length
-    gaps = np.diff(nodes)
-    if closed and len(nodes) > 1:
-        gaps = np.append(gaps, length - (nodes[-1] - nodes[0]))
-    if len(gaps) and gaps.min() <= eps:
-        raise ConstructionError("node pair closer than the kernel's diagonal tolerance")
+    nq = len(nodes)
+    K = 0
+    while K + 1 < nq:
+        j = np.arange(nq) + K + 1
+        if not closed:
+            j = j[j < nq]
+        delta = nodes[np.mod(j, nq)] - nodes[: len(j)]
+        if closed:
+            delta = delta - length * np.round(delta / length)
+        if not np.any(np.abs(delta) <= eps):
+            break
+        K += 1
+    if K == 0:
+        return 0, None
+    table = np.zeros((nq, K))
+    for k in range(1, K + 1):
+        q = np.arange(nq if closed else nq - k)
+        s = nodes[q]
+        delta = nodes[np.mod(q + k, nq)] - s
+        if closed:
+            delta = delta - length * np.round(delta / length)
+        near = np.abs(delta) <= eps
+        if near.any():
+            mid = s[near] + 0.5 * delta[near]
+            if closed:
+                mid = a + np.mod(mid - a, length)
+            table[q[near], k - 1] = speed(mid) ** 2
+    return K, table
 
 
 # -- pair log moments: the analytic near-gap table (quadrature.py:182-197,372-410) ----
@@ -360,6 +395,105 @@ def uniform_width(fine: BasisSpec):
     if not np.allclose(widths, h, rtol=DEDUP_RTOL):
         raise ConstructionError("pair log moments require a uniform element mesh")
     return float(h)
+
+
+def is_uniform_mesh(fine: BasisSpec) -> bool:
+    widths = fine.elements[:, 1] - fine.elements[:, 0]
+    return bool(np.allclose(widths, widths.mean(), rtol=DEDUP_RTOL))
+
+
+# touching / overlapping element pairs (separation <= this fraction of the
+# larger width) use the closed form, as the reference's |gap| <= 1 entries
+# (quadrature.py:458); every other pair is analytic and takes Gauss
+NEAR_TOUCH = 1e-9
+# far-pair Gauss orders by separation (< 2, < 8, >= 8 larger widths); must match
+# the tier sizes compiled into wq_general.cu
+GEN_GAUSS_TIERS = (30, 16, 12)
+
+
+def log_gauss_unit(n: int, levels: int = 30, ratio: float = 0.25, m: int = 20):
+    """n-point Gauss rule for the weight -ln x on (0, 1): Stieltjes procedure
+    on a discrete measure (composite Gauss-Legendre on panels graded toward
+    0), eigen-decomposition of the Jacobi matrix.  Exact to ~1e-16 for
+    polynomials of degree <= 2n - 1 (tests/test_host.py)."""
+    x, w = np.polynomial.legendre.leggauss(m)
+    edges = np.concatenate([[0.0], ratio ** np.arange(levels, -1, -1.0)])
+    lo, hi = edges[:-1, None], edges[1:, None]
+    X = (0.5 * (lo + hi) + 0.5 * (hi - lo) * x).ravel()
+    Wt = (0.5 * (hi - lo) * w).ravel() * (-np.log(X))
+    a = np.zeros(n)
+    b = np.zeros(n)
+    p_prev, p = np.zeros_like(X), np.ones_like(X)
+    nrm_prev = 1.0
+    for k in range(n):
+        nrm = np.sum(Wt * p * p)
+        a[k] = np.sum(Wt * X * p * p) / nrm
+        b[k] = nrm / nrm_prev if k else 0.0
+        p_prev, p, nrm_prev = p, (X - a[k]) * p - b[k] * p_prev, nrm
+    jac = np.diag(a) + np.diag(np.sqrt(b[1:]), 1) + np.diag(np.sqrt(b[1:]), -1)
+    ev, vec = np.linalg.eigh(jac)
+    return ev, Wt.sum() * vec[0] ** 2
+
+
+# touching pairs of unequal widths: Duffy split of the pair rectangle at the
+# shared corner -> ln(xi) (log-weighted rule) + smooth terms (Gauss-Legendre);
+# sizes compiled into wq_general.cu
+TOUCH_XI, TOUCH_ETA, TOUCH_LOG = 16, 30, 14
+TOUCH_MAX_RATIO = 8.0
+
+
+def touch_rules() -> np.ndarray:
+    """Packed [x16, w16, x30, w30 (Gauss-Legendre on (0,1)), xl14, wl14
+    (weight -ln x on (0,1))]."""
+    out = []
+    for n in (TOUCH_XI, TOUCH_ETA):
+        x, w = np.polynomial.legendre.leggauss(n)
+        out += [0.5 * (x + 1.0), 0.5 * w]
+    out += list(log_gauss_unit(TOUCH_LOG))
+    return np.concatenate(out)
+
+
+def element_pair_geometry(fine: BasisSpec):
+    """Widths, midpoints and, per outer element e, the contiguous (cyclic on
+    closed meshes) range of inner elements f whose separation is at most
+    NEAR_TOUCH x max(h_e, h_f): f = lo[e] + k (mod n), k < cnt[e].
+    Same predicate and operation order as the restated reference recipe."""
+    els = fine.elements
+    n = len(els)
+    h = els[:, 1] - els[:, 0]
+    mid = 0.5 * (els[:, 0] + els[:, 1])
+    L = fine.length
+    win = 4
+    while True:
+        win = min(win, n // 2 if fine.closed else n - 1)
+        off = np.arange(-win, win + 1)
+        f = np.arange(n)[:, None] + off[None, :]
+        valid = np.ones_like(f, bool) if fine.closed else (f >= 0) & (f < n)
+        f = np.mod(f, n)
+        delta = mid[:, None] - mid[f]
+        if fine.closed:
+            delta = delta - L * np.round(delta / L)
+        sep = np.abs(delta) - 0.5 * (h[:, None] + h[f])
+        near = valid & (sep <= NEAR_TOUCH * np.maximum(h[:, None], h[f]))
+        edge = near[:, 0] | near[:, -1]
+        full = (2 * win + 1 >= n) if fine.closed else (win >= n - 1)
+        if not edge.any() or full:
+            break
+        win *= 2
+    if fine.closed and 2 * win + 1 > n:  # each residue once
+        near, off = near[:, :n], off[:n]
+    first = np.argmax(near, axis=1)
+    last = near.shape[1] - 1 - np.argmax(near[:, ::-1], axis=1)
+    lo = np.mod(np.arange(n) + off[first], n)
+    cnt = last - first + 1   # gaps inside the range also take the near route
+    # touching pairs of unequal widths: the Duffy rules are sized for ratios <= 8
+    f = np.mod(np.arange(n)[:, None] + off[None, :], n)
+    ratio = np.where(near, h[f] / h[:, None], 1.0)
+    ratio = np.maximum(ratio, 1.0 / ratio)
+    if ratio.max() > TOUCH_MAX_RATIO:
+        raise ConstructionError(
+            f"adjacent element width ratio {ratio.max():.3g} > {TOUCH_MAX_RATIO:g} unsupported")
+    return h, mid, lo.astype(np.int64), cnt.astype(np.int64)
 
 
 # -- fit normal equations (assembly.py:233-243 -> banded, SURVEY F8) -------------------

@@ -147,8 +147,62 @@ def test_errors_mirror_reference():
     slit = W.load_curve({"degree": 1, "knots": [-1, -1, 1, 1], "control_points": [[-1, 0], [1, 0]]})
     graded = W.make_open_basis(2, np.array([-1, -0.9, -0.5, 0.0, 0.5, 0.9, 1.0]))
     disc = W.build_discretization(slit, graded, 1)
+    # the reference raises here (quadrature.py:489-491); graded meshes take the
+    # per-pair route instead (config 5), the uniform-width helper still raises
     with pytest.raises(ConstructionError, match="uniform element mesh"):
-        AS._log_part(disc)   # quadrature.py:489-491
+        PC.uniform_width(disc.refined.basis)
+    lp = AS._log_part(disc)
+    assert lp.graded and lp.path == "general" and lp.h is None
+
+
+def _near_brute(fine):
+    els = fine.elements
+    h = els[:, 1] - els[:, 0]
+    mid = 0.5 * (els[:, 0] + els[:, 1])
+    delta = mid[:, None] - mid[None, :]
+    if fine.closed:
+        delta = delta - fine.length * np.round(delta / fine.length)
+    sep = np.abs(delta) - 0.5 * (h[:, None] + h[None, :])
+    return sep <= PC.NEAR_TOUCH * np.maximum(h[:, None], h[None, :])
+
+
+@pytest.mark.parametrize("closed", [False, True])
+@pytest.mark.parametrize("n", [3, 7, 40])
+def test_element_pair_geometry_matches_predicate(closed, n):
+    rng = np.random.default_rng(n)
+    c = np.cumsum(rng.normal(0.0, 0.5, n))          # widths drifting over decades
+    if closed:                                      # ... and matching across the seam
+        c -= np.arange(n) / max(n - 1, 1) * (c[-1] - c[0])
+    w = np.exp(c)
+    bp = np.concatenate([[0.0], np.cumsum(w)])
+    bp = bp / bp[-1]
+    space = W.make_cyclic_basis(2, bp) if closed else W.make_open_basis(2, bp)
+    fine = W.refine_uniform(space, 1).basis
+    h, mid, lo, cnt = PC.element_pair_geometry(fine)
+    near = _near_brute(fine)
+    got = np.zeros_like(near)
+    for e in range(n):
+        got[e, np.mod(lo[e] + np.arange(cnt[e]), n)] = True
+    # ranges are contiguous covers of the near set (gaps inside would take the
+    # closed form, which is exact for any offset); here they coincide
+    assert np.array_equal(got, near)
+    assert np.all(cnt >= 1) and np.all(cnt <= n)
+
+
+def test_touching_width_ratio_limit():
+    bp = np.array([0.0, 0.01, 0.1, 0.5, 1.0])     # 0.01 next to 0.09: ratio 9
+    with pytest.raises(ConstructionError, match="width ratio"):
+        PC.element_pair_geometry(W.make_open_basis(2, bp))
+    x, w = PC.log_gauss_unit(PC.TOUCH_LOG)          # weight -ln x on (0, 1)
+    k = np.arange(2 * PC.TOUCH_LOG)
+    assert np.abs((w[None, :] * x[None, :] ** k[:, None]).sum(1) * (k + 1.0) ** 2 - 1).max() < 1e-14
+
+
+def test_config5_mesh_reading():
+    space = O.config5_space()
+    assert space.dim == 20418          # 16384 elements + 4030 doubled knots (default_rng(0))
+    h = np.diff(space.breakpoints)
+    assert h.min() / h.max() == pytest.approx(0.9 ** 60, rel=1e-9)
 
 
 def test_precompute_is_linear_time():
@@ -160,3 +214,64 @@ def test_precompute_is_linear_time():
     rb = PC.regular_rule_band(space, fine, nodes)
     assert time.perf_counter() - t0 < 30.0
     assert rb.WG == 7 and np.ptp(rb.weights, axis=0).max() < 1e-15
+
+
+def test_graded_gather_dataflow_in_numpy():
+    """numpy rendition of the graded-mesh route (wq_gen_pair_blocks per chunk
+    of outer elements + wq_gen_gather_theta / wq_gen_gather_d with the host's
+    incidence arrays and chunk index ranges) against the restatement's Theta, D."""
+    for closed in (False, True):
+        rng = np.random.default_rng(11)
+        n = 24
+        w = np.exp(0.5 * rng.normal(size=n))
+        bp = np.concatenate([[0.0], np.cumsum(w)]) / w.sum()
+        if closed:
+            th = 2 * np.pi * np.arange(16) / 16
+            curve = W.load_curve({"degree": 3, "closed": True,
+                                  "breakpoints": np.linspace(0, 1, 17).tolist(),
+                                  "control_points": np.column_stack([2 * np.cos(th), np.sin(th)]).tolist()})
+            space = W.make_cyclic_basis(2, bp)
+        else:
+            curve = W.load_curve({"degree": 1, "knots": [0, 0, 1, 1], "control_points": [[-1, 0], [1, 0]]})
+            space = W.make_open_basis(3, bp, np.where(rng.random(n - 1) < 0.3, 2, 1))
+        disc = W.build_discretization(curve, space, 1)
+        lp = AS._log_part(disc)
+        assert lp.graded
+        N, NE = space.dim, disc.refined.basis.dim
+        fine = disc.refined.basis
+        delta_all = lp.elm[:, None] - lp.elm[None, :]
+        if closed:
+            delta_all = delta_all - fine.length * np.round(delta_all / fine.length)
+        thT = np.zeros((NE, N))
+        D = np.zeros((NE, NE))
+        chunk = 5
+        for e0 in range(0, n, chunk):
+            e1 = min(n, e0 + chunk)
+            es = np.arange(e0, e1)
+            he = np.repeat(lp.elh[es], n)
+            hf = np.tile(lp.elh, len(es))
+            m2 = O.pair_moments_general(lp.da, lp.db, he, hf, delta_all[es].ravel(),
+                                        closed_period=fine.length if closed else None)
+            m2 = m2.reshape(len(es), n, lp.da + 1, lp.db + 1)
+            wt = np.einsum("eap,efab,fbq->efpq", lp.u[es], m2, lp.v)
+            wd = np.einsum("eap,efab,fbq->efpq", lp.v[es], m2[:, :, : lp.db + 1], lp.v)
+            uc, vc = lp.ucols[e0:e1], lp.vcols[e0:e1]
+            for i in range(int(uc.min()), int(uc.max()) + 1):
+                for e, a in zip(lp.u_el[i], lp.u_loc[i]):
+                    if e0 <= e < e1:
+                        for l in range(NE):
+                            for f, b in zip(lp.v_el[l], lp.v_loc[l]):
+                                if f >= 0:
+                                    thT[l, i] += wt[e - e0, f, a, b]
+            for l in range(int(vc.min()), int(vc.max()) + 1):
+                for e, a in zip(lp.v_el[l], lp.v_loc[l]):
+                    if e0 <= e < e1:
+                        for m in range(NE):
+                            for f, b in zip(lp.v_el[m], lp.v_loc[m]):
+                                if f >= 0:
+                                    D[l, m] += wd[e - e0, f, a, b]
+        od = O.build_discretization(O.Curve(curve.basis, curve.control_points),
+                                    O.Basis(space.degree, space.knots, space.closed), 1)
+        theta, dmm, _ = O.ik2_ingredients_general(od)
+        assert rel(thT.T, theta) <= 1e-13
+        assert rel(D, dmm) <= 1e-13

@@ -69,3 +69,97 @@ def test_components_pair_table_and_local_coeffs():
     ref = z["closed1024_m2"]
     scale = np.abs(ref).max(axis=0, keepdims=True)
     assert np.abs(m2 - ref).max() <= 1e-15 * np.abs(ref).max()
+
+
+# uniform meshes of every kind the reference runs (open / closed / double
+# knots / nref=2): the per-pair generalisation used for graded meshes
+# (config 5) reproduces the reference's gap-table IK2
+@pytest.mark.parametrize("name", ["c1_slit_p2_n64", "slit_p4_n24_dbl", "parabola_p3_n16",
+                                  "ell_p3_n64", "closed_smooth_p3_n24", "slit_p2_n16_nref2",
+                                  "ell_p3_n32_nref2", "slit_p5_n24"])
+def test_general_pair_moments_match_reference_on_uniform_meshes(name):
+    z, meta = load(name)
+    curve, space = oracle_objects(meta)
+    disc = O.build_discretization(curve, space, meta["nref"])
+    ik2 = O.dense_ik2_general(disc)
+    assert np.abs(ik2 - z["ik2"]).max() / np.abs(z["M"]).max() <= 1e-13
+
+
+def test_general_pair_moments_scale_covariance():
+    """Graded pairs: M(e, f) of a pair scaled by s about the origin equals
+    s^(a+b+2) (M + ln s c_a(h_e) c_b(h_f)) -- the width-normalisation law."""
+    rng = np.random.default_rng(3)
+    n = 64
+    he = np.exp(rng.normal(-3, 1, n))
+    hf = he * np.exp(rng.normal(0, 0.7, n))
+    # off contact (the Gauss branch; the closed form's high slots are too
+    # ill-conditioned in delta' for a 1-ulp covariance check)
+    delta = rng.choice([-1.0, 1.0], n) * (0.5 * (he + hf) + np.maximum(he, hf) * rng.uniform(0.1, 3, n))
+    da, db = 8, 3
+    m = O.pair_moments_general(da, db, he, hf, delta)
+    s = 0.37
+    ms = O.pair_moments_general(da, db, s * he, s * hf, s * delta)
+    pa, pb = np.arange(da + 1), np.arange(db + 1)
+    ca = O.centred_integrals_scaled(da, he)
+    cb = O.centred_integrals_scaled(db, hf)
+    pred = s ** (2.0 + pa[None, :, None] + pb[None, None, :]) * (
+        m + np.log(s) * ca[:, :, None] * cb[:, None, :])
+    nat = ((s * he)[:, None, None] ** (pa[None, :, None] + 1.0)
+           * (s * hf)[:, None, None] ** (pb[None, None, :] + 1.0))
+    assert (np.abs(ms - pred) / nat).max() <= 1e-12
+    # exact for coincident and touching pairs against the uniform table
+    ut = O.unit_pair_stack(da, db, 8, False)
+    one = np.ones(3)
+    got = O.pair_moments_general(da, db, one, one, np.array([0.0, 1.0, -1.0]))
+    assert np.abs(got - ut[[7, 6, 8]]).max() <= 1e-15
+
+
+def _composite_pair_moments(da, db, rho, dl, n=24, levels=16, ratio=0.15):
+    """Independent check: tensor Gauss on panels graded geometrically toward
+    the closest corner of the pair (outer width 1, inner rho, offset dl)."""
+    x, w = np.polynomial.legendre.leggauss(n)
+
+    def panels(a, b, toward_a):
+        L = b - a
+        inner = [a + L * ratio ** k for k in range(levels, 0, -1)] if toward_a else \
+            [b - L * ratio ** k for k in range(1, levels + 1)]
+        e = np.array(sorted([a, b] + inner))
+        lo, hi = e[:-1, None], e[1:, None]
+        return (0.5 * (lo + hi) + 0.5 * (hi - lo) * x).ravel(), (0.5 * (hi - lo) * w).ravel()
+
+    U, WU = panels(-0.5, 0.5, dl > 0)
+    V, WV = panels(-rho / 2, rho / 2, dl < 0)
+    K = np.log(np.abs(V[None, :] - U[:, None] - dl))
+    A = WU[:, None] * U[:, None] ** np.arange(da + 1)[None, :]
+    B = WV[:, None] * V[:, None] ** np.arange(db + 1)[None, :]
+    return A.T @ K @ B
+
+
+def test_gauss_beats_closed_form_off_contact():
+    """The measurement behind NEAR_TOUCH: off contact, 30x30 Gauss is at
+    rounding level from separation 0.05 max(h) while the closed form loses
+    digits in the high slots; at contact the closed form is the reference's
+    own choice."""
+    da, db = 16, 4
+    pa, pb = np.arange(da + 1)[:, None], np.arange(db + 1)[None, :]
+    one = np.ones(1)
+    for rho in (1.0, 0.9, 2.0, 0.1):
+        nat = 0.5 ** pa * rho * (rho / 2) ** pb
+        for sepf in (0.05, 0.25, 1.0):
+            dl = 0.5 * (1 + rho) + sepf * max(1.0, rho)
+            ref = _composite_pair_moments(da, db, rho, dl, n=30)
+            g = O.pair_moments_gauss(da, db, one, rho * one, dl * one)[0]
+            c = O.pair_moments_closed(da, db, one, rho * one, dl * one)[0]
+            assert (np.abs(g - ref) / nat).max() <= 2e-14
+            assert (np.abs(c - ref) / nat).max() >= 1e-4
+            m = O.pair_moments_general(da, db, one, rho * one, dl * one)[0]
+            assert np.array_equal(m, g)        # off contact -> Gauss
+        dl = 0.5 * (1 + rho)                   # touching
+        m = O.pair_moments_general(da, db, one, rho * one, dl * one)[0]
+        if rho == 1.0:                         # the reference's closed form
+            assert np.array_equal(m, O.pair_moments_closed(da, db, one, one, dl * one)[0])
+        else:                                  # graded composite, independent of it
+            ref = _composite_pair_moments(da, db, rho, dl, n=30, levels=18, ratio=0.2)
+            assert (np.abs(m - ref) / nat).max() <= 5e-15
+            c = O.pair_moments_closed(da, db, one, rho * one, dl * one)[0]
+            assert (np.abs(c - ref) / nat).max() >= 1e-4
