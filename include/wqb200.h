@@ -304,7 +304,11 @@ int wq_b2_inner(int64_t M, const double* fx, const double* fy, const double* tx,
  * Gauss-Legendre on (0,1), xl14 wl14 for the weight -ln x); all other pairs
  * tensor Gauss (quadrature.py:413-438) with gx/gw = orders 30 | 16 | 12 on
  * (-1/2, 1/2), concatenated (30 below two larger widths of separation, 16
- * below eight, 12 beyond).
+ * below eight, 12 beyond).  Open meshes may pass m2u = wq_pair_table's UNIT
+ * gap table (h = 1, n_gap = 2 n_el - 1): far pairs of equal widths (1e-10
+ * relative) at integer offsets read M' there and scale it by their own width,
+ * M = h^(a+b+2) (M' + ln h c_a c_b) -- the reference's recipe
+ * (quadrature.py:497-500); NULL integrates every far pair.
  * ca/cb: centred monomial integrals c_a (da+1), c_b (db+1).  closed != 0 adds the
  * periodic gap term (quadrature.py:459-468) for period `period`.
  */
@@ -312,8 +316,9 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
                        double period, const double* elh, const double* elm, const double* u,
                        const double* v, const int64_t* near_lo, const int64_t* near_cnt,
                        int max_near, const double* near_unit, const double* touch,
-                       const double* gx, const double* gw, const double* ca,
-                       const double* cb, double* wt, double* wd, void* stream);
+                       const double* gx, const double* gw, const double* m2u,
+                       const double* ca, const double* cb, double* wt, double* wd,
+                       void* stream);
 
 /* thetaT[l][i] += sum over the chunk's incidences of i (u_el/u_loc, width wu) and
  * all incidences of l (v_el/v_loc, width wv, -1 padded) of wt blocks; i in [i0, i1). */

@@ -831,6 +831,10 @@ class CirculantRows:
 # (tests/test_oracle.py::test_gauss_beats_closed_form_off_contact).
 
 NEAR_TOUCH = 1e-9
+# widths equal to 1e-10 relative count as equal (rho = 1): breakpoints near 1 carry
+# ~1e-12 relative width noise at h ~ 1e-4 (C5), the reference's uniform check is
+# np.allclose(..., rtol=1e-12) with numpy's default atol 1e-8 (quadrature.py:489)
+WIDTH_SNAP = 1e-10
 
 
 def centred_integrals_scaled(n, rho):
@@ -876,7 +880,7 @@ def pair_moments_general(da, db, he, hf, delta, closed_period=None):
     dl = delta / he
     # equal widths at (rounding-)integer offsets: use the exact integer, as the
     # reference's gap-indexed unit table does (quadrature.py:452-456)
-    same = np.abs(rho - 1.0) < 1e-12
+    same = np.abs(rho - 1.0) < WIDTH_SNAP
     rho = np.where(same, 1.0, rho)
     snap = same & (np.abs(dl - np.rint(dl)) < 1e-9)
     dl = np.where(snap, np.rint(dl), dl)

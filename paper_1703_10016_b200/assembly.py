@@ -551,6 +551,25 @@ def _ik2_x2_into(disc, X, accumulate=True):
 
 # device bytes for one chunk of per-pair Theta / D blocks (graded meshes)
 _GEN_CHUNK_BYTES = 1 << 30
+# graded open meshes: read far pairs of equal widths from the unit gap table
+_GEN_GAP_TABLE = True
+
+
+def _gap_table(disc, lp: LogPart, h0: float):
+    """The reference's gap-indexed pair table (quadrature.py:441-504) for an
+    open mesh of n_el elements of width h0 (device, wq_pair_table; h0 = 1
+    gives the unit moments M')."""
+    torch = _torch()
+    n = lp.n_el
+    gx, gw = PC.gauss_unit(PC.PAIR_FAR_ORDER)
+    m2 = torch.empty((2 * n - 1, lp.da + 1, lp.db + 1), dtype=torch.float64, device="cuda")
+    keep = [_to_dev(torch, lp.near_unit), _to_dev(torch, gx), _to_dev(torch, gw),
+            _to_dev(torch, PC.centred_monomial_integrals(lp.da)),
+            _to_dev(torch, PC.centred_monomial_integrals(lp.db))]
+    _lib.call("wq_pair_table", n, 0, lp.da, lp.db, h0, _lib.ptr(keep[0]), _lib.ptr(keep[1]),
+              _lib.ptr(keep[2]), len(gx), _lib.ptr(keep[3]), _lib.ptr(keep[4]), _lib.ptr(m2),
+              _lib.stream_handle())
+    return m2
 
 
 def _graded_theta_d(disc, lp: LogPart, d):
@@ -570,6 +589,9 @@ def _graded_theta_d(disc, lp: LogPart, d):
     D = torch.zeros((NE, NE), dtype=torch.float64, device="cuda")
     max_near = int(lp.near_cnt.max())
     period = float(disc.refined.basis.length) if disc.closed else 0.0
+    # open meshes: the reference's unit gap table serves every far pair of
+    # equal widths at an integer offset (scaled per pair by the width)
+    m2u = _gap_table(disc, lp, 1.0) if not disc.closed and _GEN_GAP_TABLE else None
     wu, wv = lp.u_el.shape[1], lp.v_el.shape[1]
     for e0 in range(0, n, chunk):
         e1 = min(n, e0 + chunk)
@@ -577,7 +599,8 @@ def _graded_theta_d(disc, lp: LogPart, d):
                   _lib.ptr(d["elh"]), _lib.ptr(d["elm"]), _lib.ptr(d["u"]), _lib.ptr(d["v"]),
                   _lib.ptr(d["near_lo"]), _lib.ptr(d["near_cnt"]), max_near,
                   _lib.ptr(d["near_unit"]), _lib.ptr(d["touch"]), _lib.ptr(d["gx"]),
-                  _lib.ptr(d["gw"]), _lib.ptr(d["ca"]), _lib.ptr(d["cb"]), _lib.ptr(wt),
+                  _lib.ptr(d["gw"]), _lib.ptr(m2u) if m2u is not None else None,
+                  _lib.ptr(d["ca"]), _lib.ptr(d["cb"]), _lib.ptr(wt),
                   _lib.ptr(wd), st)
         uc, vc = lp.ucols[e0:e1], lp.vcols[e0:e1]
         _lib.call("wq_gen_gather_theta", N, NE, n, e0, e1, int(uc.min()), int(uc.max()) + 1, wu,

@@ -114,6 +114,7 @@ struct GenArgs {
   const double* touch;      // packed Duffy rules: x16 w16 x30 w30 on (0,1), xl14 wl14
   const double* gx;         // tier Gauss nodes on (-1/2, 1/2), 30 | 16 | 12 concatenated
   const double* gw;         // weights
+  const double* m2u;        // (2 n_el - 1, da+1, db+1) UNIT gap table (open meshes) or NULL
   const double* ca;         // (da+1) unit centred integrals
   const double* cb;         // (db+1)
   double* wt;               // (e1-e0, n_el, pu+1, db+1) Theta blocks
@@ -130,12 +131,108 @@ __device__ __forceinline__ bool is_near(const GenArgs& A, int64_t e, int64_t f) 
   return k < A.near_cnt[e];
 }
 
+// equal widths (to WIDTH_SNAP relative) at an integer offset: the reference's
+// unit gap-table recipe applies (quadrature.py:452-456, 497-500); same
+// predicate as oracle/wq_oracle.py::pair_moments_general
+constexpr double WIDTH_SNAP = 1e-10;
+
+__device__ __forceinline__ bool snapped_gap(double he, double hf, double delta, double* gap) {
+  const double rho = hf / he;
+  if (!(fabs(rho - 1.0) < WIDTH_SNAP)) return false;
+  const double dl = delta / he, r = rint(dl);
+  if (!(fabs(dl - r) < 1e-9)) return false;
+  *gap = -r;  // keff = f - e in element units
+  return true;
+}
+
 constexpr int FP_THREADS = 64;
 
-// One CTA per (64 inner elements f, one outer element e of the chunk); one
-// thread per pair.  NP = p + 1 = d + 1 columns on both sides (compile time, so
-// the 2 x NP^2 block accumulators stay in registers).  The outer element's
-// weighted polynomial values at every tier's nodes sit in shared memory.
+// Far pairs of snapped widths: unit moments from the gap table M' (rows
+// f - e + n - 1), staged for the CTA's 64 consecutive inner elements, scaled
+// M = h_e^(a+b+2) (M' + ln h_e c_a c_b) and contracted to the blocks.
+template <int NP>
+__global__ void __launch_bounds__(FP_THREADS)
+pair_table_kernel(GenArgs A) {
+  extern __shared__ double sm[];
+  const int nA = A.da + 1;
+  const int64_t e = A.e0 + blockIdx.y;
+  const int64_t f0 = (int64_t)blockIdx.x * FP_THREADS;
+  const int nf = (int)min((int64_t)FP_THREADS, A.n_el - f0);
+  double* Mt = sm;                              // [FP_THREADS][nA * NP]
+  double* Ue = Mt + FP_THREADS * nA * NP;       // [nA][NP]
+  double* Ve = Ue + nA * NP;                    // [NP][NP]
+  double* Sc = Ve + NP * NP;                    // [nA] h^(a+2), [NP] h^b, [nA*NP] ln h c_a c_b
+  const double he = A.elh[e];
+  const int64_t row0 = f0 - e + A.n_el - 1;
+  for (int k = threadIdx.x; k < nf * nA * NP; k += FP_THREADS) Mt[k] = A.m2u[row0 * nA * NP + k];
+  for (int k = threadIdx.x; k < nA * NP; k += FP_THREADS) Ue[k] = A.u[e * nA * NP + k];
+  for (int k = threadIdx.x; k < NP * NP; k += FP_THREADS) Ve[k] = A.v[e * NP * NP + k];
+  if (threadIdx.x == 0) {
+    double p = he * he;
+    for (int a = 0; a < nA; ++a, p *= he) Sc[a] = p;
+    p = 1.0;
+    for (int b = 0; b < NP; ++b, p *= he) Sc[nA + b] = p;
+  }
+  const double lh = log(he);
+  for (int k = threadIdx.x; k < nA * NP; k += FP_THREADS)
+    Sc[nA + NP + k] = lh * (A.ca[k / NP] * A.cb[k % NP]);
+  __syncthreads();
+  const int64_t f = f0 + threadIdx.x;
+  if (threadIdx.x >= nf || is_near(A, e, f)) return;
+  const double hf = A.elh[f];
+  double gap;
+  if (!snapped_gap(he, hf, A.elm[e] - A.elm[f], &gap) || fabs(gap) > (double)(A.n_el - 1)) return;
+  double vf[NP][NP];
+#pragma unroll
+  for (int b = 0; b < NP; ++b)
+#pragma unroll
+    for (int bp = 0; bp < NP; ++bp) vf[b][bp] = A.v[(f * NP + b) * NP + bp];
+  double wT[NP][NP], wD[NP][NP];
+#pragma unroll
+  for (int a = 0; a < NP; ++a)
+#pragma unroll
+    for (int b = 0; b < NP; ++b) wT[a][b] = wD[a][b] = 0.0;
+  // staged rows are indexed by f - e; equal widths at a different integer
+  // geometric offset (e.g. mirrored graded elements) read their own row
+  const double* M = gap == (double)(f - e) ? Mt + threadIdx.x * nA * NP
+                                           : A.m2u + ((int64_t)gap + A.n_el - 1) * nA * NP;
+  const double* L = Sc + nA + NP;
+#pragma unroll 1
+  for (int al = 0; al < nA; ++al) {
+    const double ha = Sc[al];
+    double mv[NP];
+#pragma unroll
+    for (int bp = 0; bp < NP; ++bp) mv[bp] = 0.0;
+#pragma unroll
+    for (int be = 0; be < NP; ++be) {
+      const double m = ha * Sc[nA + be] * (M[al * NP + be] + L[al * NP + be]);
+#pragma unroll
+      for (int bp = 0; bp < NP; ++bp) mv[bp] = fma(m, vf[be][bp], mv[bp]);
+    }
+#pragma unroll
+    for (int a = 0; a < NP; ++a)
+#pragma unroll
+      for (int bp = 0; bp < NP; ++bp) wT[a][bp] = fma(Ue[al * NP + a], mv[bp], wT[a][bp]);
+    if (al < NP) {
+#pragma unroll
+      for (int a = 0; a < NP; ++a)
+#pragma unroll
+        for (int bp = 0; bp < NP; ++bp) wD[a][bp] = fma(Ve[al * NP + a], mv[bp], wD[a][bp]);
+    }
+  }
+  double* wt = A.wt + ((e - A.e0) * A.n_el + f) * NP * NP;
+  double* wd = A.wd + ((e - A.e0) * A.n_el + f) * NP * NP;
+#pragma unroll
+  for (int a = 0; a < NP; ++a)
+#pragma unroll
+    for (int bp = 0; bp < NP; ++bp) {
+      wt[a * NP + bp] = wT[a][bp];
+      wd[a * NP + bp] = wD[a][bp];
+    }
+}
+
+// Far pairs off the table: tensor Gauss on the contracted integrand, one
+// thread per pair, tier tables of the outer element in shared memory.
 template <int NP>
 __global__ void __launch_bounds__(FP_THREADS)
 pair_far_kernel(GenArgs A) {
@@ -146,6 +243,13 @@ pair_far_kernel(GenArgs A) {
   const int nA = A.da + 1;
   const int64_t e = A.e0 + blockIdx.y;
   const double he = A.elh[e];
+  const int64_t f = (int64_t)blockIdx.x * FP_THREADS + threadIdx.x;
+  bool mine = f < A.n_el && !is_near(A, e, f);
+  double gap;
+  if (mine && A.m2u && snapped_gap(he, A.elh[f], A.elm[e] - A.elm[f], &gap) &&
+      fabs(gap) <= (double)(A.n_el - 1))
+    mine = false;  // pair_table_kernel's
+  if (!__syncthreads_or(mine)) return;
   for (int g = threadIdx.x; g < GTSUM; g += FP_THREADS) {
     Gx[g] = A.gx[g];
     Gw[g] = A.gw[g];
@@ -165,12 +269,13 @@ pair_far_kernel(GenArgs A) {
     }
   }
   __syncthreads();
-  const int64_t f = (int64_t)blockIdx.x * FP_THREADS + threadIdx.x;
-  if (f >= A.n_el || is_near(A, e, f)) return;
+  if (!mine) return;
   const double hf = A.elh[f];
   const double delta = wrap_delta(A, A.elm[e] - A.elm[f]);
   const double sep = fabs(delta) - 0.5 * (he + hf);
   const double hm = fmax(he, hf);
+  // Gauss order by separation in units of the larger width (measured: <= 5e-15
+  // of the natural slot scale at degree 16 x 4 for every tier)
   const int t0 = sep < 2.0 * hm ? 0 : (sep < 8.0 * hm ? GT0 : GT0 + GT1);
   const int ng = sep < 2.0 * hm ? GT0 : (sep < 8.0 * hm ? GT1 : GT2);
   double vf[NP][NP];
@@ -229,142 +334,147 @@ pair_far_kernel(GenArgs A) {
 }
 
 constexpr int TOUCH_XI = 16, TOUCH_ETA = 30, TOUCH_LOG = 14;
+constexpr int NP_WARPS = 4;
 
-// Touching pair of unequal widths (outer 1, inner rho, dl = sig (1 + rho)/2):
-// with t, y the distances from the shared corner, ln|v - u - dl| = ln(t + y);
-// the Duffy split y <= rho t (y = rho xi eta) / y >= rho t (t = xi eta, y = rho xi)
-// gives  rho xi [ln xi + g(eta)],  g = ln(1 + rho eta) | ln(rho + eta):
-// ln xi by the -ln-weighted rule, the rest by Gauss-Legendre (exact in xi for
-// the degree <= P + d + 1 polynomials; g analytic for rho in [1/8, 8]).
-__device__ void pair_touch(int da, int db, double rho, double sig, const double* R, double* out,
-                           int ldo) {
-  const double* x16 = R;
-  const double* w16 = R + TOUCH_XI;
-  const double* x30 = R + 2 * TOUCH_XI;
-  const double* w30 = x30 + TOUCH_ETA;
-  const double* xl = w30 + TOUCH_ETA;
-  const double* wl = xl + TOUCH_LOG;
-  for (int tri = 0; tri < 2; ++tri) {
-    for (int k = 0; k < TOUCH_ETA; ++k) {
-      const double eta = x30[k];
-      const double g = tri == 0 ? log1p(rho * eta) : log(rho + eta);
-      for (int j = 0; j < TOUCH_XI + TOUCH_LOG; ++j) {
-        const bool lg = j >= TOUCH_XI;
-        const double xi = lg ? xl[j - TOUCH_XI] : x16[j];
-        const double wx = lg ? -wl[j - TOUCH_XI] : w16[j] * g;
-        double u, v;
-        if (tri == 0) {
-          u = sig * (xi - 0.5);
-          v = -sig * rho * (xi * eta - 0.5);
-        } else {
-          u = sig * (xi * eta - 0.5);
-          v = -sig * rho * (xi - 0.5);
-        }
-        double ua = w30[k] * wx * rho * xi;
-        for (int a = 0; a <= da; ++a) {
-          double t = ua;
-          for (int b = 0; b <= db; ++b) {
-            out[a * ldo + b] += t;
-            t *= v;
-          }
-          ua *= u;
-        }
-      }
-    }
-  }
-}
-
-constexpr int NP_THREADS = 32;
-
-// Near pairs: one thread per (e, k < near_cnt[e]); moment matrix in shared memory.
-__global__ void __launch_bounds__(NP_THREADS)
+// Near (touching / overlapping) pairs, one warp per pair.  Unit moments M'
+// (he = 1, hf = rho, delta' = dl) with the 85 (a, b) slots spread over the
+// lanes:
+//   rho == 1 at integer dl: the host's closed-form unit rows (the reference's
+//     |gap| <= 1 entries, quadrature.py:372-410);
+//   rho != 1 (touching): Duffy split at the shared corner -- with t, y the
+//     distances from the corner, ln|v - u - dl| = ln(t + y); y <= rho t as
+//     (xi, rho xi eta), y >= rho t as (xi eta, rho xi), Jacobian rho xi:
+//     ln xi by the -ln-weighted rule, g = ln(1 + rho eta) | ln(rho + eta) by
+//     Gauss-Legendre (exact in xi for the degree <= P + d + 1 polynomials;
+//     g analytic for rho in [1/8, 8]);
+//   closed meshes add the periodic term ln|sinc| by 30 x 30 Gauss.
+// Then M = h_e^(a+b+2) (M' + ln h_e c_a C_b(rho)) and the contraction.
+__global__ void __launch_bounds__(NP_WARPS * 32)
 pair_near_kernel(GenArgs A, int max_near) {
   extern __shared__ double sh[];
-  const int nA = A.da + 1, nB = A.db + 1, nU = A.pu + 1;
+  const int nA = A.da + 1, nB = A.db + 1, nU = A.pu + 1, ns = nA * nB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t e = A.e0 + blockIdx.y;
-  const int k = blockIdx.x * NP_THREADS + threadIdx.x;
+  const int k = blockIdx.x * NP_WARPS + warp;
   if (k >= A.near_cnt[e] || k >= max_near) return;
   int64_t f = A.near_lo[e] + k;
   if (f >= A.n_el) f -= A.n_el;
-  double* M = sh + threadIdx.x * nA * nB;
-  for (int i = 0; i < nA * nB; ++i) M[i] = 0.0;
+  double* M = sh + warp * ns;
   const double he = A.elh[e], hf = A.elh[f];
   const double delta = wrap_delta(A, A.elm[e] - A.elm[f]);
   double rho = hf / he, dl = delta / he;
-  if (fabs(rho - 1.0) < 1e-12) {  // exact integer gaps as the unit table (quadrature.py:452-456)
+  if (fabs(rho - 1.0) < WIDTH_SNAP) {  // exact integer gaps as the unit table (quadrature.py:452-456)
     rho = 1.0;
     if (fabs(dl - rint(dl)) < 1e-9) dl = rint(dl);
   }
+  // lane-owned slots s = lane + 32 j
+  constexpr int SL = (GMAXA * GMAXB + 31) / 32;   // slots per lane
+  double acc[SL];
+  int sa[SL], sb[SL];
+  for (int j = 0; j < SL; ++j) {
+    acc[j] = 0.0;
+    const int s = lane + 32 * j;
+    sa[j] = s < ns ? s / nB : -1;
+    sb[j] = s < ns ? s % nB : 0;
+  }
   if (rho == 1.0 && (dl == -1.0 || dl == 0.0 || dl == 1.0)) {
-    // equal widths: the reference's closed-form unit entries, host-computed
-    const double* t = A.near_unit + (int)(1.0 - dl) * nA * nB;  // rows keff = -dl = -1, 0, 1
-    for (int i = 0; i < nA * nB; ++i) M[i] = t[i];
+    const double* t = A.near_unit + (int)(1.0 - dl) * ns;  // rows keff = -dl = -1, 0, 1
+    for (int j = 0; j < SL; ++j)
+      if (sa[j] >= 0) acc[j] = t[lane + 32 * j];
   } else if (rho == 1.0) {
-    pair_closed(A.da, A.db, rho, dl, M, nB);
+    if (lane == 0) {
+      for (int i = 0; i < ns; ++i) M[i] = 0.0;
+      pair_closed(A.da, A.db, rho, dl, M, nB);
+    }
+    __syncwarp();
+    for (int j = 0; j < SL; ++j)
+      if (sa[j] >= 0) acc[j] = M[lane + 32 * j];
+    __syncwarp();
   } else {
-    pair_touch(A.da, A.db, rho, dl > 0.0 ? 1.0 : -1.0, A.touch, M, nB);
+    const double sig = dl > 0.0 ? 1.0 : -1.0;
+    const double* R = A.touch;
+    const double* x16 = R;
+    const double* w16 = R + TOUCH_XI;
+    const double* x30 = R + 2 * TOUCH_XI;
+    const double* w30 = x30 + TOUCH_ETA;
+    const double* xl = w30 + TOUCH_ETA;
+    const double* wl = xl + TOUCH_LOG;
+    for (int tri = 0; tri < 2; ++tri) {
+      for (int q = 0; q < TOUCH_ETA; ++q) {
+        const double eta = x30[q];
+        const double g = tri == 0 ? log1p(rho * eta) : log(rho + eta);
+        for (int jx = 0; jx < TOUCH_XI + TOUCH_LOG; ++jx) {
+          const bool lg = jx >= TOUCH_XI;
+          const double xi = lg ? xl[jx - TOUCH_XI] : x16[jx];
+          const double wx = w30[q] * rho * xi * (lg ? -wl[jx - TOUCH_XI] : w16[jx] * g);
+          double u, v;
+          if (tri == 0) {
+            u = sig * (xi - 0.5);
+            v = -sig * rho * (xi * eta - 0.5);
+          } else {
+            u = sig * (xi * eta - 0.5);
+            v = -sig * rho * (xi - 0.5);
+          }
+          for (int j = 0; j < SL; ++j) {
+            if (sa[j] < 0) continue;
+            double t = wx;
+            for (int i = 0; i < sa[j]; ++i) t *= u;
+            for (int i = 0; i < sb[j]; ++i) t *= v;
+            acc[j] += t;
+          }
+        }
+      }
+    }
   }
   if (A.closed) {  // periodic gap term, 30 x 30 Gauss (quadrature.py:459-468)
     const double per = A.period / he;
     for (int g = 0; g < GT0; ++g) {
-      double t[GMAXB];
-      for (int b = 0; b < nB; ++b) t[b] = 0.0;
+      const double xg = A.gx[g];
       for (int h = 0; h < GT0; ++h) {
         const double xh = A.gx[h];
-        const double arg = (rho * xh - A.gx[g]) - dl;
-        const double yy = arg / per;
+        const double yy = ((rho * xh - xg) - dl) / per;
         const double kv = yy == 0.0 ? 0.0 : log(fabs(sinpi(yy) / (kPi * yy)));
-        double wv = A.gw[h] * rho;
-        for (int b = 0; b < nB; ++b) {
-          t[b] = fma(kv, wv, t[b]);
-          wv *= rho * xh;
+        const double w = A.gw[g] * A.gw[h] * rho * kv;
+        for (int j = 0; j < SL; ++j) {
+          if (sa[j] < 0) continue;
+          double t = w;
+          for (int i = 0; i < sa[j]; ++i) t *= xg;
+          for (int i = 0; i < sb[j]; ++i) t *= rho * xh;
+          acc[j] += t;
         }
-      }
-      double wu = A.gw[g];
-      for (int a = 0; a < nA; ++a) {
-        for (int b = 0; b < nB; ++b) M[a * nB + b] = fma(wu, t[b], M[a * nB + b]);
-        wu *= A.gx[g];
       }
     }
   }
   const double lh = log(he);
-  double hea = he * he;
-  double rp = rho;
-  double cbr[GMAXB];
-  for (int b = 0; b < nB; ++b) {
-    cbr[b] = rp * A.cb[b];
-    rp *= rho;
+  for (int j = 0; j < SL; ++j) {
+    if (sa[j] < 0) continue;
+    const int a = sa[j], b = sb[j];
+    double s = 1.0, rp = rho;
+    for (int i = 0; i < a + b + 2; ++i) s *= he;
+    for (int i = 0; i < b; ++i) rp *= rho;
+    M[lane + 32 * j] = s * (acc[j] + lh * (A.ca[a] * (rp * A.cb[b])));
   }
-  for (int a = 0; a < nA; ++a) {
-    double s = hea;
-    for (int b = 0; b < nB; ++b) {
-      M[a * nB + b] = s * (M[a * nB + b] + lh * (A.ca[a] * cbr[b]));
-      s *= he;
-    }
-    hea *= he;
-  }
+  __syncwarp();
+  // contraction: 2 nU nB... outputs over the lanes
   const double* ue = A.u + e * nA * nU;
   const double* ve = A.v + e * nB * nB;
   const double* vf = A.v + f * nB * nB;
   double* wt = A.wt + ((e - A.e0) * A.n_el + f) * nU * nB;
   double* wd = A.wd + ((e - A.e0) * A.n_el + f) * nB * nB;
-  for (int bp = 0; bp < nB; ++bp) {
-    double mv[GMAXA];
-    for (int al = 0; al < nA; ++al) {
-      double s = 0.0;
-      for (int be = 0; be < nB; ++be) s = fma(M[al * nB + be], vf[be * nB + bp], s);
-      mv[al] = s;
+  for (int o = lane; o < nU * nB + nB * nB; o += 32) {
+    const bool th = o < nU * nB;
+    const int oo = th ? o : o - nU * nB;
+    const int ap = oo / nB, bp = oo % nB;
+    const int na = th ? nA : nB;
+    const double* c = th ? ue : ve;
+    const int ldc = th ? nU : nB;
+    double s = 0.0;
+    for (int al = 0; al < na; ++al) {
+      double mv = 0.0;
+      for (int be = 0; be < nB; ++be) mv = fma(M[al * nB + be], vf[be * nB + bp], mv);
+      s = fma(c[al * ldc + ap], mv, s);
     }
-    for (int ap = 0; ap < nU; ++ap) {
-      double s = 0.0;
-      for (int al = 0; al < nA; ++al) s = fma(ue[al * nU + ap], mv[al], s);
-      wt[ap * nB + bp] = s;
-    }
-    for (int ap = 0; ap < nB; ++ap) {
-      double s = 0.0;
-      for (int al = 0; al < nB; ++al) s = fma(ve[al * nB + ap], mv[al], s);
-      wd[ap * nB + bp] = s;
-    }
+    if (th) wt[oo] = s; else wd[oo] = s;
   }
 }
 
@@ -461,35 +571,50 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
                        double period, const double* elh, const double* elm, const double* u,
                        const double* v, const int64_t* near_lo, const int64_t* near_cnt,
                        int max_near, const double* near_unit, const double* touch,
-                       const double* gx, const double* gw, const double* ca, const double* cb, double* wt, double* wd,
+                       const double* gx, const double* gw, const double* m2u,
+                       const double* ca, const double* cb, double* wt, double* wd,
                        void* stream) {
   if (n_el <= 0 || e0 < 0 || e1 > n_el || e1 <= e0 || da + 1 > GMAXA || db + 1 > GMAXB ||
       db < 1 || pu != db || max_near < 0 || !near_unit || !touch || !gx || !gw || !elh || !elm || !u || !v || !near_lo || !near_cnt ||
-      !ca || !cb || !wt || !wd || (closed && !(period > 0))) {
+      !ca || !cb || !wt || !wd || (closed && !(period > 0)) || (m2u && closed)) {
     set_error("wq_gen_pair_blocks: bad arguments");
     return WQ_EINVAL;
   }
   int rc = ensure_consts();
   if (rc) return rc;
   GenArgs A{n_el, e0, e1, da, db, pu, closed, period, elh, elm, u, v, near_lo, near_cnt,
-            near_unit, touch, gx, gw, ca, cb, wt, wd};
+            near_unit, touch, gx, gw, m2u, ca, cb, wt, wd};
   cudaStream_t st = (cudaStream_t)stream;
   dim3 g1(ceil_div(n_el, FP_THREADS), (unsigned)(e1 - e0));
-  switch (db + 1) {
-    case 2: pair_far_kernel<2><<<g1, FP_THREADS, 0, st>>>(A); break;
-    case 3: pair_far_kernel<3><<<g1, FP_THREADS, 0, st>>>(A); break;
-    case 4: pair_far_kernel<4><<<g1, FP_THREADS, 0, st>>>(A); break;
-    case 5: pair_far_kernel<5><<<g1, FP_THREADS, 0, st>>>(A); break;
-    case 6: pair_far_kernel<6><<<g1, FP_THREADS, 0, st>>>(A); break;
-    case 7: pair_far_kernel<7><<<g1, FP_THREADS, 0, st>>>(A); break;
-    default: pair_far_kernel<8><<<g1, FP_THREADS, 0, st>>>(A); break;
+  const int nA = da + 1, np1 = db + 1;
+  const size_t tsm = (size_t)(FP_THREADS * nA * np1 + nA * np1 + np1 * np1 + nA + np1 + nA * np1) * 8;
+#define WQ_GEN_CASE(NP)                                                                      \
+  case NP:                                                                                   \
+    if (m2u) {                                                                               \
+      cudaFuncSetAttribute(pair_table_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)tsm);                                                        \
+      pair_table_kernel<NP><<<g1, FP_THREADS, tsm, st>>>(A);                                 \
+    }                                                                                        \
+    pair_far_kernel<NP><<<g1, FP_THREADS, 0, st>>>(A);                                       \
+    break;
+  switch (np1) {
+    WQ_GEN_CASE(2)
+    WQ_GEN_CASE(3)
+    WQ_GEN_CASE(4)
+    WQ_GEN_CASE(5)
+    WQ_GEN_CASE(6)
+    WQ_GEN_CASE(7)
+    WQ_GEN_CASE(8)
+    default:
+      set_error("wq_gen_pair_blocks: degree %d unsupported", db);
+      return WQ_EUNSUPPORTED;
   }
+#undef WQ_GEN_CASE
   rc = check_launch("wq_gen_pair_blocks(far)");
   if (rc || max_near == 0) return rc;
-  const size_t smem = (size_t)NP_THREADS * (da + 1) * (db + 1) * sizeof(double);
-  cudaFuncSetAttribute(pair_near_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 g2(ceil_div(max_near, NP_THREADS), (unsigned)(e1 - e0));
-  pair_near_kernel<<<g2, NP_THREADS, smem, st>>>(A, max_near);
+  const size_t smem = (size_t)NP_WARPS * nA * np1 * sizeof(double);
+  dim3 g2(ceil_div(max_near, NP_WARPS), (unsigned)(e1 - e0));
+  pair_near_kernel<<<g2, NP_WARPS * 32, smem, st>>>(A, max_near);
   return check_launch("wq_gen_pair_blocks(near)");
 }
 
