@@ -293,24 +293,25 @@ int wq_b2_inner(int64_t M, const double* fx, const double* fy, const double* tx,
  * Theta / D accumulation of _log_part (assembly.py:206-236), per element pair.
  *
  * wq_gen_pair_blocks: for outer elements e in [e0, e1) and every inner element f,
- *   wt[e-e0][f] = U_e^T M(e,f) V_f  ((pu+1) x (db+1); pu must equal db)
- *   wd[e-e0][f] = V_e^T M(e,f) V_f  ((db+1) x (db+1))
- * elh/elm: element widths / midpoints; u (n_el, da+1, pu+1), v (n_el, db+1, db+1)
- * centred-monomial coefficients (splines.py:427-472; u times the fitted J);
- * near (touching / overlapping) pairs of e are f = near_lo[e] + k (mod n_el),
- * k < near_cnt[e] <= max_near: equal widths take near_unit (3 x (da+1) x (db+1),
- * the closed-form unit entries at dl = -1, 0, 1, quadrature.py:372-410, 458),
- * unequal widths a Duffy split with the packed rules `touch` (x16 w16 x30 w30
- * Gauss-Legendre on (0,1), xl14 wl14 for the weight -ln x); all other pairs
- * tensor Gauss (quadrature.py:413-438) with gx/gw = orders 30 | 16 | 12 on
- * (-1/2, 1/2), concatenated (30 below two larger widths of separation, 16
- * below eight, 12 beyond).  Open meshes may pass m2u = wq_pair_table's UNIT
- * gap table (h = 1, n_gap = 2 n_el - 1): far pairs of equal widths (1e-10
- * relative) at integer offsets read M' there and scale it by their own width,
+ *   WT[f][a'][b'][e-e0] = (U_e^T M(e,f) V_f)[a'][b']   ((pu+1) x (db+1); pu == db)
+ *   WD[f][a'][b'][e-e0] = (V_e^T M(e,f) V_f)[a'][b']   ((db+1) x (db+1))
+ * (chunk-minor, leading dimension ldc >= e1 - e0).  elh/elm: element widths /
+ * midpoints; u (n_el, da+1, pu+1), v (n_el, db+1, db+1) centred-monomial
+ * coefficients (splines.py:427-472; u times the fitted J).  Near (touching /
+ * overlapping) pairs of e are f = near_lo[e] + k (mod n_el), k < near_cnt[e] <=
+ * max_near: equal widths take near_unit (3 x (da+1) x (db+1), the closed-form unit
+ * entries at dl = -1, 0, 1, quadrature.py:372-410, 458), unequal widths a Duffy
+ * split with the packed rules `touch` (x16 w16 x30 w30 Gauss-Legendre on (0,1),
+ * xl14 wl14 for the weight -ln x).  Other pairs: with m2u (wq_pair_table's UNIT
+ * gap table, h = 1, n_gap = 2 n_el - 1; open meshes) equal widths (1e-10
+ * relative) at integer offsets read M' and scale it by their own width,
  * M = h^(a+b+2) (M' + ln h c_a c_b) -- the reference's recipe
- * (quadrature.py:497-500); NULL integrates every far pair.
- * ca/cb: centred monomial integrals c_a (da+1), c_b (db+1).  closed != 0 adds the
- * periodic gap term (quadrature.py:459-468) for period `period`.
+ * (quadrature.py:497-500); the rest tensor Gauss (quadrature.py:413-438), gx/gw
+ * = orders 30 | 16 | 12 on (-1/2, 1/2) concatenated (30 below two larger widths
+ * of separation, 16 below eight, 12 beyond).  tile_flag (device ints,
+ * n_el x ceil((e1-e0)/64), required with m2u) is scratch marking the tiles that
+ * still need Gauss.  ca/cb: centred monomial integrals (da+1), (db+1); closed != 0
+ * adds the periodic gap term (quadrature.py:459-468) for period `period`.
  */
 int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int pu, int closed,
                        double period, const double* elh, const double* elm, const double* u,
@@ -318,17 +319,18 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
                        int max_near, const double* near_unit, const double* touch,
                        const double* gx, const double* gw, const double* m2u,
                        const double* ca, const double* cb, double* wt, double* wd,
-                       void* stream);
+                       int64_t ldc, int* tile_flag, void* stream);
 
 /* thetaT[l][i] += sum over the chunk's incidences of i (u_el/u_loc, width wu) and
- * all incidences of l (v_el/v_loc, width wv, -1 padded) of wt blocks; i in [i0, i1). */
-int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1,
+ * all incidences of l (v_el/v_loc, width wv, -1 padded) of WT blocks; i in [i0, i1). */
+int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc,
                         int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
                         const int64_t* u_el, const int64_t* u_loc, const int64_t* v_el,
                         const int64_t* v_loc, const double* wt, double* thetaT, void* stream);
 
-/* D[l][m] += chunk contributions of wd blocks, l in [l0, l1), all m. */
-int wq_gen_gather_d(int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1, int64_t l0, int64_t l1,
+/* D (symmetric, N_E x N_E) += chunk contributions of WD blocks for rows l in
+ * [l0, l1), stored transposed (D[m][l]) so the stores are coalesced. */
+int wq_gen_gather_d(int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc, int64_t l0, int64_t l1,
                     int wv, int nB, const int64_t* v_el, const int64_t* v_loc, const double* wd,
                     double* D, void* stream);
 

@@ -882,7 +882,9 @@ def pair_moments_general(da, db, he, hf, delta, closed_period=None):
     # reference's gap-indexed unit table does (quadrature.py:452-456)
     same = np.abs(rho - 1.0) < WIDTH_SNAP
     rho = np.where(same, 1.0, rho)
-    snap = same & (np.abs(dl - np.rint(dl)) < 1e-9)
+    # integer offsets to 1e-9 relative: dl = delta / h carries the breakpoints'
+    # ~1e-12 relative rounding times |dl| (up to ~1.6e-8 at |dl| = 16000, C5)
+    snap = same & (np.abs(dl - np.rint(dl)) < 1e-9 * np.maximum(1.0, np.abs(dl)))
     dl = np.where(snap, np.rint(dl), dl)
     sep = np.abs(delta) - 0.5 * (he + hf)
     near = sep <= NEAR_TOUCH * np.maximum(he, hf)

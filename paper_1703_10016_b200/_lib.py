@@ -93,7 +93,7 @@ _SIGS = {
     "wq_probe_phi": [c_int, c_int, c_int, c_vp, c_vp, c_vp],
     "wq_gen_pair_blocks": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_vp,
                            c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
-                           c_vp, c_vp, c_vp, c_vp, c_vp],
+                           c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],
     "wq_gen_gather_theta": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_int,
                             c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "wq_gen_gather_d": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,

@@ -582,9 +582,10 @@ def _graded_theta_d(disc, lp: LogPart, d):
     N, NE, n = disc.space.dim, disc.refined.basis.dim, lp.n_el
     nU, nB = lp.u.shape[2], lp.db + 1
     per_e = n * (nU * nB + nB * nB) * 8
-    chunk = int(max(1, min(n, _GEN_CHUNK_BYTES // per_e)))
-    wt = torch.empty((chunk, n, nU, nB), dtype=torch.float64, device="cuda")
-    wd = torch.empty((chunk, n, nB, nB), dtype=torch.float64, device="cuda")
+    chunk = int(min(n, max(64, _GEN_CHUNK_BYTES // per_e // 64 * 64)))   # whole 64-element tiles
+    wt = torch.empty((n, nU, nB, chunk), dtype=torch.float64, device="cuda")   # chunk-minor
+    wd = torch.empty((n, nB, nB, chunk), dtype=torch.float64, device="cuda")
+    flags = torch.empty((n, -(-chunk // 64)), dtype=torch.int32, device="cuda")
     thetaT = torch.zeros((NE, N), dtype=torch.float64, device="cuda")
     D = torch.zeros((NE, NE), dtype=torch.float64, device="cuda")
     max_near = int(lp.near_cnt.max())
@@ -601,12 +602,12 @@ def _graded_theta_d(disc, lp: LogPart, d):
                   _lib.ptr(d["near_unit"]), _lib.ptr(d["touch"]), _lib.ptr(d["gx"]),
                   _lib.ptr(d["gw"]), _lib.ptr(m2u) if m2u is not None else None,
                   _lib.ptr(d["ca"]), _lib.ptr(d["cb"]), _lib.ptr(wt),
-                  _lib.ptr(wd), st)
+                  _lib.ptr(wd), chunk, _lib.ptr(flags), st)
         uc, vc = lp.ucols[e0:e1], lp.vcols[e0:e1]
-        _lib.call("wq_gen_gather_theta", N, NE, n, e0, e1, int(uc.min()), int(uc.max()) + 1, wu,
+        _lib.call("wq_gen_gather_theta", N, NE, e0, e1, chunk, int(uc.min()), int(uc.max()) + 1, wu,
                   wv, nU, nB, _lib.ptr(d["u_el"]), _lib.ptr(d["u_loc"]), _lib.ptr(d["v_el"]),
                   _lib.ptr(d["v_loc"]), _lib.ptr(wt), _lib.ptr(thetaT), st)
-        _lib.call("wq_gen_gather_d", NE, n, e0, e1, int(vc.min()), int(vc.max()) + 1, wv, nB,
+        _lib.call("wq_gen_gather_d", NE, e0, e1, chunk, int(vc.min()), int(vc.max()) + 1, wv, nB,
                   _lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(wd), _lib.ptr(D), st)
     return thetaT, D
 

@@ -117,8 +117,10 @@ struct GenArgs {
   const double* m2u;        // (2 n_el - 1, da+1, db+1) UNIT gap table (open meshes) or NULL
   const double* ca;         // (da+1) unit centred integrals
   const double* cb;         // (db+1)
-  double* wt;               // (e1-e0, n_el, pu+1, db+1) Theta blocks
-  double* wd;               // (e1-e0, n_el, db+1, db+1) D blocks
+  double* wt;               // [f][a'][b'][e - e0] Theta blocks, leading dimension ldc
+  double* wd;               // [f][a'][b'][e - e0] D blocks
+  int64_t ldc;              // >= e1 - e0
+  int* tile_flag;           // (n_el, ceil((e1-e0)/64)): tile holds off-table far pairs
 };
 
 __device__ __forceinline__ double wrap_delta(const GenArgs& A, double d) {
@@ -140,197 +142,203 @@ __device__ __forceinline__ bool snapped_gap(double he, double hf, double delta, 
   const double rho = hf / he;
   if (!(fabs(rho - 1.0) < WIDTH_SNAP)) return false;
   const double dl = delta / he, r = rint(dl);
-  if (!(fabs(dl - r) < 1e-9)) return false;
+  if (!(fabs(dl - r) < 1e-9 * fmax(1.0, fabs(dl)))) return false;  // relative: |dl| up to n_el
   *gap = -r;  // keff = f - e in element units
   return true;
 }
 
 constexpr int FP_THREADS = 64;
 
-// Far pairs of snapped widths: unit moments from the gap table M' (rows
-// f - e + n - 1), staged for the CTA's 64 consecutive inner elements, scaled
-// M = h_e^(a+b+2) (M' + ln h_e c_a c_b) and contracted to the blocks.
+// Block layout (chunk-minor, so both the pair kernels' stores and the
+// gathers' loads are coalesced): W[f][a'][b'][e - e0], leading dimension ldc.
+__device__ __forceinline__ int64_t wslot(const GenArgs& A, int64_t f, int ab, int nab, int64_t ec) {
+  return ((f * nab) + ab) * A.ldc + ec;
+}
+
+// Far pairs of snapped widths: unit moments from the gap table M' (row
+// f - e + n - 1), staged for the CTA's 64 consecutive outer elements e and its
+// one inner element f, scaled M = h_e^(a+b+2) (M' + ln h_e c_a c_b) and
+// contracted to the blocks.  One thread per outer element.
 template <int NP>
 __global__ void __launch_bounds__(FP_THREADS)
 pair_table_kernel(GenArgs A) {
   extern __shared__ double sm[];
   const int nA = A.da + 1;
-  const int64_t e = A.e0 + blockIdx.y;
-  const int64_t f0 = (int64_t)blockIdx.x * FP_THREADS;
-  const int nf = (int)min((int64_t)FP_THREADS, A.n_el - f0);
-  double* Mt = sm;                              // [FP_THREADS][nA * NP]
-  double* Ue = Mt + FP_THREADS * nA * NP;       // [nA][NP]
-  double* Ve = Ue + nA * NP;                    // [NP][NP]
-  double* Sc = Ve + NP * NP;                    // [nA] h^(a+2), [NP] h^b, [nA*NP] ln h c_a c_b
-  const double he = A.elh[e];
-  const int64_t row0 = f0 - e + A.n_el - 1;
-  for (int k = threadIdx.x; k < nf * nA * NP; k += FP_THREADS) Mt[k] = A.m2u[row0 * nA * NP + k];
-  for (int k = threadIdx.x; k < nA * NP; k += FP_THREADS) Ue[k] = A.u[e * nA * NP + k];
-  for (int k = threadIdx.x; k < NP * NP; k += FP_THREADS) Ve[k] = A.v[e * NP * NP + k];
-  if (threadIdx.x == 0) {
-    double p = he * he;
-    for (int a = 0; a < nA; ++a, p *= he) Sc[a] = p;
-    p = 1.0;
-    for (int b = 0; b < NP; ++b, p *= he) Sc[nA + b] = p;
+  const int64_t f = blockIdx.y;
+  const int64_t eb = A.e0 + (int64_t)blockIdx.x * FP_THREADS;
+  const int ne = (int)min((int64_t)FP_THREADS, A.e1 - eb);
+  double* Mt = sm;                              // [FP_THREADS][nA * NP], row of e = eb + t
+  __shared__ double vf[NP][NP];
+  __shared__ double cab[GMAXA * GMAXB];         // c_a c_b
+  // rows f - e + n - 1 for e = eb .. eb + ne - 1 are contiguous (descending in e)
+  const int64_t rlo = f - (eb + ne - 1) + A.n_el - 1;
+  for (int k = threadIdx.x; k < ne * nA * NP; k += FP_THREADS) {
+    const int r = k / (nA * NP);               // staged row r <-> e = eb + ne - 1 - r
+    Mt[(ne - 1 - r) * nA * NP + (k - r * nA * NP)] = A.m2u[rlo * nA * NP + k];
   }
+  for (int k = threadIdx.x; k < NP * NP; k += FP_THREADS) vf[k / NP][k % NP] = A.v[f * NP * NP + k];
+  for (int k = threadIdx.x; k < nA * NP; k += FP_THREADS) cab[k] = A.ca[k / NP] * A.cb[k % NP];
+  const int64_t e = eb + threadIdx.x;
+  const bool valid = threadIdx.x < ne && !is_near(A, e, f);
+  const double he = valid ? A.elh[e] : 1.0;
+  double gap = 0.0;
+  const bool tab = valid && snapped_gap(he, A.elh[f], A.elm[e] - A.elm[f], &gap) &&
+                   fabs(gap) <= (double)(A.n_el - 1);
+  // tiles with off-table far pairs are left to pair_far_kernel
+  const int need = __syncthreads_or(valid && !tab);
+  if (threadIdx.x == 0) A.tile_flag[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = need;
+  if (!tab) return;
+  // staged rows are indexed by f - e; equal widths at a different integer
+  // geometric offset (e.g. mirrored graded elements) read their own row
+  const double* M = gap == (double)(f - e) ? Mt + threadIdx.x * nA * NP
+                                           : A.m2u + ((int64_t)gap + A.n_el - 1) * nA * NP;
+  const double* ue = A.u + e * nA * NP;
+  const double* ve = A.v + e * NP * NP;
   const double lh = log(he);
-  for (int k = threadIdx.x; k < nA * NP; k += FP_THREADS)
-    Sc[nA + NP + k] = lh * (A.ca[k / NP] * A.cb[k % NP]);
-  __syncthreads();
-  const int64_t f = f0 + threadIdx.x;
-  if (threadIdx.x >= nf || is_near(A, e, f)) return;
-  const double hf = A.elh[f];
-  double gap;
-  if (!snapped_gap(he, hf, A.elm[e] - A.elm[f], &gap) || fabs(gap) > (double)(A.n_el - 1)) return;
-  double vf[NP][NP];
+  double hb[NP];
+  hb[0] = 1.0;
 #pragma unroll
-  for (int b = 0; b < NP; ++b)
-#pragma unroll
-    for (int bp = 0; bp < NP; ++bp) vf[b][bp] = A.v[(f * NP + b) * NP + bp];
+  for (int b = 1; b < NP; ++b) hb[b] = hb[b - 1] * he;
   double wT[NP][NP], wD[NP][NP];
 #pragma unroll
   for (int a = 0; a < NP; ++a)
 #pragma unroll
     for (int b = 0; b < NP; ++b) wT[a][b] = wD[a][b] = 0.0;
-  // staged rows are indexed by f - e; equal widths at a different integer
-  // geometric offset (e.g. mirrored graded elements) read their own row
-  const double* M = gap == (double)(f - e) ? Mt + threadIdx.x * nA * NP
-                                           : A.m2u + ((int64_t)gap + A.n_el - 1) * nA * NP;
-  const double* L = Sc + nA + NP;
+  double ha = he * he;
 #pragma unroll 1
-  for (int al = 0; al < nA; ++al) {
-    const double ha = Sc[al];
+  for (int al = 0; al < nA; ++al, ha *= he) {
     double mv[NP];
 #pragma unroll
     for (int bp = 0; bp < NP; ++bp) mv[bp] = 0.0;
 #pragma unroll
     for (int be = 0; be < NP; ++be) {
-      const double m = ha * Sc[nA + be] * (M[al * NP + be] + L[al * NP + be]);
+      const double m = ha * hb[be] * (M[al * NP + be] + lh * cab[al * NP + be]);
 #pragma unroll
       for (int bp = 0; bp < NP; ++bp) mv[bp] = fma(m, vf[be][bp], mv[bp]);
     }
 #pragma unroll
-    for (int a = 0; a < NP; ++a)
+    for (int a = 0; a < NP; ++a) {
+      const double u = __ldg(ue + al * NP + a);
 #pragma unroll
-      for (int bp = 0; bp < NP; ++bp) wT[a][bp] = fma(Ue[al * NP + a], mv[bp], wT[a][bp]);
+      for (int bp = 0; bp < NP; ++bp) wT[a][bp] = fma(u, mv[bp], wT[a][bp]);
+    }
     if (al < NP) {
 #pragma unroll
-      for (int a = 0; a < NP; ++a)
+      for (int a = 0; a < NP; ++a) {
+        const double v = __ldg(ve + al * NP + a);
 #pragma unroll
-        for (int bp = 0; bp < NP; ++bp) wD[a][bp] = fma(Ve[al * NP + a], mv[bp], wD[a][bp]);
+        for (int bp = 0; bp < NP; ++bp) wD[a][bp] = fma(v, mv[bp], wD[a][bp]);
+      }
     }
   }
-  double* wt = A.wt + ((e - A.e0) * A.n_el + f) * NP * NP;
-  double* wd = A.wd + ((e - A.e0) * A.n_el + f) * NP * NP;
+  const int64_t ec = e - A.e0;
 #pragma unroll
   for (int a = 0; a < NP; ++a)
 #pragma unroll
     for (int bp = 0; bp < NP; ++bp) {
-      wt[a * NP + bp] = wT[a][bp];
-      wd[a * NP + bp] = wD[a][bp];
+      A.wt[wslot(A, f, a * NP + bp, NP * NP, ec)] = wT[a][bp];
+      A.wd[wslot(A, f, a * NP + bp, NP * NP, ec)] = wD[a][bp];
     }
 }
 
 // Far pairs off the table: tensor Gauss on the contracted integrand, one
-// thread per pair, tier tables of the outer element in shared memory.
+// thread per outer element e, the inner element f's weighted polynomial values
+// at every tier's nodes in shared memory.  Persistent over (f, 64 outer
+// elements) tiles; with a gap table only the tiles pair_table_kernel flagged.
 template <int NP>
 __global__ void __launch_bounds__(FP_THREADS)
-pair_far_kernel(GenArgs A) {
-  __shared__ double Ut[GTSUM][NP];   // h_e w_g U_e(h_e x_g)
-  __shared__ double Vt[GTSUM][NP];   // h_e w_g V_e(h_e x_g)
-  __shared__ double Xt[GTSUM];       // h_e x_g
+pair_far_kernel(GenArgs A, int64_t ntiles, int nbx) {
+  __shared__ double Vt[GTSUM][NP];   // h_f w_h V_f(h_f x_h)
+  __shared__ double Yt[GTSUM];       // h_f x_h
   __shared__ double Gx[GTSUM], Gw[GTSUM];
   const int nA = A.da + 1;
-  const int64_t e = A.e0 + blockIdx.y;
-  const double he = A.elh[e];
-  const int64_t f = (int64_t)blockIdx.x * FP_THREADS + threadIdx.x;
-  bool mine = f < A.n_el && !is_near(A, e, f);
-  double gap;
-  if (mine && A.m2u && snapped_gap(he, A.elh[f], A.elm[e] - A.elm[f], &gap) &&
-      fabs(gap) <= (double)(A.n_el - 1))
-    mine = false;  // pair_table_kernel's
-  if (!__syncthreads_or(mine)) return;
   for (int g = threadIdx.x; g < GTSUM; g += FP_THREADS) {
     Gx[g] = A.gx[g];
     Gw[g] = A.gw[g];
-    const double x = he * A.gx[g], w = he * A.gw[g];
-    Xt[g] = x;
-    const double* ue = A.u + e * nA * NP;
-    const double* ve = A.v + e * NP * NP;
-#pragma unroll
-    for (int ap = 0; ap < NP; ++ap) {
-      double s = 0.0;
-      for (int al = nA - 1; al >= 0; --al) s = fma(s, x, ue[al * NP + ap]);
-      Ut[g][ap] = w * s;
-      s = 0.0;
-#pragma unroll
-      for (int al = NP - 1; al >= 0; --al) s = fma(s, x, ve[al * NP + ap]);
-      Vt[g][ap] = w * s;
-    }
   }
-  __syncthreads();
-  if (!mine) return;
-  const double hf = A.elh[f];
-  const double delta = wrap_delta(A, A.elm[e] - A.elm[f]);
-  const double sep = fabs(delta) - 0.5 * (he + hf);
-  const double hm = fmax(he, hf);
-  // Gauss order by separation in units of the larger width (measured: <= 5e-15
-  // of the natural slot scale at degree 16 x 4 for every tier)
-  const int t0 = sep < 2.0 * hm ? 0 : (sep < 8.0 * hm ? GT0 : GT0 + GT1);
-  const int ng = sep < 2.0 * hm ? GT0 : (sep < 8.0 * hm ? GT1 : GT2);
-  double vf[NP][NP];
-#pragma unroll
-  for (int b = 0; b < NP; ++b)
-#pragma unroll
-    for (int bp = 0; bp < NP; ++bp) vf[b][bp] = A.v[(f * NP + b) * NP + bp];
-  double wT[NP][NP], wD[NP][NP];
-#pragma unroll
-  for (int a = 0; a < NP; ++a)
-#pragma unroll
-    for (int b = 0; b < NP; ++b) wT[a][b] = wD[a][b] = 0.0;
-  const bool closed = A.closed;
-  const double invL = closed ? 1.0 / A.period : 0.0;
-  const double lnLpi = closed ? log(A.period / kPi) : 0.0;
-  for (int h = 0; h < ng; ++h) {
-    const double y = hf * Gx[t0 + h], wy = hf * Gw[t0 + h];
-    double vy[NP];
-#pragma unroll
-    for (int bp = 0; bp < NP; ++bp) {
-      double s = 0.0;
-#pragma unroll
-      for (int b = NP - 1; b >= 0; --b) s = fma(s, y, vf[b][bp]);
-      vy[bp] = wy * s;
-    }
-    const double base = y - delta;  // r = y - x - delta
-    double tU[NP], tV[NP];
-#pragma unroll
-    for (int a = 0; a < NP; ++a) tU[a] = tV[a] = 0.0;
-    for (int g = 0; g < ng; ++g) {
-      const double r = base - Xt[t0 + g];
-      const double k = closed ? log(fabs(sinpi(r * invL))) + lnLpi : log(fabs(r));
-#pragma unroll
-      for (int a = 0; a < NP; ++a) {
-        tU[a] = fma(Ut[t0 + g][a], k, tU[a]);
-        tV[a] = fma(Vt[t0 + g][a], k, tV[a]);
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < NP; ++a)
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (A.m2u && !A.tile_flag[tile]) continue;
+    __syncthreads();   // previous tile's tables are dead; Gx/Gw visible
+    const int64_t f = tile / nbx;
+    const int64_t e = A.e0 + (tile % nbx) * FP_THREADS + threadIdx.x;
+    const double hf = A.elh[f];
+    bool mine = e < A.e1 && !is_near(A, e, f);
+    double gap;
+    if (mine && A.m2u && snapped_gap(A.elh[e], hf, A.elm[e] - A.elm[f], &gap) &&
+        fabs(gap) <= (double)(A.n_el - 1))
+      mine = false;  // pair_table_kernel's
+    for (int h = threadIdx.x; h < GTSUM; h += FP_THREADS) {
+      const double y = hf * Gx[h], w = hf * Gw[h];
+      Yt[h] = y;
 #pragma unroll
       for (int bp = 0; bp < NP; ++bp) {
-        wT[a][bp] = fma(tU[a], vy[bp], wT[a][bp]);
-        wD[a][bp] = fma(tV[a], vy[bp], wD[a][bp]);
+        double s = 0.0;
+#pragma unroll
+        for (int b = NP - 1; b >= 0; --b) s = fma(s, y, A.v[(f * NP + b) * NP + bp]);
+        Vt[h][bp] = w * s;
       }
-  }
-  double* wt = A.wt + ((e - A.e0) * A.n_el + f) * NP * NP;
-  double* wd = A.wd + ((e - A.e0) * A.n_el + f) * NP * NP;
-#pragma unroll
-  for (int a = 0; a < NP; ++a)
-#pragma unroll
-    for (int bp = 0; bp < NP; ++bp) {
-      wt[a * NP + bp] = wT[a][bp];
-      wd[a * NP + bp] = wD[a][bp];
     }
+    __syncthreads();
+    if (mine) {
+      const double he = A.elh[e];
+      const double delta = wrap_delta(A, A.elm[e] - A.elm[f]);
+      const double sep = fabs(delta) - 0.5 * (he + hf);
+      const double hm = fmax(he, hf);
+      // Gauss order by separation in units of the larger width (measured:
+      // <= 5e-15 of the natural slot scale at degree 16 x 4 for every tier)
+      const int t0 = sep < 2.0 * hm ? 0 : (sep < 8.0 * hm ? GT0 : GT0 + GT1);
+      const int ng = sep < 2.0 * hm ? GT0 : (sep < 8.0 * hm ? GT1 : GT2);
+      const double* ue = A.u + e * nA * NP;
+      const double* ve = A.v + e * NP * NP;
+      double wT[NP][NP], wD[NP][NP];
+#pragma unroll
+      for (int a = 0; a < NP; ++a)
+#pragma unroll
+        for (int b = 0; b < NP; ++b) wT[a][b] = wD[a][b] = 0.0;
+      const bool closed = A.closed;
+      const double invL = closed ? 1.0 / A.period : 0.0;
+      const double lnLpi = closed ? log(A.period / kPi) : 0.0;
+      for (int g = 0; g < ng; ++g) {
+        const double x = he * Gx[t0 + g], wx = he * Gw[t0 + g];
+        double uu[NP], vv[NP];
+#pragma unroll
+        for (int a = 0; a < NP; ++a) {
+          double s = 0.0;
+          for (int al = nA - 1; al >= 0; --al) s = fma(s, x, __ldg(ue + al * NP + a));
+          uu[a] = wx * s;
+          s = 0.0;
+#pragma unroll
+          for (int al = NP - 1; al >= 0; --al) s = fma(s, x, __ldg(ve + al * NP + a));
+          vv[a] = wx * s;
+        }
+        const double base = -x - delta;   // r = y - x - delta
+        double t[NP];
+#pragma unroll
+        for (int b = 0; b < NP; ++b) t[b] = 0.0;
+        for (int h = 0; h < ng; ++h) {
+          const double r = Yt[t0 + h] + base;
+          const double k = closed ? log(fabs(sinpi(r * invL))) + lnLpi : log(fabs(r));
+#pragma unroll
+          for (int b = 0; b < NP; ++b) t[b] = fma(Vt[t0 + h][b], k, t[b]);
+        }
+#pragma unroll
+        for (int a = 0; a < NP; ++a)
+#pragma unroll
+          for (int bp = 0; bp < NP; ++bp) {
+            wT[a][bp] = fma(uu[a], t[bp], wT[a][bp]);
+            wD[a][bp] = fma(vv[a], t[bp], wD[a][bp]);
+          }
+      }
+      const int64_t ec = e - A.e0;
+#pragma unroll
+      for (int a = 0; a < NP; ++a)
+#pragma unroll
+        for (int bp = 0; bp < NP; ++bp) {
+          A.wt[wslot(A, f, a * NP + bp, NP * NP, ec)] = wT[a][bp];
+          A.wd[wslot(A, f, a * NP + bp, NP * NP, ec)] = wD[a][bp];
+        }
+    }
+  }
 }
 
 constexpr int TOUCH_XI = 16, TOUCH_ETA = 30, TOUCH_LOG = 14;
@@ -365,7 +373,7 @@ pair_near_kernel(GenArgs A, int max_near) {
   double rho = hf / he, dl = delta / he;
   if (fabs(rho - 1.0) < WIDTH_SNAP) {  // exact integer gaps as the unit table (quadrature.py:452-456)
     rho = 1.0;
-    if (fabs(dl - rint(dl)) < 1e-9) dl = rint(dl);
+    if (fabs(dl - rint(dl)) < 1e-9 * fmax(1.0, fabs(dl))) dl = rint(dl);
   }
   // lane-owned slots s = lane + 32 j
   constexpr int SL = (GMAXA * GMAXB + 31) / 32;   // slots per lane
@@ -459,8 +467,7 @@ pair_near_kernel(GenArgs A, int max_near) {
   const double* ue = A.u + e * nA * nU;
   const double* ve = A.v + e * nB * nB;
   const double* vf = A.v + f * nB * nB;
-  double* wt = A.wt + ((e - A.e0) * A.n_el + f) * nU * nB;
-  double* wd = A.wd + ((e - A.e0) * A.n_el + f) * nB * nB;
+  const int64_t ec = e - A.e0;
   for (int o = lane; o < nU * nB + nB * nB; o += 32) {
     const bool th = o < nU * nB;
     const int oo = th ? o : o - nU * nB;
@@ -474,12 +481,14 @@ pair_near_kernel(GenArgs A, int max_near) {
       for (int be = 0; be < nB; ++be) mv = fma(M[al * nB + be], vf[be * nB + bp], mv);
       s = fma(c[al * ldc + ap], mv, s);
     }
-    if (th) wt[oo] = s; else wd[oo] = s;
+    if (th) A.wt[wslot(A, f, oo, nU * nB, ec)] = s;
+    else A.wd[wslot(A, f, oo, nB * nB, ec)] = s;
   }
 }
 
-// Theta^T[l][i] += sum_{(e,a) in inc_u(i), e in chunk} sum_{(f,b) in inc_v(l)} WT[e][f][a][b]
-__global__ void gather_theta_kernel(int64_t n_rows, int64_t n_el, int64_t e0, int64_t e1,
+// Theta^T[l][i] += sum_{(e,a) in inc_u(i), e in chunk} sum_{(f,b) in inc_v(l)} WT[f][a][b][e-e0]
+// (threads over i: consecutive e, coalesced in the chunk-minor layout)
+__global__ void gather_theta_kernel(int64_t n_rows, int64_t e0, int64_t e1, int64_t ldc,
                                     int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
                                     const int64_t* u_el, const int64_t* u_loc,
                                     const int64_t* v_el, const int64_t* v_loc, const double* wt,
@@ -492,72 +501,99 @@ __global__ void gather_theta_kernel(int64_t n_rows, int64_t n_el, int64_t e0, in
     const int64_t e = u_el[i * wu + ua];
     if (e < e0 || e >= e1) continue;
     const int a = (int)u_loc[i * wu + ua];
-    const double* blk = wt + (e - e0) * n_el * nU * nB + a * nB;
     for (int vb = 0; vb < wv; ++vb) {
       const int64_t f = v_el[l * wv + vb];
       if (f < 0) continue;
-      acc += blk[f * nU * nB + v_loc[l * wv + vb]];
+      acc += wt[((f * nU + a) * nB + v_loc[l * wv + vb]) * ldc + (e - e0)];
     }
   }
   thetaT[l * n_rows + i] += acc;
 }
 
-// D[l][m] += sum_{(e,a) in inc_v(l), e in chunk} sum_{(f,b) in inc_v(m)} WD[e][f][a][b]
-__global__ void gather_d_kernel(int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1, int64_t l0,
+// D (symmetric) from the chunk: entry (l, m) = sum_{(e,a) in inc_v(l), e in
+// chunk} sum_{(f,b) in inc_v(m)} WD[f][a][b][e-e0], stored at D[m][l] --
+// threads over l (consecutive e: coalesced loads and stores)
+__global__ void gather_d_kernel(int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc, int64_t l0,
                                 int64_t l1, int wv, int nB, const int64_t* v_el,
                                 const int64_t* v_loc, const double* wd, double* D) {
-  const int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t l = l0 + blockIdx.y;
-  if (m >= n_fine || l >= l1) return;
+  const int64_t l = l0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t m = blockIdx.y;
+  if (l >= l1) return;
   double acc = 0.0;
   for (int va = 0; va < wv; ++va) {
     const int64_t e = v_el[l * wv + va];
     if (e < e0 || e >= e1) continue;
     const int a = (int)v_loc[l * wv + va];
-    const double* blk = wd + (e - e0) * n_el * nB * nB + a * nB;
     for (int vb = 0; vb < wv; ++vb) {
       const int64_t f = v_el[m * wv + vb];
       if (f < 0) continue;
-      acc += blk[f * nB * nB + v_loc[m * wv + vb]];
+      acc += wd[((f * nB + a) * nB + v_loc[m * wv + vb]) * ldc + (e - e0)];
     }
   }
-  D[l * n_fine + m] += acc;
+  D[m * n_fine + l] += acc;
 }
 
 // Banded Cholesky solves X <- L^{-T} L^{-1} X per column with the last BW
-// values of the column in registers (one load + one store per row).
+// values of the column in registers (one load + one store per row).  Rows are
+// processed in batches of RB whose loads are issued together, so a thread
+// keeps RB independent HBM requests in flight instead of one per dependent step.
 template <int BW>
 __global__ void band_solve_win_kernel(int64_t n, const double* Lb, double* X, int64_t ncols,
                                       int64_t ldx) {
+  constexpr int RB = 8;
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= ncols) return;
   double* x = X + c;
   double w[BW];
 #pragma unroll
   for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = y_{k-1-j}
-  for (int64_t k = 0; k < n; ++k) {
-    const double* lk = Lb + k * (BW + 1);
-    double s = x[k * ldx];
+  for (int64_t k0 = 0; k0 < n; k0 += RB) {
+    double xb[RB];
 #pragma unroll
-    for (int j = 1; j <= BW; ++j) s = fma(-lk[j], w[j - 1], s);  // zero window before row 0
-    s = s / lk[0];
-    x[k * ldx] = s;
+    for (int r = 0; r < RB; ++r) xb[r] = k0 + r < n ? x[(k0 + r) * ldx] : 0.0;
 #pragma unroll
-    for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
-    w[0] = s;
+    for (int r = 0; r < RB; ++r) {
+      const int64_t k = k0 + r;
+      if (k < n) {
+        const double* lk = Lb + k * (BW + 1);
+        double s = xb[r];
+#pragma unroll
+        for (int j = 1; j <= BW; ++j) s = fma(-lk[j], w[j - 1], s);  // zero window before row 0
+        s = s / lk[0];
+        xb[r] = s;
+#pragma unroll
+        for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
+        w[0] = s;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (k0 + r < n) x[(k0 + r) * ldx] = xb[r];
   }
 #pragma unroll
   for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = z_{k+1+j}
-  for (int64_t k = n - 1; k >= 0; --k) {
-    double s = x[k * ldx];
+  for (int64_t k1 = n - 1; k1 >= 0; k1 -= RB) {
+    double xb[RB];
 #pragma unroll
-    for (int j = 1; j <= BW; ++j)
-      if (k + j < n) s = fma(-Lb[(k + j) * (BW + 1) + j], w[j - 1], s);
-    s = s / Lb[k * (BW + 1)];
-    x[k * ldx] = s;
+    for (int r = 0; r < RB; ++r) xb[r] = k1 - r >= 0 ? x[(k1 - r) * ldx] : 0.0;
 #pragma unroll
-    for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
-    w[0] = s;
+    for (int r = 0; r < RB; ++r) {
+      const int64_t k = k1 - r;
+      if (k >= 0) {
+        double s = xb[r];
+#pragma unroll
+        for (int j = 1; j <= BW; ++j)
+          if (k + j < n) s = fma(-Lb[(k + j) * (BW + 1) + j], w[j - 1], s);
+        s = s / Lb[k * (BW + 1)];
+        xb[r] = s;
+#pragma unroll
+        for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
+        w[0] = s;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (k1 - r >= 0) x[(k1 - r) * ldx] = xb[r];
   }
 }
 
@@ -573,21 +609,29 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
                        int max_near, const double* near_unit, const double* touch,
                        const double* gx, const double* gw, const double* m2u,
                        const double* ca, const double* cb, double* wt, double* wd,
-                       void* stream) {
+                       int64_t ldc, int* tile_flag, void* stream) {
   if (n_el <= 0 || e0 < 0 || e1 > n_el || e1 <= e0 || da + 1 > GMAXA || db + 1 > GMAXB ||
       db < 1 || pu != db || max_near < 0 || !near_unit || !touch || !gx || !gw || !elh || !elm || !u || !v || !near_lo || !near_cnt ||
-      !ca || !cb || !wt || !wd || (closed && !(period > 0)) || (m2u && closed)) {
+      !ca || !cb || !wt || !wd || (closed && !(period > 0)) || ldc < e1 - e0 || (m2u && (closed || !tile_flag))) {
     set_error("wq_gen_pair_blocks: bad arguments");
     return WQ_EINVAL;
   }
   int rc = ensure_consts();
   if (rc) return rc;
   GenArgs A{n_el, e0, e1, da, db, pu, closed, period, elh, elm, u, v, near_lo, near_cnt,
-            near_unit, touch, gx, gw, m2u, ca, cb, wt, wd};
+            near_unit, touch, gx, gw, m2u, ca, cb, wt, wd, ldc, tile_flag};
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 g1(ceil_div(n_el, FP_THREADS), (unsigned)(e1 - e0));
+  dim3 g1(ceil_div(e1 - e0, FP_THREADS), (unsigned)n_el);   // (64 outer elements, inner f)
   const int nA = da + 1, np1 = db + 1;
-  const size_t tsm = (size_t)(FP_THREADS * nA * np1 + nA * np1 + np1 * np1 + nA + np1 + nA * np1) * 8;
+  const int64_t ntiles = (int64_t)g1.x * g1.y;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t fgrid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
+  const size_t tsm = (size_t)FP_THREADS * nA * np1 * 8;
 #define WQ_GEN_CASE(NP)                                                                      \
   case NP:                                                                                   \
     if (m2u) {                                                                               \
@@ -595,7 +639,7 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
                            (int)tsm);                                                        \
       pair_table_kernel<NP><<<g1, FP_THREADS, tsm, st>>>(A);                                 \
     }                                                                                        \
-    pair_far_kernel<NP><<<g1, FP_THREADS, 0, st>>>(A);                                       \
+    pair_far_kernel<NP><<<(unsigned)fgrid, FP_THREADS, 0, st>>>(A, ntiles, (int)g1.x);      \
     break;
   switch (np1) {
     WQ_GEN_CASE(2)
@@ -618,7 +662,7 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
   return check_launch("wq_gen_pair_blocks(near)");
 }
 
-int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1,
+int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc,
                         int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
                         const int64_t* u_el, const int64_t* u_loc, const int64_t* v_el,
                         const int64_t* v_loc, const double* wt, double* thetaT, void* stream) {
@@ -628,22 +672,22 @@ int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t n_el, int64_t e0
     return WQ_EINVAL;
   }
   dim3 grid(ceil_div(i1 - i0, 64), (unsigned)n_fine);
-  gather_theta_kernel<<<grid, 64, 0, (cudaStream_t)stream>>>(n_rows, n_el, e0, e1, i0, i1, wu, wv,
+  gather_theta_kernel<<<grid, 64, 0, (cudaStream_t)stream>>>(n_rows, e0, e1, ldc, i0, i1, wu, wv,
                                                             nU, nB, u_el, u_loc, v_el, v_loc, wt,
                                                             thetaT);
   return check_launch("wq_gen_gather_theta");
 }
 
-int wq_gen_gather_d(int64_t n_fine, int64_t n_el, int64_t e0, int64_t e1, int64_t l0, int64_t l1,
+int wq_gen_gather_d(int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc, int64_t l0, int64_t l1,
                     int wv, int nB, const int64_t* v_el, const int64_t* v_loc, const double* wd,
                     double* D, void* stream) {
   if (l1 <= l0 || l0 < 0 || l1 > n_fine || !v_el || !v_loc || !wd || !D) {
     set_error("wq_gen_gather_d: bad arguments");
     return WQ_EINVAL;
   }
-  dim3 grid(ceil_div(n_fine, 128), (unsigned)(l1 - l0));
-  gather_d_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(n_fine, n_el, e0, e1, l0, l1, wv, nB,
-                                                         v_el, v_loc, wd, D);
+  dim3 grid(ceil_div(l1 - l0, 64), (unsigned)n_fine);
+  gather_d_kernel<<<grid, 64, 0, (cudaStream_t)stream>>>(n_fine, e0, e1, ldc, l0, l1, wv, nB,
+                                                        v_el, v_loc, wd, D);
   return check_launch("wq_gen_gather_d");
 }
 

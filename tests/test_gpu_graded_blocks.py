@@ -26,16 +26,18 @@ def test_pair_blocks_match_restatement(cuda, table):
     lp, d = AS._logpart_dev(disc)
     n = lp.n_el
     nU, nB = lp.u.shape[2], lp.db + 1
-    wt = torch.full((n, n, nU, nB), np.nan, dtype=torch.float64, device="cuda")
-    wd = torch.full((n, n, nB, nB), np.nan, dtype=torch.float64, device="cuda")
+    wt = torch.full((n, nU, nB, n), np.nan, dtype=torch.float64, device="cuda")   # [f][a][b][e]
+    wd = torch.full((n, nB, nB, n), np.nan, dtype=torch.float64, device="cuda")
+    flags = torch.empty((n, -(-n // 64)), dtype=torch.int32, device="cuda")
     m2u = AS._gap_table(disc, lp, 1.0) if table else None
     _lib.call("wq_gen_pair_blocks", n, 0, n, lp.da, lp.db, nU - 1, 0, 0.0,
               _lib.ptr(d["elh"]), _lib.ptr(d["elm"]), _lib.ptr(d["u"]), _lib.ptr(d["v"]),
               _lib.ptr(d["near_lo"]), _lib.ptr(d["near_cnt"]), int(lp.near_cnt.max()),
               _lib.ptr(d["near_unit"]), _lib.ptr(d["touch"]), _lib.ptr(d["gx"]), _lib.ptr(d["gw"]),
               _lib.ptr(m2u) if m2u is not None else None, _lib.ptr(d["ca"]), _lib.ptr(d["cb"]),
-              _lib.ptr(wt), _lib.ptr(wd), _lib.stream_handle())
-    wt, wd = wt.cpu().numpy(), wd.cpu().numpy()
+              _lib.ptr(wt), _lib.ptr(wd), n, _lib.ptr(flags), _lib.stream_handle())
+    wt = wt.cpu().numpy().transpose(3, 0, 1, 2)   # -> [e][f][a][b]
+    wd = wd.cpu().numpy().transpose(3, 0, 1, 2)
     e_idx = np.repeat(np.arange(n), n)
     f_idx = np.tile(np.arange(n), n)
     m2 = O.pair_moments_general(lp.da, lp.db, lp.elh[e_idx], lp.elh[f_idx],

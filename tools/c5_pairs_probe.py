@@ -17,9 +17,10 @@ w, c = np.unique(lp.elh, return_counts=True)
 h0 = float(w[np.argmax(c)])
 print("h0", h0, "count exact", c.max(), "within 1e-12:", int(np.sum(np.abs(lp.elh - h0) <= 1e-12 * h0)))
 m2u = AS._gap_table(disc, lp, 1.0)
-chunk = 163
-wt = torch.empty((chunk, n, nU, nB), dtype=torch.float64, device="cuda")
+chunk = 128
+wt = torch.empty((n, nU, nB, chunk), dtype=torch.float64, device="cuda")
 wd = torch.empty_like(wt)
+flags = torch.empty((n, -(-chunk // 64)), dtype=torch.int32, device="cuda")
 st = _lib.stream_handle()
 for e0 in (0, 8000):
     for label, tab, mx in (("table", True, int(lp.near_cnt.max())), ("gauss", False, int(lp.near_cnt.max())),
@@ -32,7 +33,7 @@ for e0 in (0, 8000):
                       _lib.ptr(d["near_lo"]), _lib.ptr(d["near_cnt"]), mx,
                       _lib.ptr(d["near_unit"]), _lib.ptr(d["touch"]), _lib.ptr(d["gx"]),
                       _lib.ptr(d["gw"]), _lib.ptr(m2u) if tab else None,
-                      _lib.ptr(d["ca"]), _lib.ptr(d["cb"]), _lib.ptr(wt), _lib.ptr(wd), st)
+                      _lib.ptr(d["ca"]), _lib.ptr(d["cb"]), _lib.ptr(wt), _lib.ptr(wd), chunk, _lib.ptr(flags), st)
             ev1.record()
             torch.cuda.synchronize()
         if label == "table":
