@@ -246,7 +246,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-rows", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
+                    help="c4: the headline (BASELINE metric config); c5: graded open slit with "
+                         "double knots (configs[4]), 1 GPU, no reference arm (the reference raises)")
     args = ap.parse_args()
+    if args.workload == "c5":
+        return run_c5(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -402,6 +407,85 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+SURVEY_W_C5 = 5.46e11         # algorithmic flop-eq of the C5 assembly
+
+
+def run_c5(args):
+    """Config 5 on one GPU: the general (graded-mesh) device path, one step =
+    one full assembly of A (per-pair blocks, gathers, banded fit solves, IK1,
+    symmetrise).  The reference cannot run it (quadrature.py:489-491)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    import paper_1703_10016_b200 as W
+    from paper_1703_10016_b200 import _lib, assembly as AS
+    if args.impl == "reference":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference raises "
+                          "ConstructionError on graded meshes (quadrature.py:489-491)"}))
+        return
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    curve, space = workload_c5()
+    t0 = time.perf_counter()
+    disc = W.build_discretization(curve, space, 1)
+    AS._log_part(disc)
+    precompute_s = time.perf_counter() - t0
+    N = space.dim
+    X = torch.empty((N, N), dtype=torch.float64, device="cuda")
+    for _ in range(args.warmup):
+        AS._assemble_into(disc, X)
+    torch.cuda.synchronize()
+    AS._check_flag(AS._smooth(disc))
+    # launches per step and per-entry-point split (host-synchronous, attribution only)
+    orig = _lib.call
+    split, count = {}, {"n": 0}
+
+    def timed(name, *a):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = orig(name, *a)
+        e1.record()
+        torch.cuda.synchronize()
+        split[name] = split.get(name, 0.0) + e0.elapsed_time(e1)
+        count["n"] += 1
+        return r
+
+    _lib.call = timed
+    AS._assemble_into(disc, X)
+    _lib.call = orig
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        time.sleep(0.3)
+        e0.record()
+        for _ in range(args.steps):
+            AS._assemble_into(disc, X)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    peak = fp64_peak_tflops(torch, _lib)
+    line = {
+        "metric": METRIC, "value": N * N / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic slit, seeded knot multiplicities, BASELINE.json configs[4])",
+        "config": {"workload": "C5: open slit [-1,1]x{0}, p=4, 16384 elements graded 0.9 toward "
+                               "both ends (growth capped at the interior width after 60 elements), "
+                               "interior knots doubled w.p. 0.25 (default_rng(0))", "N": N,
+                   "nq": disc.nodes.n, "parallelism": "single GPU",
+                   "l2": "3.3 GB output > 126 MB L2, rewritten every step"},
+        "clocks": clk.summary(),
+        "gpu_launches": count["n"] * args.steps,
+        "split_ms": {k: round(v, 3) for k, v in sorted(split.items(), key=lambda t: -t[1])},
+        "roofline": {"bound": "fp64", "kernel": "whole step (SURVEY 8(d) W for C5)",
+                     "achieved": SURVEY_W_C5 / (ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": SURVEY_W_C5 / (ms * 1e-3) / 1e12 / peak, "traffic": None},
+        "precompute_s": precompute_s,
+        "e2e": None,
+        "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
 
 
 def cpu_baseline(args, N):

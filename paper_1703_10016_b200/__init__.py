@@ -32,5 +32,6 @@ from .assembly import (
     build_discretization,
     scale_and_symmetrize,
 )
+from .solver import condition_number, solve_system
 
 __version__ = "0.1.0"

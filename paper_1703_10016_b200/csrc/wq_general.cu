@@ -156,26 +156,17 @@ __device__ __forceinline__ int64_t wslot(const GenArgs& A, int64_t f, int ab, in
 }
 
 // Far pairs of snapped widths: unit moments from the gap table M' (row
-// f - e + n - 1), staged for the CTA's 64 consecutive outer elements e and its
-// one inner element f, scaled M = h_e^(a+b+2) (M' + ln h_e c_a c_b) and
-// contracted to the blocks.  One thread per outer element.
+// gap + n - 1), scaled M = h_e^(a+b+2) (M' + ln h_e c_a c_b) and contracted to
+// the blocks.  One thread per outer element e, one inner element f per CTA.
 template <int NP>
-__global__ void __launch_bounds__(FP_THREADS)
+__global__ void __launch_bounds__(FP_THREADS, 8)
 pair_table_kernel(GenArgs A) {
-  extern __shared__ double sm[];
   const int nA = A.da + 1;
   const int64_t f = blockIdx.y;
   const int64_t eb = A.e0 + (int64_t)blockIdx.x * FP_THREADS;
   const int ne = (int)min((int64_t)FP_THREADS, A.e1 - eb);
-  double* Mt = sm;                              // [FP_THREADS][nA * NP], row of e = eb + t
   __shared__ double vf[NP][NP];
   __shared__ double cab[GMAXA * GMAXB];         // c_a c_b
-  // rows f - e + n - 1 for e = eb .. eb + ne - 1 are contiguous (descending in e)
-  const int64_t rlo = f - (eb + ne - 1) + A.n_el - 1;
-  for (int k = threadIdx.x; k < ne * nA * NP; k += FP_THREADS) {
-    const int r = k / (nA * NP);               // staged row r <-> e = eb + ne - 1 - r
-    Mt[(ne - 1 - r) * nA * NP + (k - r * nA * NP)] = A.m2u[rlo * nA * NP + k];
-  }
   for (int k = threadIdx.x; k < NP * NP; k += FP_THREADS) vf[k / NP][k % NP] = A.v[f * NP * NP + k];
   for (int k = threadIdx.x; k < nA * NP; k += FP_THREADS) cab[k] = A.ca[k / NP] * A.cb[k % NP];
   const int64_t e = eb + threadIdx.x;
@@ -188,10 +179,10 @@ pair_table_kernel(GenArgs A) {
   const int need = __syncthreads_or(valid && !tab);
   if (threadIdx.x == 0) A.tile_flag[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = need;
   if (!tab) return;
-  // staged rows are indexed by f - e; equal widths at a different integer
-  // geometric offset (e.g. mirrored graded elements) read their own row
-  const double* M = gap == (double)(f - e) ? Mt + threadIdx.x * nA * NP
-                                           : A.m2u + ((int64_t)gap + A.n_el - 1) * nA * NP;
+  // the geometric offset selects the row (equal widths away from the
+  // lattice of f, e.g. mirrored graded elements, read their own row); a
+  // warp's rows are contiguous in the table (L1/L2 resident)
+  const double* M = A.m2u + ((int64_t)gap + A.n_el - 1) * nA * NP;
   const double* ue = A.u + e * nA * NP;
   const double* ve = A.v + e * NP * NP;
   const double lh = log(he);
@@ -212,7 +203,7 @@ pair_table_kernel(GenArgs A) {
     for (int bp = 0; bp < NP; ++bp) mv[bp] = 0.0;
 #pragma unroll
     for (int be = 0; be < NP; ++be) {
-      const double m = ha * hb[be] * (M[al * NP + be] + lh * cab[al * NP + be]);
+      const double m = ha * hb[be] * (__ldg(M + al * NP + be) + lh * cab[al * NP + be]);
 #pragma unroll
       for (int bp = 0; bp < NP; ++bp) mv[bp] = fma(m, vf[be][bp], mv[bp]);
     }
@@ -631,13 +622,10 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t fgrid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
-  const size_t tsm = (size_t)FP_THREADS * nA * np1 * 8;
 #define WQ_GEN_CASE(NP)                                                                      \
   case NP:                                                                                   \
     if (m2u) {                                                                               \
-      cudaFuncSetAttribute(pair_table_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)tsm);                                                        \
-      pair_table_kernel<NP><<<g1, FP_THREADS, tsm, st>>>(A);                                 \
+      pair_table_kernel<NP><<<g1, FP_THREADS, 0, st>>>(A);                                   \
     }                                                                                        \
     pair_far_kernel<NP><<<(unsigned)fgrid, FP_THREADS, 0, st>>>(A, ntiles, (int)g1.x);      \
     break;
