@@ -82,6 +82,9 @@ int wq_dmma_peak(int64_t iters, int blocks, int mode, double* out, void* stream)
  * for i in [row0,row1), j in [col0,col1); X points at element (row0, col0),
  * leading dimension ldx.  accumulate != 0 adds into X.
  * max_span = max over tiles of the node span (host-computed, see Python).
+ * When [row0,row1) == [col0,col1) only tiles on or above the diagonal are
+ * evaluated and mirrored (K1 is symmetric).  Distinct node pairs closer than
+ * eps_diag take sm->near_j2 (J(mid)^2, geometry.py:237-245).
  */
 int wq_ik1(const wq_smooth_t* sm, int64_t row0, int64_t row1, int64_t col0, int64_t col1,
            double* X, int64_t ldx, int accumulate, int64_t max_span, int* flag, void* stream);

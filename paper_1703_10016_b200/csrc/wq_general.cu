@@ -525,37 +525,46 @@ __global__ void gather_d_kernel(int64_t n_fine, int64_t e0, int64_t e1, int64_t 
 }
 
 // Banded Cholesky solves X <- L^{-T} L^{-1} X per column with the last BW
-// values of the column in registers (one load + one store per row).  Rows are
-// processed in batches of RB whose loads are issued together, so a thread
-// keeps RB independent HBM requests in flight instead of one per dependent step.
+// values of the column in registers (one load + one store per row).  Rows go
+// in batches of RB: the batch's column values are loaded together (RB
+// independent HBM requests in flight per thread) and its factor rows are
+// staged once per CTA in shared memory as -L[k][k-j] and 1/L[k][k], so the
+// dependent chain per row is BW FMAs and one multiply.
 template <int BW>
-__global__ void band_solve_win_kernel(int64_t n, const double* Lb, double* X, int64_t ncols,
-                                      int64_t ldx) {
-  constexpr int RB = 8;
+__global__ void __launch_bounds__(128)
+band_solve_win_kernel(int64_t n, const double* Lb, double* X, int64_t ncols, int64_t ldx) {
+  constexpr int RB = 16;
+  __shared__ double cf[RB][BW + 1];   // [r][0] = 1/diag, [r][j] = -off-diagonal
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= ncols) return;
-  double* x = X + c;
+  const bool live = c < ncols;
+  double* x = X + (live ? c : 0);
   double w[BW];
 #pragma unroll
   for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = y_{k-1-j}
   for (int64_t k0 = 0; k0 < n; k0 += RB) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < RB * (BW + 1); t += blockDim.x) {
+      const int r = t / (BW + 1), j = t - r * (BW + 1);
+      const int64_t k = k0 + r;
+      double v = 0.0;
+      if (k < n) v = j == 0 ? 1.0 / Lb[k * (BW + 1)] : (k - j >= 0 ? -Lb[k * (BW + 1) + j] : 0.0);
+      cf[r][j] = v;
+    }
+    __syncthreads();
+    if (!live) continue;
     double xb[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r) xb[r] = k0 + r < n ? x[(k0 + r) * ldx] : 0.0;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      const int64_t k = k0 + r;
-      if (k < n) {
-        const double* lk = Lb + k * (BW + 1);
-        double s = xb[r];
+      double s = xb[r];
 #pragma unroll
-        for (int j = 1; j <= BW; ++j) s = fma(-lk[j], w[j - 1], s);  // zero window before row 0
-        s = s / lk[0];
-        xb[r] = s;
+      for (int j = 1; j <= BW; ++j) s = fma(cf[r][j], w[j - 1], s);
+      s *= cf[r][0];
+      xb[r] = s;
 #pragma unroll
-        for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
-        w[0] = s;
-      }
+      for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
+      w[0] = s;
     }
 #pragma unroll
     for (int r = 0; r < RB; ++r)
@@ -564,23 +573,29 @@ __global__ void band_solve_win_kernel(int64_t n, const double* Lb, double* X, in
 #pragma unroll
   for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = z_{k+1+j}
   for (int64_t k1 = n - 1; k1 >= 0; k1 -= RB) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < RB * (BW + 1); t += blockDim.x) {
+      const int r = t / (BW + 1), j = t - r * (BW + 1);
+      const int64_t k = k1 - r;
+      double v = 0.0;
+      if (k >= 0) v = j == 0 ? 1.0 / Lb[k * (BW + 1)] : (k + j < n ? -Lb[(k + j) * (BW + 1) + j] : 0.0);
+      cf[r][j] = v;
+    }
+    __syncthreads();
+    if (!live) continue;
     double xb[RB];
 #pragma unroll
     for (int r = 0; r < RB; ++r) xb[r] = k1 - r >= 0 ? x[(k1 - r) * ldx] : 0.0;
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-      const int64_t k = k1 - r;
-      if (k >= 0) {
-        double s = xb[r];
+      double s = xb[r];
 #pragma unroll
-        for (int j = 1; j <= BW; ++j)
-          if (k + j < n) s = fma(-Lb[(k + j) * (BW + 1) + j], w[j - 1], s);
-        s = s / Lb[k * (BW + 1)];
-        xb[r] = s;
+      for (int j = 1; j <= BW; ++j) s = fma(cf[r][j], w[j - 1], s);
+      s *= cf[r][0];
+      xb[r] = s;
 #pragma unroll
-        for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
-        w[0] = s;
-      }
+      for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
+      w[0] = s;
     }
 #pragma unroll
     for (int r = 0; r < RB; ++r)
@@ -685,17 +700,17 @@ int wq_band_solve_win(int64_t n, int64_t bw, const double* Lb, double* X, int64_
     set_error("wq_band_solve_win: bad arguments");
     return WQ_EINVAL;
   }
-  const unsigned grid = ceil_div(ncols, 64);
+  const unsigned grid = ceil_div(ncols, 128);
   cudaStream_t st = (cudaStream_t)stream;
   switch (bw) {
-    case 1: band_solve_win_kernel<1><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
-    case 2: band_solve_win_kernel<2><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
-    case 3: band_solve_win_kernel<3><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
-    case 4: band_solve_win_kernel<4><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
-    case 5: band_solve_win_kernel<5><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
-    case 6: band_solve_win_kernel<6><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
-    case 7: band_solve_win_kernel<7><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
-    default: band_solve_win_kernel<8><<<grid, 64, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 1: band_solve_win_kernel<1><<<grid, 128, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 2: band_solve_win_kernel<2><<<grid, 128, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 3: band_solve_win_kernel<3><<<grid, 128, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 4: band_solve_win_kernel<4><<<grid, 128, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 5: band_solve_win_kernel<5><<<grid, 128, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 6: band_solve_win_kernel<6><<<grid, 128, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    case 7: band_solve_win_kernel<7><<<grid, 128, 0, st>>>(n, Lb, X, ncols, ldx); break;
+    default: band_solve_win_kernel<8><<<grid, 128, 0, st>>>(n, Lb, X, ncols, ldx); break;
   }
   return check_launch("wq_band_solve_win");
 }

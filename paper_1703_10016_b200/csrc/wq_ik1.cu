@@ -65,8 +65,11 @@ __device__ __forceinline__ double k1_value(const wq_smooth_t& sm, int64_t qa, co
 
 __global__ void __launch_bounds__(IK1_THREADS)
 ik1_tile_kernel(wq_smooth_t sm, int64_t row0, int64_t row1, int64_t col0, int64_t col1, double* X,
-                int64_t ldx, int accumulate, int span, int* flag) {
+                int64_t ldx, int accumulate, int span, int* flag, int sym) {
   extern __shared__ double smem[];
+  // sym: rows == cols; only tiles on or above the diagonal, mirrored (K1 is
+  // symmetric in (q, r), so IK1 = G K1 G^T is)
+  if (sym && blockIdx.x < blockIdx.y) return;
   const int wg = (int)sm.wg;
   const int64_t I0 = row0 + (int64_t)blockIdx.y * IK1_TI;
   const int64_t J0 = col0 + (int64_t)blockIdx.x * IK1_TJ;
@@ -138,6 +141,10 @@ ik1_tile_kernel(wq_smooth_t sm, int64_t row0, int64_t row1, int64_t col0, int64_
     for (int w = 0; w < wg; ++w) acc = fma(gi[w], T[(q0 + w) * IK1_TJ + jj], acc);
     double* dst = X + (I0 - row0 + ii) * ldx + (J0 - col0 + jj);
     *dst = accumulate ? *dst + acc : acc;
+    if (sym && J0 > I0) {
+      double* mir = X + (J0 - col0 + jj) * ldx + (I0 - row0 + ii);
+      *mir = accumulate ? *mir + acc : acc;
+    }
   }
 }
 
@@ -167,7 +174,9 @@ extern "C" int wq_ik1(const wq_smooth_t* sm, int64_t row0, int64_t row1, int64_t
   }
   cudaFuncSetAttribute(ik1_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(ceil_div(col1 - col0, IK1_TJ), ceil_div(row1 - row0, IK1_TI));
+  // the full square (the assemble_ik1 / general-path call) uses the symmetry
+  const int sym = row0 == col0 && row1 == col1 && IK1_TI == IK1_TJ;
   ik1_tile_kernel<<<grid, IK1_THREADS, smem, (cudaStream_t)stream>>>(*sm, row0, row1, col0, col1, X,
-                                                                     ldx, accumulate, span, flag);
+                                                                     ldx, accumulate, span, flag, sym);
   return check_launch("wq_ik1");
 }
