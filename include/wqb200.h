@@ -337,6 +337,45 @@ int wq_gen_gather_d(int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc, int64_t
                     int wv, int nB, const int64_t* v_el, const int64_t* v_loc, const double* wd,
                     double* D, void* stream);
 
+/* Moments mode of the near-pair kernel: physical moments M(e,f) ((da+1) x (db+1))
+ * of touching pairs with e lattice (gidx[e] < 0) and f in G (gidx[f] >= 0) into
+ * mgc[gidx[f]][e] (n_g x n_el x (da+1) x (db+1)); other arguments as wq_gen_pair_blocks. */
+int wq_gen_near_moments(int64_t n_el, int da, int db, const double* elh, const double* elm,
+                        const int64_t* near_lo, const int64_t* near_cnt, int max_near,
+                        const double* near_unit, const double* touch, const double* ca,
+                        const double* cb, const int* gidx, double* mgc, void* stream);
+
+/* Far physical moments of the pairs (e lattice, f = glist[j] in G) into mgc[j][e]
+ * (tensor Gauss, orders 30 | 16 | 12 by separation; gx/gw as wq_gen_pair_blocks);
+ * touching pairs are left to wq_gen_near_moments. */
+int wq_gen_moments_far(int64_t n_el, int da1, int nb, int64_t n_g, const int64_t* glist,
+                       const int* gidx, const double* elh, const double* elm,
+                       const int64_t* near_lo, const int64_t* near_cnt, const double* gx,
+                       const double* gw, double* mgc, void* stream);
+
+/*
+ * Lattice route for graded open meshes (replaces the Theta / D accumulation of
+ * _log_part, assembly.py:206-236, for outer elements on the width-h0 lattice):
+ *   Y[r][f][b] = sum_{(e,a) in inc(r), kidx[e] valid} sum_al coef_e[al][a] M(e,f)[al][b]
+ *   out[c][r]  = sum_{(f,b) in inc(c)} sum_be Y[r][f][be] v_f[be][b]
+ * M(e,f) = h_e^(al+b+2) (m2u[k_f - k_e] + ln h_e c_al c_b) for lattice f (the
+ * reference's unit-table recipe, quadrature.py:497-500), mgc[gidx[f]][e] otherwise.
+ * Rows: coarse functions (coef = u, nal = da+1) -> out = Theta^T; or fine functions
+ * (coef = v, nal = db+1) -> out = D (symmetric, stored D[c][r]).  e_rows (n_el x nloc):
+ * the row function of local index a on element e (splines.py:427-472 cols).  r_emin/r_emax,
+ * c_emin/c_emax: first / last element of each support; espan / fspan: the largest
+ * element span of a 16-row / 64-column tile.  Column degree nb - 1 = 4.  Writes
+ * (does not accumulate) out; outer elements off the lattice are added afterwards by
+ * the block route (wq_gen_pair_blocks + gathers).
+ */
+int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, int wc,
+              const int64_t* e_rows, const int64_t* r_emin, const int64_t* r_emax,
+              const int64_t* c_el, const int64_t* c_loc, const int64_t* c_emin,
+              const int64_t* c_emax, const double* coef, int ldal, const double* v, int nb,
+              const double* elh, const int64_t* kidx, const int* gidx, const double* m2u,
+              int da1, const double* mgc, const double* ca, const double* cb, int64_t fspan,
+              int64_t espan, double* out, int64_t ldo, void* stream);
+
 /* wq_band_solve_cols with the last bw (<= 8) solution values kept in registers:
  * one load and one store per row and column (large n). */
 int wq_band_solve_win(int64_t n, int64_t bw, const double* Lb, double* X, int64_t ncols,

@@ -99,6 +99,13 @@ _SIGS = {
     "wq_gen_gather_d": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,
                         c_vp, c_vp],
     "wq_band_solve_win": [c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp],
+    "wq_gen_near_moments": [c_i64, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,
+                            c_vp, c_vp, c_vp, c_vp],
+    "wq_gen_moments_far": [c_i64, c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                           c_vp, c_vp, c_vp],
+    "wq_ystage": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                  c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,
+                  c_i64, c_i64, c_vp, c_i64, c_vp],
 }
 
 EXPORTED = tuple(_SIGS)

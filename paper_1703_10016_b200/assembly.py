@@ -572,11 +572,118 @@ def _gap_table(disc, lp: LogPart, h0: float):
     return m2
 
 
+# graded open meshes: lattice route (Theta / D straight from the gap table for
+# outer elements on the width-h0 lattice) when at most this many elements are off it
+_LATTICE_MAX_OFF = 4096
+_NOT_LATTICE = np.iinfo(np.int64).min
+
+
+def lattice_classes(elh, elm):
+    """Elements on the lattice of the median width h0 (width within 2e-11,
+    centre on the h0 grid to 1e-10 relative): returns (kidx, gidx, glist), kidx
+    the lattice index (or int64 min), gidx the index among the others (or -1).
+    The tolerances are tighter than the per-pair snap (1e-10 width, 1e-9
+    offset), so every lattice pair is one the reference's table recipe covers."""
+    h0 = float(np.median(elh))
+    on = np.abs(elh / h0 - 1.0) < 2e-11
+    kidx = np.full(len(elh), _NOT_LATTICE, np.int64)
+    if on.any():
+        ref = elm[np.argmax(on)]
+        k = (elm - ref) / h0
+        kr = np.rint(k)
+        on &= np.abs(k - kr) < 1e-10 * np.maximum(1.0, np.abs(k))
+        kidx[on] = kr[on].astype(np.int64)
+    glist = np.flatnonzero(~on).astype(np.int64)
+    gidx = np.full(len(elh), -1, np.int32)
+    gidx[glist] = np.arange(len(glist), dtype=np.int32)
+    return kidx, gidx, glist
+
+
+def _support_ranges(el):
+    """First / last element of each function's support from a (-1 padded)
+    incidence array (open meshes: contiguous)."""
+    big = np.iinfo(np.int64).max
+    lo = np.where(el >= 0, el, big).min(axis=1)
+    hi = np.where(el >= 0, el, -1).max(axis=1)
+    return lo.astype(np.int64), hi.astype(np.int64)
+
+
+def _tile_span(lo, hi, tile):
+    n = len(lo)
+    starts = np.arange(0, n, tile)
+    ends = np.minimum(starts + tile, n) - 1
+    return int((hi[ends] - lo[starts] + 1).max())
+
+
 def _graded_theta_d(disc, lp: LogPart, d):
+    consecutive = all(np.array_equal(c, c[:, :1] + np.arange(c.shape[1])[None, :])
+                      for c in (lp.ucols, lp.vcols))     # element functions are consecutive rows
+    if not disc.closed and _GEN_GAP_TABLE and lp.db == 4 and consecutive:
+        kidx, gidx, glist = lattice_classes(lp.elh, lp.elm)
+        if len(glist) <= _LATTICE_MAX_OFF:
+            return _lattice_theta_d(disc, lp, d, kidx, gidx, glist)
+    return _blocks_theta_d(disc, lp, d)
+
+
+def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist):
+    """Theta^T and D of a graded open mesh: lattice outer elements straight
+    from the unit gap table (wq_ystage), the few others by the block route."""
+    torch = _torch()
+    st = _lib.stream_handle()
+    N, NE, n = disc.space.dim, disc.refined.basis.dim, lp.n_el
+    nU, nB = lp.u.shape[2], lp.db + 1
+    da1 = lp.da + 1
+    key = "lattice"
+    if key not in d:
+        u_lo, u_hi = _support_ranges(lp.u_el)
+        v_lo, v_hi = _support_ranges(lp.v_el)
+        d[key] = {
+            "kidx": _to_dev(torch, kidx), "gidx": _to_dev(torch, gidx),
+            "glist": _to_dev(torch, glist) if len(glist) else None,
+            "u_lo": _to_dev(torch, u_lo), "u_hi": _to_dev(torch, u_hi),
+            "v_lo": _to_dev(torch, v_lo), "v_hi": _to_dev(torch, v_hi),
+            "u_es": _tile_span(u_lo, u_hi, 16), "v_es": _tile_span(v_lo, v_hi, 16),
+            "v_fs": _tile_span(v_lo, v_hi, 64),
+            "ucols": _to_dev(torch, lp.ucols.astype(np.int64)),
+            "vcols": _to_dev(torch, lp.vcols.astype(np.int64)),
+        }
+    L = d[key]
+    m2u = _gap_table(disc, lp, 1.0)
+    mgc = None
+    max_near = int(lp.near_cnt.max())
+    if len(glist):
+        mgc = torch.zeros((len(glist), n, da1, nB), dtype=torch.float64, device="cuda")
+        _lib.call("wq_gen_moments_far", n, da1, nB, len(glist), _lib.ptr(L["glist"]),
+                  _lib.ptr(L["gidx"]), _lib.ptr(d["elh"]), _lib.ptr(d["elm"]),
+                  _lib.ptr(d["near_lo"]), _lib.ptr(d["near_cnt"]), _lib.ptr(d["gx"]),
+                  _lib.ptr(d["gw"]), _lib.ptr(mgc), st)
+        _lib.call("wq_gen_near_moments", n, lp.da, lp.db, _lib.ptr(d["elh"]), _lib.ptr(d["elm"]),
+                  _lib.ptr(d["near_lo"]), _lib.ptr(d["near_cnt"]), max_near,
+                  _lib.ptr(d["near_unit"]), _lib.ptr(d["touch"]), _lib.ptr(d["ca"]),
+                  _lib.ptr(d["cb"]), _lib.ptr(L["gidx"]), _lib.ptr(mgc), st)
+    thetaT = torch.empty((NE, N), dtype=torch.float64, device="cuda")
+    D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
+    mg = _lib.ptr(mgc) if mgc is not None else None
+    cols = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]))
+    tail = (_lib.ptr(d["v"]), nB, _lib.ptr(d["elh"]), _lib.ptr(L["kidx"]), _lib.ptr(L["gidx"]),
+            _lib.ptr(m2u), da1, mg, _lib.ptr(d["ca"]), _lib.ptr(d["cb"]))
+    _lib.call("wq_ystage", N, NE, n, da1, nU, lp.v_el.shape[1], _lib.ptr(L["ucols"]),
+              _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *cols, _lib.ptr(d["u"]), da1, *tail,
+              L["v_fs"], L["u_es"], _lib.ptr(thetaT), N, st)
+    _lib.call("wq_ystage", NE, NE, n, nB, nB, lp.v_el.shape[1], _lib.ptr(L["vcols"]),
+              _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *cols, _lib.ptr(d["v"]), nB, *tail,
+              L["v_fs"], L["v_es"], _lib.ptr(D), NE, st)
+    if len(glist):
+        _blocks_theta_d(disc, lp, d, outer=glist, thetaT=thetaT, D=D)
+    return thetaT, D
+
+
+def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None):
     """Theta^T (N_E x N) and D (N_E x N_E) of a graded mesh: per-pair blocks
-    for a chunk of outer elements, then deterministic gathers (replaces the
-    gap-table accumulation of assembly.py:206-236, which the reference only
-    supports on uniform meshes)."""
+    for chunks of outer elements (all of them, or the runs of ``outer``), then
+    deterministic gathers, accumulating into ``thetaT`` / ``D`` when given
+    (replaces the gap-table accumulation of assembly.py:206-236, which the
+    reference only supports on uniform meshes)."""
     torch = _torch()
     st = _lib.stream_handle()
     N, NE, n = disc.space.dim, disc.refined.basis.dim, lp.n_el
@@ -586,16 +693,25 @@ def _graded_theta_d(disc, lp: LogPart, d):
     wt = torch.empty((n, nU, nB, chunk), dtype=torch.float64, device="cuda")   # chunk-minor
     wd = torch.empty((n, nB, nB, chunk), dtype=torch.float64, device="cuda")
     flags = torch.empty((n, -(-chunk // 64)), dtype=torch.int32, device="cuda")
-    thetaT = torch.zeros((NE, N), dtype=torch.float64, device="cuda")
-    D = torch.zeros((NE, NE), dtype=torch.float64, device="cuda")
+    if thetaT is None:
+        thetaT = torch.zeros((NE, N), dtype=torch.float64, device="cuda")
+        D = torch.zeros((NE, NE), dtype=torch.float64, device="cuda")
+    if outer is None:
+        ranges = [(e0, min(n, e0 + chunk)) for e0 in range(0, n, chunk)]
+    else:   # contiguous runs of the listed outer elements, split into chunks
+        cuts = np.flatnonzero(np.diff(outer) != 1) + 1
+        ranges = []
+        for run in np.split(outer, cuts):
+            for a in range(int(run[0]), int(run[-1]) + 1, chunk):
+                ranges.append((a, min(int(run[-1]) + 1, a + chunk)))
     max_near = int(lp.near_cnt.max())
     period = float(disc.refined.basis.length) if disc.closed else 0.0
     # open meshes: the reference's unit gap table serves every far pair of
     # equal widths at an integer offset (scaled per pair by the width)
-    m2u = _gap_table(disc, lp, 1.0) if not disc.closed and _GEN_GAP_TABLE else None
+    m2u = _gap_table(disc, lp, 1.0) if (not disc.closed and _GEN_GAP_TABLE
+                                        and outer is None) else None
     wu, wv = lp.u_el.shape[1], lp.v_el.shape[1]
-    for e0 in range(0, n, chunk):
-        e1 = min(n, e0 + chunk)
+    for e0, e1 in ranges:
         _lib.call("wq_gen_pair_blocks", n, e0, e1, lp.da, lp.db, nU - 1, int(disc.closed), period,
                   _lib.ptr(d["elh"]), _lib.ptr(d["elm"]), _lib.ptr(d["u"]), _lib.ptr(d["v"]),
                   _lib.ptr(d["near_lo"]), _lib.ptr(d["near_cnt"]), max_near,

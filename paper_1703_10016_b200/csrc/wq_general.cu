@@ -121,6 +121,8 @@ struct GenArgs {
   double* wd;               // [f][a'][b'][e - e0] D blocks
   int64_t ldc;              // >= e1 - e0
   int* tile_flag;           // (n_el, ceil((e1-e0)/64)): tile holds off-table far pairs
+  double* mg_out;           // near kernel, moments mode: (n_g, n_el, da+1, db+1) or NULL
+  const int* gidx;          // (n_el) index in G or -1 (moments mode)
 };
 
 __device__ __forceinline__ double wrap_delta(const GenArgs& A, double d) {
@@ -454,6 +456,12 @@ pair_near_kernel(GenArgs A, int max_near) {
     M[lane + 32 * j] = s * (acc[j] + lh * (A.ca[a] * (rp * A.cb[b])));
   }
   __syncwarp();
+  if (A.mg_out) {  // moments of (e lattice, f in G) for the lattice route (wq_ystage.cu)
+    const int gf = A.gidx[f];
+    if (gf >= 0 && A.gidx[e] < 0)
+      for (int i = lane; i < ns; i += 32) A.mg_out[((int64_t)gf * A.n_el + e) * ns + i] = M[i];
+    return;
+  }
   // contraction: 2 nU nB... outputs over the lanes
   const double* ue = A.u + e * nA * nU;
   const double* ve = A.v + e * nB * nB;
@@ -625,7 +633,7 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
   int rc = ensure_consts();
   if (rc) return rc;
   GenArgs A{n_el, e0, e1, da, db, pu, closed, period, elh, elm, u, v, near_lo, near_cnt,
-            near_unit, touch, gx, gw, m2u, ca, cb, wt, wd, ldc, tile_flag};
+            near_unit, touch, gx, gw, m2u, ca, cb, wt, wd, ldc, tile_flag, nullptr, nullptr};
   cudaStream_t st = (cudaStream_t)stream;
   dim3 g1(ceil_div(e1 - e0, FP_THREADS), (unsigned)n_el);   // (64 outer elements, inner f)
   const int nA = da + 1, np1 = db + 1;
@@ -663,6 +671,24 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
   dim3 g2(ceil_div(max_near, NP_WARPS), (unsigned)(e1 - e0));
   pair_near_kernel<<<g2, NP_WARPS * 32, smem, st>>>(A, max_near);
   return check_launch("wq_gen_pair_blocks(near)");
+}
+
+int wq_gen_near_moments(int64_t n_el, int da, int db, const double* elh, const double* elm,
+                        const int64_t* near_lo, const int64_t* near_cnt, int max_near,
+                        const double* near_unit, const double* touch, const double* ca,
+                        const double* cb, const int* gidx, double* mgc, void* stream) {
+  if (n_el <= 0 || da + 1 > GMAXA || db + 1 > GMAXB || max_near < 1 || !elh || !elm ||
+      !near_lo || !near_cnt || !near_unit || !touch || !ca || !cb || !gidx || !mgc) {
+    set_error("wq_gen_near_moments: bad arguments");
+    return WQ_EINVAL;
+  }
+  GenArgs A{n_el, 0, n_el, da, db, db, 0, 0.0, elh, elm, nullptr, nullptr, near_lo, near_cnt,
+            near_unit, touch, nullptr, nullptr, nullptr, ca, cb, nullptr, nullptr, 1, nullptr,
+            mgc, gidx};
+  const size_t smem = (size_t)NP_WARPS * (da + 1) * (db + 1) * sizeof(double);
+  dim3 g2(ceil_div(max_near, NP_WARPS), (unsigned)n_el);
+  pair_near_kernel<<<g2, NP_WARPS * 32, smem, (cudaStream_t)stream>>>(A, max_near);
+  return check_launch("wq_gen_near_moments");
 }
 
 int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc,
