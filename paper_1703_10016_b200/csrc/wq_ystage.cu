@@ -21,7 +21,8 @@ namespace wq {
 
 constexpr int YS_TR = 16;       // row functions per CTA (two groups of 8)
 constexpr int YS_TC = 64;       // column functions per CTA
-constexpr int YS_THREADS = 64 * YS_TR;   // (inner element lane, row warp-pair)
+constexpr int YS_RPT = 4;      // tile rows per thread
+constexpr int YS_THREADS = 64 * (YS_TR / YS_RPT);   // (inner element lane, row group)
 constexpr int YS_NB = 5;        // d + 1 (p = 4)
 constexpr int YS_MAXLOC = 8;    // local functions per element (p + 1 <= 8)
 constexpr int64_t YS_NOT_LATTICE = INT64_MIN;
@@ -54,7 +55,7 @@ struct YsArgs {
   int64_t ldo;
 };
 
-// Thread (inner element f, tile row r): Y[r][f][0..NB) in registers.
+// Thread (inner element f, group of YS_RPT tile rows): Y in registers.
 template <int NB>
 __global__ void __launch_bounds__(YS_THREADS)
 ystage_kernel(YsArgs A) {
@@ -107,65 +108,79 @@ ystage_kernel(YsArgs A) {
   }
   __syncthreads();
 
-  // phase 1: thread (f, r) accumulates Y[r][f][0..NB) in registers.  An
-  // element's nloc local functions are consecutive rows r0 .. r0+nloc-1
-  // (host-checked); lanes run over f, warps over rows, so whether row r meets
-  // element e is warp-uniform.
+  // phase 1: thread (f, row group of YS_RPT consecutive rows) accumulates
+  // Y[r][f][0..NB) in registers; every table value feeds the group's rows.
+  // An element's nloc local functions are consecutive rows r0 .. r0+nloc-1
+  // (host-checked); lanes run over f, warps over row groups, so which group
+  // rows meet element e is warp-uniform.
   {
-    const int r = tid / 64;
+    const int q = tid / 64;                  // row group
     for (int fl = tid % 64; fl < nf; fl += 64) {
       const int64_t f = fa + fl;
       const int64_t kf = A.kidx[f];
       const int gf = A.gidx[f];
-      double y[NB];
+      double y[YS_RPT][NB];
 #pragma unroll
-      for (int b = 0; b < NB; ++b) y[b] = 0.0;
-      if (r < nr) {
-        for (int el = 0; el < ne; ++el) {
-          const int a = r - Rw[el * nloc];   // local index of row r on element e
-          if (a < 0 || a >= nloc) continue;
-          const int64_t e = ea + el;
-          const int64_t ke = A.kidx[e];
-          if (ke == YS_NOT_LATTICE) continue;   // outer element in G: block route
-          double t[NB];
+      for (int j = 0; j < YS_RPT; ++j)
 #pragma unroll
-          for (int b = 0; b < NB; ++b) t[b] = 0.0;
-          const double* cs = Cs + el * nal * nloc + a;
-          if (kf != YS_NOT_LATTICE) {
-            const int64_t g = kf - ke;
-            const int64_t wrow = g - g0;
-            if (wrow >= 0 && wrow < nrow && g == f - e) {
-              const double* M = Mr + wrow * nal * NB;
-              for (int al = 0; al < nal; ++al) {
-                const double c = cs[al * nloc];
+        for (int b = 0; b < NB; ++b) y[j][b] = 0.0;
+      for (int el = 0; el < ne; ++el) {
+        const int a0 = YS_RPT * q - Rw[el * nloc];   // local index of the group's first row
+        if (a0 >= nloc || a0 + YS_RPT <= 0) continue;
+        const int64_t e = ea + el;
+        const int64_t ke = A.kidx[e];
+        if (ke == YS_NOT_LATTICE) continue;   // outer element in G: block route
+        double t[YS_RPT][NB];
 #pragma unroll
-                for (int b = 0; b < NB; ++b) t[b] = fma(c, M[al * NB + b], t[b]);
-              }
-            } else {   // off the staged index window: global table row
-              const double* __restrict__ M = A.m2u + ((g + A.n_el - 1) * da1) * NB;
-              for (int al = 0; al < nal; ++al) {
-                const double c = cs[al * nloc];
+        for (int j = 0; j < YS_RPT; ++j)
 #pragma unroll
-                for (int b = 0; b < NB; ++b) t[b] = fma(c, __ldg(M + al * NB + b), t[b]);
-              }
+          for (int b = 0; b < NB; ++b) t[j][b] = 0.0;
+        const double* cs = Cs + el * nal * nloc;
+        const bool table = kf != YS_NOT_LATTICE;
+        const double* __restrict__ Mg = nullptr;
+        const double* Ms = nullptr;
+        if (table) {
+          const int64_t g = kf - ke;
+          const int64_t wrow = g - g0;
+          if (wrow >= 0 && wrow < nrow && g == f - e) Ms = Mr + wrow * nal * NB;
+          else Mg = A.m2u + ((g + A.n_el - 1) * da1) * NB;   // off the staged window
+        } else {
+          if (!A.mgc) continue;
+          Mg = A.mgc + ((int64_t)gf * A.n_el + e) * da1 * NB;   // G partner, scaled moments
+        }
+        for (int al = 0; al < nal; ++al) {
+          double m[NB];
+          if (Ms) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) m[b] = Ms[al * NB + b];
+          } else {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) m[b] = __ldg(Mg + al * NB + b);
+          }
+#pragma unroll
+          for (int j = 0; j < YS_RPT; ++j) {
+            const int a = a0 + j;
+            if (a >= 0 && a < nloc) {
+              const double c = table ? cs[al * nloc + a] : A.coef[(e * A.ldal + al) * nloc + a];
+#pragma unroll
+              for (int b = 0; b < NB; ++b) t[j][b] = fma(c, m[b], t[j][b]);
             }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < YS_RPT; ++j) {
+          const int a = a0 + j;
+          if (a >= 0 && a < nloc)
 #pragma unroll
             for (int b = 0; b < NB; ++b)
-              y[b] += fma(Hb[el * NB + b], t[b], Lt[(el * nloc + a) * NB + b]);
-          } else if (A.mgc) {   // G partner: scaled moments, unscaled coefficients
-            const double* __restrict__ M = A.mgc + ((int64_t)gf * A.n_el + e) * da1 * NB;
-            for (int al = 0; al < nal; ++al) {
-              const double c = A.coef[(e * A.ldal + al) * nloc + a];
-#pragma unroll
-              for (int b = 0; b < NB; ++b) t[b] = fma(c, __ldg(M + al * NB + b), t[b]);
-            }
-#pragma unroll
-            for (int b = 0; b < NB; ++b) y[b] += t[b];
-          }
+              y[j][b] += table ? fma(Hb[el * NB + b], t[j][b], Lt[(el * nloc + a) * NB + b])
+                               : t[j][b];
         }
       }
 #pragma unroll
-      for (int b = 0; b < NB; ++b) Ys[(r * A.fspan + fl) * NB + b] = y[b];
+      for (int j = 0; j < YS_RPT; ++j)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) Ys[((YS_RPT * q + j) * A.fspan + fl) * NB + b] = y[j][b];
     }
   }
   __syncthreads();
