@@ -26,6 +26,7 @@
 #include <algorithm>
 
 #include "wq_common.cuh"
+#include "wq_log.cuh"
 
 namespace wq {
 
@@ -66,6 +67,22 @@ static int upload_logtab(const void* sym, int bins) {
   return WQ_OK;
 }
 
+int ensure_logtab();
+
+// device address of the 16-entry table (for kernels in other translation units)
+int logtab16_device(const double** out) {
+  int rc = ensure_logtab();
+  if (rc) return rc;
+  void* p = nullptr;
+  cudaError_t e = cudaGetSymbolAddress(&p, g_logtab16);
+  if (e != cudaSuccess) {
+    set_error("log table address: %s", cudaGetErrorString(e));
+    return WQ_ECUDA;
+  }
+  *out = static_cast<const double*>(p);
+  return WQ_OK;
+}
+
 int ensure_logtab() {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -78,9 +95,7 @@ int ensure_logtab() {
   return WQ_OK;
 }
 
-// 0.5 ln 2 = HLN2_A + HLN2_B, HLN2_A with 41 significant bits (e*A exact)
-constexpr double HLN2_A = 0.3465735902798315;
-constexpr double HLN2_B = 1.4117645281515789e-13;
+
 
 __device__ __forceinline__ double half_ln(double x, const double* __restrict__ tab) {
   const int hi = __double2hiint(x);
@@ -107,27 +122,6 @@ __device__ __forceinline__ double half_ln(double x, const double* __restrict__ t
   const double de = (double)e;
   const double t_hi = fma(de, HLN2_A, tab[LOGTAB + j]);
   const double t_lo = fma(de, HLN2_B, tab[2 * LOGTAB + j]);
-  return t_hi + fma(r, 0.5, fma(r2, q, t_lo));
-}
-
-__device__ __forceinline__ double half_ln16(double x, const double* __restrict__ tab) {
-  const int hi = __double2hiint(x);
-  const int lo = __double2loint(x);
-  const int e = (hi >> 20) - 1023;
-  const int j = (hi >> 16) & 15;
-  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-  const double r = fma(m, tab[j], -1.0);  // |r| < 2^-5
-  double q = fma(r, 0.5 / 9.0, -0.5 / 8.0);  // degree 9: truncation < 1.1e-19
-  q = fma(r, q, 0.5 / 7.0);
-  q = fma(r, q, -0.5 / 6.0);
-  q = fma(r, q, 0.5 / 5.0);
-  q = fma(r, q, -0.5 / 4.0);
-  q = fma(r, q, 0.5 / 3.0);
-  q = fma(r, q, -0.25);
-  const double r2 = r * r;
-  const double de = (double)e;
-  const double t_hi = fma(de, HLN2_A, tab[16 + j]);
-  const double t_lo = fma(de, HLN2_B, tab[32 + j]);
   return t_hi + fma(r, 0.5, fma(r2, q, t_lo));
 }
 
