@@ -324,12 +324,14 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
                        const double* ca, const double* cb, double* wt, double* wd,
                        int64_t ldc, int* tile_flag, void* stream);
 
-/* thetaT[l][i] += sum over the chunk's incidences of i (u_el/u_loc, width wu) and
- * all incidences of l (v_el/v_loc, width wv, -1 padded) of WT blocks; i in [i0, i1). */
+/* thetaT[l][i - i_off] (leading dimension ldt) += sum over the chunk's incidences
+ * of i (u_el/u_loc, width wu) and all incidences of l (v_el/v_loc, width wv, -1
+ * padded) of WT blocks; i in [i0, i1). */
 int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc,
                         int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
                         const int64_t* u_el, const int64_t* u_loc, const int64_t* v_el,
-                        const int64_t* v_loc, const double* wt, double* thetaT, void* stream);
+                        const int64_t* v_loc, const double* wt, double* thetaT, int64_t ldt,
+                        int64_t i_off, void* stream);
 
 /* D (symmetric, N_E x N_E) += chunk contributions of WD blocks for rows l in
  * [l0, l1), stored transposed (D[m][l]) so the stores are coalesced. */
@@ -364,7 +366,8 @@ int wq_gen_moments_far(int64_t n_el, int da1, int nb, int64_t n_g, const int64_t
  * (coef = v, nal = db+1) -> out = D (symmetric, stored D[c][r]).  e_rows (n_el x nloc):
  * the row function of local index a on element e (splines.py:427-472 cols).  r_emin/r_emax,
  * c_emin/c_emax: first / last element of each support; espan / fspan: the largest
- * element span of a 16-row / 64-column tile.  Column degree nb - 1 = 4.  Writes
+ * element span of a 16-row / 64-column tile.  Rows [row0, row1) only (row0 a
+ * multiple of 16), written to out[c][r - row0].  Column degree nb - 1 = 4.  Writes
  * (does not accumulate) out; outer elements off the lattice are added afterwards by
  * the block route (wq_gen_pair_blocks + gathers).
  */
@@ -374,7 +377,18 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
               const int64_t* c_emax, const double* coef, int ldal, const double* v, int nb,
               const double* elh, const int64_t* kidx, const int* gidx, const double* m2u,
               int da1, const double* mgc, const double* ca, const double* cb, int64_t fspan,
-              int64_t espan, double* out, int64_t ldo, void* stream);
+              int64_t espan, double* out, int64_t ldo, int64_t row0, int64_t row1,
+              void* stream);
+
+/* General-path row blocks (multi-GPU; X-form, assembly.py:233-245):
+ * wq_gather_fs_rows: P[m][i - i0] = alpha P[m][i - i0] - sum_t F[m][s_i + t] S_i[t],
+ *   i in [i0, i1), P with leading dimension ldp (the block's Theta^T columns);
+ * wq_phi_s_rows: X[i - i0][j] (+)= sum_t S_j[t] PhiT[i - i0][s_j + t] for all j
+ *   (PhiT = the block's Phi columns transposed, (i1 - i0) x N_E). */
+int wq_gather_fs_rows(const wq_logpart_t* lp, double alpha, const double* F, double* P,
+                      int64_t i0, int64_t i1, int64_t ldp, void* stream);
+int wq_phi_s_rows(const wq_logpart_t* lp, const double* PhiT, int64_t i0, int64_t i1, double* X,
+                  int64_t ldx, int accumulate, void* stream);
 
 /* wq_band_solve_cols with the last bw (<= 8) solution values kept in registers:
  * one load and one store per row and column (large n). */

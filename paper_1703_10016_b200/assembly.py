@@ -510,8 +510,25 @@ def _ik2_x2_into(disc, X, accumulate=True):
     if lp.path == "circulant":
         return _ik2_x2_rows(disc, X, 0, N, accumulate)
     NE = disc.refined.basis.dim
+    thetaT, D = _theta_d(disc, lp, d)
+    F = _fit_f(disc, lp, d, D)
+    hsolve = _hsolver(lp, d, NE)
+    # Phi = 2 H^{-1} Theta^T - F S
+    hsolve(thetaT, N)
+    _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(F), _lib.ptr(thetaT), st)
+    # X[j][i] (+)= sum_m S[m, j] Phi[m, i]  (= X2^T)
+    _lib.call("wq_add_st_phi", ctypes_ref(d["struct"]), _lib.ptr(thetaT), 0, N, _lib.ptr(X),
+              X.stride(0), int(accumulate), st)
+    return X
+
+
+def _theta_d(disc, lp: LogPart, d, rows=None):
+    """Theta^T (all columns, or the block rows = (row0, row1)) and D."""
+    torch = _torch()
+    st = _lib.stream_handle()
+    N, NE = disc.space.dim, disc.refined.basis.dim
     if lp.graded:
-        thetaT, D = _graded_theta_d(disc, lp, d)
+        thetaT, D = _graded_theta_d(disc, lp, d, rows)
     else:
         m2, keep = _m2_table(disc, lp)
         pp = _lib.WqPairs(N, NE, lp.n_el, m2.shape[0], lp.da, lp.db, int(disc.closed),
@@ -523,6 +540,14 @@ def _ik2_x2_into(disc, X, accumulate=True):
         D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
         _lib.call("wq_theta_t", ctypes_ref(pp), _lib.ptr(thetaT), st)
         _lib.call("wq_dmat", ctypes_ref(pp), _lib.ptr(D), st)
+        if rows is not None:
+            thetaT = thetaT[:, rows[0]:rows[1]].contiguous()
+    return thetaT, D
+
+
+def _hsolver(lp: LogPart, d, NE):
+    """Y <- H^{-1} Y on ncols columns (banded / arrow Cholesky of the fit)."""
+    st = _lib.stream_handle()
 
     def hsolve(Y, ncols):
         if lp.L21 is None and lp.bw <= 8:
@@ -534,19 +559,55 @@ def _ik2_x2_into(disc, X, accumulate=True):
         else:
             _lib.call("wq_cyc_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(d["L21"]),
                       _lib.ptr(d["L22"]), _lib.ptr(Y), ncols, Y.stride(0), st)
+    return hsolve
 
-    # E = H^{-1} D ; F = H^{-1} E^T = H^{-1} D H^{-1}
+
+def _fit_f(disc, lp: LogPart, d, D):
+    """F = H^{-1} D H^{-1} (D is overwritten by H^{-1} D)."""
+    torch = _torch()
+    NE = disc.refined.basis.dim
+    hsolve = _hsolver(lp, d, NE)
     hsolve(D, NE)
     F = torch.empty_like(D)
-    _lib.call("wq_transpose", _lib.ptr(D), NE, NE, _lib.ptr(F), st)
+    _lib.call("wq_transpose", _lib.ptr(D), NE, NE, _lib.ptr(F), _lib.stream_handle())
     hsolve(F, NE)
-    # Phi = 2 H^{-1} Theta^T - F S
-    hsolve(thetaT, N)
-    _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(F), _lib.ptr(thetaT), st)
-    # X[j][i] (+)= sum_m S[m, j] Phi[m, i]  (= X2^T)
-    _lib.call("wq_add_st_phi", ctypes_ref(d["struct"]), _lib.ptr(thetaT), 0, N, _lib.ptr(X),
-              X.stride(0), int(accumulate), st)
-    return X
+    return F
+
+
+def general_prepare(disc):
+    """F = H^{-1} D H^{-1} of the general path (replicated per rank; computed
+    once per assembly and shared by its row blocks)."""
+    lp, d = _logpart_dev(disc)
+    N = disc.space.dim
+    _, D = _theta_d(disc, lp, d, rows=(0, min(N, 64)))
+    return _fit_f(disc, lp, d, D)
+
+
+def general_rows_into(disc, X_rows, row0: int, row1: int, F=None):
+    """Rows [row0, row1) of the unsymmetrised X = IK1 + X2 of the general
+    (non-circulant) path into X_rows (leading dimension N): IK1 rows, the
+    block's Theta^T columns, replicated D and F, Phi = 2 H^{-1} Theta^T - F S on
+    the block's columns, X2[i][j] = sum_t S_j[t] Phi[s_j + t][i].  No
+    communication."""
+    lp, d = _logpart_dev(disc)
+    sm = _smooth(disc)
+    st = _lib.stream_handle()
+    N, NE = disc.space.dim, disc.refined.basis.dim
+    nr = row1 - row0
+    _lib.call("wq_ik1", ctypes_ref(sm["struct"]), row0, row1, 0, N, _lib.ptr(X_rows),
+              X_rows.stride(0), 0, sm["span"], _lib.ptr(sm["flag"]), st)
+    T, D = _theta_d(disc, lp, d, rows=(row0, row1))
+    if F is None:
+        F = _fit_f(disc, lp, d, D)
+    _hsolver(lp, d, NE)(T, nr)
+    _lib.call("wq_gather_fs_rows", ctypes_ref(d["struct"]), 2.0, _lib.ptr(F), _lib.ptr(T), row0,
+              row1, nr, st)
+    torch = _torch()
+    PhiT = torch.empty((nr, NE), dtype=torch.float64, device="cuda")
+    _lib.call("wq_transpose", _lib.ptr(T), NE, nr, _lib.ptr(PhiT), st)
+    _lib.call("wq_phi_s_rows", ctypes_ref(d["struct"]), _lib.ptr(PhiT), row0, row1,
+              _lib.ptr(X_rows), X_rows.stride(0), 1, st)
+    return X_rows
 
 
 # device bytes for one chunk of per-pair Theta / D blocks (graded meshes)
@@ -615,17 +676,19 @@ def _tile_span(lo, hi, tile):
     return int((hi[ends] - lo[starts] + 1).max())
 
 
-def _graded_theta_d(disc, lp: LogPart, d):
+def _graded_theta_d(disc, lp: LogPart, d, rows=None):
+    """Theta^T (N_E x N, or N_E x (row1 - row0) for rows = (row0, row1)) and D
+    (N_E x N_E) of a graded mesh."""
     consecutive = all(np.array_equal(c, c[:, :1] + np.arange(c.shape[1])[None, :])
                       for c in (lp.ucols, lp.vcols))     # element functions are consecutive rows
     if not disc.closed and _GEN_GAP_TABLE and lp.db == 4 and consecutive:
         kidx, gidx, glist = lattice_classes(lp.elh, lp.elm)
         if len(glist) <= _LATTICE_MAX_OFF:
-            return _lattice_theta_d(disc, lp, d, kidx, gidx, glist)
-    return _blocks_theta_d(disc, lp, d)
+            return _lattice_theta_d(disc, lp, d, kidx, gidx, glist, rows)
+    return _blocks_theta_d(disc, lp, d, rows=rows)
 
 
-def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist):
+def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None):
     """Theta^T and D of a graded open mesh: lattice outer elements straight
     from the unit gap table (wq_ystage), the few others by the block route."""
     torch = _torch()
@@ -661,7 +724,8 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist):
                   _lib.ptr(d["near_lo"]), _lib.ptr(d["near_cnt"]), max_near,
                   _lib.ptr(d["near_unit"]), _lib.ptr(d["touch"]), _lib.ptr(d["ca"]),
                   _lib.ptr(d["cb"]), _lib.ptr(L["gidx"]), _lib.ptr(mgc), st)
-    thetaT = torch.empty((NE, N), dtype=torch.float64, device="cuda")
+    r0, r1 = (0, N) if rows is None else rows
+    thetaT = torch.empty((NE, r1 - r0), dtype=torch.float64, device="cuda")
     D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
     mg = _lib.ptr(mgc) if mgc is not None else None
     cols = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]))
@@ -669,16 +733,16 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist):
             _lib.ptr(m2u), da1, mg, _lib.ptr(d["ca"]), _lib.ptr(d["cb"]))
     _lib.call("wq_ystage", N, NE, n, da1, nU, lp.v_el.shape[1], _lib.ptr(L["ucols"]),
               _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *cols, _lib.ptr(d["u"]), da1, *tail,
-              L["v_fs"], L["u_es"], _lib.ptr(thetaT), N, st)
+              L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, st)
     _lib.call("wq_ystage", NE, NE, n, nB, nB, lp.v_el.shape[1], _lib.ptr(L["vcols"]),
               _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *cols, _lib.ptr(d["v"]), nB, *tail,
-              L["v_fs"], L["v_es"], _lib.ptr(D), NE, st)
+              L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, st)
     if len(glist):
-        _blocks_theta_d(disc, lp, d, outer=glist, thetaT=thetaT, D=D)
+        _blocks_theta_d(disc, lp, d, outer=glist, thetaT=thetaT, D=D, rows=rows)
     return thetaT, D
 
 
-def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None):
+def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None, rows=None):
     """Theta^T (N_E x N) and D (N_E x N_E) of a graded mesh: per-pair blocks
     for chunks of outer elements (all of them, or the runs of ``outer``), then
     deterministic gathers, accumulating into ``thetaT`` / ``D`` when given
@@ -693,8 +757,9 @@ def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None):
     wt = torch.empty((n, nU, nB, chunk), dtype=torch.float64, device="cuda")   # chunk-minor
     wd = torch.empty((n, nB, nB, chunk), dtype=torch.float64, device="cuda")
     flags = torch.empty((n, -(-chunk // 64)), dtype=torch.int32, device="cuda")
+    r0, r1 = (0, N) if rows is None else rows
     if thetaT is None:
-        thetaT = torch.zeros((NE, N), dtype=torch.float64, device="cuda")
+        thetaT = torch.zeros((NE, r1 - r0), dtype=torch.float64, device="cuda")
         D = torch.zeros((NE, NE), dtype=torch.float64, device="cuda")
     if outer is None:
         ranges = [(e0, min(n, e0 + chunk)) for e0 in range(0, n, chunk)]
@@ -720,9 +785,11 @@ def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None):
                   _lib.ptr(d["ca"]), _lib.ptr(d["cb"]), _lib.ptr(wt),
                   _lib.ptr(wd), chunk, _lib.ptr(flags), st)
         uc, vc = lp.ucols[e0:e1], lp.vcols[e0:e1]
-        _lib.call("wq_gen_gather_theta", N, NE, e0, e1, chunk, int(uc.min()), int(uc.max()) + 1, wu,
-                  wv, nU, nB, _lib.ptr(d["u_el"]), _lib.ptr(d["u_loc"]), _lib.ptr(d["v_el"]),
-                  _lib.ptr(d["v_loc"]), _lib.ptr(wt), _lib.ptr(thetaT), st)
+        i0, i1 = max(int(uc.min()), r0), min(int(uc.max()) + 1, r1)
+        if i1 > i0:
+            _lib.call("wq_gen_gather_theta", N, NE, e0, e1, chunk, i0, i1, wu, wv, nU, nB,
+                      _lib.ptr(d["u_el"]), _lib.ptr(d["u_loc"]), _lib.ptr(d["v_el"]),
+                      _lib.ptr(d["v_loc"]), _lib.ptr(wt), _lib.ptr(thetaT), r1 - r0, r0, st)
         _lib.call("wq_gen_gather_d", NE, e0, e1, chunk, int(vc.min()), int(vc.max()) + 1, wv, nB,
                   _lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(wd), _lib.ptr(D), st)
     return thetaT, D

@@ -487,9 +487,9 @@ pair_near_kernel(GenArgs A, int max_near) {
 
 // Theta^T[l][i] += sum_{(e,a) in inc_u(i), e in chunk} sum_{(f,b) in inc_v(l)} WT[f][a][b][e-e0]
 // (threads over i: consecutive e, coalesced in the chunk-minor layout)
-__global__ void gather_theta_kernel(int64_t n_rows, int64_t e0, int64_t e1, int64_t ldc,
-                                    int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
-                                    const int64_t* u_el, const int64_t* u_loc,
+__global__ void gather_theta_kernel(int64_t ldt, int64_t i_off, int64_t e0, int64_t e1,
+                                    int64_t ldc, int64_t i0, int64_t i1, int wu, int wv, int nU,
+                                    int nB, const int64_t* u_el, const int64_t* u_loc,
                                     const int64_t* v_el, const int64_t* v_loc, const double* wt,
                                     double* thetaT) {
   const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -506,7 +506,7 @@ __global__ void gather_theta_kernel(int64_t n_rows, int64_t e0, int64_t e1, int6
       acc += wt[((f * nU + a) * nB + v_loc[l * wv + vb]) * ldc + (e - e0)];
     }
   }
-  thetaT[l * n_rows + i] += acc;
+  thetaT[l * ldt + (i - i_off)] += acc;
 }
 
 // D (symmetric) from the chunk: entry (l, m) = sum_{(e,a) in inc_v(l), e in
@@ -694,14 +694,15 @@ int wq_gen_near_moments(int64_t n_el, int da, int db, const double* elh, const d
 int wq_gen_gather_theta(int64_t n_rows, int64_t n_fine, int64_t e0, int64_t e1, int64_t ldc,
                         int64_t i0, int64_t i1, int wu, int wv, int nU, int nB,
                         const int64_t* u_el, const int64_t* u_loc, const int64_t* v_el,
-                        const int64_t* v_loc, const double* wt, double* thetaT, void* stream) {
-  if (i1 <= i0 || i0 < 0 || i1 > n_rows || n_fine <= 0 || !u_el || !u_loc || !v_el || !v_loc ||
-      !wt || !thetaT) {
+                        const int64_t* v_loc, const double* wt, double* thetaT, int64_t ldt,
+                        int64_t i_off, void* stream) {
+  if (i1 <= i0 || i0 < i_off || i1 > n_rows || n_fine <= 0 || !u_el || !u_loc || !v_el ||
+      !v_loc || !wt || !thetaT || ldt < i1 - i_off) {
     set_error("wq_gen_gather_theta: bad arguments");
     return WQ_EINVAL;
   }
   dim3 grid(ceil_div(i1 - i0, 64), (unsigned)n_fine);
-  gather_theta_kernel<<<grid, 64, 0, (cudaStream_t)stream>>>(n_rows, e0, e1, ldc, i0, i1, wu, wv,
+  gather_theta_kernel<<<grid, 64, 0, (cudaStream_t)stream>>>(ldt, i_off, e0, e1, ldc, i0, i1, wu, wv,
                                                             nU, nB, u_el, u_loc, v_el, v_loc, wt,
                                                             thetaT);
   return check_launch("wq_gen_gather_theta");

@@ -51,8 +51,11 @@ struct YsArgs {
   const double* ca;           // (da + 1) c_a
   const double* cb;           // (NB) c_b
   int64_t fspan, espan;       // max element span of a column / row tile (host)
-  double* out;                // (n_cols, ldo) output, Out[c][r]
+  double* out;                // (n_cols, ldo) output, Out[c][r - out_row0]
   int64_t ldo;
+  int64_t t0;                 // first row tile (rows t0*YS_TR ...)
+  int64_t out_row0;
+  int64_t row_end;            // rows >= row_end are not produced
 };
 
 // Thread (inner element f, group of YS_RPT tile rows): Y in registers.
@@ -60,8 +63,8 @@ template <int NB>
 __global__ void __launch_bounds__(YS_THREADS)
 ystage_kernel(YsArgs A) {
   extern __shared__ double sm[];
-  const int64_t R0 = (int64_t)blockIdx.x * YS_TR, C0 = (int64_t)blockIdx.y * YS_TC;
-  const int nr = (int)min((int64_t)YS_TR, A.n_rows - R0);
+  const int64_t R0 = (A.t0 + blockIdx.x) * YS_TR, C0 = (int64_t)blockIdx.y * YS_TC;
+  const int nr = (int)min((int64_t)YS_TR, A.row_end - R0);
   const int nc = (int)min((int64_t)YS_TC, A.n_cols - C0);
   const int64_t ea = A.r_emin[R0], eb = A.r_emax[R0 + nr - 1];
   const int64_t fa = A.c_emin[C0], fb = A.c_emax[C0 + nc - 1];
@@ -200,7 +203,7 @@ ystage_kernel(YsArgs A) {
 #pragma unroll
       for (int be = 0; be < NB; ++be) acc = fma(yr[be], vf[be * NB + b], acc);
     }
-    A.out[c * A.ldo + R0 + r] = acc;
+    A.out[c * A.ldo + R0 + r - A.out_row0] = acc;
   }
 }
 
@@ -264,17 +267,19 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
               const int64_t* c_emax, const double* coef, int ldal, const double* v, int nb,
               const double* elh, const int64_t* kidx, const int* gidx, const double* m2u,
               int da1, const double* mgc, const double* ca, const double* cb, int64_t fspan,
-              int64_t espan, double* out, int64_t ldo, void* stream) {
+              int64_t espan, double* out, int64_t ldo, int64_t row0, int64_t row1,
+              void* stream) {
   if (n_rows <= 0 || n_cols <= 0 || nal < 1 || nal > da1 || nloc < 1 || nloc > YS_MAXLOC ||
       wc < 1 || !e_rows || !r_emin || !r_emax || !c_el || !c_loc || !c_emin || !c_emax ||
       !coef || ldal < nal || !v || nb != YS_NB || !elh || !kidx || !gidx || !m2u || !ca || !cb ||
-      fspan < 1 || espan < 1 || !out || ldo < n_rows) {
+      fspan < 1 || espan < 1 || !out || row0 < 0 || row1 > n_rows || row1 <= row0 ||
+      row0 % YS_TR != 0 || ldo < row1 - row0) {
     set_error("wq_ystage: bad arguments (column degree must be %d)", YS_NB - 1);
     return WQ_EINVAL;
   }
   YsArgs A{n_rows, n_cols, n_el, nal, nloc, wc, e_rows, r_emin, r_emax, c_el, c_loc, c_emin,
            c_emax, coef, ldal, v, elh, kidx, gidx, m2u, da1, mgc, ca, cb, fspan, espan, out,
-           ldo};
+           ldo, row0 / YS_TR, row0, row1};
   const size_t smem = (size_t)(espan * nal * nloc + espan * nloc * YS_NB + espan * YS_NB +
                                (fspan + espan - 1) * nal * YS_NB + YS_TR * fspan * YS_NB) * 8 +
                       (size_t)espan * nloc * 4;
@@ -283,7 +288,9 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
     return WQ_EUNSUPPORTED;
   }
   cudaFuncSetAttribute(ystage_kernel<YS_NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid(ceil_div(n_rows, YS_TR), ceil_div(n_cols, YS_TC));
+  // rows [row0, row1): the last tile may run past row1 (up to n_rows) -- clip
+  const int64_t nrow_tiles = ceil_div(row1 - row0, YS_TR);
+  dim3 grid((unsigned)nrow_tiles, ceil_div(n_cols, YS_TC));
   ystage_kernel<YS_NB><<<grid, YS_THREADS, smem, (cudaStream_t)stream>>>(A);
   return check_launch("wq_ystage");
 }

@@ -46,15 +46,16 @@ def gather_rows(local_block, full, per, group=None):
     return full
 
 
-def assemble_rows_device(disc, X_block, row0: int, row1: int, zext=None):
+def assemble_rows_device(disc, X_block, row0: int, row1: int, zext=None, F=None):
     """Rows [row0, row1) of the unsymmetrised X = IK1 + X2 into X_block
-    (leading dimension N), circulant path (closed uniform simple-knot meshes).
-    row0 must be a multiple of the 64-row tile; no communication."""
+    (leading dimension N): the circulant fast path's row kernels, or the
+    general path's (assembly.general_rows_into).  row0 must be a multiple of
+    the 64-row tile; no communication."""
     from . import assembly as AS
     from . import _lib
 
-    if not AS._use_v2(disc):
-        raise NotImplementedError("row-block sharding needs the circulant (closed uniform) path")
+    if not AS._use_v2(disc):   # general path (open / repeated knots / graded meshes)
+        return AS.general_rows_into(disc, X_block, row0, row1, F=F)
     T = _lib.WQ_FTILE
     if row0 % T:
         raise ValueError("row blocks must start on a 64-row tile boundary")
@@ -119,10 +120,12 @@ def assemble_distributed_pipelined(disc, Xpad, chunks: int = 8, group=None, zext
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     N = disc.space.dim
-    Z = AS._zext_table(disc) if zext is None else zext
+    v2 = AS._use_v2(disc)
+    Z = (AS._zext_table(disc) if zext is None else zext) if v2 else None
+    F = None if v2 else AS.general_prepare(disc)   # replicated D / F, once per assembly
 
     def compute(r0, r1, view):
-        assemble_rows_device(disc, view, r0, r1, zext=Z)
+        assemble_rows_device(disc, view, r0, r1, zext=Z, F=F)
 
     pipeline_rows(N, world, rank, chunks, compute, Xpad, group)
     _lib.call("wq_symmetrize", _lib.ptr(Xpad), N, -1.0 / (4.0 * np.pi), _lib.stream_handle())

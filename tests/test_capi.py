@@ -40,3 +40,19 @@ def test_product_has_no_cpu_fallback():
         if fn.endswith(".py"):
             assert "oracle" not in open(os.path.join(pkg, fn)).read().replace(
                 "oracle`", "").split('"""', 2)[-1], fn
+
+
+def test_ctypes_signatures_match_header_arity():
+    """Every ctypes argtypes list has as many entries as the prototype in
+    include/wqb200.h has parameters."""
+    import re
+    from paper_1703_10016_b200 import _lib
+    hdr = open(HEADER).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    protos = {}
+    for m in re.finditer(r"\b(?:int|const char\*)\s+(wq_\w+)\s*\(([^)]*)\)\s*;", hdr):
+        params = m.group(2).strip()
+        protos[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    for name, args in _lib._SIGS.items():
+        assert name in protos, name
+        assert len(args) == protos[name], (name, len(args), protos[name])
