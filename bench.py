@@ -414,29 +414,47 @@ SURVEY_W_C5 = 5.46e11         # algorithmic flop-eq of the C5 assem
 
 
 def run_c5(args):
-    """Config 5 on one GPU: the general (graded-mesh) device path, one step =
-    one full assembly of A (per-pair blocks, gathers, banded fit solves, IK1,
-    symmetrise).  The reference cannot run it (quadrature.py:489-491)."""
+    """Config 5: the general (graded-mesh) device path, one step = one full
+    assembly of A (lattice Theta / D from the unit gap table, graded outer
+    elements by per-pair blocks, banded fit solves, IK1, symmetrise).  N > 1:
+    cyclic row blocks of the general path (replicated D / F) with the chunked
+    in-place NCCL all-gather.  The reference cannot run it
+    (quadrature.py:489-491)."""
     rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps({"impl": "reference", "unavailable": "the reference raises "
+                              "ConstructionError on graded meshes (quadrature.py:489-491)"}))
         return
     import torch
+    import torch.distributed as dist
     import paper_1703_10016_b200 as W
-    from paper_1703_10016_b200 import _lib, assembly as AS
-    if args.impl == "reference":
-        print(json.dumps({"impl": "reference", "unavailable": "the reference raises "
-                          "ConstructionError on graded meshes (quadrature.py:489-491)"}))
-        return
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    from paper_1703_10016_b200 import _lib, assembly as AS, distributed as D
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     curve, space = workload_c5()
     t0 = time.perf_counter()
     disc = W.build_discretization(curve, space, 1)
     AS._log_part(disc)
     precompute_s = time.perf_counter() - t0
     N = space.dim
-    X = torch.empty((N, N), dtype=torch.float64, device="cuda")
+    chunks = 4
+    if world == 1:
+        X = torch.empty((N, N), dtype=torch.float64, device="cuda")
+
+        def step():
+            AS._assemble_into(disc, X)
+    else:
+        sub, n_pad = D.cyclic_blocks(N, world, chunks)
+        Xpad = torch.empty((n_pad, N), dtype=torch.float64, device="cuda")
+
+        def step():
+            D.assemble_distributed_pipelined(disc, Xpad, chunks=chunks)
     for _ in range(args.warmup):
-        AS._assemble_into(disc, X)
+        step()
     torch.cuda.synchronize()
     AS._check_flag(AS._smooth(disc))
     # launches per step and per-entry-point split (host-synchronous, attribution only)
@@ -454,39 +472,55 @@ def run_c5(args):
         return r
 
     _lib.call = timed
-    AS._assemble_into(disc, X)
+    step()
     _lib.call = orig
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    with ClockSampler(local) as clk:
         time.sleep(0.3)
         e0.record()
         for _ in range(args.steps):
-            AS._assemble_into(disc, X)
+            step()
         e1.record()
         torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    t_dev = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    ms = float(t_dev.item())
     peak = fp64_peak_tflops(torch, _lib)
-    line = {
-        "metric": METRIC, "value": N * N / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (analytic slit, seeded knot multiplicities, BASELINE.json configs[4])",
-        "config": {"workload": "C5: open slit [-1,1]x{0}, p=4, 16384 elements graded 0.9 toward "
-                               "both ends (growth capped at the interior width after 60 elements), "
-                               "interior knots doubled w.p. 0.25 (default_rng(0))", "N": N,
-                   "nq": disc.nodes.n, "parallelism": "single GPU",
-                   "l2": "3.3 GB output > 126 MB L2, rewritten every step"},
-        "clocks": clk.summary(),
-        "gpu_launches": count["n"] * args.steps,
-        "split_ms": {k: round(v, 3) for k, v in sorted(split.items(), key=lambda t: -t[1])},
-        "roofline": {"bound": "fp64", "kernel": "whole step (SURVEY 8(d) W for C5)",
-                     "achieved": SURVEY_W_C5 / (ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
-                     "frac": SURVEY_W_C5 / (ms * 1e-3) / 1e12 / peak, "traffic": None},
-        "precompute_s": precompute_s,
-        "e2e": None,
-        "cpu_baseline": None,
-    }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": N * N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic slit, seeded knot multiplicities, BASELINE.json configs[4])",
+            "config": {"workload": "C5: open slit [-1,1]x{0}, p=4, 16384 elements graded 0.9 "
+                                   "toward both ends (growth capped at the interior width after "
+                                   "60 elements), interior knots doubled w.p. 0.25 "
+                                   "(default_rng(0))", "N": N, "nq": disc.nodes.n,
+                       "parallelism": (f"general-path cyclic row blocks x{world}, {chunks} chunks, "
+                                       "replicated D/F, in-place NCCL all-gather") if world > 1
+                       else "single GPU",
+                       "l2": "3.3 GB output > 126 MB L2, rewritten every step"},
+            "clocks": clk.summary(),
+            "gpu_launches": count["n"] * args.steps,
+            "split_ms": {k: round(v, 3) for k, v in sorted(split.items(), key=lambda t: -t[1])},
+            "roofline": {"bound": "fp64", "kernel": "whole step (SURVEY 8(d) W for C5)",
+                         "achieved": SURVEY_W_C5 / (ms * 1e-3) / 1e12 / world, "peak": peak,
+                         "unit": "TFLOP/s per GPU",
+                         "frac": SURVEY_W_C5 / (ms * 1e-3) / 1e12 / world / peak, "traffic": None},
+            "precompute_s": precompute_s,
+            "e2e": None,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def cpu_baseline(args, N):
