@@ -367,7 +367,9 @@ int wq_gen_moments_far(int64_t n_el, int da1, int nb, int64_t n_g, const int64_t
  * the row function of local index a on element e (splines.py:427-472 cols).  r_emin/r_emax,
  * c_emin/c_emax: first / last element of each support; espan / fspan: the largest
  * element span of a 16-row / 64-column tile.  Rows [row0, row1) only (row0 a
- * multiple of 16), written to out[c][r - row0].  Column degree nb - 1 = 4.  Writes
+ * multiple of 16), written to out[c][r - row0].  sym_d != 0 with rows == columns over
+ * the full range (D): only the storage entries out[c][r] with c >= r are produced
+ * (complete them, then wq_mirror_lower; D is symmetric).  Column degree nb - 1 = 4.  Writes
  * (does not accumulate) out; outer elements off the lattice are added afterwards by
  * the block route (wq_gen_pair_blocks + gathers).
  */
@@ -378,7 +380,10 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
               const double* elh, const int64_t* kidx, const int* gidx, const double* m2u,
               int da1, const double* mgc, const double* ca, const double* cb, int64_t fspan,
               int64_t espan, double* out, int64_t ldo, int64_t row0, int64_t row1,
-              void* stream);
+              int sym_d, void* stream);
+
+/* out[j][i] = out[i][j] for i > j (n x n, leading dimension ld). */
+int wq_mirror_lower(double* out, int64_t n, int64_t ld, void* stream);
 
 /* General-path row blocks (multi-GPU; X-form, assembly.py:233-245):
  * wq_gather_fs_rows: P[m][i - i0] = alpha P[m][i - i0] - sum_t F[m][s_i + t] S_i[t],

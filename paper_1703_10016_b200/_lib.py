@@ -96,6 +96,7 @@ _SIGS = {
                            c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],
     "wq_gen_gather_theta": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_int,
                             c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp],
+    "wq_mirror_lower": [c_vp, c_i64, c_i64, c_vp],
     "wq_gather_fs_rows": [ctypes.POINTER(WqLogpart), c_dbl, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp],
     "wq_phi_s_rows": [ctypes.POINTER(WqLogpart), c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_vp],
     "wq_gen_gather_d": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,
@@ -107,7 +108,7 @@ _SIGS = {
                            c_vp, c_vp, c_vp],
     "wq_ystage": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                   c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,
-                  c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp],
+                  c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_vp],
 }
 
 EXPORTED = tuple(_SIGS)

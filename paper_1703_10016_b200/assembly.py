@@ -636,6 +636,8 @@ def _gap_table(disc, lp: LogPart, h0: float):
 # graded open meshes: lattice route (Theta / D straight from the gap table for
 # outer elements on the width-h0 lattice) when at most this many elements are off it
 _LATTICE_MAX_OFF = 4096
+# D by its lower storage triangle + mirror (D is symmetric)
+_YS_SYM_D = True
 _NOT_LATTICE = np.iinfo(np.int64).min
 
 
@@ -733,12 +735,15 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None):
             _lib.ptr(m2u), da1, mg, _lib.ptr(d["ca"]), _lib.ptr(d["cb"]))
     _lib.call("wq_ystage", N, NE, n, da1, nU, lp.v_el.shape[1], _lib.ptr(L["ucols"]),
               _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *cols, _lib.ptr(d["u"]), da1, *tail,
-              L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, st)
+              L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, 0, st)
     _lib.call("wq_ystage", NE, NE, n, nB, nB, lp.v_el.shape[1], _lib.ptr(L["vcols"]),
               _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *cols, _lib.ptr(d["v"]), nB, *tail,
-              L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, st)
+              L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), st)
     if len(glist):
         _blocks_theta_d(disc, lp, d, outer=glist, thetaT=thetaT, D=D, rows=rows)
+    # D's lower storage triangle is complete (lattice + block parts): mirror it
+    if _YS_SYM_D:
+        _lib.call("wq_mirror_lower", _lib.ptr(D), NE, NE, st)
     return thetaT, D
 
 

@@ -56,16 +56,18 @@ struct YsArgs {
   int64_t t0;                 // first row tile (rows t0*YS_TR ...)
   int64_t out_row0;
   int64_t row_end;            // rows >= row_end are not produced
+  int sym;                    // rows == cols (D): only tiles meeting c >= r; mirrored after
 };
 
 // Thread (inner element f, group of YS_RPT tile rows): Y in registers.
-template <int NB>
+template <int NB, bool SYM>
 __global__ void __launch_bounds__(YS_THREADS)
 ystage_kernel(YsArgs A) {
   extern __shared__ double sm[];
   const int64_t R0 = (A.t0 + blockIdx.x) * YS_TR, C0 = (int64_t)blockIdx.y * YS_TC;
   const int nr = (int)min((int64_t)YS_TR, A.row_end - R0);
   const int nc = (int)min((int64_t)YS_TC, A.n_cols - C0);
+  if (SYM && C0 + nc - 1 < R0) return;   // strictly below the diagonal: mirrored later
   const int64_t ea = A.r_emin[R0], eb = A.r_emax[R0 + nr - 1];
   const int64_t fa = A.c_emin[C0], fb = A.c_emax[C0 + nc - 1];
   const int ne = (int)(eb - ea + 1), nf = (int)(fb - fa + 1);
@@ -207,6 +209,24 @@ ystage_kernel(YsArgs A) {
   }
 }
 
+// out[j][i] = out[i][j] for i > j (copy the lower triangle onto the upper one),
+// 32 x 32 tiles through shared memory
+__global__ void mirror_lower_kernel(double* out, int64_t n, int64_t ld) {
+  __shared__ double t[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;   // source tile rows bi, cols bj
+  if (bj > bi) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = bi * 32 + y, c = bj * 32 + tx;
+    t[y][tx] = (r < n && c < n) ? out[r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = bj * 32 + y, c = bi * 32 + tx;   // destination (upper) entry (r, c) = src (c, r)
+    if (r < n && c < n && c > r) out[r * ld + c] = t[tx][y];
+  }
+}
+
 // Far moments of pairs (e in L, f in G), physical: thread per outer element,
 // tensor Gauss by separation tier (30 / 16 / 12 as wq_gen_pair_blocks).
 constexpr int GM_THREADS = 64;
@@ -268,7 +288,7 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
               const double* elh, const int64_t* kidx, const int* gidx, const double* m2u,
               int da1, const double* mgc, const double* ca, const double* cb, int64_t fspan,
               int64_t espan, double* out, int64_t ldo, int64_t row0, int64_t row1,
-              void* stream) {
+              int sym_d, void* stream) {
   if (n_rows <= 0 || n_cols <= 0 || nal < 1 || nal > da1 || nloc < 1 || nloc > YS_MAXLOC ||
       wc < 1 || !e_rows || !r_emin || !r_emax || !c_el || !c_loc || !c_emin || !c_emax ||
       !coef || ldal < nal || !v || nb != YS_NB || !elh || !kidx || !gidx || !m2u || !ca || !cb ||
@@ -279,7 +299,7 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
   }
   YsArgs A{n_rows, n_cols, n_el, nal, nloc, wc, e_rows, r_emin, r_emax, c_el, c_loc, c_emin,
            c_emax, coef, ldal, v, elh, kidx, gidx, m2u, da1, mgc, ca, cb, fspan, espan, out,
-           ldo, row0 / YS_TR, row0, row1};
+           ldo, row0 / YS_TR, row0, row1, 0};
   const size_t smem = (size_t)(espan * nal * nloc + espan * nloc * YS_NB + espan * YS_NB +
                                (fspan + espan - 1) * nal * YS_NB + YS_TR * fspan * YS_NB) * 8 +
                       (size_t)espan * nloc * 4;
@@ -287,12 +307,29 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
     set_error("wq_ystage: tile needs %zu B of shared memory", smem);
     return WQ_EUNSUPPORTED;
   }
-  cudaFuncSetAttribute(ystage_kernel<YS_NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(ystage_kernel<YS_NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  cudaFuncSetAttribute(ystage_kernel<YS_NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
   // rows [row0, row1): the last tile may run past row1 (up to n_rows) -- clip
   const int64_t nrow_tiles = ceil_div(row1 - row0, YS_TR);
   dim3 grid((unsigned)nrow_tiles, ceil_div(n_cols, YS_TC));
-  ystage_kernel<YS_NB><<<grid, YS_THREADS, smem, (cudaStream_t)stream>>>(A);
+  // D (rows == cols, full range): only the storage entries out[c][r], c >= r
+  // (the caller completes D and mirrors it, wq_mirror_lower)
+  A.sym = n_rows == n_cols && row0 == 0 && row1 == n_rows && sym_d;
+  if (A.sym) ystage_kernel<YS_NB, true><<<grid, YS_THREADS, smem, (cudaStream_t)stream>>>(A);
+  else ystage_kernel<YS_NB, false><<<grid, YS_THREADS, smem, (cudaStream_t)stream>>>(A);
   return check_launch("wq_ystage");
+}
+
+int wq_mirror_lower(double* out, int64_t n, int64_t ld, void* stream) {
+  if (!out || n <= 0 || ld < n) {
+    set_error("wq_mirror_lower: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 mg(ceil_div(n, 32), ceil_div(n, 32));
+  mirror_lower_kernel<<<mg, dim3(32, 8), 0, (cudaStream_t)stream>>>(out, n, ld);
+  return check_launch("wq_mirror_lower");
 }
 
 int wq_gen_moments_far(int64_t n_el, int da1, int nb, int64_t n_g, const int64_t* glist,
