@@ -20,6 +20,11 @@ __host__ __device__ __forceinline__ int64_t pmod(int64_t a, int64_t n) {
   return r < 0 ? r + n : r;
 }
 
+// a mod n for a in (-n, 2n): two compares instead of an int64 division
+__host__ __device__ __forceinline__ int64_t wrap1(int64_t a, int64_t n) {
+  return a < 0 ? a + n : (a >= n ? a - n : a);
+}
+
 __host__ __device__ __forceinline__ int ceil_div(int64_t a, int64_t b) {
   return (int)((a + b - 1) / b);
 }

@@ -376,33 +376,52 @@ __global__ void transpose_kernel(const double* in, int64_t rows, int64_t cols, d
   }
 }
 
-// P[m][i] = alpha P[m][i] - sum_t F[m][(s_i + t) mod nf] S_i[t]
+// P[m][i] = alpha P[m][i] - sum_t F[m][(s_i + t) mod nf] S_i[t]; each CTA keeps
+// the S band of its 128 columns i in registers and sweeps GF_ROWS rows m
+constexpr int GF_ROWS = 32;
+constexpr int GF_MAXWS = 16;
 __global__ void gather_fs_kernel(wq_logpart_t lp, double alpha, const double* F, double* P) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t m = blockIdx.y;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t m0 = (int64_t)blockIdx.y * GF_ROWS;
   if (i >= lp.n_rows) return;
   const int64_t nf = lp.n_fine;
-  double acc = alpha * P[m * lp.n_rows + i];
-  for (int t = 0; t < lp.ws; ++t) {
-    double s = lp.s_w[i * lp.ws + t];
-    if (s != 0.0) acc = fma(-F[m * nf + pmod(lp.s_start[i] + t, nf)], s, acc);
+  double sw[GF_MAXWS];
+  int64_t col[GF_MAXWS];
+#pragma unroll
+  for (int t = 0; t < GF_MAXWS; ++t) {
+    sw[t] = t < lp.ws ? lp.s_w[i * lp.ws + t] : 0.0;
+    col[t] = t < lp.ws ? pmod(lp.s_start[i] + t, nf) : 0;
   }
-  P[m * lp.n_rows + i] = acc;
+  const int64_t m1 = m0 + GF_ROWS < nf ? m0 + GF_ROWS : nf;
+  for (int64_t m = m0; m < m1; ++m) {
+    double acc = alpha * P[m * lp.n_rows + i];
+    const double* fr = F + m * nf;
+#pragma unroll
+    for (int t = 0; t < GF_MAXWS; ++t)
+      if (t < lp.ws && sw[t] != 0.0) acc = fma(-fr[col[t]], sw[t], acc);
+    P[m * lp.n_rows + i] = acc;
+  }
 }
 
-// X[j][i] (+)= sum_t S_j[t] Phi[(s_j + t) mod nf][i]
-__global__ void add_st_phi_kernel(wq_logpart_t lp, const double* Phi, int64_t row0, double* X,
-                                  int64_t ldx, int accumulate) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t j = row0 + blockIdx.y;
+// X[j][i] (+)= sum_t S_j[t] Phi[(s_j + t) mod nf][i]; each CTA sweeps ST_ROWS
+// consecutive j, whose Phi rows overlap (L1 reuse)
+constexpr int ST_ROWS = 16;
+__global__ void add_st_phi_kernel(wq_logpart_t lp, const double* Phi, int64_t row0, int64_t row1,
+                                  double* X, int64_t ldx, int accumulate) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j0 = row0 + (int64_t)blockIdx.y * ST_ROWS;
   if (i >= lp.n_rows) return;
-  double acc = 0.0;
-  for (int t = 0; t < lp.ws; ++t) {
-    double s = lp.s_w[j * lp.ws + t];
-    if (s != 0.0) acc = fma(s, Phi[pmod(lp.s_start[j] + t, lp.n_fine) * lp.n_rows + i], acc);
+  const int64_t j1 = j0 + ST_ROWS < row1 ? j0 + ST_ROWS : row1;
+  for (int64_t j = j0; j < j1; ++j) {
+    double acc = 0.0;
+    const int64_t sj = pmod(lp.s_start[j], lp.n_fine);   // unwrapped start -> [0, nf)
+    for (int t = 0; t < lp.ws; ++t) {
+      const double s = lp.s_w[j * lp.ws + t];
+      if (s != 0.0) acc = fma(s, Phi[wrap1(sj + t, lp.n_fine) * lp.n_rows + i], acc);
+    }
+    double* dst = X + (j - row0) * ldx + i;
+    *dst = accumulate ? *dst + acc : acc;
   }
-  double* dst = X + (j - row0) * ldx + i;
-  *dst = accumulate ? *dst + acc : acc;
 }
 
 }  // namespace wq
@@ -524,7 +543,11 @@ int wq_gather_fs(const wq_logpart_t* lp, double alpha, const double* F, double* 
     set_error("wq_gather_fs: bad arguments");
     return WQ_EINVAL;
   }
-  dim3 grid(ceil_div(lp->n_rows, 128), (unsigned)lp->n_fine);
+  if (lp->ws > GF_MAXWS) {
+    set_error("wq_gather_fs: S band wider than %d", GF_MAXWS);
+    return WQ_EUNSUPPORTED;
+  }
+  dim3 grid(ceil_div(lp->n_rows, 128), ceil_div(lp->n_fine, GF_ROWS));
   gather_fs_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, alpha, F, P);
   return check_launch("wq_gather_fs");
 }
@@ -535,8 +558,9 @@ int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64
     set_error("wq_add_st_phi: bad arguments");
     return WQ_EINVAL;
   }
-  dim3 grid(ceil_div(lp->n_rows, 128), (unsigned)(row1 - row0));
-  add_st_phi_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, Phi, row0, X, ldx, accumulate);
+  dim3 grid(ceil_div(lp->n_rows, 128), ceil_div(row1 - row0, ST_ROWS));
+  add_st_phi_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, Phi, row0, row1, X, ldx,
+                                                            accumulate);
   return check_launch("wq_add_st_phi");
 }
 

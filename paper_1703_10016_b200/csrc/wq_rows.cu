@@ -17,9 +17,10 @@ __global__ void gather_fs_rows_kernel(wq_logpart_t lp, double alpha, const doubl
   if (i >= i1) return;
   const int64_t nf = lp.n_fine;
   double acc = alpha * P[m * ldp + (i - i0)];
+  const int64_t si = pmod(lp.s_start[i], nf);
   for (int t = 0; t < lp.ws; ++t) {
     const double s = lp.s_w[i * lp.ws + t];
-    if (s != 0.0) acc = fma(-F[m * nf + pmod(lp.s_start[i] + t, nf)], s, acc);
+    if (s != 0.0) acc = fma(-F[m * nf + wrap1(si + t, nf)], s, acc);
   }
   P[m * ldp + (i - i0)] = acc;
 }
@@ -33,9 +34,10 @@ __global__ void phi_s_rows_kernel(wq_logpart_t lp, const double* PhiT, int64_t i
   const int64_t nf = lp.n_fine;
   const double* ph = PhiT + il * nf;
   double acc = 0.0;
+  const int64_t sj = pmod(lp.s_start[j], nf);
   for (int t = 0; t < lp.ws; ++t) {
     const double s = lp.s_w[j * lp.ws + t];
-    if (s != 0.0) acc = fma(s, ph[pmod(lp.s_start[j] + t, nf)], acc);
+    if (s != 0.0) acc = fma(s, ph[wrap1(sj + t, nf)], acc);
   }
   double* dst = X + il * ldx + j;
   *dst = accumulate ? *dst + acc : acc;
