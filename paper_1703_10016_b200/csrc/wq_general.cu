@@ -541,7 +541,7 @@ __global__ void gather_d_kernel(int64_t n_fine, int64_t e0, int64_t e1, int64_t 
 template <int BW>
 __global__ void __launch_bounds__(128)
 band_solve_win_kernel(int64_t n, const double* Lb, double* X, int64_t ncols, int64_t ldx) {
-  constexpr int RB = 16;
+  constexpr int RB = 32;
   __shared__ double cf[RB][BW + 1];   // [r][0] = 1/diag, [r][j] = -off-diagonal
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool live = c < ncols;
