@@ -28,6 +28,7 @@ from .assembly import (
     assemble_ik1,
     assemble_ik2,
     assemble_matrix_device,
+    assemble_matrix_to_host,
     assemble_weighted_matrix,
     build_discretization,
     scale_and_symmetrize,

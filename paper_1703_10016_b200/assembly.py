@@ -958,6 +958,64 @@ def assemble_matrix_device(disc: Discretization, scaled: bool = True, out=None):
     return X
 
 
+def _copy_stream(torch):
+    if not hasattr(_copy_stream, "s"):
+        _copy_stream.s = torch.cuda.Stream()
+    return _copy_stream.s
+
+
+def assemble_matrix_to_host(disc: Discretization, out=None, scaled: bool = True,
+                            chunks: int = 32, work=None):
+    """A (scaled) or M into a host tensor, streaming finished row blocks to the
+    host while the next ones are assembled (closed uniform meshes: tile pairs
+    are processed in tile-row order, so once the pairs of tile rows < R are
+    done, rows < 64 R are final).  ``out``: (N, N) float64 CPU tensor, pinned
+    for full PCIe speed (allocated when None).  Other meshes assemble, then
+    copy.  ``work``: optional (N, N) device buffer for the assembly (else one is
+    cached on the discretization).  Returns ``out`` after the last copy."""
+    torch = _torch()
+    N = disc.space.dim
+    if out is None:
+        out = torch.empty((N, N), dtype=torch.float64, pin_memory=True)
+    X = work if work is not None else _dev(disc, "host_stage", lambda: _new_square(disc))
+    if not _use_v2(disc) or chunks <= 1:
+        _assemble_into(disc, X, scaled)
+        _check_flag(_smooth(disc))
+        out.copy_(X)
+        return out
+    alpha = -1.0 / (2.0 * TWO_PI) if scaled else 0.5
+    lp, d = _logpart_dev(disc)
+    sm = _smooth(disc)
+    main = torch.cuda.current_stream()
+    st = _lib.stream_handle(main)
+    Zext = _zext_table(disc)
+    x2args = (N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1], lp.uext.shape[1],
+              lp.zstride, _lib.ptr(d["uext"]), _lib.ptr(Zext), _lib.ptr(d["s_w"]), alpha, 2.0)
+    T = _lib.WQ_FTILE
+    nb = -(-N // T)
+    start = lambda r: r * nb - r * (r - 1) // 2     # first pair of tile row r
+    rows_per = max(1, -(-nb // chunks))
+    cs = _copy_stream(torch)
+    cs.wait_stream(main)
+    done = 0
+    for r0 in range(0, nb, rows_per):
+        r1 = min(nb, r0 + rows_per)
+        a, b = start(r0), start(r1)
+        _lib.call("wq_ik1_pairs", ctypes_ref(sm["struct"]), a, b, _lib.ptr(X), X.stride(0),
+                  _lib.ptr(sm["flag"]), st)
+        _lib.call("wq_x2_pairs_range", *x2args, a, b, _lib.ptr(X), X.stride(0), st)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        end = min(N, r1 * T)
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            out[done:end].copy_(X[done:end], non_blocking=True)
+        done = end
+    cs.synchronize()
+    _check_flag(sm)
+    return out
+
+
 def assemble_ik1(disc: Discretization) -> np.ndarray:
     """Smooth-part Galerkin matrix IK1 = G K1 G^T (assembly.py:175-183)."""
     X = _new_square(disc)
