@@ -90,6 +90,17 @@ int wq_ik1(const wq_smooth_t* sm, int64_t row0, int64_t row1, int64_t col0, int6
            double* X, int64_t ldx, int accumulate, int64_t max_span, int* flag, void* stream);
 
 /*
+ * IK1 for any rule band (irregular starts, widths <= wg <= 16; open, graded,
+ * repeated-knot meshes): register sliding windows over per-rule starts, 64 x 64
+ * tiles, table-based ln.  tile_row0 < 0: the whole matrix from its upper tile
+ * pairs, mirrored; else tile rows [tile_row0, tile_row1) x all columns into X
+ * (row tile_row0 * 64 at X).  span64: the largest node span of a 64-row tile
+ * (<= 144).  Writes (does not accumulate).
+ */
+int wq_ik1_band(const wq_smooth_t* sm, int64_t tile_row0, int64_t tile_row1, double* X,
+                int64_t ldx, int64_t span64, int* flag, void* stream);
+
+/*
  * Gap-indexed pair log-moment table (replaces uniform_pair_log_moments,
  * quadrature.py:472-504 / _unit_pair_stack :441-469):
  *   far gaps: 30x30 Gauss of ln|v-u-delta| (quadrature.py:413-438);

@@ -54,6 +54,7 @@ _SIGS = {
     "wq_dmma_peak": [c_i64, c_int, c_int, c_vp, c_vp],
     "wq_ik1": [ctypes.POINTER(WqSmooth), c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_int, c_i64,
                c_vp, c_vp],
+    "wq_ik1_band": [ctypes.POINTER(WqSmooth), c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp],
     "wq_pair_table": [c_i64, c_int, c_int, c_int, c_dbl, c_vp, c_vp, c_vp, c_int, c_vp, c_vp,
                       c_vp, c_vp],
     "wq_circ_tables": [c_i64, c_int, c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp,

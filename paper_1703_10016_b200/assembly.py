@@ -398,11 +398,25 @@ def _check_flag(sm):
         raise GeometryError("R <= 0 on assembly grid")
 
 
+# band IK1 kernel (sliding windows over per-rule starts) when the tile spans allow it
+_IK1_BAND = True
+
+
 def _ik1_into(disc, X, accumulate=False, row0=0, row1=None):
+    """IK1 (all rows, or rows [row0, row1) x all columns with row0 on a
+    64-row tile boundary) into X."""
     torch = _torch()
     sm = _smooth(disc)
     N = disc.space.dim
     row1 = N if row1 is None else row1
+    T = _lib.WQ_FTILE
+    if (_IK1_BAND and not accumulate and sm["span64"] <= 144 and 2 <= disc.rules.WG <= 16
+            and row0 % T == 0 and (row1 == N or row1 % T == 0)):
+        full = row0 == 0 and row1 == N
+        _lib.call("wq_ik1_band", ctypes_ref(sm["struct"]), -1 if full else row0 // T,
+                  -1 if full else -(-row1 // T), _lib.ptr(X), X.stride(0), sm["span64"],
+                  _lib.ptr(sm["flag"]), _lib.stream_handle())
+        return X
     _lib.call("wq_ik1", ctypes_ref(sm["struct"]), row0, row1, 0, N, _lib.ptr(X), X.stride(0),
               int(accumulate), sm["span"], _lib.ptr(sm["flag"]), _lib.stream_handle())
     return X
@@ -594,8 +608,7 @@ def general_rows_into(disc, X_rows, row0: int, row1: int, F=None):
     st = _lib.stream_handle()
     N, NE = disc.space.dim, disc.refined.basis.dim
     nr = row1 - row0
-    _lib.call("wq_ik1", ctypes_ref(sm["struct"]), row0, row1, 0, N, _lib.ptr(X_rows),
-              X_rows.stride(0), 0, sm["span"], _lib.ptr(sm["flag"]), st)
+    _ik1_into(disc, X_rows, accumulate=False, row0=row0, row1=row1)
     T, D = _theta_d(disc, lp, d, rows=(row0, row1))
     if F is None:
         F = _fit_f(disc, lp, d, D)

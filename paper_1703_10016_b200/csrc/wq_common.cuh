@@ -29,6 +29,21 @@ __host__ __device__ __forceinline__ int ceil_div(int64_t a, int64_t b) {
   return (int)((a + b - 1) / b);
 }
 
+// J(mid)^2 for a distinct node pair within eps_diag, from the host table
+__device__ __forceinline__ bool near_pair_j2(const wq_smooth_t& sm, int64_t qa, int64_t ra,
+                                             double* R) {
+  int64_t lo = qa < ra ? qa : ra, d = qa < ra ? ra - qa : qa - ra;
+  if (sm.closed && sm.nq - d < d) {  // seam pair: forward from the larger index
+    lo = qa < ra ? ra : qa;
+    d = sm.nq - d;
+  }
+  if (d > sm.near_k) return false;
+  const double v = sm.near_j2[lo * sm.near_k + (d - 1)];
+  if (!(v > 0.0)) return false;
+  *R = v;
+  return true;
+}
+
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kTwoPi = 6.28318530717958647692;
 

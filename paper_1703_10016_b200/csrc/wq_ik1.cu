@@ -22,21 +22,6 @@ struct NodeRec {
   double s, fx, fy, J;
 };
 
-// J(mid)^2 for a distinct node pair within eps_diag, from the host table
-__device__ __forceinline__ bool near_pair_j2(const wq_smooth_t& sm, int64_t qa, int64_t ra,
-                                             double* R) {
-  int64_t lo = qa < ra ? qa : ra, d = qa < ra ? ra - qa : qa - ra;
-  if (sm.closed && sm.nq - d < d) {  // seam pair: forward from the larger index
-    lo = qa < ra ? ra : qa;
-    d = sm.nq - d;
-  }
-  if (d > sm.near_k) return false;
-  const double v = sm.near_j2[lo * sm.near_k + (d - 1)];
-  if (!(v > 0.0)) return false;
-  *R = v;
-  return true;
-}
-
 __device__ __forceinline__ double k1_value(const wq_smooth_t& sm, int64_t qa, const NodeRec& a,
                                            int64_t ra, const NodeRec& b, int* bad,
                                            const double* ltab) {
