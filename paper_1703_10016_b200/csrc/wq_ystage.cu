@@ -27,6 +27,12 @@ constexpr int YS_NB = 5;        // d + 1 (p = 4)
 constexpr int YS_MAXLOC = 8;    // local functions per element (p + 1 <= 8)
 constexpr int64_t YS_NOT_LATTICE = INT64_MIN;
 
+__device__ __forceinline__ void ys_cp8(void* smem_dst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void ys_cp_wait() { asm volatile("cp.async.wait_all;\n" ::); }
+
 struct YsArgs {
   int64_t n_rows, n_cols, n_el;
   int nal;                    // outer polynomial slots (P + 1 for Theta, d + 1 for D)
@@ -105,12 +111,15 @@ ystage_kernel(YsArgs A) {
   // table rows for the index gaps f - e in [fa - eb, fb - ea]
   const int nrow = nf + ne - 1;
   const int64_t g0 = fa - eb;
+  // the window is one contiguous run of the table: asynchronous copies keep
+  // many loads in flight per thread
   for (int k = tid; k < nrow * nal * NB; k += YS_THREADS) {
     const int row = k / (nal * NB), rem = k - row * nal * NB;
     const int64_t g = g0 + row;
-    const bool ok = g > -A.n_el && g < A.n_el;
-    Mr[k] = ok ? A.m2u[((g + A.n_el - 1) * da1) * NB + rem] : 0.0;
+    if (g > -A.n_el && g < A.n_el) ys_cp8(Mr + k, A.m2u + ((g + A.n_el - 1) * da1) * NB + rem);
+    else Mr[k] = 0.0;
   }
+  ys_cp_wait();
   __syncthreads();
 
   // phase 1: thread (f, row group of YS_RPT consecutive rows) accumulates
