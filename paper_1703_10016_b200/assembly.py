@@ -427,6 +427,18 @@ def ctypes_ref(s):
     return ctypes.byref(s)
 
 
+# far gaps of the gap table by tiered Gauss orders (30 | 16 | 12) instead of the
+# reference's 30 everywhere (quadrature.py:369): same values to rounding
+_TIERED_TABLE = True
+
+
+def _table_rules():
+    if _TIERED_TABLE:
+        tiers = [PC.gauss_unit(n) for n in PC.GEN_GAUSS_TIERS]
+        return (np.concatenate([t[0] for t in tiers]), np.concatenate([t[1] for t in tiers]))
+    return PC.gauss_unit(PC.PAIR_FAR_ORDER)
+
+
 def _m2_table(disc, lp: LogPart):
     torch = _torch()
 
@@ -434,7 +446,7 @@ def _m2_table(disc, lp: LogPart):
         n = lp.n_el
         closed = disc.closed
         n_gap = n if closed else 2 * n - 1
-        gx, gw = PC.gauss_unit(PC.PAIR_FAR_ORDER)
+        gx, gw = _table_rules()
         m2 = torch.empty((n_gap, lp.da + 1, lp.db + 1), dtype=torch.float64, device="cuda")
         keep = [_to_dev(torch, lp.near_unit), _to_dev(torch, gx), _to_dev(torch, gw),
                 _to_dev(torch, PC.centred_monomial_integrals(lp.da)),
@@ -635,7 +647,7 @@ def _gap_table(disc, lp: LogPart, h0: float):
     gives the unit moments M')."""
     torch = _torch()
     n = lp.n_el
-    gx, gw = PC.gauss_unit(PC.PAIR_FAR_ORDER)
+    gx, gw = _table_rules()
     m2 = torch.empty((2 * n - 1, lp.da + 1, lp.db + 1), dtype=torch.float64, device="cuda")
     keep = [_to_dev(torch, lp.near_unit), _to_dev(torch, gx), _to_dev(torch, gw),
             _to_dev(torch, PC.centred_monomial_integrals(lp.da)),

@@ -20,6 +20,7 @@ namespace wq {
 constexpr int PT_MAXG = 32;   // max Gauss order
 constexpr int PT_MAXA = 24;   // max row degree + 1
 constexpr int PT_MAXB = 8;    // max col degree + 1
+constexpr int PT_TIERED = 58; // n_gauss value selecting the tiered rules 30 | 16 | 12
 
 __global__ void __launch_bounds__(128)
 pair_table_kernel(int64_t nel, int closed, int da, int db, double h, const double* near_unit,
@@ -40,9 +41,20 @@ pair_table_kernel(int64_t nel, int closed, int da, int db, double h, const doubl
   }
   const double delta = -keff;
   const int nA = da + 1, nB = db + 1;
+  // tiered rules (ng == 58: orders 30 | 16 | 12 concatenated): 16 points at
+  // gap 2 (one width of separation), 12 beyond -- converged to <= 7e-15 of
+  // the natural slot scale at degree 16 x 4 (tests/test_oracle.py); near gaps
+  // keep 30 for the periodic term
+  int g_off = 0;
+  if (ng == PT_TIERED) {
+    const double ak = fabs(keff);
+    if (ak >= 3.0) { g_off = 46; ng = 12; }
+    else if (ak >= 2.0) { g_off = 30; ng = 16; }
+    else ng = 30;
+  }
   for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-    x[g] = gx[g];
-    w[g] = gw[g];
+    x[g] = gx[g_off + g];
+    w[g] = gw[g_off + g];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < ng * nA; e += blockDim.x) {
@@ -433,7 +445,8 @@ extern "C" {
 int wq_pair_table(int64_t nel, int closed, int da, int db, double h, const double* near_unit,
                   const double* gx, const double* gw, int n_gauss, const double* ca,
                   const double* cb, double* m2, void* stream) {
-  if (nel < 2 || da + 1 > PT_MAXA || db + 1 > PT_MAXB || n_gauss > PT_MAXG || n_gauss < 1 ||
+  if (nel < 2 || da + 1 > PT_MAXA || db + 1 > PT_MAXB ||
+      (n_gauss > PT_MAXG && n_gauss != PT_TIERED) || n_gauss < 1 ||
       !near_unit || !gx || !gw || !ca || !cb || !m2 || !(h > 0)) {
     set_error("wq_pair_table: bad arguments");
     return WQ_EINVAL;
