@@ -259,27 +259,14 @@ int wq_x2_runs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
                double w_ik1, const int* runs, int64_t n_runs, double* X, int64_t ldx,
                void* stream);
 
-/*
- * Fused single launch of the circulant pipeline: IK1 tiles and log-part tile
- * pairs as interleaved CTAs (2 x pairs blocks) sharing every SM; x2 pair k
- * waits for ready[k] == epoch (published by the IK1 tile of pair k).  ready:
- * pairs ints, zero-initialised once; epoch: nonzero, distinct per call.  lead:
- * IK1 tiles scheduled ahead of the first x2 pair.  Same results as
- * wq_ik1_sym + wq_x2_pairs (bit-identical).
- */
-int wq_assemble_fused(const wq_smooth_t* sm, int p, int nA, int nApad, int ws, int ktot, int zstride,
-                      const double* Uext, const double* Zext, const double* s_w, double alpha,
-                      double w_ik1, int* ready, int epoch, int64_t lead, double* X, int64_t ldx,
-                      int* flag, void* stream);
-
-/* Self-test hooks (unit tests): fast 0.5*ln vs libdevice; one DMMA 8x8x4. */
+/* Self-test hooks (unit tests): the IK1 kernel's table 0.5*ln vs libdevice; one DMMA 8x8x4. */
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream);
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream);
 /* Throughput probe of 0.5*ln (tools): mode 0 table ln, 1 without I2F, 2 libdevice. */
 int wq_probe_log(int64_t iters, int blocks, int mode, double* out, void* stream);
 /* DMMA inner-loop probe (tools): blocks x 8 warps x iters x 180 DMMA (p = 3 layout). */
 int wq_probe_phi(int iters, int blocks, int mode, const double* Uext, double* out, void* stream);
-/* Tuning knob: column passes of the ik1 tile kernel (1: 2 CTAs/SM, 2: 3 CTAs/SM). */
+/* Tuning knob of ik1_sym: 1 = column loop unrolled 4 (default), 2 = unrolled 2. */
 int wq_set_ik1_passes(int npass);
 /* Profiling hook: per-CTA phase clock64 stamps of wq_x2_pairs (8 per CTA) into
  * buf (device memory), or NULL to disable. */

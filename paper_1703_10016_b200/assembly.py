@@ -859,24 +859,6 @@ def _diag_runs(disc):
     return _dev(disc, "runs", lambda: _to_dev(torch, diag_runs(disc.space.dim)))
 
 
-_FUSED = False       # single-launch interleaved IK1 / log-part CTAs (wq_assemble_fused):
-                     # bit-identical but measured 8% slower than two launches on B200
-_FUSED_LEAD = 1024   # IK1 tiles scheduled ahead of the first log-part pair
-
-
-def _ready_flags(disc):
-    """Per-pair readiness flags of the fused launch and a fresh epoch."""
-    torch = _torch()
-    N = disc.space.dim
-    nb = -(-N // _lib.WQ_FTILE)
-    d = disc._dev
-    if "ready" not in d:
-        d["ready"] = torch.zeros(nb * (nb + 1) // 2, dtype=torch.int32, device="cuda")
-        d["epoch"] = 0
-    d["epoch"] = d["epoch"] % 2000000000 + 1
-    return d["ready"], d["epoch"]
-
-
 _AUX_STREAMS = {}
 _USE_RUNS = False   # x2_runs (1 CTA/SM, resident windows) measured slower than x2_pairs (2 CTA/SM)
 
@@ -920,11 +902,6 @@ def _assemble_v2(disc: Discretization, X, alpha: float, w_ik1: float = 2.0, zext
     if chunks is None:
         chunks = 1
     ranges = pair_chunks(N, chunks)
-    if _FUSED and len(ranges) == 1:
-        ready, epoch = _ready_flags(disc)
-        _lib.call("wq_assemble_fused", ctypes_ref(sm["struct"]), *x2args[1:], _lib.ptr(ready),
-                  epoch, _FUSED_LEAD, _lib.ptr(X), X.stride(0), _lib.ptr(sm["flag"]), st)
-        return X
     if len(ranges) == 1:
         _lib.call("wq_ik1_sym", ctypes_ref(sm["struct"]), _lib.ptr(X), X.stride(0), sm["span64"],
                   _lib.ptr(sm["flag"]), st)

@@ -165,44 +165,6 @@ __device__ __forceinline__ void x2_mark(int slot) {
   if (d != nullptr && threadIdx.x == 0) d[(int64_t)blockIdx.x * 8 + slot] = clock64();
 }
 
-constexpr int IK1_THREADS = 288;  // 9 warps: 2*nQ (q, half) items
-
-template <int P, int MODE>
-struct Ik1Cfg {
-  static constexpr int WG = 2 * P + 1;           // rule width (nodes)
-  static constexpr int NQ = 2 * (FT - 1) + WG;   // nodes touched by a 64-row tile
-  static constexpr int NQP = NQ | 1;             // odd stride for T1 rows
-  static constexpr int HJ = FT / 2;              // columns per half
-};
-
-template <int MODE, int TAB>
-__device__ __forceinline__ double k1_half_ln(double qx, double qy, int qa, double qJ, double qs,
-                                             double rx, double ry, int ra, double rs,
-                                             const double* __restrict__ invp2, double period,
-                                             const double* tab, int& bad) {
-  double R;
-  if (qa == ra) {
-    R = qJ * qJ;  // continuity limit J^2 (geometry.py:240-245)
-  } else {
-    const double dx = qx - rx, dy = qy - ry;
-    const double d2 = fma(dx, dx, dy * dy);
-    if (MODE == WQ_K1_TABLE) {
-      R = d2 * __ldg(invp2 + (qa > ra ? qa - ra : ra - qa));
-    } else {
-      // periodic distance from the UNWRAPPED |t - s| (geometry.py:136-138)
-      const double xx = fabs(rs - qs);
-      const double p = (period / kPi) * fabs(sin(kPi * xx / period));
-      R = d2 / (p * p);
-    }
-  }
-  // R must be a positive finite normal double (geometry.py:246-247): test the
-  // high word on the integer pipe; a failing pair raises GeometryError on the
-  // host, so its (garbage) logarithm is never used
-  const unsigned rh = (unsigned)__double2hiint(R);
-  bad |= (rh - 0x00100000u) >= 0x7fe00000u;
-  return TAB == 0 ? half_ln16(R, tab) : half_ln(R, tab);
-}
-
 // Tile mapping: sym (tile_row0 < 0): upper-triangle pairs of an nb x nb tile grid;
 // rect: tile rows tile_row0 .. + gridDim.x / nbj, all nbj tile columns, output rows
 // offset by tile_row0 * FT (a rank's row block).
@@ -215,146 +177,249 @@ __device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int64_t pai
   }
 }
 
-// NPASS column passes per tile: 1 pass keeps T1 for all 64 columns (68 KB smem,
-// 2 CTAs/SM); 2 passes halve T1 (3 CTAs/SM) at +8% halo kernel evaluations.
-// NOTE: one CTA per upper-triangle tile pair (non-persistent): measured faster
-// than persistent / multi-pass / multi-stream variants on B200.
-// shared-memory footprint (doubles) of one ik1 tile: T1 | node data | rules | table | indices
+
+// ---------------------------------------------------------------------------
+// v5 IK1 tile (ik1_sym_kernel).  The v3 tile was bound by L1/shared-memory
+// instruction throughput (ncu: L1/TEX 89.7 %, FP64 pipe 47.6 %), and a first
+// rework by instruction issue (~50 issued instructions per kernel value, half
+// of them integer).  Here:
+//  * each thread owns TWO outer nodes q and q + QH of one column half, so
+//    every r-node load ({x, y} as one 16-byte load) and every rule-weight load
+//    (16-byte loads of a padded row) serves both;
+//  * the ln uses a 64-bin accurate table (one 16-byte load, degree-7 series,
+//    exponent by an exact DADD instead of I2F);
+//  * tile pairs whose node ranges neither wrap at the seam nor touch (all
+//    but O(nb) of them) take a fast path: the node-index gap is q - r + const
+//    with one sign across the tile, so 1/p^2 is read through one per-thread
+//    pointer walked with the r loop (immediate offsets), no diagonal select,
+//    and the R-validity test is a running integer min/max of R's high word.
+//  The rest (and the closed-form distance mode) take the general path with
+//  a running node index.  ~21.5 FP64 and ~12 other instructions per value.
+// 160 threads, 3 CTAs per SM at p = 3 (75.3 KB shared memory each).
+// ---------------------------------------------------------------------------
+
+constexpr int IK4_THREADS = 160;
+
 template <int P, int MODE>
-struct Ik1Smem {
-  using C = Ik1Cfg<P, MODE>;
-  static constexpr int T1 = FT * C::NQP;
-  static constexpr int NODE = 7 * C::NQ;
-  static constexpr int RULE = 2 * FT * C::WG;
-  static constexpr int TAB = 3 * 16;
-  static constexpr int IDX = C::NQ + 1;  // 2 NQ ints
-  static constexpr int TOTAL = T1 + NODE + RULE + TAB + IDX;
+struct Ik4Cfg {
+  static constexpr int WG = 2 * P + 1;
+  static constexpr int NQ = 2 * (FT - 1) + WG;
+  static constexpr int NQP = NQ | 1;
+  static constexpr int QH = (NQ + 1) / 2;     // outer-node pairs (u, u + QH)
+  static constexpr int HJ = FT / 2;
+  static constexpr int GW = (WG + 1) / 2 * 2;  // padded rule row (16-byte aligned)
+  static constexpr int T1 = (FT * NQP + 1) / 2 * 2;
+  // T1 | rxy (2 NQ) | rs (NQ, closed-form mode only, padded even) | G (FT GW) | table (128)
+  static constexpr int RS = MODE == WQ_K1_TABLE ? 0 : (NQ + 1) / 2 * 2;
+  static constexpr int TOTAL = T1 + 2 * NQ + RS + FT * GW + 128;
+  static_assert(2 * QH <= IK4_THREADS, "ik1 v5: too many outer-node pairs");
 };
 
-// One upper-triangle 64 x 64 tile (bi, bj) of IK1 (all 288 threads of the CTA).
-template <int P, int MODE, int TAB>
-__device__ __forceinline__ void ik1_tile(const wq_smooth_t& sm, int bi, int bj, int64_t row_off,
-                                         double* X, int64_t ldx, int& bad, double* dsm) {
-  using C = Ik1Cfg<P, MODE>;
-  using L = Ik1Smem<P, MODE>;
-  constexpr int WG = C::WG, NQ = C::NQ, NQP = C::NQP, HJ = C::HJ;
-  double* T1 = dsm;                        // [FT][NQP]: T1[j][q] = sum_w K1[q][2j + w] G_j[w]
-  double* qx = T1 + L::T1;
-  double* qy = qx + NQ;
-  double* qJ = qy + NQ;
-  double* qs = qJ + NQ;
-  double* rx = qs + NQ;
-  double* ry = rx + NQ;
-  double* rs = ry + NQ;
-  double (*Gi)[WG] = reinterpret_cast<double (*)[WG]>(rs + NQ);
-  double (*Gj)[WG] = reinterpret_cast<double (*)[WG]>(rs + NQ + FT * WG);
-  double* stab = rs + NQ + 2 * FT * WG;
-  int* qa = reinterpret_cast<int*>(stab + 3 * 16);
-  int* ra = qa + NQ;
+// general path: running node index ra, diagonal continuity limit, closed-form mode
+template <int MODE>
+__device__ __forceinline__ double k1_gen(double qx, double qy, double qJ2, double qs, int qa,
+                                         double2 rxy, double rs, int ra,
+                                         const double* __restrict__ invp2, double period,
+                                         const double2* tab, int& bad) {
+  const double dx = qx - rxy.x, dy = qy - rxy.y;
+  const double d2 = fma(dx, dx, dy * dy);
+  const int g = abs(qa - ra);
+  double R;
+  if (MODE == WQ_K1_TABLE) {
+    R = d2 * __ldg(invp2 + g);
+  } else {
+    const double xx = fabs(rs - qs);
+    const double p = (period / kPi) * fabs(sin(kPi * xx / period));
+    R = d2 / (p * p);
+  }
+  R = g == 0 ? qJ2 : R;  // continuity limit J^2 (geometry.py:240-245)
+  const unsigned rh = (unsigned)__double2hiint(R);
+  bad |= (rh - 0x00100000u) >= 0x7fe00000u;
+  return half_ln64t(R, tab);
+}
+
+// fast path: 1/p^2 at a known address, R's high word folded into min/max
+__device__ __forceinline__ double k1_fast(double qx, double qy, double2 rxy, double ip, int& hmin,
+                                          int& hmax, const double2* tab) {
+  const double dx = qx - rxy.x, dy = qy - rxy.y;
+  const double R = fma(dx, dx, dy * dy) * ip;
+  const int h = __double2hiint(R);
+  hmin = min(hmin, h);
+  hmax = max(hmax, h);
+  return half_ln64t(R, tab);
+}
+
+// phase 1 of a tile for the thread's outer nodes A, B and column half jb..jb+HJ-1.
+// FAST: SGN = +1 if every q node index exceeds every r node index, -1 if below.
+template <int P, int MODE, bool FAST, int SGN, int UNR>
+__device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const double* rsv,
+                                           const double* G, const double2* tab,
+                                           const wq_smooth_t& sm, int64_t q0, int64_t r0, int u,
+                                           int h, int& bad) {
+  using C = Ik4Cfg<P, MODE>;
+  constexpr int WG = C::WG, NQ = C::NQ, NQP = C::NQP, QH = C::QH, HJ = C::HJ, GW = C::GW;
+  const int64_t nq = sm.nq;
+  const int qA = u, qB = u + QH < NQ ? u + QH : NQ - 1;
+  const bool hasB = u + QH < NQ;
+  const int64_t gA = (q0 + qA) % nq, gB = (q0 + qB) % nq;
+  const double xA = sm.fx[gA], yA = sm.fy[gA];
+  const double xB = sm.fx[gB], yB = sm.fy[gB];
+  const int jb = h * HJ;
+  double wA[WG], wB[WG];
+  // general-path state
+  const int qaA = (int)gA, qaB = (int)gB;
+  const double J2A = sm.J[gA] * sm.J[gA], J2B = sm.J[gB] * sm.J[gB];
+  const double sA = sm.s[gA], sB = sm.s[gB];
+  const int nqi = (int)nq;
+  int ra = (int)((r0 + 2 * jb) % nq);
+  // fast-path state: ip(q, r) = invp2[SGN (q0 - r0 + q - r)] = pA[-SGN r'] with r' = r - 2 jb
+  const double* __restrict__ pA = sm.invp2 + SGN * (q0 - r0 + qA - 2 * jb);
+  const double* __restrict__ pB = sm.invp2 + SGN * (q0 - r0 + qB - 2 * jb);
+  int hmin = 0x7fffffff, hmax = (int)0x80000000;
+  // fast path: 1/p^2 of the next column's two new r nodes is loaded one column ahead
+  double ipA0 = 0.0, ipA1 = 0.0, ipB0 = 0.0, ipB1 = 0.0;
+  auto eval = [&](int r, int rr, double& vA, double& vB, double ipa, double ipb) {
+    const double2 p = rxy[r];
+    if (FAST) {
+      vA = k1_fast(xA, yA, p, ipa, hmin, hmax, tab);
+      vB = k1_fast(xB, yB, p, ipb, hmin, hmax, tab);
+    } else {
+      const double rs = MODE != WQ_K1_TABLE ? rsv[r] : 0.0;
+      vA = k1_gen<MODE>(xA, yA, J2A, sA, qaA, p, rs, ra, sm.invp2, sm.period, tab, bad);
+      vB = k1_gen<MODE>(xB, yB, J2B, sB, qaB, p, rs, ra, sm.invp2, sm.period, tab, bad);
+      if (++ra == nqi) ra = 0;
+    }
+  };
+#pragma unroll
+  for (int w = 0; w < WG - 2; ++w)
+    eval(2 * jb + w, w, wA[w], wB[w], FAST ? __ldg(pA - SGN * w) : 0.0,
+         FAST ? __ldg(pB - SGN * w) : 0.0);
+  if (FAST) {
+    ipA0 = __ldg(pA - SGN * (WG - 2));
+    ipA1 = __ldg(pA - SGN * (WG - 1));
+    ipB0 = __ldg(pB - SGN * (WG - 2));
+    ipB1 = __ldg(pB - SGN * (WG - 1));
+  }
+#pragma unroll UNR
+  for (int jj = 0; jj < HJ; ++jj) {
+    const int j = jb + jj;
+    const int r = 2 * j + WG - 2;
+    const double a0 = ipA0, a1 = ipA1, b0 = ipB0, b1 = ipB1;
+    if (FAST && jj + 1 < HJ) {
+      const int rn = 2 * (jj + 1) + WG - 2;
+      ipA0 = __ldg(pA - SGN * rn);
+      ipA1 = __ldg(pA - SGN * (rn + 1));
+      ipB0 = __ldg(pB - SGN * rn);
+      ipB1 = __ldg(pB - SGN * (rn + 1));
+    }
+    eval(r, 2 * jj + WG - 2, wA[WG - 2], wB[WG - 2], a0, b0);
+    eval(r + 1, 2 * jj + WG - 1, wA[WG - 1], wB[WG - 1], a1, b1);
+    const double2* g2 = reinterpret_cast<const double2*>(G + j * GW);
+    double g[GW];
+#pragma unroll
+    for (int w = 0; w < GW / 2; ++w) {
+      const double2 t = g2[w];
+      g[2 * w] = t.x;
+      g[2 * w + 1] = t.y;
+    }
+    double accA = 0.0, accB = 0.0;
+#pragma unroll
+    for (int w = 0; w < WG; ++w) {
+      accA = fma(wA[w], g[w], accA);
+      accB = fma(wB[w], g[w], accB);
+    }
+    T1[j * NQP + qA] = accA;
+    if (hasB) T1[j * NQP + qB] = accB;
+#pragma unroll
+    for (int w = 0; w < WG - 2; ++w) {
+      wA[w] = wA[w + 2];
+      wB[w] = wB[w + 2];
+    }
+  }
+  if (FAST) bad |= (hmin < 0x00100000) | (hmax >= 0x7ff00000);
+}
+
+template <int P, int MODE, int UNR>
+__device__ __forceinline__ void ik1_tile_v5(const wq_smooth_t& sm, int bi, int bj, int64_t row_off,
+                                            double* X, int64_t ldx, int& bad, double* dsm) {
+  using C = Ik4Cfg<P, MODE>;
+  constexpr int WG = C::WG, NQ = C::NQ, NQP = C::NQP, QH = C::QH, GW = C::GW;
+  double* T1 = dsm;                                            // [FT][NQP]
+  double2* rxy = reinterpret_cast<double2*>(dsm + C::T1);      // [NQ]
+  double* rsv = dsm + C::T1 + 2 * NQ;                          // [NQ] (closed-form mode)
+  double* G = rsv + C::RS;                                     // [FT][GW]: G_J, then G_I
+  double2* tab = reinterpret_cast<double2*>(G + FT * GW);      // [64]
 
   const int64_t N = sm.n_rows, nq = sm.nq;
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
   const int nj = (int)min((int64_t)FT, N - J0);
   const int tid = threadIdx.x;
-  {
-    // node ranges (unwrapped starts are 2(i-p)+1; index modulo nq)
-    const int64_t qlo = sm.g_start[I0], rlo = sm.g_start[J0];
-    int64_t q0 = qlo % nq;
-    if (q0 < 0) q0 += nq;
-    int64_t r0 = rlo % nq;
-    if (r0 < 0) r0 += nq;
-    for (int k = tid; k < NQ; k += IK1_THREADS) {
-      int64_t a = q0 + k;
-      if (a >= nq) a -= nq;
-      if (a >= nq) a %= nq;
-      qa[k] = (int)a;
-      qx[k] = sm.fx[a]; qy[k] = sm.fy[a]; qJ[k] = sm.J[a]; qs[k] = sm.s[a];
-      int64_t b = r0 + k;
-      if (b >= nq) b -= nq;
-      if (b >= nq) b %= nq;
-      ra[k] = (int)b;
-      rx[k] = sm.fx[b]; ry[k] = sm.fy[b]; rs[k] = sm.s[b];
-    }
-    for (int k = tid; k < FT * WG; k += IK1_THREADS) {
-      const int ii = k / WG, w = k - ii * WG;
-      Gi[ii][w] = ii < ni ? sm.g_w[(I0 + ii) * WG + w] : 0.0;
-      Gj[ii][w] = ii < nj ? sm.g_w[(J0 + ii) * WG + w] : 0.0;
-    }
-    if (TAB == 0)
-      for (int k = tid; k < 3 * 16; k += IK1_THREADS) stab[k] = g_logtab16[k];
+  int64_t q0 = sm.g_start[I0] % nq;
+  if (q0 < 0) q0 += nq;
+  int64_t r0 = sm.g_start[J0] % nq;
+  if (r0 < 0) r0 += nq;
+  for (int k = tid; k < NQ; k += blockDim.x) {
+    const int64_t b = (r0 + k) % nq;
+    rxy[k] = make_double2(sm.fx[b], sm.fy[b]);
+    if (MODE != WQ_K1_TABLE) rsv[k] = sm.s[b];
   }
-  x2_mark(0);
-  __syncthreads();
-  x2_mark(1);
-
-  // ---- phase 1: item (q, half): sliding window over r = 2j .. 2j+WG-1 ----
-  const double* __restrict__ tab = TAB == 0 ? stab : g_logtab;
-  const double* __restrict__ invp2 = sm.invp2;
-  const double period = sm.period;
-  // (q, half) items: half 0 on threads 0..143, half 1 on 144..287, so a warp
-  // (but one) shares its column j: G_j and r-node loads are broadcasts
-  constexpr int HALF_THREADS = IK1_THREADS / 2;
-  static_assert(NQ <= HALF_THREADS, "tile too tall for the (q, half) mapping");
-  const int h = tid >= HALF_THREADS ? 1 : 0;
-  const int q = tid - h * HALF_THREADS;
-  if (q < NQ) {
-    const double mx = qx[q], my = qy[q], mJ = qJ[q], ms = qs[q];
-    const int ma = qa[q];
-    const int jb = h * HJ;
-    double win[WG];
-#pragma unroll
-    for (int w = 0; w < WG - 2; ++w) {
-      const int r = 2 * jb + w;
-      win[w] = k1_half_ln<MODE, TAB>(mx, my, ma, mJ, ms, rx[r], ry[r], ra[r], rs[r], invp2, period, tab,
-                                bad);
-    }
-#pragma unroll 4
-    for (int jj = 0; jj < HJ; ++jj) {
-      const int j = jb + jj;
-      const int r = 2 * j + WG - 2;
-      win[WG - 2] = k1_half_ln<MODE, TAB>(mx, my, ma, mJ, ms, rx[r], ry[r], ra[r], rs[r], invp2, period,
-                                     tab, bad);
-      win[WG - 1] = k1_half_ln<MODE, TAB>(mx, my, ma, mJ, ms, rx[r + 1], ry[r + 1], ra[r + 1], rs[r + 1],
-                                     invp2, period, tab, bad);
-      double acc = 0.0;
-#pragma unroll
-      for (int w = 0; w < WG; ++w) acc = fma(win[w], Gj[j][w], acc);
-      T1[j * NQP + q] = acc;
-#pragma unroll
-      for (int w = 0; w < WG - 2; ++w) win[w] = win[w + 2];
-    }
+  for (int k = tid; k < FT * GW; k += blockDim.x) {
+    const int jj = k / GW, w = k - jj * GW;
+    G[k] = (jj < nj && w < WG) ? sm.g_w[(J0 + jj) * WG + w] : 0.0;
   }
-  x2_mark(2);
+  for (int k = tid; k < 128; k += blockDim.x) reinterpret_cast<double*>(tab)[k] = kTang64[k];
   __syncthreads();
-  x2_mark(3);
 
-  // ---- phase 2: item (j, quarter c): IK1[i][j], i in 16c .. 16c+15 ----
-  if (tid < 4 * FT) {
+  // ---- phase 1 ----
+  if (tid < 2 * QH) {
+    const int h = tid >= QH ? 1 : 0;
+    const int u = tid - h * QH;
+    const bool nowrap = q0 + NQ <= nq && r0 + NQ <= nq;
+    if (MODE == WQ_K1_TABLE && nowrap && q0 >= r0 + NQ)
+      ik1_phase1<P, MODE, true, 1, UNR>(T1, rxy, rsv, G, tab, sm, q0, r0, u, h, bad);
+    else if (MODE == WQ_K1_TABLE && nowrap && r0 >= q0 + NQ)
+      ik1_phase1<P, MODE, true, -1, UNR>(T1, rxy, rsv, G, tab, sm, q0, r0, u, h, bad);
+    else
+      ik1_phase1<P, MODE, false, 1, UNR>(T1, rxy, rsv, G, tab, sm, q0, r0, u, h, bad);
+  }
+  __syncthreads();
+  for (int k = tid; k < FT * GW; k += blockDim.x) {
+    const int ii = k / GW, w = k - ii * GW;
+    G[k] = (ii < ni && w < WG) ? sm.g_w[(I0 + ii) * WG + w] : 0.0;
+  }
+  __syncthreads();
+
+  // ---- phase 2: item (j, half c): IK1[i][j], i in 32c .. 32c+31 ----
+  if (tid < 2 * FT) {
     const int j = tid & (FT - 1), c = tid >> 6;
     const double* t = T1 + j * NQP;
-    const int i0 = 16 * c;
+    const int i0 = 32 * c;
     double win[WG];
 #pragma unroll
     for (int w = 0; w < WG - 2; ++w) win[w] = t[2 * i0 + w];
 #pragma unroll 4
-    for (int ii = 0; ii < 16; ++ii) {
+    for (int ii = 0; ii < 32; ++ii) {
       const int i = i0 + ii;
       win[WG - 2] = t[2 * i + WG - 2];
       win[WG - 1] = t[2 * i + WG - 1];
+      const double2* g2 = reinterpret_cast<const double2*>(G + i * GW);
       double acc = 0.0;
 #pragma unroll
-      for (int w = 0; w < WG; ++w) acc = fma(Gi[i][w], win[w], acc);
+      for (int w = 0; w < GW / 2; ++w) {
+        const double2 gg = g2[w];
+        acc = fma(gg.x, win[2 * w], acc);
+        if (2 * w + 1 < WG) acc = fma(gg.y, win[2 * w + 1], acc);
+      }
       if (i < ni && j < nj) X[(I0 - row_off + i) * ldx + J0 + j] = acc;
 #pragma unroll
       for (int w = 0; w < WG - 2; ++w) win[w] = win[w + 2];
     }
   }
-  x2_mark(4);
 }
 
 template <int P, int MODE, int TAB>
-__global__ void __launch_bounds__(IK1_THREADS, 2)
+__global__ void __launch_bounds__(IK4_THREADS, 3)
 ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, int64_t ldx,
                int* flag) {
   extern __shared__ double dsm[];
@@ -362,7 +427,7 @@ ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, 
   tile_of_block(nb, tile_row0, pair0, bi, bj);
   const int64_t row_off = tile_row0 < 0 ? 0 : (int64_t)tile_row0 * FT;
   int bad = 0;
-  ik1_tile<P, MODE, TAB>(sm, bi, bj, row_off, X, ldx, bad, dsm);
+  ik1_tile_v5<P, MODE, TAB == 1 ? 2 : 4>(sm, bi, bj, row_off, X, ldx, bad, dsm);
   if (bad) atomicOr(flag, WQ_FLAG_R_NONPOSITIVE);
 }
 
@@ -638,68 +703,6 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   const bool rect = tile_row0 >= 0;
   x2_tile<P>(N, Uext, Zext, sw, alpha, w_ik1, X, ldx, bi, bj, rect,
              rect ? (int64_t)tile_row0 * FT : 0, smem);
-}
-
-// ---------------------------------------------------------------------------
-// Fused single launch: IK1 tiles (FP64 DFMA, issue-bound) and log-part tile
-// pairs (DMMA) as interleaved CTAs, so both kinds share every SM.  Block
-// order: ik1(0..L-1), then x2(k) / ik1(k+L) alternating, then the remaining
-// x2.  x2(k) needs IK1(k): it waits for ready[k] == epoch, published by
-// ik1(k) after its tile is globally visible.  CTAs are dispatched in blockIdx
-// order and ik1 CTAs never wait, so every awaited producer is already
-// resident or finished; the wait is bounded (trap instead of a hang).
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int P, int MODE, int TAB>
-__global__ void __launch_bounds__(IK1_THREADS, 2)
-fused_pairs_kernel(wq_smooth_t sm, const double* __restrict__ Uext,
-                   const double* __restrict__ Zext, const double* __restrict__ sw, double alpha,
-                   double w_ik1, double* X, int64_t ldx, int nb, int64_t n_pairs, int64_t lead,
-                   int* ready, int epoch, int* flag) {
-  extern __shared__ double dsm[];
-  const int64_t b = blockIdx.x;
-  const int64_t m = n_pairs - lead;
-  bool is_x2;
-  int64_t t;
-  if (b < lead) {
-    is_x2 = false;
-    t = b;
-  } else {
-    const int64_t j = b - lead;
-    if (j < 2 * m) {
-      is_x2 = (j & 1) == 0;
-      t = is_x2 ? (j >> 1) : lead + (j >> 1);
-    } else {
-      is_x2 = true;
-      t = m + (j - 2 * m);
-    }
-  }
-  int bi, bj;
-  tri_index(t, nb, bi, bj);
-  if (!is_x2) {
-    int bad = 0;
-    ik1_tile<P, MODE, TAB>(sm, bi, bj, 0, X, ldx, bad, dsm);
-    if (bad) atomicOr(flag, WQ_FLAG_R_NONPOSITIVE);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) atomicExch(ready + t, epoch);
-  } else {
-    if (threadIdx.x == 0) {
-      unsigned spins = 0;
-      while (ld_acquire(ready + t) != epoch) {
-        __nanosleep(200);
-        if (++spins > (1u << 27)) __trap();
-      }
-    }
-    __syncthreads();
-    x2_tile<P>(sm.n_rows, Uext, Zext, sw, alpha, w_ik1, X, ldx, bi, bj, false, 0, dsm);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1114,12 +1117,12 @@ __global__ void __launch_bounds__(256) probe_log_kernel(int64_t iters, int mode,
 
 // self-test hooks: fast ln vs libdevice, and a DMMA fragment-layout check
 __global__ void selftest_log_kernel(int64_t n, const double* x, double* out_fast, double* out_ref) {
-  __shared__ double tab[3 * LOGTAB];
-  for (int k = threadIdx.x; k < 3 * LOGTAB; k += blockDim.x) tab[k] = g_logtab[k];
+  __shared__ double2 tab[64];  // the ln of the C4 IK1 kernel (ik1_sym_kernel)
+  for (int k = threadIdx.x; k < 128; k += blockDim.x) reinterpret_cast<double*>(tab)[k] = kTang64[k];
   __syncthreads();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  out_fast[i] = half_ln(x[i], tab);
+  out_fast[i] = half_ln64t(x[i], tab);
   out_ref[i] = 0.5 * log(x[i]);
 }
 
@@ -1131,17 +1134,17 @@ __global__ void selftest_dmma_kernel(const double* A, const double* B, double* C
   C[r * 8 + 2 * c + 1] = c1;
 }
 
-static int g_ik1_tab = 0;  // 0: 16-entry smem ln table, 1: 1024-entry table via L1
+static int g_ik1_tab = 0;  // ik1_sym_kernel column loop: 0 unrolled 4, 1 unrolled 2
 
 template <int P, int MODE>
 static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, cudaStream_t st,
                       int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
-  using C = Ik1Cfg<P, MODE>;
+  using C = Ik4Cfg<P, MODE>;
   if (sm->wg != C::WG) {
     set_error("wq_ik1_sym: rule band width %lld != 2p+1", (long long)sm->wg);
     return WQ_EINVAL;
   }
-  const size_t smem = (size_t)Ik1Smem<P, MODE>::TOTAL * 8;
+  const size_t smem = (size_t)Ik4Cfg<P, MODE>::TOTAL * 8;
   auto kern = g_ik1_tab == 1 ? ik1_sym_kernel<P, MODE, 1> : ik1_sym_kernel<P, MODE, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(sm->n_rows, FT);
@@ -1150,7 +1153,7 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
   if (pair0 < 0) pair0 = 0;
   const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
   if (blocks <= 0) return WQ_OK;
-  kern<<<(unsigned)blocks, IK1_THREADS, smem, st>>>(*sm, nb, tile_row0, pair0, X, ldx, flag);
+  kern<<<(unsigned)blocks, IK4_THREADS, smem, st>>>(*sm, nb, tile_row0, pair0, X, ldx, flag);
   return check_launch("wq_ik1_sym");
 }
 
@@ -1209,31 +1212,6 @@ static int launch_x2_runs(int64_t N, const double* Uext, const double* Zext, con
   x2_runs_kernel<P><<<(unsigned)n_runs, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
                                                                 ldx, nb, runs);
   return check_launch("wq_x2_runs");
-}
-
-template <int P, int MODE>
-static int launch_fused(const wq_smooth_t* sm, const double* Uext, const double* Zext,
-                        const double* s_w, double alpha, double w_ik1, double* X, int64_t ldx,
-                        int* ready, int epoch, int64_t lead, int* flag, cudaStream_t st) {
-  using C = Ik1Cfg<P, MODE>;
-  if (sm->wg != C::WG) {
-    set_error("wq_assemble_fused: rule band width %lld != 2p+1", (long long)sm->wg);
-    return WQ_EINVAL;
-  }
-  const size_t smem = (size_t)std::max(Ik1Smem<P, MODE>::TOTAL, X2Smem<P>::TOTAL) * 8;
-  if (smem > 227 * 1024) {
-    set_error("wq_assemble_fused: %zu B shared memory needed", smem);
-    return WQ_EUNSUPPORTED;
-  }
-  auto kern = g_ik1_tab == 1 ? fused_pairs_kernel<P, MODE, 1> : fused_pairs_kernel<P, MODE, 0>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int nb = ceil_div(sm->n_rows, FT);
-  const int64_t pairs = (int64_t)nb * (nb + 1) / 2;
-  if (lead < 1) lead = 1;
-  if (lead > pairs) lead = pairs;
-  kern<<<(unsigned)(2 * pairs), IK1_THREADS, smem, st>>>(*sm, Uext, Zext, s_w, alpha, w_ik1, X, ldx,
-                                                          nb, pairs, lead, ready, epoch, flag);
-  return check_launch("wq_assemble_fused");
 }
 
 template <int P>
@@ -1405,46 +1383,6 @@ int wq_x2_runs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
 #undef WQ_XR_CASE
 }
 
-int wq_assemble_fused(const wq_smooth_t* sm, int p, int nA, int nApad, int ws, int ktot, int zstride,
-                      const double* Uext, const double* Zext, const double* s_w, double alpha,
-                      double w_ik1, int* ready, int epoch, int64_t lead, double* X, int64_t ldx,
-                      int* flag, void* stream) {
-  if (!sm || !Uext || !Zext || !s_w || !ready || !X || !flag || !sm->closed || epoch == 0 ||
-      sm->near_k > 0) {
-    set_error("wq_assemble_fused: bad arguments");
-    return WQ_EINVAL;
-  }
-  if (sm->k1_mode == WQ_K1_TABLE && !sm->invp2) {
-    set_error("wq_assemble_fused: table mode without invp2");
-    return WQ_EINVAL;
-  }
-  int rc = ensure_logtab();
-  if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  const bool tab = sm->k1_mode == WQ_K1_TABLE;
-#define WQ_FU_CASE(PP)                                                                         \
-  case PP:                                                                                     \
-    if (nA != X2Cfg<PP>::NA || nApad != X2Cfg<PP>::NAPAD || ws != X2Cfg<PP>::WS ||              \
-        ktot != X2Cfg<PP>::KTOT || zstride != X2Cfg<PP>::ZSTRIDE) {                             \
-      set_error("wq_assemble_fused: layout mismatch for p=%d", PP);                            \
-      return WQ_EINVAL;                                                                        \
-    }                                                                                          \
-    return tab ? launch_fused<PP, WQ_K1_TABLE>(sm, Uext, Zext, s_w, alpha, w_ik1, X, ldx, ready,\
-                                               epoch, lead, flag, st)                          \
-               : launch_fused<PP, WQ_K1_CLOSED>(sm, Uext, Zext, s_w, alpha, w_ik1, X, ldx,      \
-                                                ready, epoch, lead, flag, st);
-  switch (p) {
-    WQ_FU_CASE(2)
-    WQ_FU_CASE(3)
-    WQ_FU_CASE(4)
-    WQ_FU_CASE(5)
-    default:
-      set_error("wq_assemble_fused: degree %d unsupported (2..5)", p);
-      return WQ_EUNSUPPORTED;
-  }
-#undef WQ_FU_CASE
-}
-
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream) {
   int rc = ensure_logtab();
   if (rc) return rc;
@@ -1472,7 +1410,7 @@ int wq_probe_phi(int iters, int blocks, int mode, const double* Uext, double* ou
 
 int wq_set_ik1_passes(int mode) {
   if (mode < 1 || mode > 2) {
-    set_error("wq_set_ik1_passes: 1 (16-entry smem ln table) or 2 (1024-entry, L1)");
+    set_error("wq_set_ik1_passes: 1 (column loop unrolled 4) or 2 (unrolled 2)");
     return WQ_EINVAL;
   }
   g_ik1_tab = mode - 1;
