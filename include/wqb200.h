@@ -247,18 +247,6 @@ int wq_x2_pairs_range(int64_t N, int p, int nA, int nApad, int ws, int ktot, int
                       double w_ik1, int64_t pair0, int64_t pair1, double* X, int64_t ldx,
                       void* stream);
 
-/*
- * Diagonal-run variant of wq_x2_pairs (same arithmetic, bit-identical): runs
- * (n_runs x 3 int32: delta, first tile row, length) list tile pairs
- * (I, I + delta), I = first .. first + length - 1, covering the upper triangle;
- * a CTA keeps both skewed Z' windows of its diagonal resident and prefetches
- * the next pair's IK1 tile / S bands while computing the current one.
- */
-int wq_x2_runs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
-               const double* Uext, const double* Zext, const double* s_w, double alpha,
-               double w_ik1, const int* runs, int64_t n_runs, double* X, int64_t ldx,
-               void* stream);
-
 /* Self-test hooks (unit tests): the IK1 kernel's table 0.5*ln vs libdevice; one DMMA 8x8x4. */
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream);
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream);

@@ -78,8 +78,6 @@ _SIGS = {
     "wq_ik1_pairs": [ctypes.POINTER(WqSmooth), c_i64, c_i64, c_vp, c_i64, c_vp, c_vp],
     "wq_x2_pairs_range": [c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_dbl,
                           c_dbl, c_i64, c_i64, c_vp, c_i64, c_vp],
-    "wq_x2_runs": [c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl,
-                   c_vp, c_i64, c_vp, c_i64, c_vp],
     "wq_ik1_rows": [ctypes.POINTER(WqSmooth), c_i64, c_i64, c_vp, c_i64, c_vp, c_vp],
     "wq_x2_rows": [c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                    c_i64, c_i64, c_vp, c_i64, c_vp],

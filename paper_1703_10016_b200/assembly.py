@@ -843,24 +843,7 @@ def _zext_table(disc):
     return Zext
 
 
-def diag_runs(N: int, run_len: int = 16) -> np.ndarray:
-    """(n_runs, 3) int32 table (delta, first tile row, length) of runs of
-    upper-triangle 64-tile pairs (I, I + delta) along the diagonals."""
-    nb = -(-N // _lib.WQ_FTILE)
-    out = []
-    for delta in range(nb):
-        for i0 in range(0, nb - delta, run_len):
-            out.append((delta, i0, min(run_len, nb - delta - i0)))
-    return np.asarray(out, dtype=np.int32)
-
-
-def _diag_runs(disc):
-    torch = _torch()
-    return _dev(disc, "runs", lambda: _to_dev(torch, diag_runs(disc.space.dim)))
-
-
 _AUX_STREAMS = {}
-_USE_RUNS = False   # x2_runs (1 CTA/SM, resident windows) measured slower than x2_pairs (2 CTA/SM)
 
 
 def _aux_stream(torch):
@@ -905,12 +888,7 @@ def _assemble_v2(disc: Discretization, X, alpha: float, w_ik1: float = 2.0, zext
     if len(ranges) == 1:
         _lib.call("wq_ik1_sym", ctypes_ref(sm["struct"]), _lib.ptr(X), X.stride(0), sm["span64"],
                   _lib.ptr(sm["flag"]), st)
-        if _USE_RUNS and disc.space.degree <= 4:
-            runs = _diag_runs(disc)
-            _lib.call("wq_x2_runs", *x2args, _lib.ptr(runs), runs.shape[0], _lib.ptr(X),
-                      X.stride(0), st)
-        else:
-            _lib.call("wq_x2_pairs", *x2args, _lib.ptr(X), X.stride(0), st)
+        _lib.call("wq_x2_pairs", *x2args, _lib.ptr(X), X.stride(0), st)
         return X
     aux = _aux_stream(torch)
     aux.wait_stream(main)

@@ -154,6 +154,40 @@ __device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gsrc
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// 1-D bulk copies (TMA engine) completing on a shared-memory mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WQ_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WQ_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// order this thread's generic-proxy shared-memory accesses before later async-proxy writes
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // ik1_sym_kernel: closed uniform nodes, rule i on nodes 2(i-p)+1 .. 2(i-p)+2p+1
 // ---------------------------------------------------------------------------
@@ -529,15 +563,13 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64
   }
 }
 
-// out[a][b] = sum_m Phs[a][m] S_b[m - b + d]; warp owns row block `warp`
+// acc[b][.] += sum_m Phs[a][m] S_b[m - b + d]; warp owns row block `warp`
 template <int P>
-__device__ __forceinline__ void s_contract(const double* Phs, const double* Bfr, double (&acc)[8][2],
-                                           int warp) {
+__device__ __forceinline__ void s_contract_acc(const double* Phs, const double* Bfr,
+                                               double (&acc)[8][2], int warp) {
   using C = X2Cfg<P>;
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
-#pragma unroll
-  for (int jb = 0; jb < 8; ++jb) acc[jb][0] = acc[jb][1] = 0.0;
 #pragma unroll
   for (int jb = 0; jb < 8; ++jb) {
 #pragma unroll
@@ -549,16 +581,23 @@ __device__ __forceinline__ void s_contract(const double* Phs, const double* Bfr,
   }
 }
 
+constexpr int T2STRIDE = 68;  // orientation hand-off tile (== 4 mod 16: conflict-free fragment reads)
+
 template <int P>
 struct X2Smem {
   using C = X2Cfg<P>;
-  static constexpr int TOTAL = C::ZROWS * C::ZSTRIDE + FT * PSTRIDE + FT * TSTRIDE + FT * 16 +
-                               8 * (C::KS / 4) * 32;
+  static constexpr int SROW = C::WS <= 8 ? 8 : 16;
+  static constexpr int TOTAL = C::ZROWS * C::ZSTRIDE + FT * PSTRIDE + FT * T2STRIDE + FT * SROW +
+                               8 * (C::KS / 4) * 32 + 2;  // + 2 mbarriers (window, IK1 tile)
 };
 
 // One tile pair (bi, bj) of the log part + fused symmetric epilogue (or, rect,
-// the unsymmetrised row block).  Threads >= X2_THREADS of a larger CTA only
-// take part in the barriers.
+// the unsymmetrised row block).  The epilogue runs inside the DMMA
+// accumulators: orientation 0 starts from alpha w IK1(I,J) and contracts with
+// alpha S_J, giving T = alpha (w IK1 + X2(I,J)) (kept in shared memory);
+// orientation 1 starts from T^T and contracts with alpha S_I, giving
+// A(J,I) = alpha (w IK1 + X2(I,J) + X2(J,I)^T)^T directly, so no FP64
+// instructions compete with the neighbour CTA's DMMAs in the epilogue.
 template <int P>
 __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Uext,
                                         const double* __restrict__ Zext,
@@ -566,37 +605,58 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
                                         double* X, int64_t ldx, int bi, int bj, bool rect,
                                         int64_t row_off, double* smem) {
   using C = X2Cfg<P>;
+  using L = X2Smem<P>;
+  constexpr int SROW = L::SROW;
   double* Zsm = smem;                              // ZROWS * ZSTRIDE
-  double* Phs = Zsm + C::ZROWS * C::ZSTRIDE;       // FT * PSTRIDE (also output staging)
-  double* Tst = Phs + FT * PSTRIDE;                // FT * TSTRIDE: w IK1 + X2(I,J)
-  double* Ssm = Tst + FT * TSTRIDE;                // FT * 16 (S band rows)
-  double* Bfr = Ssm + FT * 16;                     // 8 * KS/4 * 32 (fragment order)
+  double* Phs = Zsm + C::ZROWS * C::ZSTRIDE;       // FT * PSTRIDE (also output staging, stride 65)
+  double* Tst = Phs + FT * PSTRIDE;                // FT * T2STRIDE: IK1(I,J), then T
+  double* Ssm = Tst + FT * T2STRIDE;               // FT * SROW (S band rows)
+  double* Bfr = Ssm + FT * SROW;                   // 8 * KS/4 * 32 (fragment order, alpha S)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bfr + 8 * (C::KS / 4) * 32);
   const int64_t n = N;
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
   const int nj = (int)min((int64_t)FT, N - J0);
   const int tid = threadIdx.x;
-  const bool act = tid < X2_THREADS;
   const int lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 2, c = lane & 3;
+  const bool with_ik1 = w_ik1 != 0.0;
 
   x2_mark(0);
-  // IK1(I,J) tile -> Tst (asynchronous)
-  if (act) {
-    if (w_ik1 != 0.0) {
+  // bulk (TMA) staging needs whole 16-byte-aligned rows and a table of >= ZROWS rows
+  const bool zbulk = n >= C::ZROWS;
+  const double* src = X + (I0 - row_off) * ldx + J0;
+  const bool tbulk = with_ik1 && zbulk && ni == FT && nj == FT && (ldx & 1) == 0 &&
+                     (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  if (zbulk) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+    }
+    fence_proxy_async();
+    __syncthreads();
+  }
+  // IK1(I,J) tile -> Tst: 64 row copies on the TMA engine, or cp.async
+  if (tbulk) {
+    if (tid < 32) {
+      // own barrier: the tile is first needed after phi0, so its HBM latency hides behind it
+      if (tid == 0) mbar_arrive_expect_tx(bar + 1, FT * FT * 8);
+      __syncwarp();
+      for (int a = tid; a < FT; a += 32) bulk_g2s(Tst + a * T2STRIDE, src + a * ldx, FT * 8, bar + 1);
+    }
+  } else if (with_ik1) {
+    {
       for (int k = tid; k < FT * FT; k += X2_THREADS) {
         const int a = k >> 6, b = k & 63;
-        if (a < ni && b < nj) cp_async8(Tst + a * TSTRIDE + b, X + (I0 - row_off + a) * ldx + J0 + b);
-        else Tst[a * TSTRIDE + b] = 0.0;
+        if (a < ni && b < nj) cp_async8(Tst + a * T2STRIDE + b, src + a * ldx + b);
+        else Tst[a * T2STRIDE + b] = 0.0;
       }
-    } else {
-      for (int k = tid; k < FT * TSTRIDE; k += X2_THREADS) Tst[k] = 0.0;
     }
-    // Phs pad columns must be finite (they multiply zero B entries)
-    for (int k = tid; k < FT * (PSTRIDE - C::SPAN); k += X2_THREADS) {
-      const int row = k / (PSTRIDE - C::SPAN), col = C::SPAN + k % (PSTRIDE - C::SPAN);
-      Phs[row * PSTRIDE + col] = 0.0;
-    }
+  }
+  // Phs pad columns must be finite (they multiply zero B entries)
+  for (int k = tid; k < FT * (PSTRIDE - C::SPAN); k += X2_THREADS) {
+    const int row = k / (PSTRIDE - C::SPAN), col = C::SPAN + k % (PSTRIDE - C::SPAN);
+    Phs[row * PSTRIDE + col] = 0.0;
   }
 
   double acc[8][2];
@@ -609,77 +669,157 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
     const int nc = orient == 0 ? nj : ni;
     const int64_t M0 = C0 - C::D;
     const int64_t gmin = M0 - (R0 + 63) + P - C::AMAX;
-    if (orient == 1) __syncthreads();  // Zsm / Phs / Ssm reuse
+    if (orient == 1) {
+      fence_proxy_async();  // generic reads of Zsm before the async-proxy overwrite
+      __syncthreads();      // Zsm / Phs / Bfr reuse, T complete
+    }
     int64_t g0 = gmin % n;
     if (g0 < 0) g0 += n;
-    for (int k = tid; act && k < C::ZROWS * (C::ZSTRIDE / 2); k += X2_THREADS) {
-      const int row = k / (C::ZSTRIDE / 2), cc = 2 * (k - row * (C::ZSTRIDE / 2));
-      int64_t g = g0 + row;
-      if (g >= n) g %= n;
-      cp_async16(Zsm + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
+    constexpr int NBF = 8 * (C::KS / 4) * 32;
+    constexpr int BPT = (NBF + X2_THREADS - 1) / X2_THREADS;
+    if (zbulk) {
+      // skewed Z' window: ZROWS contiguous table rows (two pieces at the seam)
+      if (tid == 0) {
+        constexpr unsigned RB = C::ZSTRIDE * 8;
+        const int64_t first = min((int64_t)C::ZROWS, n - g0);
+        mbar_arrive_expect_tx(bar, C::ZROWS * RB);
+        bulk_g2s(Zsm, Zext + g0 * C::ZSTRIDE, (unsigned)first * RB, bar);
+        if (first < C::ZROWS)
+          bulk_g2s(Zsm + first * C::ZSTRIDE, Zext, (unsigned)(C::ZROWS - first) * RB, bar);
+      }
+      // alpha S band in B-fragment order, Bfr[jb][s][lane] = alpha S_{8jb+r}[4s+c-r],
+      // straight from global memory while the copies fly
+      double bv[BPT];
+#pragma unroll
+      for (int u = 0; u < BPT; ++u) {
+        const int k = tid + u * X2_THREADS;
+        const int ln = k & 31, s = (k >> 5) % (C::KS / 4), jb = (k >> 5) / (C::KS / 4);
+        const int rr = ln >> 2, cc = ln & 3;
+        const int t = 4 * s + cc - rr, row = 8 * jb + rr;
+        bv[u] = (k < NBF && t >= 0 && t <= 2 * C::D && row < nc) ? alpha * __ldg(sw + (C0 + row) * C::WS + t)
+                                                                  : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < BPT; ++u)
+        if (tid + u * X2_THREADS < NBF) Bfr[tid + u * X2_THREADS] = bv[u];
+      if (orient == 0 && with_ik1 && !tbulk) cp_async_wait_all();
+      mbar_wait(bar, (unsigned)orient);
+      __syncthreads();
+    } else {
+      constexpr int CH = C::ZSTRIDE / 2;  // 16-byte chunks per table row
+      for (int k = tid; k < C::ZROWS * CH; k += X2_THREADS) {
+        const int row = k / CH, cc = 2 * (k - row * CH);
+        int64_t g = g0 + row;
+        while (g >= n) g -= n;
+        cp_async16(Zsm + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
+      }
+      for (int k = tid; k < FT * SROW; k += X2_THREADS) {
+        const int row = k / SROW, t = k - row * SROW;
+        const bool ok = row < nc && t < C::WS;
+        cp_async8_zfill(Ssm + k, sw + (ok ? (C0 + row) * C::WS + t : 0), ok);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      for (int k = tid; k < NBF; k += X2_THREADS) {
+        const int ln = k & 31, s = (k >> 5) % (C::KS / 4), jb = (k >> 5) / (C::KS / 4);
+        const int rr = ln >> 2, cc = ln & 3;
+        const int t = 4 * s + cc - rr;
+        Bfr[k] = (t >= 0 && t <= 2 * C::D) ? alpha * Ssm[(8 * jb + rr) * SROW + t] : 0.0;
+      }
+      __syncthreads();
     }
-    for (int k = tid; act && k < FT * 16; k += X2_THREADS) {
-      const int row = k >> 4, t = k & 15;
-      const bool ok = row < nc && t < C::WS;
-      cp_async8_zfill(Ssm + k, sw + (ok ? (C0 + row) * C::WS + t : 0), ok);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    // S band in B-fragment order: Bfr[jb][s][lane] = S_{8jb+r}[4s+c-r] (0 outside the band)
-    for (int k = tid; act && k < 8 * (C::KS / 4) * 32; k += X2_THREADS) {
-      const int ln = k & 31, s = (k >> 5) % (C::KS / 4), jb = (k >> 5) / (C::KS / 4);
-      const int rr = ln >> 2, cc = ln & 3;
-      const int t = 4 * s + cc - rr;
-      Bfr[k] = (t >= 0 && t <= 2 * C::D) ? Ssm[(8 * jb + rr) * 16 + t] : 0.0;
-    }
-    __syncthreads();
     x2_mark(1 + 3 * orient);
-    if (act) phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
+    phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
+    // accumulator start: orientation 0 alpha w IK1(I,J) (lane: i = 8warp + r,
+    // j = 8jb + 2c + e); orientation 1 T^T (lane: j = 8warp + r, i = 8ib + 2c + e)
+    if (orient == 0) {
+      if (tbulk) mbar_wait(bar + 1, 0);
+      const double aw = alpha * w_ik1;
+#pragma unroll
+      for (int jb = 0; jb < 8; ++jb) {
+        if (with_ik1) {
+          const double2 t =
+              *reinterpret_cast<const double2*>(Tst + (8 * warp + r) * T2STRIDE + 8 * jb + 2 * c);
+          acc[jb][0] = aw * t.x;
+          acc[jb][1] = aw * t.y;
+        } else {
+          acc[jb][0] = acc[jb][1] = 0.0;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int ib = 0; ib < 8; ++ib)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[ib][e] = Tst[(8 * ib + 2 * c + e) * T2STRIDE + 8 * warp + r];
+    }
     __syncthreads();
     x2_mark(2 + 3 * orient);
-    if (act) s_contract<P>(Phs, Bfr, acc, warp);
+    s_contract_acc<P>(Phs, Bfr, acc, warp);
     x2_mark(3 + 3 * orient);
-    if (orient == 0 && act) {
-      // Tst[i][j] = w IK1 + X2(I,J); lane holds (i = 8warp + r, j = 8jb + 2c + e)
+    if (orient == 0) {
+      // T[i][j] (each lane rewrites the entries it read)
 #pragma unroll
       for (int jb = 0; jb < 8; ++jb)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double* t = Tst + (8 * warp + r) * TSTRIDE + 8 * jb + 2 * c + e;
-          *t = fma(w_ik1, *t, acc[jb][e]);
-        }
+        *reinterpret_cast<double2*>(Tst + (8 * warp + r) * T2STRIDE + 8 * jb + 2 * c) =
+            make_double2(acc[jb][0], acc[jb][1]);
     }
   }
   __syncthreads();
   if (rect) {
-    // unsymmetrised row block: X(I,J) = alpha (w IK1 + X2(I,J))
-    for (int k = tid; act && k < FT * FT; k += X2_THREADS) {
+    // unsymmetrised row block: X(I,J) = alpha (w IK1 + X2(I,J)) = T
+    for (int k = tid; k < FT * FT; k += X2_THREADS) {
       const int a = k >> 6, b = k & 63;
-      if (a < ni && b < nj) X[(I0 - row_off + a) * ldx + J0 + b] = alpha * Tst[a * TSTRIDE + b];
+      if (a < ni && b < nj) X[(I0 - row_off + a) * ldx + J0 + b] = Tst[a * T2STRIDE + b];
     }
     return;
   }
-  // acc holds X2(J,I): lane (j = 8warp + r, i = 8ib + 2c + e).  A(J,I)[j][i] =
-  // alpha (Tst[i][j] + X2(J,I)[j][i]) -> staged in Phs as [j][i]
-  if (act) {
+  // acc holds A(J,I) (lane: j = 8warp + r, i = 8ib + 2c + e)
+  const bool sbulk = zbulk && bi != bj && ni == FT && nj == FT && (ldx & 1) == 0 &&
+                     (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  if (sbulk) {
+    // both output tiles staged row-contiguous (16-byte aligned rows, stride 66) in the
+    // Phs | Tst region, then 128 row copies shared -> global on the TMA engine
+    constexpr int OS = 66;
+    double* Oji = Phs;            // A(J,I)[j][i]
+    double* Oij = Phs + FT * OS;  // A(I,J)[i][j] = A(J,I)[j][i]
+    static_assert(2 * FT * OS <= FT * PSTRIDE + FT * T2STRIDE, "output staging overflows");
 #pragma unroll
-    for (int ib = 0; ib < 8; ++ib)
+    for (int ib = 0; ib < 8; ++ib) {
+      *reinterpret_cast<double2*>(Oji + (8 * warp + r) * OS + 8 * ib + 2 * c) =
+          make_double2(acc[ib][0], acc[ib][1]);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int jl = 8 * warp + r, il = 8 * ib + 2 * c + e;
-        Phs[jl * TSTRIDE + il] = alpha * (Tst[il * TSTRIDE + jl] + acc[ib][e]);
-      }
+      for (int e = 0; e < 2; ++e) Oij[(8 * ib + 2 * c + e) * OS + 8 * warp + r] = acc[ib][e];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid < 2 * FT) {
+      const int a = tid & (FT - 1);
+      const bool ji = tid < FT;
+      double* dst = ji ? X + (J0 + a) * ldx + I0 : X + (I0 + a) * ldx + J0;
+      const double* srcs = (ji ? Oji : Oij) + a * OS;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+                   "r"(smem_u32(srcs)), "r"(FT * 8)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+    x2_mark(7);
+    return;
   }
+#pragma unroll
+  for (int ib = 0; ib < 8; ++ib)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) Phs[(8 * warp + r) * TSTRIDE + 8 * ib + 2 * c + e] = acc[ib][e];
   __syncthreads();
   // A(J,I) rows (coalesced), A(I,J) = transpose; diagonal tiles mirror their
   // lower-staged triangle so A is exactly symmetric
   if (bi != bj) {
-    for (int k = tid; act && k < FT * FT; k += X2_THREADS) {
+    for (int k = tid; k < FT * FT; k += X2_THREADS) {
       const int a = k >> 6, b = k & 63;  // row J0 + a, col I0 + b
       if (a < nj && b < ni) X[(J0 + a) * ldx + I0 + b] = Phs[a * TSTRIDE + b];
     }
   }
-  for (int k = tid; act && k < FT * FT; k += X2_THREADS) {
+  for (int k = tid; k < FT * FT; k += X2_THREADS) {
     const int a = k >> 6, b = k & 63;  // row I0 + a, col J0 + b
     if (a < ni && b < nj) {
       const double v = (bi == bj && b > a) ? Phs[a * TSTRIDE + b] : Phs[b * TSTRIDE + a];
@@ -703,316 +843,6 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
   const bool rect = tile_row0 >= 0;
   x2_tile<P>(N, Uext, Zext, sw, alpha, w_ik1, X, ldx, bi, bj, rect,
              rect ? (int64_t)tile_row0 * FT : 0, smem);
-}
-
-// ---------------------------------------------------------------------------
-// x2_runs_kernel: one CTA walks a run of tile pairs (I, I + delta) along one
-// diagonal.  Both skewed Z' windows depend only on delta, so they are staged
-// once per run and stay resident; the next pair's IK1 tile and S bands are
-// prefetched with cp.async while the current pair runs on the DMMA pipe.
-// Per pair: Phi (both orientations) + banded S contraction + fused epilogue,
-// identical arithmetic to x2_pairs_kernel (bit-identical results).
-// ---------------------------------------------------------------------------
-
-constexpr int RUN_SROW = 8;  // padded S band row (WS <= 8 doubles for p <= 3; 16 otherwise)
-
-template <int P>
-struct RunCfg {
-  static constexpr int SROW = (2 * P + 1) <= 8 ? 8 : 16;
-};
-
-template <int P>
-__global__ void __launch_bounds__(X2_THREADS, 1)
-x2_runs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
-               const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
-               int nb, const int* __restrict__ runs) {
-  using C = X2Cfg<P>;
-  constexpr int SROW = RunCfg<P>::SROW;
-  constexpr int ZW = C::ZROWS * C::ZSTRIDE;
-  constexpr int NKS = C::KS / 4;
-  extern __shared__ double smem[];
-  double* Zsm0 = smem;                          // orientation 0 window
-  double* Zsm1 = Zsm0 + ZW;                     // orientation 1 window
-  double* Phs = Zsm1 + ZW;                      // FT * PSTRIDE (also output staging)
-  double* Tbuf = Phs + FT * PSTRIDE;            // 2 x FT * TSTRIDE (w IK1 + X2(I,J))
-  double* Sbuf = Tbuf + 2 * FT * TSTRIDE;       // 2 bufs x 2 (I, J) x FT * SROW
-  double* Bfr = Sbuf + 4 * FT * SROW;           // 8 * NKS * 32
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int r = lane >> 2, c = lane & 3;
-  const int delta = runs[3 * blockIdx.x], i_start = runs[3 * blockIdx.x + 1];
-  const int len = runs[3 * blockIdx.x + 2];
-  const int64_t n = N;
-
-  x2_mark(0);
-  // resident skewed windows: orientation 0 (rows I, m over J) and 1 (rows J, m over I)
-  for (int o = 0; o < 2; ++o) {
-    const int64_t dd = (o == 0 ? 1 : -1) * (int64_t)delta * FT;
-    const int64_t gmin = dd - C::D - 63 + P - C::AMAX;
-    int64_t g0 = gmin % n;
-    if (g0 < 0) g0 += n;
-    double* Z = o == 0 ? Zsm0 : Zsm1;
-    for (int k = tid; k < C::ZROWS * (C::ZSTRIDE / 2); k += X2_THREADS) {
-      const int row = k / (C::ZSTRIDE / 2), cc = 2 * (k - row * (C::ZSTRIDE / 2));
-      int64_t g = g0 + row;
-      if (g >= n) g %= n;
-      cp_async16(Z + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
-    }
-  }
-  // Phs pad columns must be finite (they multiply zero B entries)
-  for (int k = tid; k < FT * (PSTRIDE - C::SPAN); k += X2_THREADS) {
-    const int row = k / (PSTRIDE - C::SPAN), col = C::SPAN + k % (PSTRIDE - C::SPAN);
-    Phs[row * PSTRIDE + col] = 0.0;
-  }
-
-  auto prefetch = [&](int t, int buf) {
-    const int bi = i_start + t, bj = bi + delta;
-    const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
-    const int ni = (int)min((int64_t)FT, N - I0), nj = (int)min((int64_t)FT, N - J0);
-    double* T = Tbuf + buf * FT * TSTRIDE;
-    if (w_ik1 != 0.0) {
-      for (int k = tid; k < FT * FT; k += X2_THREADS) {
-        const int a = k >> 6, b = k & 63;
-        const bool ok = a < ni && b < nj;
-        cp_async8_zfill(T + a * TSTRIDE + b, X + (ok ? (I0 + a) * ldx + J0 + b : 0), ok);
-      }
-    } else {
-      for (int k = tid; k < FT * FT; k += X2_THREADS) T[(k >> 6) * TSTRIDE + (k & 63)] = 0.0;
-    }
-    double* S = Sbuf + buf * 2 * FT * SROW;
-    for (int k = tid; k < 2 * FT * SROW; k += X2_THREADS) {
-      const int side = k / (FT * SROW), rem = k - side * FT * SROW;
-      const int row = rem / SROW, tt = rem - row * SROW;
-      const int64_t base = side == 0 ? I0 : J0;
-      const int nr = side == 0 ? ni : nj;
-      const bool ok = row < nr && tt < C::WS;
-      cp_async8_zfill(S + k, sw + (ok ? (base + row) * C::WS + tt : 0), ok);
-    }
-    cp_async_commit();
-  };
-
-  prefetch(0, 0);
-  for (int t = 0; t < len; ++t) {
-    const int buf = t & 1;
-    const int bi = i_start + t, bj = bi + delta;
-    const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
-    const int ni = (int)min((int64_t)FT, N - I0), nj = (int)min((int64_t)FT, N - J0);
-    double* Tst = Tbuf + buf * FT * TSTRIDE;
-    const double* S = Sbuf + buf * 2 * FT * SROW;
-    cp_async_wait_group0();
-    __syncthreads();
-    if (t + 1 < len) prefetch(t + 1, buf ^ 1);
-    x2_mark(1);
-    double acc[8][2];
-    for (int orient = 0; orient < 2; ++orient) {
-      const int64_t R0 = orient == 0 ? I0 : J0;
-      const int64_t C0 = orient == 0 ? J0 : I0;
-      const int64_t M0 = C0 - C::D;
-      const int64_t gmin = M0 - (R0 + 63) + P - C::AMAX;
-      // S band of the contraction side in fragment order (side 1 = J for orient 0)
-      const double* Sside = S + (orient == 0 ? 1 : 0) * FT * SROW;
-      for (int k = tid; k < 8 * NKS * 32; k += X2_THREADS) {
-        const int ln = k & 31, s = (k >> 5) % NKS, jb = (k >> 5) / NKS;
-        const int rr = ln >> 2, cc = ln & 3;
-        const int tt = 4 * s + cc - rr;
-        Bfr[k] = (tt >= 0 && tt <= 2 * C::D) ? Sside[(8 * jb + rr) * SROW + tt] : 0.0;
-      }
-      phi_block<P>(Uext, N, orient == 0 ? Zsm0 : Zsm1, Phs, M0, R0, gmin, warp);
-      __syncthreads();
-      s_contract<P>(Phs, Bfr, acc, warp);
-      if (orient == 0) {
-#pragma unroll
-        for (int jb = 0; jb < 8; ++jb)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            double* tp = Tst + (8 * warp + r) * TSTRIDE + 8 * jb + 2 * c + e;
-            *tp = fma(w_ik1, *tp, acc[jb][e]);
-          }
-        __syncthreads();  // Phs / Bfr reuse by orientation 1
-      }
-    }
-    __syncthreads();
-    x2_mark(2);
-#pragma unroll
-    for (int ib = 0; ib < 8; ++ib)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int jl = 8 * warp + r, il = 8 * ib + 2 * c + e;
-        Phs[jl * TSTRIDE + il] = alpha * (Tst[il * TSTRIDE + jl] + acc[ib][e]);
-      }
-    __syncthreads();
-    if (bi != bj) {
-      for (int k = tid; k < FT * FT; k += X2_THREADS) {
-        const int a = k >> 6, b = k & 63;
-        if (a < nj && b < ni) X[(J0 + a) * ldx + I0 + b] = Phs[a * TSTRIDE + b];
-      }
-    }
-    for (int k = tid; k < FT * FT; k += X2_THREADS) {
-      const int a = k >> 6, b = k & 63;
-      if (a < ni && b < nj) {
-        const double v = (bi == bj && b > a) ? Phs[a * TSTRIDE + b] : Phs[b * TSTRIDE + a];
-        X[(I0 + a) * ldx + J0 + b] = v;
-      }
-    }
-    __syncthreads();  // Phs reuse by the next pair
-    x2_mark(3);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// x2_runs16_kernel: diagonal runs with 16 warps -- warps 0-7 compute orientation
-// 0 (X2(I,J)) while warps 8-15 compute orientation 1 (X2(J,I)) of the same tile
-// pair, each with its own Phi buffer, so the DMMA pipe sees 16 warps; both
-// skewed windows stay resident for the whole run; the next pair's IK1 tile and
-// S bands are prefetched with cp.async.  Bit-identical to x2_pairs_kernel.
-// p <= 3 (223 KB shared memory, 1 CTA/SM).
-// ---------------------------------------------------------------------------
-
-constexpr int X2R16_THREADS = 512;
-
-template <int P>
-__global__ void __launch_bounds__(X2R16_THREADS, 1)
-x2_runs16_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
-                 const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
-                 int nb, const int* __restrict__ runs) {
-  using C = X2Cfg<P>;
-  constexpr int SROW = 8;
-  static_assert(C::WS <= SROW, "x2_runs16 needs 2p+1 <= 8");
-  constexpr int ZW = C::ZROWS * C::ZSTRIDE;
-  constexpr int NKS = C::KS / 4;
-  constexpr int BFR = 8 * NKS * 32;
-  extern __shared__ double smem[];
-  double* Zsm = smem;                            // 2 x ZW: orientation windows
-  double* Phs = Zsm + 2 * ZW;                    // 2 x FT * PSTRIDE
-  double* Tbuf = Phs + 2 * FT * PSTRIDE;         // 2 x FT * TSTRIDE (IK1 tile -> w IK1 + X2(I,J))
-  double* Sbuf = Tbuf + 2 * FT * TSTRIDE;        // 2 bufs x 2 sides (I, J) x FT * SROW
-  double* Bfr = Sbuf + 4 * FT * SROW;            // 2 x BFR
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, gw = tid >> 5;
-  const int grp = gw >> 3, warp = gw & 7;        // orientation group, warp within group
-  const int gtid = tid & 255;
-  const int r = lane >> 2, c = lane & 3;
-  const int delta = runs[3 * blockIdx.x], i_start = runs[3 * blockIdx.x + 1];
-  const int len = runs[3 * blockIdx.x + 2];
-  const int64_t n = N;
-
-  x2_mark(0);
-  {
-    // resident windows (group g stages window g)
-    const int64_t dd = (grp == 0 ? 1 : -1) * (int64_t)delta * FT;
-    const int64_t gmin = dd - C::D - 63 + P - C::AMAX;
-    int64_t g0 = gmin % n;
-    if (g0 < 0) g0 += n;
-    double* Z = Zsm + grp * ZW;
-    for (int k = gtid; k < C::ZROWS * (C::ZSTRIDE / 2); k += 256) {
-      const int row = k / (C::ZSTRIDE / 2), cc = 2 * (k - row * (C::ZSTRIDE / 2));
-      int64_t g = g0 + row;
-      if (g >= n) g %= n;
-      cp_async16(Z + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
-    }
-    double* Pg = Phs + grp * FT * PSTRIDE;
-    for (int k = gtid; k < FT * (PSTRIDE - C::SPAN); k += 256) {
-      const int row = k / (PSTRIDE - C::SPAN), col = C::SPAN + k % (PSTRIDE - C::SPAN);
-      Pg[row * PSTRIDE + col] = 0.0;
-    }
-  }
-
-  auto prefetch = [&](int t, int buf) {
-    const int pbi = i_start + t, pbj = pbi + delta;
-    const int64_t pI0 = (int64_t)pbi * FT, pJ0 = (int64_t)pbj * FT;
-    const int pni = (int)min((int64_t)FT, N - pI0), pnj = (int)min((int64_t)FT, N - pJ0);
-    double* T = Tbuf + buf * FT * TSTRIDE;
-    if (w_ik1 != 0.0) {
-      for (int k = tid; k < FT * FT; k += X2R16_THREADS) {
-        const int a = k >> 6, b = k & 63;
-        const bool ok = a < pni && b < pnj;
-        cp_async8_zfill(T + a * TSTRIDE + b, X + (ok ? (pI0 + a) * ldx + pJ0 + b : 0), ok);
-      }
-    } else {
-      for (int k = tid; k < FT * FT; k += X2R16_THREADS) T[(k >> 6) * TSTRIDE + (k & 63)] = 0.0;
-    }
-    double* S = Sbuf + buf * 2 * FT * SROW;
-    for (int k = tid; k < 2 * FT * SROW; k += X2R16_THREADS) {
-      const int side = k / (FT * SROW), rem = k - side * FT * SROW;
-      const int row = rem / SROW, tt = rem - row * SROW;
-      const int64_t base = side == 0 ? pI0 : pJ0;
-      const int nr = side == 0 ? pni : pnj;
-      const bool ok = row < nr && tt < C::WS;
-      cp_async8_zfill(S + k, sw + (ok ? (base + row) * C::WS + tt : 0), ok);
-    }
-    cp_async_commit();
-  };
-
-  prefetch(0, 0);
-  for (int t = 0; t < len; ++t) {
-    const int buf = t & 1;
-    const int bi = i_start + t, bj = bi + delta;
-    const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
-    const int ni = (int)min((int64_t)FT, N - I0), nj = (int)min((int64_t)FT, N - J0);
-    double* Tst = Tbuf + buf * FT * TSTRIDE;
-    const double* S = Sbuf + buf * 2 * FT * SROW;
-    cp_async_wait_group0();
-    __syncthreads();
-    if (t + 1 < len) prefetch(t + 1, buf ^ 1);
-    // this group's orientation: 0 -> rows I, m over J, S_J ; 1 -> rows J, m over I, S_I
-    const int64_t R0 = grp == 0 ? I0 : J0;
-    const int64_t C0 = grp == 0 ? J0 : I0;
-    const int64_t M0 = C0 - C::D;
-    const int64_t gmin = M0 - (R0 + 63) + P - C::AMAX;
-    double* Pg = Phs + grp * FT * PSTRIDE;
-    double* Bg = Bfr + grp * BFR;
-    {
-      const double* Sside = S + (grp == 0 ? 1 : 0) * FT * SROW;
-      for (int k = gtid; k < BFR; k += 256) {
-        const int ln = k & 31, s = (k >> 5) % NKS, jb = (k >> 5) / NKS;
-        const int rr = ln >> 2, cc = ln & 3;
-        const int tt = 4 * s + cc - rr;
-        Bg[k] = (tt >= 0 && tt <= 2 * C::D) ? Sside[(8 * jb + rr) * SROW + tt] : 0.0;
-      }
-    }
-    x2_mark(1);
-    phi_block<P>(Uext, N, Zsm + grp * ZW, Pg, M0, R0, gmin, warp);
-    __syncthreads();
-    double acc[8][2];
-    s_contract<P>(Pg, Bg, acc, warp);
-    if (grp == 0) {
-      // Tst[i][j] = w IK1 + X2(I,J); lane holds (i = 8warp + r, j = 8jb + 2c + e)
-#pragma unroll
-      for (int jb = 0; jb < 8; ++jb)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double* tp = Tst + (8 * warp + r) * TSTRIDE + 8 * jb + 2 * c + e;
-          *tp = fma(w_ik1, *tp, acc[jb][e]);
-        }
-    }
-    __syncthreads();
-    x2_mark(2);
-    double* Ost = Phs + FT * PSTRIDE;  // group 1's Phi buffer, free now: output staging [j][i]
-    if (grp == 1) {
-#pragma unroll
-      for (int ib = 0; ib < 8; ++ib)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int jl = 8 * warp + r, il = 8 * ib + 2 * c + e;
-          Ost[jl * TSTRIDE + il] = alpha * (Tst[il * TSTRIDE + jl] + acc[ib][e]);
-        }
-    }
-    __syncthreads();
-    if (bi != bj) {
-      for (int k = tid; k < FT * FT; k += X2R16_THREADS) {
-        const int a = k >> 6, b = k & 63;
-        if (a < nj && b < ni) X[(J0 + a) * ldx + I0 + b] = Ost[a * TSTRIDE + b];
-      }
-    }
-    for (int k = tid; k < FT * FT; k += X2R16_THREADS) {
-      const int a = k >> 6, b = k & 63;
-      if (a < ni && b < nj) {
-        const double v = (bi == bj && b > a) ? Ost[a * TSTRIDE + b] : Ost[b * TSTRIDE + a];
-        X[(I0 + a) * ldx + J0 + b] = v;
-      }
-    }
-    x2_mark(3);
-  }
 }
 
 // DMMA loop probe (tools only): the phi_block inner loop on resident shared
@@ -1162,8 +992,7 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
                      double alpha, double w_ik1, double* X, int64_t ldx, cudaStream_t st,
                      int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
   using C = X2Cfg<P>;
-  const size_t smem = ((size_t)C::ZROWS * C::ZSTRIDE + (size_t)FT * PSTRIDE + (size_t)FT * TSTRIDE +
-                       (size_t)FT * 16 + (size_t)8 * (C::KS / 4) * 32) * 8;
+  const size_t smem = (size_t)X2Smem<P>::TOTAL * 8;
   cudaFuncSetAttribute(x2_pairs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(N, FT);
   const int64_t all = (int64_t)nb * (nb + 1) / 2;
@@ -1174,54 +1003,6 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
   x2_pairs_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
                                                                  ldx, nb, tile_row0, pair0);
   return check_launch("wq_x2_pairs");
-}
-
-template <int P>
-static int launch_x2_runs16(int64_t N, const double* Uext, const double* Zext, const double* s_w,
-                            double alpha, double w_ik1, double* X, int64_t ldx, const int* runs,
-                            int n_runs, cudaStream_t st) {
-  using C = X2Cfg<P>;
-  const size_t smem = ((size_t)2 * C::ZROWS * C::ZSTRIDE + (size_t)2 * FT * PSTRIDE +
-                       (size_t)2 * FT * TSTRIDE + (size_t)4 * FT * 8 +
-                       (size_t)2 * 8 * (C::KS / 4) * 32) * 8;
-  if (smem > 227 * 1024) {
-    set_error("wq_x2_runs: %zu B shared memory needed", smem);
-    return WQ_EUNSUPPORTED;
-  }
-  cudaFuncSetAttribute(x2_runs16_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int nb = ceil_div(N, FT);
-  x2_runs16_kernel<P><<<(unsigned)n_runs, X2R16_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha,
-                                                                      w_ik1, X, ldx, nb, runs);
-  return check_launch("wq_x2_runs");
-}
-
-template <int P>
-static int launch_x2_runs(int64_t N, const double* Uext, const double* Zext, const double* s_w,
-                          double alpha, double w_ik1, double* X, int64_t ldx, const int* runs,
-                          int n_runs, cudaStream_t st) {
-  using C = X2Cfg<P>;
-  const size_t smem = ((size_t)2 * C::ZROWS * C::ZSTRIDE + (size_t)FT * PSTRIDE +
-                       (size_t)2 * FT * TSTRIDE + (size_t)4 * FT * RunCfg<P>::SROW +
-                       (size_t)8 * (C::KS / 4) * 32) * 8;
-  if (smem > 227 * 1024) {
-    set_error("wq_x2_runs: %zu B shared memory needed", smem);
-    return WQ_EUNSUPPORTED;
-  }
-  cudaFuncSetAttribute(x2_runs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int nb = ceil_div(N, FT);
-  x2_runs_kernel<P><<<(unsigned)n_runs, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
-                                                                ldx, nb, runs);
-  return check_launch("wq_x2_runs");
-}
-
-template <int P>
-static int launch_x2_runs_any(int64_t N, const double* Uext, const double* Zext, const double* s_w,
-                              double alpha, double w_ik1, double* X, int64_t ldx, const int* runs,
-                              int n_runs, cudaStream_t st) {
-  if constexpr (P <= 3)
-    return launch_x2_runs16<P>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, runs, n_runs, st);
-  else
-    return launch_x2_runs<P>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, runs, n_runs, st);
 }
 
 }  // namespace wq
@@ -1352,35 +1133,6 @@ int wq_x2_rows(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
   }
   return x2_dispatch(N, p, nA, nApad, ws, ktot, zstride, Uext, Zext, s_w, alpha, w_ik1, Xrows, ldx,
                      stream, (int)tile_row0, (int)tile_row1);
-}
-
-int wq_x2_runs(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
-               const double* Uext, const double* Zext, const double* s_w, double alpha,
-               double w_ik1, const int* runs, int64_t n_runs, double* X, int64_t ldx,
-               void* stream) {
-  if (N <= 0 || !Uext || !Zext || !s_w || !X || !runs || n_runs <= 0) {
-    set_error("wq_x2_runs: bad arguments");
-    return WQ_EINVAL;
-  }
-  cudaStream_t st = (cudaStream_t)stream;
-#define WQ_XR_CASE(PP)                                                                         \
-  case PP:                                                                                     \
-    if (nA != X2Cfg<PP>::NA || nApad != X2Cfg<PP>::NAPAD || ws != X2Cfg<PP>::WS ||              \
-        ktot != X2Cfg<PP>::KTOT || zstride != X2Cfg<PP>::ZSTRIDE) {                             \
-      set_error("wq_x2_runs: layout mismatch for p=%d", PP);                                   \
-      return WQ_EINVAL;                                                                        \
-    }                                                                                          \
-    return launch_x2_runs_any<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, runs, (int)n_runs, st);
-  switch (p) {
-    WQ_XR_CASE(2)
-    WQ_XR_CASE(3)
-    WQ_XR_CASE(4)
-    WQ_XR_CASE(5)
-    default:
-      set_error("wq_x2_runs: degree %d unsupported (2..5)", p);
-      return WQ_EUNSUPPORTED;
-  }
-#undef WQ_XR_CASE
 }
 
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream) {

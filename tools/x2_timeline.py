@@ -26,16 +26,3 @@ print("per-CTA cycles: mean total %.0f" % tot.mean())
 for k, nm in enumerate(names):
     print(f"  {nm:10s} mean {d[:, k].mean():8.0f}  ({100 * d[:, k].mean() / tot.mean():5.1f}%)  p10 {np.percentile(d[:, k], 10):8.0f} p90 {np.percentile(d[:, k], 90):8.0f}")
 
-# ik1_sym timeline: slots 0 start(after staging loads issued),1 after barrier,2 phase1 done (thread 0),3 after barrier,4 end
-buf.zero_()
-_lib.call("wq_debug_x2_timing", _lib.ptr(buf))
-sm = AS._smooth(disc)
-_lib.call("wq_ik1_sym", AS.ctypes_ref(sm["struct"]), _lib.ptr(X), N, 0, _lib.ptr(sm["flag"]), _lib.stream_handle())
-torch.cuda.synchronize()
-_lib.call("wq_debug_x2_timing", None)
-t = buf.cpu().numpy().astype(np.float64)[:, :5]
-d = np.diff(t, axis=1)
-tot = t[:, 4] - t[:, 0]
-print("ik1 per-CTA cycles: mean total %.0f" % tot.mean())
-for k, nm in enumerate(["stage-wait", "phase1 (thread0)", "phase1 barrier", "phase2+stores"]):
-    print(f"  {nm:18s} mean {d[:, k].mean():8.0f}  ({100 * d[:, k].mean() / tot.mean():5.1f}%)")
