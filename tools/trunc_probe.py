@@ -7,6 +7,66 @@ import numpy as np
 import _cases as CS
 import paper_1703_10016_b200 as W
 from paper_1703_10016_b200 import assembly as A, splines as S
+from scipy.interpolate import BSpline
+
+def cheb_truncated_coeffs(basis, elements, degree, scale_fn=None, tol=1e-11):
+    """``local_basis_coeffs`` with the interpolant's Chebyshev tail dropped.
+
+    The reference interpolates B_i(s)·J(s) at ``degree + 1`` Chebyshev points
+    and converts with the inverse monomial Vandermonde (splines.py:427-472).
+    The interpolant is the same polynomial as sum_k c_k T_k(x) with the
+    discrete Chebyshev coefficients c_k of those values; for k above the
+    B-spline degree they carry J's variation across one element (decaying
+    like (h/curve scale)^k) and then the round-off of the sample positions
+    (≈1e-13 of max|c| on fine meshes), which the monomial conversion amplifies
+    into coefficients of size ~1e-10 that cancel pointwise.  Terms with
+    max|c_k| ≤ tol·max|c| for every k above a cut D are dropped, so the
+    polynomial moves pointwise by at most sum_{k>D} |c_k| (the reference's own
+    noise level) and its monomial coefficients vanish above D.  The log part
+    then contracts only D + 1 powers (``LogPart.na_used``).
+
+    Returns ``(coeffs (n_el, degree+1, basis.degree+1), cols, D)``; coeffs is
+    zero in powers > D.
+    """
+    from numpy.polynomial import chebyshev as npc
+
+    x, _ = S._cheb_setup(degree)
+    n = degree + 1
+    elements = np.asarray(elements, dtype=float)
+    n_el = len(elements)
+    half = 0.5 * (elements[:, 1] - elements[:, 0])
+    mid = 0.5 * (elements[:, 0] + elements[:, 1])
+    pts = (mid[:, None] + half[:, None] * x[None, :]).ravel()
+    mat = BSpline.design_matrix(pts, basis.knots, basis.degree)
+    width = basis.degree + 1
+    if mat.indptr[-1] != len(pts) * width:
+        raise ValueError("local interpolation points must lie strictly inside knot spans")
+    cols_all = mat.indices.reshape(n_el, n, width)
+    if np.any(cols_all[:, 0, :] != cols_all[:, -1, :]):
+        raise ValueError("each element must lie inside a single knot span")
+    cols = cols_all[:, 0, :].copy()
+    if basis.closed:
+        cols[cols >= basis.dim] -= basis.dim
+    vals = mat.data.reshape(n_el, n, width)
+    if scale_fn is not None:
+        vals = vals * np.asarray(scale_fn(pts), dtype=float).reshape(n_el, n, 1)
+    # discrete Chebyshev transform at the first-kind points (exact orthogonality)
+    tk = np.cos(np.outer(np.arange(n), np.arccos(x)))
+    c = np.einsum("kj,ejb->ekb", tk, vals) * (2.0 / n)
+    c[:, 0] *= 0.5
+    prof = np.abs(c).max(axis=(0, 2))
+    big = np.nonzero(prof > tol * prof.max())[0]
+    D = int(max(big.max() if len(big) else 0, basis.degree))
+    conv = np.zeros((D + 1, D + 1))  # conv[k, a]: coefficient of x^a in T_k
+    for k in range(D + 1):
+        e = np.zeros(k + 1)
+        e[k] = 1.0
+        conv[k, : k + 1] = npc.cheb2poly(e)
+    coeffs = np.zeros((n_el, n, width))
+    coeffs[:, : D + 1, :] = np.einsum("ka,ekb->eab", conv, c[:, : D + 1, :])
+    coeffs[:, : D + 1, :] *= (half[:, None] ** -np.arange(D + 1)[None, :])[:, :, None]
+    return coeffs, cols, D
+
 
 def patch(disc, tol):
     lp = A._log_part(disc)
@@ -15,7 +75,7 @@ def patch(disc, tol):
     cb = curve.basis
     jac = lambda pts: np.linalg.norm(curve.spline(1)(np.clip(pts, cb.a, cb.b)), axis=-1)
     fine = disc.refined.basis
-    u, ucols, D = S.cheb_truncated_coeffs(space, fine.elements, lp.da, scale_fn=jac, tol=tol)
+    u, ucols, D = cheb_truncated_coeffs(space, fine.elements, lp.da, scale_fn=jac, tol=tol)
     n = fine.n_elements; N = space.dim; tu = lp.U.shape[1]
     e_start = np.arange(N) - space.degree
     for a in range(tu):
