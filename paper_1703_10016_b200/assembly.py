@@ -687,6 +687,30 @@ def lattice_classes(elh, elm):
     return kidx, gidx, glist
 
 
+_YS_MMA = True        # pure-lattice 64 x 64 tiles of the Y-stage on DMMA (wq_ystage_mma)
+_YM_T, _YM_FSP, _YM_ESP, _YM_ZR, _YM_TFRONT = 64, 72, 68, 152, 8
+_YM_NOT_PURE = -2 ** 31
+
+
+def _ym_tiles(lo, hi, ko_el, start, stop, rows):
+    """Per 64-function tile from ``start``: the common lattice offset k_e - e of every
+    element the tile's supports touch, or INT32_MIN when the tile is partial, leaves
+    the lattice, changes offset, or exceeds the tensor-core kernel's spans (row tiles:
+    first elements within 68; column tiles: at most 72 elements)."""
+    out = []
+    for t0 in range(start, stop, _YM_T):
+        t1 = t0 + _YM_T - 1
+        ok = t1 < stop
+        if ok:
+            ea, eb = int(lo[t0]), int(hi[t1])
+            ks = ko_el[ea: eb + 1]
+            ok = bool(np.all(ks == ks[0])) and ks[0] != _YM_NOT_PURE
+            span_ok = (int(lo[t1]) - ea <= _YM_ESP) if rows else (eb - ea + 1 <= _YM_FSP)
+            ok = ok and span_ok
+        out.append(int(ko_el[int(lo[t0])]) if ok else _YM_NOT_PURE)
+    return np.asarray(out, np.int32)
+
+
 def _support_ranges(el):
     """First / last element of each function's support from a (-1 padded)
     incidence array (open meshes: contiguous)."""
@@ -755,15 +779,53 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None):
     thetaT = torch.empty((NE, r1 - r0), dtype=torch.float64, device="cuda")
     D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
     mg = _lib.ptr(mgc) if mgc is not None else None
+    wc = lp.v_el.shape[1]
     cols = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]))
     tail = (_lib.ptr(d["v"]), nB, _lib.ptr(d["elh"]), _lib.ptr(L["kidx"]), _lib.ptr(L["gidx"]),
             _lib.ptr(m2u), da1, mg, _lib.ptr(d["ca"]), _lib.ptr(d["cb"]))
-    _lib.call("wq_ystage", N, NE, n, da1, nU, lp.v_el.shape[1], _lib.ptr(L["ucols"]),
+    mma = _YS_MMA and r0 % _YM_T == 0 and nU == 5 and nB == 5 and da1 <= 20
+    kT = kD = kC = None
+    if mma:
+        mkey = ("ym", r0, r1)
+        if mkey not in L:
+            ko_el = np.where(kidx != _NOT_LATTICE, kidx - np.arange(n), _YM_NOT_PURE)
+            u_lo, u_hi = _support_ranges(lp.u_el)
+            v_lo, v_hi = _support_ranges(lp.v_el)
+            L[mkey] = {"T": _to_dev(torch, _ym_tiles(u_lo, u_hi, ko_el, r0, r1, True)),
+                       "D": _to_dev(torch, _ym_tiles(v_lo, v_hi, ko_el, 0, NE, True)),
+                       "C": _to_dev(torch, _ym_tiles(v_lo, v_hi, ko_el, 0, NE, False))}
+        Y = L[mkey]
+        kT, kD, kC = _lib.ptr(Y["T"]), _lib.ptr(Y["D"]), _lib.ptr(Y["C"])
+        n_tab = 2 * n - 1 + _YM_ZR + _YM_TFRONT
+        f64 = dict(dtype=torch.float64, device="cuda")
+        Tb = torch.empty((5, n_tab, 20), **f64)
+        vsum = torch.empty((NE, 5), **f64)
+        CrT, HrT, LtT = torch.empty((N, 5, 20), **f64), torch.empty((N, 5, 5), **f64), torch.empty((N, 5), **f64)
+        CrD, HrD, LtD = torch.empty((NE, 5, 8), **f64), torch.empty((NE, 5, 5), **f64), torch.empty((NE, 5), **f64)
+        common = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]))
+        _lib.call("wq_ystage_mma_prep", N, NE, n, da1, 20, nU, wc, _lib.ptr(L["ucols"]),
+                  _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *common, _lib.ptr(d["u"]), da1,
+                  _lib.ptr(d["v"]), _lib.ptr(d["elh"]), _lib.ptr(m2u), da1, _lib.ptr(d["ca"]),
+                  _lib.ptr(d["cb"]), _lib.ptr(CrT), _lib.ptr(HrT), _lib.ptr(LtT), _lib.ptr(vsum),
+                  _lib.ptr(Tb), n_tab, st)
+        _lib.call("wq_ystage_mma_prep", NE, NE, n, nB, 8, nB, wc, _lib.ptr(L["vcols"]),
+                  _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *common, _lib.ptr(d["v"]), nB,
+                  _lib.ptr(d["v"]), _lib.ptr(d["elh"]), None, da1, _lib.ptr(d["ca"]),
+                  _lib.ptr(d["cb"]), _lib.ptr(CrD), _lib.ptr(HrD), _lib.ptr(LtD), _lib.ptr(vsum),
+                  None, n_tab, st)
+        mcols = (wc,) + common + (_lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), _lib.ptr(d["v"]))
+        _lib.call("wq_ystage_mma", N, NE, n, 20, wc, _lib.ptr(L["u_lo"]), *mcols[1:],
+                  _lib.ptr(CrT), _lib.ptr(HrT), _lib.ptr(LtT), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
+                  kT, kC, _lib.ptr(thetaT), r1 - r0, r0, r1, 0, st)
+        _lib.call("wq_ystage_mma", NE, NE, n, 8, wc, _lib.ptr(L["v_lo"]), *mcols[1:],
+                  _lib.ptr(CrD), _lib.ptr(HrD), _lib.ptr(LtD), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
+                  kD, kC, _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), st)
+    _lib.call("wq_ystage", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
               _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *cols, _lib.ptr(d["u"]), da1, *tail,
-              L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, 0, st)
-    _lib.call("wq_ystage", NE, NE, n, nB, nB, lp.v_el.shape[1], _lib.ptr(L["vcols"]),
+              L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, 0, kT, kC, st)
+    _lib.call("wq_ystage", NE, NE, n, nB, nB, wc, _lib.ptr(L["vcols"]),
               _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *cols, _lib.ptr(d["v"]), nB, *tail,
-              L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), st)
+              L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), kD, kC, st)
     if len(glist):
         _blocks_theta_d(disc, lp, d, outer=glist, thetaT=thetaT, D=D, rows=rows)
     # D's lower storage triangle is complete (lattice + block parts): mirror it

@@ -24,7 +24,7 @@ struct NodeRec {
 
 __device__ __forceinline__ double k1_value(const wq_smooth_t& sm, int64_t qa, const NodeRec& a,
                                            int64_t ra, const NodeRec& b, int* bad,
-                                           const double* ltab) {
+                                           const double2* ltab) {
   double R;
   if (qa == ra) {
     R = a.J * a.J;  // continuity limit J^2 (geometry.py:240-245)
@@ -50,14 +50,14 @@ __device__ __forceinline__ double k1_value(const wq_smooth_t& sm, int64_t qa, co
     *bad = 1;
     return 0.5 * log(R);
   }
-  return half_ln16(R, ltab);   // table-based 0.5 ln, ~1 ulp (tests/test_gpu_kernels.py)
+  return half_ln64t(R, ltab);   // table-based 0.5 ln, ~1 ulp (tests/test_gpu_kernels.py)
 }
 
 __global__ void __launch_bounds__(IK1_THREADS)
 ik1_tile_kernel(wq_smooth_t sm, int64_t row0, int64_t row1, int64_t col0, int64_t col1, double* X,
-                int64_t ldx, int accumulate, int span, int* flag, int sym, const double* gtab) {
+                int64_t ldx, int accumulate, int span, int* flag, int sym) {
   extern __shared__ double smem[];
-  __shared__ double ltab[48];
+  __shared__ double2 ltab[64];
   // sym: rows == cols; only tiles on or above the diagonal, mirrored (K1 is
   // symmetric in (q, r), so IK1 = G K1 G^T is)
   if (sym && blockIdx.x < blockIdx.y) return;
@@ -80,7 +80,7 @@ ik1_tile_kernel(wq_smooth_t sm, int64_t row0, int64_t row1, int64_t col0, int64_
   int* qidx = reinterpret_cast<int*>(Gj + IK1_TJ * wg);   // span
   int* ridx = qidx + span;                                // span
 
-  for (int k = threadIdx.x; k < 48; k += blockDim.x) ltab[k] = gtab[k];
+  for (int k = threadIdx.x; k < 128; k += blockDim.x) reinterpret_cast<double*>(ltab)[k] = kTang64[k];
   for (int k = threadIdx.x; k < nQ; k += blockDim.x) {
     int64_t a = pmod(qlo + k, sm.nq);
     qidx[k] = (int)a;
@@ -168,11 +168,7 @@ extern "C" int wq_ik1(const wq_smooth_t* sm, int64_t row0, int64_t row1, int64_t
   dim3 grid(ceil_div(col1 - col0, IK1_TJ), ceil_div(row1 - row0, IK1_TI));
   // the full square (the assemble_ik1 / general-path call) uses the symmetry
   const int sym = row0 == col0 && row1 == col1 && IK1_TI == IK1_TJ;
-  const double* gtab = nullptr;
-  int rc = logtab16_device(&gtab);
-  if (rc) return rc;
   ik1_tile_kernel<<<grid, IK1_THREADS, smem, (cudaStream_t)stream>>>(*sm, row0, row1, col0, col1, X,
-                                                                     ldx, accumulate, span, flag, sym,
-                                                                     gtab);
+                                                                     ldx, accumulate, span, flag, sym);
   return check_launch("wq_ik1");
 }

@@ -35,7 +35,7 @@ __device__ __forceinline__ void tri_index_g(int64_t t, int nb, int& bi, int& bj)
 template <int MODE>
 __device__ __forceinline__ double k1g(const wq_smooth_t& sm, double qx, double qy, int qa,
                                       double qJ, double qs, double rx, double ry, int ra,
-                                      double rs, const double* tab, int& bad) {
+                                      double rs, const double2* tab, int& bad) {
   double R;
   if (qa == ra) {
     R = qJ * qJ;  // continuity limit J^2 (geometry.py:240-245)
@@ -59,15 +59,14 @@ __device__ __forceinline__ double k1g(const wq_smooth_t& sm, double qx, double q
     bad = 1;
     return 0.0;
   }
-  return half_ln16(R, tab);
+  return half_ln64t(R, tab);
 }
 
 // sym: upper tile pairs (bi <= bj) of the full matrix, mirrored; rect: tile rows
 // [tile_row0, ...) x all tile columns, rows offset by tile_row0 * 64
 template <int WG, int MODE>
 __global__ void __launch_bounds__(IG_THREADS, 2)
-ik1g_kernel(wq_smooth_t sm, int nb, int tile_row0, int sym, double* X, int64_t ldx, int* flag,
-            const double* gtab) {
+ik1g_kernel(wq_smooth_t sm, int nb, int tile_row0, int sym, double* X, int64_t ldx, int* flag) {
   extern __shared__ double dsm[];
   int bi, bj;
   if (sym) {
@@ -85,7 +84,8 @@ ik1g_kernel(wq_smooth_t sm, int nb, int tile_row0, int sym, double* X, int64_t l
   const int nQ = (int)(sm.g_start[I0 + ni - 1] + WG - qlo);
   const int nR = (int)(sm.g_start[J0 + nj - 1] + WG - rlo);
   constexpr int NQP = IG_HALF | 1;
-  double* T1 = dsm;                      // [64][NQP]
+  double2* stab = reinterpret_cast<double2*>(dsm);   // [64] ln table (16-byte aligned)
+  double* T1 = dsm + 128;                // [64][NQP]
   double* qx = T1 + IG_T * NQP;          // node data, outer range
   double* qy = qx + IG_HALF;
   double* qJ = qy + IG_HALF;
@@ -96,8 +96,7 @@ ik1g_kernel(wq_smooth_t sm, int nb, int tile_row0, int sym, double* X, int64_t l
   double* rs = rJ + IG_HALF;
   double (*Gi)[WG] = reinterpret_cast<double (*)[WG]>(rs + IG_HALF);
   double (*Gj)[WG] = reinterpret_cast<double (*)[WG]>(rs + IG_HALF + IG_T * WG);
-  double* stab = rs + IG_HALF + 2 * IG_T * WG;
-  int* qa = reinterpret_cast<int*>(stab + 48);
+  int* qa = reinterpret_cast<int*>(rs + IG_HALF + 2 * IG_T * WG);
   int* ra = qa + IG_HALF;
   int* si = ra + IG_HALF;                // rule starts of the tile rows, relative to qlo
   int* sj = si + IG_T;                   // ... of the tile columns, relative to rlo
@@ -123,7 +122,7 @@ ik1g_kernel(wq_smooth_t sm, int nb, int tile_row0, int sym, double* X, int64_t l
     si[k] = k < ni ? (int)(sm.g_start[I0 + k] - qlo) : nQ - WG;
     sj[k] = k < nj ? (int)(sm.g_start[J0 + k] - rlo) : nR - WG;
   }
-  for (int k = tid; k < 48; k += IG_THREADS) stab[k] = gtab[k];
+  for (int k = tid; k < 128; k += IG_THREADS) reinterpret_cast<double*>(stab)[k] = kTang64[k];
   __syncthreads();
 
   int bad = 0;
@@ -207,13 +206,10 @@ extern "C" int wq_ik1_band(const wq_smooth_t* sm, int64_t tile_row0, int64_t til
     set_error("wq_ik1_band: table mode without invp2");
     return WQ_EINVAL;
   }
-  const double* gtab = nullptr;
-  int rc = logtab16_device(&gtab);
-  if (rc) return rc;
   const int sym = tile_row0 < 0;
   const int64_t blocks = sym ? (int64_t)nb * (nb + 1) / 2 : (tile_row1 - tile_row0) * nb;
   const int wg = (int)sm->wg;
-  const size_t smem = ((size_t)IG_T * (IG_HALF | 1) + 8 * IG_HALF + 2 * IG_T * wg + 48) * 8 +
+  const size_t smem = ((size_t)IG_T * (IG_HALF | 1) + 8 * IG_HALF + 2 * IG_T * wg + 128) * 8 +
                       (size_t)(2 * IG_HALF + 2 * IG_T) * 4;
   cudaStream_t st = (cudaStream_t)stream;
   const int mode = (int)sm->k1_mode;
@@ -222,7 +218,7 @@ extern "C" int wq_ik1_band(const wq_smooth_t* sm, int64_t tile_row0, int64_t til
     cudaFuncSetAttribute(ik1g_kernel<W, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                          (int)smem);                                                            \
     ik1g_kernel<W, M><<<(unsigned)blocks, IG_THREADS, smem, st>>>(                             \
-        *sm, nb, (int)tile_row0, sym, X, ldx, flag, gtab);                                     \
+        *sm, nb, (int)tile_row0, sym, X, ldx, flag);                                           \
   }
 #define WQ_IG_CASE(W)                                                                           \
   case W:                                                                                       \

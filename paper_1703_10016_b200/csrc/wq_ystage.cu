@@ -63,6 +63,9 @@ struct YsArgs {
   int64_t out_row0;
   int64_t row_end;            // rows >= row_end are not produced
   int sym;                    // rows == cols (D): only tiles meeting c >= r; mirrored after
+  const int* row_ko;          // 64-row tiles from out_row0 (wq_ystage_mma) or NULL
+  const int* col_ko;          // 64-column tiles; tiles with row_ko == col_ko != NOT_PURE are
+                              // done on the tensor cores by wq_ystage_mma
 };
 
 // Thread (inner element f, group of YS_RPT tile rows): Y in registers.
@@ -74,6 +77,10 @@ ystage_kernel(YsArgs A) {
   const int nr = (int)min((int64_t)YS_TR, A.row_end - R0);
   const int nc = (int)min((int64_t)YS_TC, A.n_cols - C0);
   if (SYM && C0 + nc - 1 < R0) return;   // strictly below the diagonal: mirrored later
+  if (A.row_ko) {
+    const int ko = A.row_ko[(R0 - A.out_row0) / 64];
+    if (ko != INT32_MIN && A.col_ko[blockIdx.y] == ko) return;   // wq_ystage_mma's tile
+  }
   const int64_t ea = A.r_emin[R0], eb = A.r_emax[R0 + nr - 1];
   const int64_t fa = A.c_emin[C0], fb = A.c_emax[C0 + nc - 1];
   const int ne = (int)(eb - ea + 1), nf = (int)(fb - fa + 1);
@@ -297,18 +304,18 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
               const double* elh, const int64_t* kidx, const int* gidx, const double* m2u,
               int da1, const double* mgc, const double* ca, const double* cb, int64_t fspan,
               int64_t espan, double* out, int64_t ldo, int64_t row0, int64_t row1,
-              int sym_d, void* stream) {
+              int sym_d, const int* row_ko, const int* col_ko, void* stream) {
   if (n_rows <= 0 || n_cols <= 0 || nal < 1 || nal > da1 || nloc < 1 || nloc > YS_MAXLOC ||
       wc < 1 || !e_rows || !r_emin || !r_emax || !c_el || !c_loc || !c_emin || !c_emax ||
       !coef || ldal < nal || !v || nb != YS_NB || !elh || !kidx || !gidx || !m2u || !ca || !cb ||
       fspan < 1 || espan < 1 || !out || row0 < 0 || row1 > n_rows || row1 <= row0 ||
-      row0 % YS_TR != 0 || ldo < row1 - row0) {
+      row0 % YS_TR != 0 || ldo < row1 - row0 || (row_ko && (row0 % 64 != 0 || !col_ko))) {
     set_error("wq_ystage: bad arguments (column degree must be %d)", YS_NB - 1);
     return WQ_EINVAL;
   }
   YsArgs A{n_rows, n_cols, n_el, nal, nloc, wc, e_rows, r_emin, r_emax, c_el, c_loc, c_emin,
            c_emax, coef, ldal, v, elh, kidx, gidx, m2u, da1, mgc, ca, cb, fspan, espan, out,
-           ldo, row0 / YS_TR, row0, row1, 0};
+           ldo, row0 / YS_TR, row0, row1, 0, row_ko, col_ko};
   const size_t smem = (size_t)(espan * nal * nloc + espan * nloc * YS_NB + espan * YS_NB +
                                (fspan + espan - 1) * nal * YS_NB + YS_TR * fspan * YS_NB) * 8 +
                       (size_t)espan * nloc * 4;
