@@ -375,26 +375,25 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
  * (from row0, a multiple of 64) and 64-column tiles whose elements all lie on one lattice
  * run -- row_ko[t] == col_ko[u] != INT32_MIN, the common offset k_e - e -- the inner sum is
  * a GEMM in skewed coordinates u = f - e_r on DMMA (m8n8k4.f64), one per column power b,
- * with the Toeplitz A operand from Tb (table slices) and the B operand from Cr / Hr; the
- * column contraction and the ln h term (LtR, vsum) follow in shared memory.  wq_ystage
- * given the same row_ko / col_ko skips exactly these tiles.  nalp: 20 (Theta, nal <= 20)
- * or 8 (D).  n_tab >= 2 n_el - 1 + 168.
- * wq_ystage_mma_prep fills Cr (n_rows x 5 x nalp), Hr (n_rows x 5 x 5), LtR (n_rows x 5),
- * vsum (n_cols x 5) and, when Tb is not NULL, Tb (5 x n_tab x 20) from m2u.
+ * with the Toeplitz A operand from Tb (table slices) and the B operand from Cr; the column
+ * contraction and the ln h term (LtR, vsum) follow in shared memory.  wq_ystage given the
+ * same row_ko / col_ko skips exactly these tiles.  nal: 17 (Theta, p = 4) or 5 (D).
+ * n_tab >= 2 n_el - 1 + 160.
+ * wq_ystage_mma_prep fills Cr (5 x n_rows x kp, kp = 5 nal rounded up to 4), LtR
+ * (n_rows x 5), vsum (n_cols x 5) and, when Tb is not NULL, Tb (5 x n_tab x 20) from m2u.
  */
-int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nalp, int nloc,
-                       int wc, const int64_t* e_rows, const int64_t* r_emin,
-                       const int64_t* r_emax, const int64_t* c_el, const int64_t* c_loc,
-                       const double* coef, int ldal, const double* v, const double* elh,
-                       const double* m2u, int da1, const double* ca, const double* cb,
-                       double* Cr, double* Hr, double* LtR, double* vsum, double* Tb,
-                       int64_t n_tab, void* stream);
-int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nalp, int wc,
+int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, int wc,
+                       const int64_t* e_rows, const int64_t* r_emin, const int64_t* r_emax,
+                       const int64_t* c_el, const int64_t* c_loc, const double* coef, int ldal,
+                       const double* v, const double* elh, const double* m2u, int da1,
+                       const double* ca, const double* cb, double* Cr, double* LtR,
+                       double* vsum, double* Tb, int64_t n_tab, void* stream);
+int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
                   const int64_t* r_emin, const int64_t* c_el, const int64_t* c_loc,
                   const int64_t* c_emin, const int64_t* c_emax, const double* v,
-                  const double* Cr, const double* Hr, const double* LtR, const double* vsum,
-                  const double* Tb, int64_t n_tab, const int* row_ko, const int* col_ko,
-                  double* out, int64_t ldo, int64_t row0, int64_t row1, int sym, void* stream);
+                  const double* Cr, const double* LtR, const double* vsum, const double* Tb,
+                  int64_t n_tab, const int* row_ko, const int* col_ko, double* out, int64_t ldo,
+                  int64_t row0, int64_t row1, int sym, void* stream);
 
 /* out[j][i] = out[i][j] for i > j (n x n, leading dimension ld). */
 int wq_mirror_lower(double* out, int64_t n, int64_t ld, void* stream);

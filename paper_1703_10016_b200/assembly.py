@@ -783,7 +783,7 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None):
     cols = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]))
     tail = (_lib.ptr(d["v"]), nB, _lib.ptr(d["elh"]), _lib.ptr(L["kidx"]), _lib.ptr(L["gidx"]),
             _lib.ptr(m2u), da1, mg, _lib.ptr(d["ca"]), _lib.ptr(d["cb"]))
-    mma = _YS_MMA and r0 % _YM_T == 0 and nU == 5 and nB == 5 and da1 <= 20
+    mma = _YS_MMA and r0 % _YM_T == 0 and nU == 5 and nB == 5 and da1 == 17 and wc <= 5
     kT = kD = kC = None
     if mma:
         mkey = ("ym", r0, r1)
@@ -798,27 +798,27 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None):
         kT, kD, kC = _lib.ptr(Y["T"]), _lib.ptr(Y["D"]), _lib.ptr(Y["C"])
         n_tab = 2 * n - 1 + _YM_ZR + _YM_TFRONT
         f64 = dict(dtype=torch.float64, device="cuda")
+        kpT, kpD = -(-5 * da1 // 4) * 4, -(-5 * nB // 4) * 4
         Tb = torch.empty((5, n_tab, 20), **f64)
         vsum = torch.empty((NE, 5), **f64)
-        CrT, HrT, LtT = torch.empty((N, 5, 20), **f64), torch.empty((N, 5, 5), **f64), torch.empty((N, 5), **f64)
-        CrD, HrD, LtD = torch.empty((NE, 5, 8), **f64), torch.empty((NE, 5, 5), **f64), torch.empty((NE, 5), **f64)
+        CrT, LtT = torch.empty((5, N, kpT), **f64), torch.empty((N, 5), **f64)
+        CrD, LtD = torch.empty((5, NE, kpD), **f64), torch.empty((NE, 5), **f64)
         common = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]))
-        _lib.call("wq_ystage_mma_prep", N, NE, n, da1, 20, nU, wc, _lib.ptr(L["ucols"]),
+        _lib.call("wq_ystage_mma_prep", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
                   _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *common, _lib.ptr(d["u"]), da1,
                   _lib.ptr(d["v"]), _lib.ptr(d["elh"]), _lib.ptr(m2u), da1, _lib.ptr(d["ca"]),
-                  _lib.ptr(d["cb"]), _lib.ptr(CrT), _lib.ptr(HrT), _lib.ptr(LtT), _lib.ptr(vsum),
-                  _lib.ptr(Tb), n_tab, st)
-        _lib.call("wq_ystage_mma_prep", NE, NE, n, nB, 8, nB, wc, _lib.ptr(L["vcols"]),
+                  _lib.ptr(d["cb"]), _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum), _lib.ptr(Tb),
+                  n_tab, st)
+        _lib.call("wq_ystage_mma_prep", NE, NE, n, nB, nB, wc, _lib.ptr(L["vcols"]),
                   _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *common, _lib.ptr(d["v"]), nB,
                   _lib.ptr(d["v"]), _lib.ptr(d["elh"]), None, da1, _lib.ptr(d["ca"]),
-                  _lib.ptr(d["cb"]), _lib.ptr(CrD), _lib.ptr(HrD), _lib.ptr(LtD), _lib.ptr(vsum),
-                  None, n_tab, st)
-        mcols = (wc,) + common + (_lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), _lib.ptr(d["v"]))
-        _lib.call("wq_ystage_mma", N, NE, n, 20, wc, _lib.ptr(L["u_lo"]), *mcols[1:],
-                  _lib.ptr(CrT), _lib.ptr(HrT), _lib.ptr(LtT), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
+                  _lib.ptr(d["cb"]), _lib.ptr(CrD), _lib.ptr(LtD), _lib.ptr(vsum), None, n_tab, st)
+        mcols = common + (_lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), _lib.ptr(d["v"]))
+        _lib.call("wq_ystage_mma", N, NE, n, da1, wc, _lib.ptr(L["u_lo"]), *mcols,
+                  _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
                   kT, kC, _lib.ptr(thetaT), r1 - r0, r0, r1, 0, st)
-        _lib.call("wq_ystage_mma", NE, NE, n, 8, wc, _lib.ptr(L["v_lo"]), *mcols[1:],
-                  _lib.ptr(CrD), _lib.ptr(HrD), _lib.ptr(LtD), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
+        _lib.call("wq_ystage_mma", NE, NE, n, nB, wc, _lib.ptr(L["v_lo"]), *mcols,
+                  _lib.ptr(CrD), _lib.ptr(LtD), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
                   kD, kC, _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), st)
     _lib.call("wq_ystage", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
               _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *cols, _lib.ptr(d["u"]), da1, *tail,

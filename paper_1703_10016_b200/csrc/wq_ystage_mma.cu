@@ -10,8 +10,8 @@
 //   Y_b[r][e_r + u] = sum_{s, al} (Cs_{e_r+s}[al][a(r, e_r+s)] h^b) M'_b[u - s][al]
 // -- the A operand is the Toeplitz matrix of the unit gap table slice b (the
 // same for every row function), the B operand the rows' scaled coefficients.
-// This is the x2_pairs scheme (wq_fast.cu) with K = 5 shifts x 20 (or 8)
-// powers and one GEMM per column power b; Out accumulates the column
+// This is the x2_pairs scheme (wq_fast.cu) with K = 5 shifts x 17 (or 5)
+// powers, packed densely, and one GEMM per column power b; Out accumulates the column
 // contraction of each Y_b in shared memory, and the ln h_e term enters as
 //   Out[c][r] += sum_b LtR[r][b] vsum[c][b].
 // One CTA = 64 row functions x 64 column functions, 8 warps x 8 row functions;
@@ -36,7 +36,7 @@ constexpr int YM_PST = YM_FSP + 1;   // Phs row stride (odd)
 constexpr int YM_PF = 10;            // B-fragment prefetch depth
 constexpr int YM_NOT_PURE = INT32_MIN;
 constexpr int YM_TFRONT = 8;         // zero table rows before gap -(n_el - 1)
-constexpr int YM_WCM = 8;            // max column incidences (elements per fine function)
+constexpr int YM_WCM = 5;            // max column incidences (elements per fine function, p = 4)
 
 struct YmArgs {
   int64_t n_cols, n_el;
@@ -47,8 +47,7 @@ struct YmArgs {
   const int64_t* c_emin;
   const int64_t* c_emax;
   const double* v;         // (n_el, NB, NB) column coefficients v_f[be][b]
-  const double* Cr;        // (n_rows, NS, NALP) scaled row coefficients
-  const double* Hr;        // (n_rows, NS, NB) h_{e_r+s}^b
+  const double* Cr;        // (NB, n_rows, KP) B operand: Cs_{e_r+s}[al][a] h^b at k = s NAL + al
   const double* LtR;       // (n_rows, NB)
   const double* vsum;      // (n_cols, NB)
   const double* Tb;        // (NB, n_tab, ZST) table slices, row g + n_el - 1 + TFRONT
@@ -60,19 +59,19 @@ struct YmArgs {
   int sym;
 };
 
-template <int NALP>
+template <int NAL>
 struct YmCfg {
-  static constexpr int QS = NALP / 4;           // k-steps per shift
-  static constexpr int NSTEPS = YM_NS * QS;
+  static constexpr int KP = (YM_NS * NAL + 3) / 4 * 4;   // contraction (s, al) packed densely
+  static constexpr int NSTEPS = KP / 4;
   static constexpr int PF = NSTEPS < YM_PF ? NSTEPS : YM_PF;
   // Zsm[2] | Phs | Cv (column incidences' v_f[b][b'] per b) | 2 mbarriers | Ci (ints)
   static constexpr int SMEM = 2 * YM_ZR * YM_ZST + YM_T * YM_PST + YM_T * YM_WCM * YM_NB + 2 +
                               YM_T * YM_WCM / 2;
 };
 
-template <int NALP>
-__global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A) {
-  using C = YmCfg<NALP>;
+template <int NAL>
+__global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int64_t n_rows) {
+  using C = YmCfg<NAL>;
   extern __shared__ double sm[];
   const int rt = blockIdx.x, ct = blockIdx.y;
   const int ko = A.row_ko[rt];
@@ -117,52 +116,51 @@ __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A) {
     for (int b = 0; b < YM_NB; ++b)
       Cv[k * YM_NB + b] = f >= 0 ? __ldg(A.v + f * (YM_NB * YM_NB) + b * YM_NB + bp) : 0.0;
   }
-  // Out[c][r] for this thread's row r and columns c = cg + 4 i, in registers; starts from
+  // Out[c][r] for this thread's column c and rows r = 16 rg + i, in registers; starts from
   // the ln h term sum_b LtR[r][b] vsum[c][b]
-  const int orow = tid & 63, cg = tid >> 6;
+  const int ocol = tid & 63, rg = tid >> 6;
   double out[YM_T / 4];
   {
-    double lt[YM_NB];
+    double vs[YM_NB];
 #pragma unroll
-    for (int b = 0; b < YM_NB; ++b) lt[b] = __ldg(A.LtR + (R0 + orow) * YM_NB + b);
+    for (int b = 0; b < YM_NB; ++b) vs[b] = __ldg(A.vsum + (C0 + ocol) * YM_NB + b);
 #pragma unroll
     for (int i = 0; i < YM_T / 4; ++i) {
-      const int c = cg + 4 * i;
+      const int64_t r = R0 + 16 * rg + i;
       double s = 0.0;
 #pragma unroll
-      for (int b = 0; b < YM_NB; ++b) s = fma(lt[b], __ldg(A.vsum + (C0 + c) * YM_NB + b), s);
+      for (int b = 0; b < YM_NB; ++b) s = fma(__ldg(A.LtR + r * YM_NB + b), vs[b], s);
       out[i] = s;
     }
   }
   // the skewed output rows of this lane's functions: f = k + e_func
   const int64_t rowf = R0 + 8 * warp + rl;                 // B-operand row
-  const double* __restrict__ brow = A.Cr + rowf * (YM_NS * NALP) + cl;
+  const double* __restrict__ brow0 = A.Cr + rowf * C::KP + cl;
   int ef[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) ef[e] = (int)(A.r_emin[R0 + 8 * warp + 2 * cl + e] - emax_w);
 
   for (int b = 0; b < YM_NB; ++b) {
     const double* zb = Zsm + (b & 1) * ZW;
-    double hr[YM_NS];
-#pragma unroll
-    for (int s = 0; s < YM_NS; ++s) hr[s] = __ldg(A.Hr + (rowf * YM_NS + s) * YM_NB + b);
+    const double* __restrict__ brow = brow0 + (int64_t)b * n_rows * C::KP;
     double bq[C::PF];
 #pragma unroll
-    for (int t = 0; t < C::PF; ++t) bq[t] = __ldg(brow + 4 * t) * hr[t / C::QS];
+    for (int t = 0; t < C::PF; ++t) bq[t] = __ldg(brow + 4 * t);
     mbar_wait(bar + (b & 1), (unsigned)((b >> 1) & 1));
 
     // ---- Y_b in skewed coordinates: acc[kb] = rows k = fa - emax_w + 8 kb + rl ----
     double acc[YM_NKB][2];
 #pragma unroll
     for (int kb = 0; kb < YM_NKB; ++kb) acc[kb][0] = acc[kb][1] = 0.0;
-    const double* zl = zb + (zoff + rl) * YM_ZST + cl;
+    const double* zl = zb + (zoff + rl) * YM_ZST;
 #pragma unroll
     for (int t = 0; t < C::NSTEPS; ++t) {
-      const int s = t / C::QS, aq = t - s * C::QS;
+      // this lane's contraction index k = 4t + cl = s NAL + al (padding: zero B, any finite A)
+      const int kk = min(4 * t + cl, YM_NS * NAL - 1);
+      const int s = kk / NAL, al = kk - s * NAL;
       const double bfrag = bq[t % C::PF];
-      if (t + C::PF < C::NSTEPS)
-        bq[t % C::PF] = __ldg(brow + 4 * (t + C::PF)) * hr[(t + C::PF) / C::QS];
-      const double* z = zl - s * YM_ZST + 4 * aq;
+      if (t + C::PF < C::NSTEPS) bq[t % C::PF] = __ldg(brow + 4 * (t + C::PF));
+      const double* z = zl - s * YM_ZST + al;
 #pragma unroll
       for (int kb = 0; kb < YM_NKB; ++kb) dmma(acc[kb][0], acc[kb][1], z[8 * kb * YM_ZST], bfrag);
     }
@@ -182,37 +180,50 @@ __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A) {
       }
     __syncthreads();
     // ---- column contraction: Out[c][r] += sum_{(f,b') in inc(c)} Y_b[r][f] v_f[b][b'] ----
+    // (this thread's column: incidences in registers, one shared load per FMA)
     {
-      const double* ph = Phs + orow * YM_PST;
+      int fi[YM_WCM];
+      double cv[YM_WCM];
 #pragma unroll
-      for (int i = 0; i < YM_T / 4; ++i) {
-        const int c = cg + 4 * i;
-#pragma unroll
-        for (int w = 0; w < YM_WCM; ++w) {
-          const int fi = Ci[c * YM_WCM + w];   // warp-uniform (broadcast)
-          if (fi >= 0) out[i] = fma(ph[fi], Cv[(c * YM_WCM + w) * YM_NB + b], out[i]);
-        }
+      for (int w = 0; w < YM_WCM; ++w) {
+        const int f = Ci[ocol * YM_WCM + w];
+        fi[w] = f >= 0 ? f : 0;
+        cv[w] = f >= 0 ? Cv[(ocol * YM_WCM + w) * YM_NB + b] : 0.0;
       }
+      const double* ph = Phs + 16 * rg * YM_PST;
+#pragma unroll
+      for (int i = 0; i < YM_T / 4; ++i)
+#pragma unroll
+        for (int w = 0; w < YM_WCM; ++w) out[i] = fma(ph[i * YM_PST + fi[w]], cv[w], out[i]);
     }
   }
-  // Out[c][r]: 64 consecutive r per column (coalesced)
+  // Out[c][r] through shared memory (the Phs region, stride T + 1) so that 64 consecutive r
+  // of a column leave together
+  __syncthreads();
+  double* Os = Phs;
 #pragma unroll
-  for (int i = 0; i < YM_T / 4; ++i)
-    A.out[(C0 + cg + 4 * i) * A.ldo + R0 + orow - A.out_row0] = out[i];
+  for (int i = 0; i < YM_T / 4; ++i) Os[ocol * (YM_T + 1) + 16 * rg + i] = out[i];
+  __syncthreads();
+  for (int k = tid; k < YM_T * YM_T; k += YM_THREADS) {
+    const int c = k >> 6, r = k & 63;
+    A.out[(C0 + c) * A.ldo + R0 + r - A.out_row0] = Os[c * (YM_T + 1) + r];
+  }
 }
 
-// Cr[r][s][al] = coef[e][al][a] h_e^(al+2), Hr[r][s][b] = h_e^b, e = e_r + s with local
-// index a of r (0 where r has no function on e or al >= nal), LtR[r][b] = sum_{(e,a)}
-// ln h_e c_b h_e^b sum_al c_al Cs_e[al][a] (the ln h part of the unit-table scaling,
-// quadrature.py:497-500)
-__global__ void ystage_mma_prep_rows(int64_t n_rows, int nal, int nalp, int nloc,
+// Cr[b][r][s nal + al] = coef[e][al][a] h_e^(al+2) h_e^b, e = e_r + s with local index a of r
+// (0 where r has no function on e, and in the padding up to kp), LtR[r][b] = sum_{(e,a)}
+// ln h_e c_b h_e^b sum_al c_al coef[e][al][a] h_e^(al+2) (the ln h part of the unit-table
+// scaling, quadrature.py:497-500)
+__global__ void ystage_mma_prep_rows(int64_t n_rows, int nal, int kp, int nloc,
                                      const int64_t* e_rows, const int64_t* r_emin,
                                      const int64_t* r_emax, const double* coef, int ldal,
                                      const double* elh, const double* ca, const double* cb,
-                                     double* Cr, double* Hr, double* LtR) {
+                                     double* Cr, double* LtR) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
   double lt[YM_NB] = {0, 0, 0, 0, 0};
+  for (int k = YM_NS * nal; k < kp; ++k)
+    for (int b = 0; b < YM_NB; ++b) Cr[((int64_t)b * n_rows + r) * kp + k] = 0.0;
   for (int s = 0; s < YM_NS; ++s) {
     const int64_t e = r_emin[r] + s;
     int a = -1;
@@ -221,20 +232,16 @@ __global__ void ystage_mma_prep_rows(int64_t n_rows, int nal, int nalp, int nloc
         if (e_rows[e * nloc + q] == r) a = q;
     const double h = a >= 0 ? elh[e] : 1.0;
     double p = h * h, sc = 0.0;
-    for (int al = 0; al < nalp; ++al) {
-      double c = 0.0;
-      if (a >= 0 && al < nal) {
-        c = coef[(e * ldal + al) * nloc + a] * p;
-        p *= h;
-        sc = fma(ca[al], c, sc);
-      }
-      Cr[(r * YM_NS + s) * nalp + al] = c;
+    for (int al = 0; al < nal; ++al, p *= h) {
+      const double c = a >= 0 ? coef[(e * ldal + al) * nloc + a] * p : 0.0;
+      sc = fma(ca[al], c, sc);
+      double hb = 1.0;
+      for (int b = 0; b < YM_NB; ++b, hb *= h) Cr[((int64_t)b * n_rows + r) * kp + s * nal + al] = c * hb;
     }
-    double hb = 1.0;
-    const double lh = a >= 0 ? log(h) : 0.0;
-    for (int b = 0; b < YM_NB; ++b, hb *= h) {
-      Hr[(r * YM_NS + s) * YM_NB + b] = a >= 0 ? hb : 0.0;
-      if (a >= 0) lt[b] += lh * cb[b] * hb * sc;
+    if (a >= 0) {
+      const double lh = log(h);
+      double hb = 1.0;
+      for (int b = 0; b < YM_NB; ++b, hb *= h) lt[b] += lh * cb[b] * hb * sc;
     }
   }
   for (int b = 0; b < YM_NB; ++b) LtR[r * YM_NB + b] = lt[b];
@@ -273,24 +280,24 @@ using namespace wq;
 
 extern "C" {
 
-int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nalp, int nloc,
-                       int wc, const int64_t* e_rows, const int64_t* r_emin,
-                       const int64_t* r_emax, const int64_t* c_el, const int64_t* c_loc,
-                       const double* coef, int ldal, const double* v, const double* elh,
-                       const double* m2u, int da1, const double* ca, const double* cb,
-                       double* Cr, double* Hr, double* LtR, double* vsum, double* Tb,
-                       int64_t n_tab, void* stream) {
-  if (n_rows <= 0 || n_cols <= 0 || n_el <= 0 || nal < 1 || (nalp != 8 && nalp != 20) ||
-      nal > nalp || nloc < 1 || nloc > 8 || wc < 1 || !e_rows || !r_emin || !r_emax || !c_el ||
-      !c_loc || !coef || ldal < nal || !v || !elh || !ca || !cb || !Cr || !Hr || !LtR ||
-      !vsum || (Tb && (!m2u || da1 < 1 || da1 > YM_ZST || n_tab < 2 * n_el - 1 + YM_ZR + YM_TFRONT))) {
+int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, int wc,
+                       const int64_t* e_rows, const int64_t* r_emin, const int64_t* r_emax,
+                       const int64_t* c_el, const int64_t* c_loc, const double* coef, int ldal,
+                       const double* v, const double* elh, const double* m2u, int da1,
+                       const double* ca, const double* cb, double* Cr, double* LtR,
+                       double* vsum, double* Tb, int64_t n_tab, void* stream) {
+  if (n_rows <= 0 || n_cols <= 0 || n_el <= 0 || (nal != 17 && nal != 5) || nloc < 1 ||
+      nloc > 8 || wc < 1 || !e_rows || !r_emin || !r_emax || !c_el || !c_loc || !coef ||
+      ldal < nal || !v || !elh || !ca || !cb || !Cr || !LtR || !vsum ||
+      (Tb && (!m2u || da1 < 1 || da1 > YM_ZST || n_tab < 2 * n_el - 1 + YM_ZR + YM_TFRONT))) {
     set_error("wq_ystage_mma_prep: bad arguments");
     return WQ_EINVAL;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  ystage_mma_prep_rows<<<ceil_div(n_rows, 128), 128, 0, st>>>(n_rows, nal, nalp, nloc, e_rows,
+  const int kp = (YM_NS * nal + 3) / 4 * 4;
+  ystage_mma_prep_rows<<<ceil_div(n_rows, 128), 128, 0, st>>>(n_rows, nal, kp, nloc, e_rows,
                                                                 r_emin, r_emax, coef, ldal, elh,
-                                                                ca, cb, Cr, Hr, LtR);
+                                                                ca, cb, Cr, LtR);
   ystage_mma_prep_cols<<<ceil_div(n_cols, 128), 128, 0, st>>>(n_cols, wc, c_el, c_loc, v, vsum);
   if (Tb)
     ystage_mma_prep_table<<<ceil_div(YM_NB * n_tab * YM_ZST, 256), 256, 0, st>>>(n_el, da1, n_tab,
@@ -298,32 +305,32 @@ int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, in
   return check_launch("wq_ystage_mma_prep");
 }
 
-int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nalp, int wc,
+int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
                   const int64_t* r_emin, const int64_t* c_el, const int64_t* c_loc,
                   const int64_t* c_emin, const int64_t* c_emax, const double* v,
-                  const double* Cr, const double* Hr, const double* LtR, const double* vsum,
-                  const double* Tb, int64_t n_tab, const int* row_ko, const int* col_ko,
-                  double* out, int64_t ldo, int64_t row0, int64_t row1, int sym, void* stream) {
-  if (n_rows <= 0 || n_cols <= 0 || (nalp != 8 && nalp != 20) || wc < 1 || !r_emin || !c_el ||
-      !c_loc || !c_emin || !c_emax || !v || !Cr || !Hr || !LtR || !vsum || !Tb || !row_ko ||
-      !col_ko || !out || row0 < 0 || row0 % YM_T != 0 || row1 > n_rows || row1 <= row0 || wc > YM_WCM ||
-      ldo < row1 - row0 || n_tab < 2 * n_el - 1 + YM_ZR + YM_TFRONT) {
+                  const double* Cr, const double* LtR, const double* vsum, const double* Tb,
+                  int64_t n_tab, const int* row_ko, const int* col_ko, double* out, int64_t ldo,
+                  int64_t row0, int64_t row1, int sym, void* stream) {
+  if (n_rows <= 0 || n_cols <= 0 || (nal != 17 && nal != 5) || wc < 1 || !r_emin || !c_el ||
+      !c_loc || !c_emin || !c_emax || !v || !Cr || !LtR || !vsum || !Tb || !row_ko ||
+      !col_ko || !out || row0 < 0 || row0 % YM_T != 0 || row1 > n_rows || row1 <= row0 ||
+      wc > YM_WCM || ldo < row1 - row0 || n_tab < 2 * n_el - 1 + YM_ZR + YM_TFRONT) {
     set_error("wq_ystage_mma: bad arguments");
     return WQ_EINVAL;
   }
-  YmArgs A{n_cols, n_el, wc, r_emin, c_el, c_loc, c_emin, c_emax, v, Cr, Hr, LtR, vsum, Tb, n_tab,
+  YmArgs A{n_cols, n_el, wc, r_emin, c_el, c_loc, c_emin, c_emax, v, Cr, LtR, vsum, Tb, n_tab,
            row_ko, col_ko, out, ldo, row0, row0, sym};
   dim3 grid((unsigned)((row1 - row0) / YM_T), (unsigned)(n_cols / YM_T));
   if (grid.x == 0 || grid.y == 0) return WQ_OK;
   cudaStream_t st = (cudaStream_t)stream;
-#define WQ_YM_LAUNCH(NP)                                                                         \
+#define WQ_YM_LAUNCH(NA)                                                                         \
   {                                                                                              \
-    const size_t smem = (size_t)YmCfg<NP>::SMEM * 8;                                             \
-    cudaFuncSetAttribute(ystage_mma_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+    const size_t smem = (size_t)YmCfg<NA>::SMEM * 8;                                             \
+    cudaFuncSetAttribute(ystage_mma_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                          (int)smem);                                                             \
-    ystage_mma_kernel<NP><<<grid, YM_THREADS, smem, st>>>(A);                                    \
+    ystage_mma_kernel<NA><<<grid, YM_THREADS, smem, st>>>(A, n_rows);                            \
   }
-  if (nalp == 20) WQ_YM_LAUNCH(20) else WQ_YM_LAUNCH(8)
+  if (nal == 17) WQ_YM_LAUNCH(17) else WQ_YM_LAUNCH(5)
 #undef WQ_YM_LAUNCH
   return check_launch("wq_ystage_mma");
 }
