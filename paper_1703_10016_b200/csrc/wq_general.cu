@@ -534,81 +534,84 @@ __global__ void gather_d_kernel(int64_t n_fine, int64_t e0, int64_t e1, int64_t 
 
 // Banded Cholesky solves X <- L^{-T} L^{-1} X per column with the last BW
 // values of the column in registers (one load + one store per row).  Rows go
-// in batches of RB: the batch's column values are loaded together (RB
-// independent HBM requests in flight per thread) and its factor rows are
-// staged once per CTA in shared memory as -L[k][k-j] and 1/L[k][k], so the
-// dependent chain per row is BW FMAs and one multiply.
+// in batches of RB: the NEXT batch's column values are loaded while the
+// current batch runs its dependent chain (RB independent HBM requests in
+// flight per thread, latency hidden behind the chain -- one thread per column
+// leaves only ~4 warps per SM), and each batch's factor rows are staged once
+// per CTA in shared memory as -L[k][k-j] and 1/L[k][k], so the dependent
+// chain per row is BW FMAs and one multiply.
+template <int BW, bool FWD>
+__device__ __forceinline__ void band_sweep(int64_t n, const double* Lb, double* x, int64_t ldx,
+                                           bool live) {
+  constexpr int RB = 16, DEPTH = 3;   // batches of RB rows; DEPTH batches of loads in flight
+  __shared__ double cf[RB][BW + 1];   // [r][0] = 1/diag, [r][j] = -off-diagonal
+  // row of batch position r in batch q: forward k = q RB + r, backward k = n - 1 - q RB - r
+  auto row = [n](int64_t q, int r) -> int64_t { return FWD ? q * RB + r : n - 1 - q * RB - r; };
+  const int64_t nbat = (n + RB - 1) / RB;
+  double w[BW];
+#pragma unroll
+  for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = previous solution values
+  double xq[DEPTH][RB];
+  auto load = [&](int64_t q, double (&dst)[RB]) {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int64_t k = row(q, r);
+      dst[r] = (live && q < nbat && k >= 0 && k < n) ? x[k * ldx] : 0.0;
+    }
+  };
+#pragma unroll
+  for (int d = 0; d < DEPTH - 1; ++d) load(d, xq[d]);
+  for (int64_t q = 0; q < nbat; q += DEPTH) {
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) {
+      const int64_t qq = q + d;
+      // batch qq + DEPTH - 1 goes into the slot batch qq - 1 used
+      load(qq + DEPTH - 1, xq[(d + DEPTH - 1) % DEPTH]);
+      __syncthreads();
+      for (int t = threadIdx.x; t < RB * (BW + 1); t += blockDim.x) {
+        const int r = t / (BW + 1), j = t - r * (BW + 1);
+        const int64_t k = row(qq, r);
+        double v = 0.0;
+        if (qq < nbat && k >= 0 && k < n) {
+          if (j == 0) v = 1.0 / Lb[k * (BW + 1)];
+          else if (FWD) v = k - j >= 0 ? -Lb[k * (BW + 1) + j] : 0.0;
+          else v = k + j < n ? -Lb[(k + j) * (BW + 1) + j] : 0.0;
+        }
+        cf[r][j] = v;
+      }
+      __syncthreads();
+      if (!live || qq >= nbat) continue;
+      double* xb = xq[d];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        // oldest values first: the newest one (w[0], the previous row) enters last, so the
+        // loop-carried dependency is one FMA and one multiply per row
+        double s = xb[r];
+#pragma unroll
+        for (int j = BW; j >= 1; --j) s = fma(cf[r][j], w[j - 1], s);
+        s *= cf[r][0];
+        xb[r] = s;
+#pragma unroll
+        for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
+        w[0] = s;
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int64_t k = row(qq, r);
+        if (k >= 0 && k < n) x[k * ldx] = xb[r];
+      }
+    }
+  }
+}
+
 template <int BW>
 __global__ void __launch_bounds__(128)
 band_solve_win_kernel(int64_t n, const double* Lb, double* X, int64_t ncols, int64_t ldx) {
-  constexpr int RB = 32;
-  __shared__ double cf[RB][BW + 1];   // [r][0] = 1/diag, [r][j] = -off-diagonal
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool live = c < ncols;
   double* x = X + (live ? c : 0);
-  double w[BW];
-#pragma unroll
-  for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = y_{k-1-j}
-  for (int64_t k0 = 0; k0 < n; k0 += RB) {
-    __syncthreads();
-    for (int t = threadIdx.x; t < RB * (BW + 1); t += blockDim.x) {
-      const int r = t / (BW + 1), j = t - r * (BW + 1);
-      const int64_t k = k0 + r;
-      double v = 0.0;
-      if (k < n) v = j == 0 ? 1.0 / Lb[k * (BW + 1)] : (k - j >= 0 ? -Lb[k * (BW + 1) + j] : 0.0);
-      cf[r][j] = v;
-    }
-    __syncthreads();
-    if (!live) continue;
-    double xb[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) xb[r] = k0 + r < n ? x[(k0 + r) * ldx] : 0.0;
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      double s = xb[r];
-#pragma unroll
-      for (int j = 1; j <= BW; ++j) s = fma(cf[r][j], w[j - 1], s);
-      s *= cf[r][0];
-      xb[r] = s;
-#pragma unroll
-      for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
-      w[0] = s;
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r)
-      if (k0 + r < n) x[(k0 + r) * ldx] = xb[r];
-  }
-#pragma unroll
-  for (int j = 0; j < BW; ++j) w[j] = 0.0;  // w[j] = z_{k+1+j}
-  for (int64_t k1 = n - 1; k1 >= 0; k1 -= RB) {
-    __syncthreads();
-    for (int t = threadIdx.x; t < RB * (BW + 1); t += blockDim.x) {
-      const int r = t / (BW + 1), j = t - r * (BW + 1);
-      const int64_t k = k1 - r;
-      double v = 0.0;
-      if (k >= 0) v = j == 0 ? 1.0 / Lb[k * (BW + 1)] : (k + j < n ? -Lb[(k + j) * (BW + 1) + j] : 0.0);
-      cf[r][j] = v;
-    }
-    __syncthreads();
-    if (!live) continue;
-    double xb[RB];
-#pragma unroll
-    for (int r = 0; r < RB; ++r) xb[r] = k1 - r >= 0 ? x[(k1 - r) * ldx] : 0.0;
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      double s = xb[r];
-#pragma unroll
-      for (int j = 1; j <= BW; ++j) s = fma(cf[r][j], w[j - 1], s);
-      s *= cf[r][0];
-      xb[r] = s;
-#pragma unroll
-      for (int j = BW - 1; j > 0; --j) w[j] = w[j - 1];
-      w[0] = s;
-    }
-#pragma unroll
-    for (int r = 0; r < RB; ++r)
-      if (k1 - r >= 0) x[(k1 - r) * ldx] = xb[r];
-  }
+  band_sweep<BW, true>(n, Lb, x, ldx, live);
+  band_sweep<BW, false>(n, Lb, x, ldx, live);
 }
 
 }  // namespace wq
