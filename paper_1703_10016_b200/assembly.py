@@ -937,19 +937,33 @@ def _assemble_v2(disc: Discretization, X, alpha: float, w_ik1: float = 2.0, zext
     sm = _smooth(disc)
     main = torch.cuda.current_stream()
     st = _lib.stream_handle(main)
-    Zext = _zext_table(disc) if zext is None else zext
     N = disc.space.dim
+    if chunks is None:
+        chunks = 1
+    ranges = pair_chunks(N, chunks)
+    ik1_first = zext is None and w_ik1 != 0.0 and len(ranges) == 1
+    if ik1_first:
+        # IK1 does not need the gap tables: they build on an auxiliary stream while
+        # the IK1 tiles run, and x2 waits for both
+        aux = _aux_stream(torch)
+        aux.wait_stream(main)          # before the IK1 launch: the tables overlap it
+        _lib.call("wq_ik1_sym", ctypes_ref(sm["struct"]), _lib.ptr(X), X.stride(0), sm["span64"],
+                  _lib.ptr(sm["flag"]), st)
+        with torch.cuda.stream(aux):
+            Zext = _zext_table(disc)
+        Zext.record_stream(main)
+        main.wait_stream(aux)
+    else:
+        Zext = _zext_table(disc) if zext is None else zext
     x2args = (N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1], lp.uext.shape[1],
               lp.zstride, _lib.ptr(d["uext"]), _lib.ptr(Zext), _lib.ptr(d["s_w"]), alpha, w_ik1)
     if w_ik1 == 0.0:
         _lib.call("wq_x2_pairs", *x2args, _lib.ptr(X), X.stride(0), st)
         return X
-    if chunks is None:
-        chunks = 1
-    ranges = pair_chunks(N, chunks)
     if len(ranges) == 1:
-        _lib.call("wq_ik1_sym", ctypes_ref(sm["struct"]), _lib.ptr(X), X.stride(0), sm["span64"],
-                  _lib.ptr(sm["flag"]), st)
+        if not ik1_first:
+            _lib.call("wq_ik1_sym", ctypes_ref(sm["struct"]), _lib.ptr(X), X.stride(0),
+                      sm["span64"], _lib.ptr(sm["flag"]), st)
         _lib.call("wq_x2_pairs", *x2args, _lib.ptr(X), X.stride(0), st)
         return X
     aux = _aux_stream(torch)
