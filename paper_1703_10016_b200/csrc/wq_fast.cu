@@ -583,14 +583,9 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
     fence_proxy_async();
     __syncthreads();
   }
-  // IK1(I,J) tile -> Tst: 64 row copies on the TMA engine, or cp.async
+  // IK1(I,J) tile -> Tst: 64 row copies on the TMA engine (issued after the
+  // orientation-0 window below, which is needed first), or cp.async
   if (tbulk) {
-    if (tid < 32) {
-      // own barrier: the tile is first needed after phi0, so its HBM latency hides behind it
-      if (tid == 0) mbar_arrive_expect_tx(bar + 1, FT * FT * 8);
-      __syncwarp();
-      for (int a = tid; a < FT; a += 32) bulk_g2s(Tst + a * T2STRIDE, src + a * ldx, FT * 8, bar + 1);
-    }
   } else if (with_ik1) {
     {
       for (int k = tid; k < FT * FT; k += X2_THREADS) {
@@ -630,9 +625,18 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
         constexpr unsigned RB = C::ZSTRIDE * 8;
         const int64_t first = min((int64_t)C::ZROWS, n - g0);
         mbar_arrive_expect_tx(bar, C::ZROWS * RB);
-        bulk_g2s(Zsm, Zext + g0 * C::ZSTRIDE, (unsigned)first * RB, bar);
+        const uint64_t pol = l2_evict_last();    // the Z' table is re-read by every tile pair
+        bulk_g2s_hint(Zsm, Zext + g0 * C::ZSTRIDE, (unsigned)first * RB, bar, pol);
         if (first < C::ZROWS)
-          bulk_g2s(Zsm + first * C::ZSTRIDE, Zext, (unsigned)(C::ZROWS - first) * RB, bar);
+          bulk_g2s_hint(Zsm + first * C::ZSTRIDE, Zext, (unsigned)(C::ZROWS - first) * RB, bar, pol);
+      }
+      if (orient == 0 && tbulk && tid < 32) {
+        // own barrier: the tile is first needed after phi0, so its HBM latency hides behind it
+        if (tid == 0) mbar_arrive_expect_tx(bar + 1, FT * FT * 8);
+        __syncwarp();
+        const uint64_t pol = l2_evict_first();   // the IK1 tile is read once
+        for (int a = tid; a < FT; a += 32)
+          bulk_g2s_hint(Tst + a * T2STRIDE, src + a * ldx, FT * 8, bar + 1, pol);
       }
       // alpha S band in B-fragment order, Bfr[jb][s][lane] = alpha S_{8jb+r}[4s+c-r],
       // straight from global memory while the copies fly
@@ -744,9 +748,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
       const bool ji = tid < FT;
       double* dst = ji ? X + (J0 + a) * ldx + I0 : X + (I0 + a) * ldx + J0;
       const double* srcs = (ji ? Oji : Oij) + a * OS;
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
-                   "r"(smem_u32(srcs)), "r"(FT * 8)
-                   : "memory");
+      bulk_s2g_hint(dst, srcs, FT * 8, l2_evict_first());   // A is written once
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
