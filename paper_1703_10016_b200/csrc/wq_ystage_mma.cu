@@ -73,7 +73,9 @@ template <int NAL>
 __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int64_t n_rows) {
   using C = YmCfg<NAL>;
   extern __shared__ double sm[];
-  const int rt = blockIdx.x, ct = blockIdx.y;
+  // column tiles fastest: the CTAs in flight share a row tile, so its B operand (Cr, 45 KB
+  // per power) is fetched from HBM once and then served from L2
+  const int ct = blockIdx.x, rt = blockIdx.y;
   const int ko = A.row_ko[rt];
   if (ko == YM_NOT_PURE || A.col_ko[ct] != ko) return;   // CUDA-core kernel handles the tile
   const int64_t R0 = A.row0 + (int64_t)rt * YM_T, C0 = (int64_t)ct * YM_T;
@@ -320,7 +322,7 @@ int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
   }
   YmArgs A{n_cols, n_el, wc, r_emin, c_el, c_loc, c_emin, c_emax, v, Cr, LtR, vsum, Tb, n_tab,
            row_ko, col_ko, out, ldo, row0, row0, sym};
-  dim3 grid((unsigned)((row1 - row0) / YM_T), (unsigned)(n_cols / YM_T));
+  dim3 grid((unsigned)(n_cols / YM_T), (unsigned)((row1 - row0) / YM_T));
   if (grid.x == 0 || grid.y == 0) return WQ_OK;
   cudaStream_t st = (cudaStream_t)stream;
 #define WQ_YM_LAUNCH(NA)                                                                         \

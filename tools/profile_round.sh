@@ -11,3 +11,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --clock-control none --import-source on -k regex:'x2_pairs|ik1_sym' -c 2 \
     -o gpurun_out/c4full python bench.py --no-cpu-baseline --steps 1 --warmup 1 --e2e-steps 0 \
     > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:'ystage_mma_kernel|band_solve' -c 3 \
+    -o gpurun_out/c5full python bench.py --workload c5 --steps 1 --warmup 0 > gpurun_out/ncu_c5.log 2>&1
