@@ -58,6 +58,17 @@ def workload(n_el: int, p: int = 3, geometry: str = "ellipse"):
     return curve, space
 
 
+def _label(args) -> str:
+    """Workload name of a closed-curve run (C4 at the defaults)."""
+    c4 = args.geometry == "ellipse" and args.p == 3 and args.n_el == 32768
+    c2 = args.geometry == "ellipse" and args.p == 3 and args.n_el == 1024
+    c3 = args.geometry == "star" and args.n_el == 4096
+    tag = "C4: " if c4 else "C2: " if c2 else f"C3 (p={args.p}): " if c3 else ""
+    geo = ("closed ellipse 2x1 (16 ctrl pts, cubic)" if args.geometry == "ellipse"
+           else "closed star r = 1 + 0.3 cos 5t (32 ctrl pts, cubic)")
+    return f"{tag}{geo}, p={args.p}, {args.n_el} uniform elements"
+
+
 def workload_c5(n_el: int = 16384, p: int = 4, seed: int = 0, zone: float = 0.2,
                 ratio: float = 0.9, growth_elems: int = 60):
     """BASELINE.json configs[4] ("C5"): open slit [-1, 1] x {0}, degree p,
@@ -246,6 +257,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-rows", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the 1-GPU assembly as a CUDA graph (auto: N <= 8192)")
     ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
                     help="c4: the headline (BASELINE metric config); c5: graded open slit with "
                          "double knots (configs[4]), 1 GPU, no reference arm (the reference raises)")
@@ -289,8 +302,19 @@ def main():
         mine = sum(1 for c in range(chunks) if (c * world + rank) * sub < N)
         per_step = 7 + 2 * mine + 1   # tables, (ik1_rows, x2_rows) per owned chunk, symmetrise
 
+    graph = None
+    if world == 1 and (args.graph == "on" or (args.graph == "auto" and N <= 8192)):
+        # launch/host-bound sizes: the whole assembly replays as one CUDA graph
+        try:
+            graph = AS.AssemblyGraph(disc, X)
+        except Exception as exc:   # capture unsupported: eager launches
+            print(f"bench: CUDA graph capture failed ({exc}); eager launches", file=sys.stderr)
+            graph = None
+
     def step():
-        if world == 1:
+        if graph is not None:
+            graph.replay()
+        elif world == 1:
             AS._assemble_into(disc, X)
         else:
             D.assemble_distributed_pipelined(disc, Xpad, chunks=chunks, zext=AS._zext_table(disc))
@@ -392,12 +416,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic analytic geometry, BASELINE.json configs[3])",
-            "config": {"workload": f"C4: closed ellipse 2x1 (16 ctrl pts, cubic), p={args.p}, "
-                                   f"{args.n_el} uniform elements", "N": N, "nq": disc.nodes.n,
+            "config": {"workload": _label(args), "N": N, "nq": disc.nodes.n,
+                       "cuda_graph": graph is not None,
                        "parallelism": (f"cyclic row blocks x{world}, {chunks} chunks, in-place NCCL "
                                        "all-gather overlapped with compute") if world > 1
                        else "single GPU",
-                       "l2": "8.6 GB output > 126 MB L2, rewritten every step (no flush needed)"},
+                       "l2": (f"{N * N * 8 / 1e9:.2g} GB output > 126 MB L2, rewritten every step "
+                              "(no flush needed)") if N * N * 8 > 126e6 else
+                             (f"{N * N * 8 / 1e6:.3g} MB output fits L2 (launch-bound size; "
+                              "not an L2-flushed timing)")},
             "clocks": clk.summary(),
             "gpu_launches": gpu_launches,
             "split_ms": dict(zip(names, [float(x) for x in split])),

@@ -439,6 +439,17 @@ def _table_rules():
     return PC.gauss_unit(PC.PAIR_FAR_ORDER)
 
 
+def _table_consts(disc, lp: LogPart):
+    """Device copies of the pair table's constant inputs (near-gap unit entries,
+    Gauss tiers, centred monomial integrals), uploaded once per discretization."""
+    torch = _torch()
+    gx, gw = _table_rules()
+    return _dev(disc, ("table_consts", _TIERED_TABLE), lambda: [
+        _to_dev(torch, lp.near_unit), _to_dev(torch, gx), _to_dev(torch, gw),
+        _to_dev(torch, PC.centred_monomial_integrals(lp.da)),
+        _to_dev(torch, PC.centred_monomial_integrals(lp.db))])
+
+
 def _m2_table(disc, lp: LogPart):
     torch = _torch()
 
@@ -448,9 +459,7 @@ def _m2_table(disc, lp: LogPart):
         n_gap = n if closed else 2 * n - 1
         gx, gw = _table_rules()
         m2 = torch.empty((n_gap, lp.da + 1, lp.db + 1), dtype=torch.float64, device="cuda")
-        keep = [_to_dev(torch, lp.near_unit), _to_dev(torch, gx), _to_dev(torch, gw),
-                _to_dev(torch, PC.centred_monomial_integrals(lp.da)),
-                _to_dev(torch, PC.centred_monomial_integrals(lp.db))]
+        keep = _table_consts(disc, lp)
         _lib.call("wq_pair_table", n, int(closed), lp.da, lp.db, lp.h, _lib.ptr(keep[0]),
                   _lib.ptr(keep[1]), _lib.ptr(keep[2]), len(gx), _lib.ptr(keep[3]),
                   _lib.ptr(keep[4]), _lib.ptr(m2), _lib.stream_handle())
@@ -649,9 +658,7 @@ def _gap_table(disc, lp: LogPart, h0: float):
     n = lp.n_el
     gx, gw = _table_rules()
     m2 = torch.empty((2 * n - 1, lp.da + 1, lp.db + 1), dtype=torch.float64, device="cuda")
-    keep = [_to_dev(torch, lp.near_unit), _to_dev(torch, gx), _to_dev(torch, gw),
-            _to_dev(torch, PC.centred_monomial_integrals(lp.da)),
-            _to_dev(torch, PC.centred_monomial_integrals(lp.db))]
+    keep = _table_consts(disc, lp)
     _lib.call("wq_pair_table", n, 0, lp.da, lp.db, h0, _lib.ptr(keep[0]), _lib.ptr(keep[1]),
               _lib.ptr(keep[2]), len(gx), _lib.ptr(keep[3]), _lib.ptr(keep[4]), _lib.ptr(m2),
               _lib.stream_handle())
@@ -1002,6 +1009,37 @@ def _assemble_into(disc: Discretization, X, scaled: bool = True):
     _ik2_x2_into(disc, X, accumulate=True)
     _lib.call("wq_symmetrize", _lib.ptr(X), X.shape[0], alpha, _lib.stream_handle())
     return X
+
+
+class AssemblyGraph:
+    """The whole device assembly of one discretization captured once as a CUDA
+    graph and replayed: one graph launch per assembly instead of ~15 kernel
+    launches plus the host-side work of ``_assemble_into`` -- the step is
+    launch/host-bound below N ~ 8k (C2: 0.34 ms eager for 0.06 ms of kernels).
+    ``X`` is the (N, N) device output, fixed at capture; replays are
+    bit-identical to eager assemblies.  The geometry flag is not checked by
+    ``replay`` (call ``check`` once after the first replay)."""
+
+    def __init__(self, disc: Discretization, X, scaled: bool = True):
+        torch = _torch()
+        self.disc, self.X = disc, X
+        _assemble_into(disc, X, scaled)          # uploads, tables, attributes: outside capture
+        torch.cuda.synchronize()
+        _check_flag(_smooth(disc))
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(self.graph, stream=side):
+                _assemble_into(disc, X, scaled)
+        torch.cuda.current_stream().wait_stream(side)
+
+    def replay(self):
+        self.graph.replay()
+        return self.X
+
+    def check(self):
+        _check_flag(_smooth(self.disc))
 
 
 def assemble_matrix_device(disc: Discretization, scaled: bool = True, out=None):
