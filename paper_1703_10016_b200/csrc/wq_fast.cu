@@ -647,15 +647,19 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
         const int ln = k & 31, s = (k >> 5) % (C::KS / 4), jb = (k >> 5) / (C::KS / 4);
         const int rr = ln >> 2, cc = ln & 3;
         const int t = 4 * s + cc - rr, row = 8 * jb + rr;
-        bv[u] = (k < NBF && t >= 0 && t <= 2 * C::D && row < nc) ? alpha * __ldg(sw + (C0 + row) * C::WS + t)
+        bv[u] = (k < NBF && t >= 0 && t <= 2 * C::D && row < nc) ? __ldg(sw + (C0 + row) * C::WS + t)
                                                                   : 0.0;
       }
-#pragma unroll
-      for (int u = 0; u < BPT; ++u)
-        if (tid + u * X2_THREADS < NBF) Bfr[tid + u * X2_THREADS] = bv[u];
+      // (stored after phi: only s_contract reads Bfr, so the loads' latency -- long for the
+      // orientation-0 S_J rows -- hides behind phi instead of delaying it)
       if (orient == 0 && with_ik1 && !tbulk) cp_async_wait_all();
       mbar_wait(bar, (unsigned)orient);
       __syncthreads();
+      x2_mark(1 + 3 * orient);
+      phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
+#pragma unroll
+      for (int u = 0; u < BPT; ++u)
+        if (tid + u * X2_THREADS < NBF) Bfr[tid + u * X2_THREADS] = alpha * bv[u];
     } else {
       constexpr int CH = C::ZSTRIDE / 2;  // 16-byte chunks per table row
       for (int k = tid; k < C::ZROWS * CH; k += X2_THREADS) {
@@ -678,9 +682,9 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
         Bfr[k] = (t >= 0 && t <= 2 * C::D) ? alpha * Ssm[(8 * jb + rr) * SROW + t] : 0.0;
       }
       __syncthreads();
+      x2_mark(1 + 3 * orient);
+      phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
     }
-    x2_mark(1 + 3 * orient);
-    phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
     // accumulator start: orientation 0 alpha w IK1(I,J) (lane: i = 8warp + r,
     // j = 8jb + 2c + e); orientation 1 T^T (lane: j = 8warp + r, i = 8ib + 2c + e)
     if (orient == 0) {
