@@ -300,7 +300,7 @@ def main():
         Xpad = torch.empty((n_pad, N), dtype=torch.float64, device="cuda")
         X = Xpad[:N]
         mine = sum(1 for c in range(chunks) if (c * world + rank) * sub < N)
-        per_step = 7 + 2 * mine + 1   # tables, (ik1_rows, x2_rows) per owned chunk, symmetrise
+        per_step = 7 + 2 * mine + 1   # tables, (ik1_pairs, x2_pairs_range) per owned chunk, mirror
 
     graph = None
     if world == 1 and (args.graph == "on" or (args.graph == "auto" and N <= 8192)):

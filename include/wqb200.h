@@ -397,6 +397,9 @@ int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
 
 /* out[j][i] = out[i][j] for i > j (n x n, leading dimension ld). */
 int wq_mirror_lower(double* out, int64_t n, int64_t ld, void* stream);
+/* out[c][r] = out[r][c] for c > r: the upper triangle copied onto the lower one (the
+ * symmetric multi-GPU path: each rank assembles the upper tile pairs of its rows). */
+int wq_mirror_upper(double* out, int64_t n, int64_t ld, void* stream);
 
 /* General-path row blocks (multi-GPU; X-form, assembly.py:233-245):
  * wq_gather_fs_rows: P[m][i - i0] = alpha P[m][i - i0] - sum_t F[m][s_i + t] S_i[t],

@@ -243,6 +243,23 @@ __global__ void mirror_lower_kernel(double* out, int64_t n, int64_t ld) {
   }
 }
 
+// out[c][r] = out[r][c] for c > r (copy the upper triangle onto the lower one)
+__global__ void mirror_upper_kernel(double* out, int64_t n, int64_t ld) {
+  __shared__ double t[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;   // source tile rows bi, cols bj (bj >= bi)
+  if (bj < bi) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = bi * 32 + y, c = bj * 32 + tx;
+    t[y][tx] = (r < n && c < n) ? out[r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = bj * 32 + y, c = bi * 32 + tx;   // destination (lower) entry (r, c) = src (c, r)
+    if (r < n && c < n && r > c) out[r * ld + c] = t[tx][y];
+  }
+}
+
 // Far moments of pairs (e in L, f in G), physical: thread per outer element,
 // tensor Gauss by separation tier (30 / 16 / 12 as wq_gen_pair_blocks).
 constexpr int GM_THREADS = 64;
@@ -346,6 +363,16 @@ int wq_mirror_lower(double* out, int64_t n, int64_t ld, void* stream) {
   dim3 mg(ceil_div(n, 32), ceil_div(n, 32));
   mirror_lower_kernel<<<mg, dim3(32, 8), 0, (cudaStream_t)stream>>>(out, n, ld);
   return check_launch("wq_mirror_lower");
+}
+
+int wq_mirror_upper(double* out, int64_t n, int64_t ld, void* stream) {
+  if (!out || n <= 0 || ld < n) {
+    set_error("wq_mirror_upper: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 mg(ceil_div(n, 32), ceil_div(n, 32));
+  mirror_upper_kernel<<<mg, dim3(32, 8), 0, (cudaStream_t)stream>>>(out, n, ld);
+  return check_launch("wq_mirror_upper");
 }
 
 int wq_gen_moments_far(int64_t n_el, int da1, int nb, int64_t n_g, const int64_t* glist,

@@ -108,11 +108,50 @@ def pipeline_rows(n, world, rank, chunks, compute, Xpad, group=None):
     return Xpad
 
 
+def upper_rows_device(disc, Xfull, row0: int, row1: int, zext=None):
+    """Closed uniform meshes: the upper-triangle tile pairs (I, J >= I) of the tile
+    rows covering [row0, row1), assembled straight into A (scaled and, inside each
+    pair, symmetric) in the full (>= N, N) buffer ``Xfull``: A(I, J) into rows I,
+    the mirror A(J, I) into rows J.  Half the arithmetic of the unsymmetrised row
+    block; rows J of other ranks are overwritten by their owners' data in the
+    all-gather, and ``wq_mirror_upper`` completes the lower triangle afterwards.
+    row0 must be a multiple of the 64-row tile; no communication."""
+    from . import assembly as AS
+    from . import _lib
+
+    T = _lib.WQ_FTILE
+    if row0 % T:
+        raise ValueError("row blocks must start on a 64-row tile boundary")
+    N = disc.space.dim
+    nb = -(-N // T)
+    start = lambda t: t * nb - t * (t - 1) // 2     # first upper-triangle pair of tile row t
+    a, b = start(row0 // T), start(-(-row1 // T))
+    lp, d = AS._logpart_dev(disc)
+    sm = AS._smooth(disc)
+    st = _lib.stream_handle()
+    Zext = AS._zext_table(disc) if zext is None else zext
+    _lib.call("wq_ik1_pairs", AS.ctypes_ref(sm["struct"]), a, b, _lib.ptr(Xfull), Xfull.stride(0),
+              _lib.ptr(sm["flag"]), st)
+    _lib.call("wq_x2_pairs_range", N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
+              lp.uext.shape[1], lp.zstride, _lib.ptr(d["uext"]), _lib.ptr(Zext), _lib.ptr(d["s_w"]),
+              -1.0 / (4.0 * np.pi), 2.0, a, b, _lib.ptr(Xfull), Xfull.stride(0), st)
+    return Xfull
+
+
 def assemble_distributed_pipelined(disc, Xpad, chunks: int = 8, group=None, zext=None):
     """A = -(X + X^T)/(4 pi) on every rank with the row-block compute of chunk
     c+1 overlapping the all-gather of chunk c (cyclic 64-aligned row blocks,
     in-place NCCL all-gather, no copies).  Xpad: (n_pad, N) CUDA tensor with
-    n_pad from ``cyclic_blocks(N, world, chunks)``; A is Xpad[:N]."""
+    n_pad from ``cyclic_blocks(N, world, chunks)``; A is Xpad[:N].
+
+    Closed uniform meshes exploit the symmetry: each rank assembles the upper
+    tile pairs of its blocks (``upper_rows_device``; cyclic dealing balances
+    the triangle), the all-gather returns every rank's rows, and a local
+    upper -> lower mirror completes A.  The mirrored tiles a rank writes into
+    other ranks' rows never overlap a gather in flight: they land in rows of
+    the current or later rounds, whose gathers are ordered after the compute
+    that wrote them.  Other meshes assemble unsymmetrised rows of X and
+    finish with A = -(X + X^T)/(4 pi)."""
     import torch.distributed as dist
     from . import assembly as AS
     from . import _lib
@@ -125,10 +164,16 @@ def assemble_distributed_pipelined(disc, Xpad, chunks: int = 8, group=None, zext
     F = None if v2 else AS.general_prepare(disc)   # replicated D / F, once per assembly
 
     def compute(r0, r1, view):
-        assemble_rows_device(disc, view, r0, r1, zext=Z, F=F)
+        if v2:
+            upper_rows_device(disc, Xpad, r0, r1, zext=Z)
+        else:
+            assemble_rows_device(disc, view, r0, r1, zext=Z, F=F)
 
     pipeline_rows(N, world, rank, chunks, compute, Xpad, group)
-    _lib.call("wq_symmetrize", _lib.ptr(Xpad), N, -1.0 / (4.0 * np.pi), _lib.stream_handle())
+    if v2:
+        _lib.call("wq_mirror_upper", _lib.ptr(Xpad), N, Xpad.stride(0), _lib.stream_handle())
+    else:
+        _lib.call("wq_symmetrize", _lib.ptr(Xpad), N, -1.0 / (4.0 * np.pi), _lib.stream_handle())
     return Xpad[:N]
 
 
