@@ -402,6 +402,22 @@ def _check_flag(sm):
 _IK1_BAND = True
 
 
+def _k1_vanishes(disc) -> bool:
+    """A straight segment traversed at unit parametric speed (degree-1 curve with
+    two control points |P1 - P0| = b - a, e.g. the slit of configs 1 and 5):
+    |f(s) - f(t)| = |s - t|, so K1 = 1/2 ln(|f(s) - f(t)|^2 / |s - t|^2) vanishes
+    identically and IK1 = 0 (geometry.py:225-248 evaluates it to rounding noise,
+    max|IK1| ~ 1e-18 of max|A| at config 1)."""
+    cb = disc.curve.basis
+    P = np.asarray(disc.curve.control_points, dtype=float)
+    if cb.degree != 1 or len(P) != 2 or disc.closed:
+        return False
+    return float(np.hypot(*(P[1] - P[0]))) == float(cb.b - cb.a)
+
+
+_K1_SHORTCUT = True   # IK1 = 0 on unit-speed straight segments (_k1_vanishes)
+
+
 def _ik1_into(disc, X, accumulate=False, row0=0, row1=None):
     """IK1 (all rows, or rows [row0, row1) x all columns with row0 on a
     64-row tile boundary) into X."""
@@ -409,6 +425,10 @@ def _ik1_into(disc, X, accumulate=False, row0=0, row1=None):
     sm = _smooth(disc)
     N = disc.space.dim
     row1 = N if row1 is None else row1
+    if _K1_SHORTCUT and _k1_vanishes(disc):
+        if not accumulate:
+            X[: row1 - row0].zero_()     # X points at row0, as for the kernels
+        return X
     T = _lib.WQ_FTILE
     if (_IK1_BAND and not accumulate and sm["span64"] <= 144 and 2 <= disc.rules.WG <= 16
             and row0 % T == 0 and (row1 == N or row1 % T == 0)):
