@@ -21,6 +21,7 @@
 // 459-468) -- far pairs use log|L/pi sin(pi r / L)|, its exact sum with log|r|.
 // Every output is a fixed-order sum (deterministic; no atomics).
 #include "wq_common.cuh"
+#include "wq_log.cuh"
 
 namespace wq {
 
@@ -244,11 +245,13 @@ pair_far_kernel(GenArgs A, int64_t ntiles, int nbx) {
   __shared__ double Vt[GTSUM][NP];   // h_f w_h V_f(h_f x_h)
   __shared__ double Yt[GTSUM];       // h_f x_h
   __shared__ double Gx[GTSUM], Gw[GTSUM];
+  __shared__ double2 lntab[64];      // accurate-table ln (wq_log.cuh), open meshes
   const int nA = A.da + 1;
   for (int g = threadIdx.x; g < GTSUM; g += FP_THREADS) {
     Gx[g] = A.gx[g];
     Gw[g] = A.gw[g];
   }
+  for (int k = threadIdx.x; k < 128; k += FP_THREADS) reinterpret_cast<double*>(lntab)[k] = kTang64[k];
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     if (A.m2u && !A.tile_flag[tile]) continue;
     __syncthreads();   // previous tile's tables are dead; Gx/Gw visible
@@ -310,7 +313,9 @@ pair_far_kernel(GenArgs A, int64_t ntiles, int nbx) {
         for (int b = 0; b < NP; ++b) t[b] = 0.0;
         for (int h = 0; h < ng; ++h) {
           const double r = Yt[t0 + h] + base;
-          const double k = closed ? log(fabs(sinpi(r * invL))) + lnLpi : log(fabs(r));
+          // ln |r| by the accurate table (~1 ulp, a third of libdevice's FP64 work); r != 0 for
+          // the separated pairs this kernel takes
+          const double k = closed ? log(fabs(sinpi(r * invL))) + lnLpi : 2.0 * half_ln64t(fabs(r), lntab);
 #pragma unroll
           for (int b = 0; b < NP; ++b) t[b] = fma(Vt[t0 + h][b], k, t[b]);
         }

@@ -16,6 +16,7 @@
 // One CTA = TR row functions x TC column functions; the table rows it needs,
 // the rows' scaled coefficients and Y live in shared memory.  Deterministic.
 #include "wq_common.cuh"
+#include "wq_log.cuh"
 
 namespace wq {
 
@@ -270,6 +271,9 @@ gen_moments_far_kernel(int64_t n_el, int da1, int nb, const int64_t* glist, cons
                        const int64_t* near_cnt, const double* gx, const double* gw,
                        double* mgc) {
   extern __shared__ double sh[];
+  __shared__ double2 lntab[64];                   // accurate-table ln (wq_log.cuh)
+  for (int q = threadIdx.x; q < 128; q += GM_THREADS) reinterpret_cast<double*>(lntab)[q] = kTang64[q];
+  __syncthreads();
   const int j = blockIdx.y;                       // index in G
   const int64_t f = glist[j];
   const int64_t e = (int64_t)blockIdx.x * GM_THREADS + threadIdx.x;
@@ -291,7 +295,7 @@ gen_moments_far_kernel(int64_t n_el, int da1, int nb, const int64_t* glist, cons
     for (int b = 0; b < nb; ++b) t[b] = 0.0;
     for (int h = 0; h < ng; ++h) {
       const double y = hf * gx[t0 + h], wy = hf * gw[t0 + h];
-      const double kv = log(fabs(y - x - delta));
+      const double kv = 2.0 * half_ln64t(fabs(y - x - delta), lntab);   // separated: y - x - delta != 0
       double w = wy * kv;
       for (int b = 0; b < nb; ++b) {
         t[b] += w;
