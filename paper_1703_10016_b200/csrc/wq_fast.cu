@@ -630,14 +630,6 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
         if (first < C::ZROWS)
           bulk_g2s_hint(Zsm + first * C::ZSTRIDE, Zext, (unsigned)(C::ZROWS - first) * RB, bar, pol);
       }
-      if (orient == 0 && tbulk && tid < 32) {
-        // own barrier: the tile is first needed after phi0, so its HBM latency hides behind it
-        if (tid == 0) mbar_arrive_expect_tx(bar + 1, FT * FT * 8);
-        __syncwarp();
-        const uint64_t pol = l2_evict_first();   // the IK1 tile is read once
-        for (int a = tid; a < FT; a += 32)
-          bulk_g2s_hint(Tst + a * T2STRIDE, src + a * ldx, FT * 8, bar + 1, pol);
-      }
       // alpha S band in B-fragment order, Bfr[jb][s][lane] = alpha S_{8jb+r}[4s+c-r],
       // straight from global memory while the copies fly
       double bv[BPT];
@@ -654,6 +646,15 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
       // orientation-0 S_J rows -- hides behind phi instead of delaying it)
       if (orient == 0 && with_ik1 && !tbulk) cp_async_wait_all();
       mbar_wait(bar, (unsigned)orient);
+      if (orient == 0 && tbulk && tid < 32) {
+        // own barrier, requested once the window is in: the tile is first needed after
+        // phi0, so its HBM latency hides behind phi0 without delaying the window
+        if (tid == 0) mbar_arrive_expect_tx(bar + 1, FT * FT * 8);
+        __syncwarp();
+        const uint64_t pol = l2_evict_first();   // the IK1 tile is read once
+        for (int a = tid; a < FT; a += 32)
+          bulk_g2s_hint(Tst + a * T2STRIDE, src + a * ldx, FT * 8, bar + 1, pol);
+      }
       __syncthreads();
       x2_mark(1 + 3 * orient);
       phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
