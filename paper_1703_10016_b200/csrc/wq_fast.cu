@@ -169,7 +169,8 @@ __device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int64_t pai
 // instruction throughput (ncu: L1/TEX 89.7 %, FP64 pipe 47.6 %), and a first
 // rework by instruction issue (~50 issued instructions per kernel value, half
 // of them integer).  Here:
-//  * each thread owns TWO outer nodes q and q + QH of one column half, so
+//  * each thread owns TWO outer nodes q and q + 64 of one column half (the fifth
+//    warp one leftover node per lane), so
 //    every r-node load ({x, y} as one 16-byte load) and every rule-weight load
 //    (16-byte loads of a padded row) serves both;
 //  * the ln uses a 64-bin accurate table (one 16-byte load, degree-7 series,
@@ -237,16 +238,16 @@ __device__ __forceinline__ double k1_fast(double qx, double qy, double2 rxy, dou
 
 // phase 1 of a tile for the thread's outer nodes A, B and column half jb..jb+HJ-1.
 // FAST: SGN = +1 if every q node index exceeds every r node index, -1 if below.
-template <int P, int MODE, bool FAST, int SGN, int UNR>
+// TWO = false: outer node A only (the leftover nodes of the fifth warp, half the work).
+template <int P, int MODE, bool FAST, int SGN, int UNR, bool TWO>
 __device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const double* rsv,
                                            const double* G, const double2* tab,
-                                           const wq_smooth_t& sm, int64_t q0, int64_t r0, int u,
-                                           int h, int& bad) {
+                                           const wq_smooth_t& sm, int64_t q0, int64_t r0, int qA,
+                                           int qB, int h, int& bad) {
   using C = Ik4Cfg<P, MODE>;
-  constexpr int WG = C::WG, NQ = C::NQ, NQP = C::NQP, QH = C::QH, HJ = C::HJ, GW = C::GW;
+  constexpr int WG = C::WG, NQP = C::NQP, HJ = C::HJ, GW = C::GW;
   const int64_t nq = sm.nq;
-  const int qA = u, qB = u + QH < NQ ? u + QH : NQ - 1;
-  const bool hasB = u + QH < NQ;
+  constexpr bool hasB = TWO;
   const int64_t gA = (q0 + qA) % nq, gB = (q0 + qB) % nq;
   const double xA = sm.fx[gA], yA = sm.fy[gA];
   const double xB = sm.fx[gB], yB = sm.fy[gB];
@@ -268,23 +269,25 @@ __device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const
     const double2 p = rxy[r];
     if (FAST) {
       vA = k1_fast(xA, yA, p, ipa, hmin, hmax, tab);
-      vB = k1_fast(xB, yB, p, ipb, hmin, hmax, tab);
+      if (TWO) vB = k1_fast(xB, yB, p, ipb, hmin, hmax, tab);
     } else {
       const double rs = MODE != WQ_K1_TABLE ? rsv[r] : 0.0;
       vA = k1_gen<MODE>(xA, yA, J2A, sA, qaA, p, rs, ra, sm.invp2, sm.period, tab, bad);
-      vB = k1_gen<MODE>(xB, yB, J2B, sB, qaB, p, rs, ra, sm.invp2, sm.period, tab, bad);
+      if (TWO) vB = k1_gen<MODE>(xB, yB, J2B, sB, qaB, p, rs, ra, sm.invp2, sm.period, tab, bad);
       if (++ra == nqi) ra = 0;
     }
   };
 #pragma unroll
   for (int w = 0; w < WG - 2; ++w)
     eval(2 * jb + w, w, wA[w], wB[w], FAST ? __ldg(pA - SGN * w) : 0.0,
-         FAST ? __ldg(pB - SGN * w) : 0.0);
+         (FAST && TWO) ? __ldg(pB - SGN * w) : 0.0);
   if (FAST) {
     ipA0 = __ldg(pA - SGN * (WG - 2));
     ipA1 = __ldg(pA - SGN * (WG - 1));
-    ipB0 = __ldg(pB - SGN * (WG - 2));
-    ipB1 = __ldg(pB - SGN * (WG - 1));
+    if (TWO) {
+      ipB0 = __ldg(pB - SGN * (WG - 2));
+      ipB1 = __ldg(pB - SGN * (WG - 1));
+    }
   }
 #pragma unroll UNR
   for (int jj = 0; jj < HJ; ++jj) {
@@ -295,8 +298,10 @@ __device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const
       const int rn = 2 * (jj + 1) + WG - 2;
       ipA0 = __ldg(pA - SGN * rn);
       ipA1 = __ldg(pA - SGN * (rn + 1));
-      ipB0 = __ldg(pB - SGN * rn);
-      ipB1 = __ldg(pB - SGN * (rn + 1));
+      if (TWO) {
+        ipB0 = __ldg(pB - SGN * rn);
+        ipB1 = __ldg(pB - SGN * (rn + 1));
+      }
     }
     eval(r, 2 * jj + WG - 2, wA[WG - 2], wB[WG - 2], a0, b0);
     eval(r + 1, 2 * jj + WG - 1, wA[WG - 1], wB[WG - 1], a1, b1);
@@ -357,17 +362,26 @@ __device__ __forceinline__ void ik1_tile_v5(const wq_smooth_t& sm, int bi, int b
   for (int k = tid; k < 128; k += blockDim.x) reinterpret_cast<double*>(tab)[k] = kTang64[k];
   __syncthreads();
 
-  // ---- phase 1 ----
-  if (tid < 2 * QH) {
-    const int h = tid >= QH ? 1 : 0;
-    const int u = tid - h * QH;
+  // ---- phase 1: warps 0-3 take outer-node pairs (u, u + 64) of column half h = warp / 2;
+  // warp 4 the NQ - 128 leftover nodes, one per lane and half (half the work per lane) ----
+  {
+    constexpr int NL = NQ - 128;
+    static_assert(NL > 0 && 2 * NL <= 32 && IK4_THREADS == 160, "ik1 v5: phase-1 mapping");
+    const int warp = tid >> 5, lane = tid & 31;
     const bool nowrap = q0 + NQ <= nq && r0 + NQ <= nq;
-    if (MODE == WQ_K1_TABLE && nowrap && q0 >= r0 + NQ)
-      ik1_phase1<P, MODE, true, 1, UNR>(T1, rxy, rsv, G, tab, sm, q0, r0, u, h, bad);
-    else if (MODE == WQ_K1_TABLE && nowrap && r0 >= q0 + NQ)
-      ik1_phase1<P, MODE, true, -1, UNR>(T1, rxy, rsv, G, tab, sm, q0, r0, u, h, bad);
-    else
-      ik1_phase1<P, MODE, false, 1, UNR>(T1, rxy, rsv, G, tab, sm, q0, r0, u, h, bad);
+    const bool fp = MODE == WQ_K1_TABLE && nowrap && q0 >= r0 + NQ;
+    const bool fm = MODE == WQ_K1_TABLE && nowrap && r0 >= q0 + NQ;
+    if (warp < 4) {
+      const int h = warp >> 1, u = tid & 63;
+      if (fp) ik1_phase1<P, MODE, true, 1, UNR, true>(T1, rxy, rsv, G, tab, sm, q0, r0, u, u + 64, h, bad);
+      else if (fm) ik1_phase1<P, MODE, true, -1, UNR, true>(T1, rxy, rsv, G, tab, sm, q0, r0, u, u + 64, h, bad);
+      else ik1_phase1<P, MODE, false, 1, UNR, true>(T1, rxy, rsv, G, tab, sm, q0, r0, u, u + 64, h, bad);
+    } else if (lane < 2 * NL) {
+      const int h = lane / NL, q = 128 + lane % NL;
+      if (fp) ik1_phase1<P, MODE, true, 1, UNR, false>(T1, rxy, rsv, G, tab, sm, q0, r0, q, q, h, bad);
+      else if (fm) ik1_phase1<P, MODE, true, -1, UNR, false>(T1, rxy, rsv, G, tab, sm, q0, r0, q, q, h, bad);
+      else ik1_phase1<P, MODE, false, 1, UNR, false>(T1, rxy, rsv, G, tab, sm, q0, r0, q, q, h, bad);
+    }
   }
   __syncthreads();
   for (int k = tid; k < FT * GW; k += blockDim.x) {
