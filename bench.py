@@ -403,7 +403,7 @@ def main():
     # ---- end to end through the public API with host buffers (N = 1 layout) ----
     e2e = None
     if world == 1 and args.e2e_steps > 0:
-        host = torch.empty((N, N), dtype=torch.float64, pin_memory=True)
+        host = AS.pinned_host_matrix(N)   # pages on the GPU's NUMA node
         sm = AS._smooth(disc)
         lp, dd = AS._logpart_dev(disc)
         inputs = [v for v in list(sm.values()) + list(dd.values())

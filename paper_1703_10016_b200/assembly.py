@@ -1072,6 +1072,50 @@ def assemble_matrix_device(disc: Discretization, scaled: bool = True, out=None):
     return X
 
 
+def _gpu_local_cpus(torch):
+    """CPUs on the NUMA node of the current GPU's PCIe root (sysfs local_cpulist), or
+    None when unknown."""
+    try:
+        pr = torch.cuda.get_device_properties(torch.cuda.current_device())
+        bdf = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/local_cpulist") as f:
+            spec = f.read().strip()
+    except (OSError, AttributeError, RuntimeError):
+        return None
+    cpus = set()
+    for part in spec.split(","):
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.update(range(int(a), int(b) + 1))
+        elif part:
+            cpus.add(int(part))
+    return cpus or None
+
+
+def pinned_host_matrix(n: int, m: int = None):
+    """(n, m) float64 pinned host tensor whose pages sit on the GPU's NUMA node: the
+    allocating (pinning) thread is moved onto the GPU-local CPUs for the call, so the
+    device-to-host stream of the streamed host path does not cross the socket
+    interconnect on multi-socket hosts (a no-op where every CPU is GPU-local)."""
+    import os
+    torch = _torch()
+    m = n if m is None else m
+    local = _gpu_local_cpus(torch)
+    old = None
+    if local and hasattr(os, "sched_setaffinity"):
+        try:
+            old = os.sched_getaffinity(0)
+            use = local & old or local
+            os.sched_setaffinity(0, use)
+        except OSError:
+            old = None
+    try:
+        return torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+
+
 def _copy_stream(torch):
     if not hasattr(_copy_stream, "s"):
         _copy_stream.s = torch.cuda.Stream()
@@ -1090,7 +1134,7 @@ def assemble_matrix_to_host(disc: Discretization, out=None, scaled: bool = True,
     torch = _torch()
     N = disc.space.dim
     if out is None:
-        out = torch.empty((N, N), dtype=torch.float64, pin_memory=True)
+        out = pinned_host_matrix(N)
     X = work if work is not None else _dev(disc, "host_stage", lambda: _new_square(disc))
     if not _use_v2(disc) or chunks <= 1:
         _assemble_into(disc, X, scaled)
