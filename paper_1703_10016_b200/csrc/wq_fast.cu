@@ -383,11 +383,19 @@ __device__ __forceinline__ void ik1_tile_v5(const wq_smooth_t& sm, int bi, int b
       else ik1_phase1<P, MODE, false, 1, UNR, false>(T1, rxy, rsv, G, tab, sm, q0, r0, q, q, h, bad);
     }
   }
-  __syncthreads();
-  for (int k = tid; k < FT * GW; k += blockDim.x) {
-    const int ii = k / GW, w = k - ii * GW;
-    G[k] = (ii < ni && w < WG) ? sm.g_w[(I0 + ii) * WG + w] : 0.0;
+  // G_I is loaded before the barrier (its latency overlaps the wait for the slowest
+  // phase-1 warp) and stored into the G region after it
+  constexpr int GPT = (FT * GW + IK4_THREADS - 1) / IK4_THREADS;
+  double gv[GPT];
+#pragma unroll
+  for (int u = 0; u < GPT; ++u) {
+    const int k = tid + u * IK4_THREADS, ii = k / GW, w = k - ii * GW;
+    gv[u] = (k < FT * GW && ii < ni && w < WG) ? __ldg(sm.g_w + (I0 + ii) * WG + w) : 0.0;
   }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < GPT; ++u)
+    if (tid + u * IK4_THREADS < FT * GW) G[tid + u * IK4_THREADS] = gv[u];
   __syncthreads();
 
   // ---- phase 2: item (j, half c): IK1[i][j], i in 32c .. 32c+31 ----
