@@ -14,7 +14,7 @@ import os
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwqb200.so")
+LIB_PATH = os.environ.get("WQB200_LIB") or os.path.join(_HERE, "libwqb200.so")  # override: A/B tools only
 
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int

@@ -550,7 +550,7 @@ __device__ __forceinline__ void s_contract_acc(const double* Phs, const double* 
   }
 }
 
-constexpr int T2STRIDE = 68;  // orientation hand-off tile (== 4 mod 16: conflict-free fragment reads)
+constexpr int T2STRIDE = 66;  // orientation hand-off tile (== 2 mod 16: conflict-free transposed reads)
 
 template <int P>
 struct X2Smem {
@@ -755,18 +755,19 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
   const bool sbulk = zbulk && bi != bj && ni == FT && nj == FT && (ldx & 1) == 0 &&
                      (reinterpret_cast<uintptr_t>(X) & 15) == 0;
   if (sbulk) {
-    // both output tiles staged row-contiguous (16-byte aligned rows, stride 66) in the
-    // Phs | Tst region, then 128 row copies shared -> global on the TMA engine
-    constexpr int OS = 66;
-    double* Oji = Phs;            // A(J,I)[j][i]
-    double* Oij = Phs + FT * OS;  // A(I,J)[i][j] = A(J,I)[j][i]
-    static_assert(2 * FT * OS <= FT * PSTRIDE + FT * T2STRIDE, "output staging overflows");
+    // both output tiles staged row-contiguous (16-byte aligned rows) in the Phs | Tst
+    // region, then 128 row copies shared -> global on the TMA engine.  Strides: 72 (== 8
+    // mod 16) for the 16-byte row-fragment stores, 66 (== 2 mod 16) for the transposed ones
+    constexpr int OSA = 72, OSB = 66;
+    double* Oji = Phs;             // A(J,I)[j][i]
+    double* Oij = Phs + FT * OSA;  // A(I,J)[i][j] = A(J,I)[j][i]
+    static_assert(FT * (OSA + OSB) <= FT * PSTRIDE + FT * T2STRIDE, "output staging overflows");
 #pragma unroll
     for (int ib = 0; ib < 8; ++ib) {
-      *reinterpret_cast<double2*>(Oji + (8 * warp + r) * OS + 8 * ib + 2 * c) =
+      *reinterpret_cast<double2*>(Oji + (8 * warp + r) * OSA + 8 * ib + 2 * c) =
           make_double2(acc[ib][0], acc[ib][1]);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) Oij[(8 * ib + 2 * c + e) * OS + 8 * warp + r] = acc[ib][e];
+      for (int e = 0; e < 2; ++e) Oij[(8 * ib + 2 * c + e) * OSB + 8 * warp + r] = acc[ib][e];
     }
     fence_proxy_async();
     __syncthreads();
@@ -774,7 +775,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
       const int a = tid & (FT - 1);
       const bool ji = tid < FT;
       double* dst = ji ? X + (J0 + a) * ldx + I0 : X + (I0 + a) * ldx + J0;
-      const double* srcs = (ji ? Oji : Oij) + a * OS;
+      const double* srcs = ji ? Oji + a * OSA : Oij + a * OSB;
       bulk_s2g_hint(dst, srcs, FT * 8, l2_evict_first());   // A is written once
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");

@@ -139,9 +139,13 @@ static __device__ const double kTang64[128] = {
     0.5020620226860046, 0.3445158078774424};
 
 // series and ln 2 constants as constant-bank operands (no per-use register
-// materialisation in the unrolled IK1 loops)
-static __constant__ double kLn64C[8] = {-0.5 / 7.0, 0.5 / 6.0, -0.5 / 5.0, 0.5 / 4.0,
-                                        -0.5 / 3.0, 0.25, HLN2_A, HLN2_B};
+// materialisation in the unrolled IK1 loops).  q(r) = (r/2 - ln(1+r)/2) / r^2 to degree 4:
+// the Taylor coefficients 1/4, -1/6, 1/8, -1/10, 1/12 with the r^5 term -r^5/14
+// Chebyshev-economised onto r^3 and r on |r| <= a = 0.0077945 (the table's largest |r|):
+// r^5 ~ (20 a^2 r^3 - 5 a^4 r) / 16.  Truncation error of 0.5 ln(1+r): <= 8.7e-18
+// absolute (`python tools/tang_table.py 64 series`), one DFMA less per ln.
+static __constant__ double kLn64C[7] = {0.08333333333333333, -0.10000542448484374, 0.125,
+                                        -0.16666666658427656, 0.25, HLN2_A, HLN2_B};
 
 __device__ __forceinline__ double half_ln64t(double x, const double2* __restrict__ tab) {
   const int hi = __double2hiint(x);
@@ -153,12 +157,11 @@ __device__ __forceinline__ double half_ln64t(double x, const double2* __restrict
   q = fma(r, q, kLn64C[2]);
   q = fma(r, q, kLn64C[3]);
   q = fma(r, q, kLn64C[4]);
-  q = fma(r, q, kLn64C[5]);
   // 0.5 ln(1+r) = 0.5 r - r^2 q
   const double r2 = r * r;
   const double de = (double)((hi >> 20) - 1023);  // I2F: the conversion pipe is idle here
-  const double t_hi = fma(de, kLn64C[6], t.y);
-  return t_hi + fma(r, 0.5, fma(-r2, q, de * kLn64C[7]));
+  const double t_hi = fma(de, kLn64C[5], t.y);
+  return t_hi + fma(r, 0.5, fma(-r2, q, de * kLn64C[6]));
 }
 
 // device address of the 16-entry table (wq_fast.cu; uploads it on first use)

@@ -35,3 +35,27 @@ for j in range(B):
     rows.append((c, h, res, rmax))
     print(f"    {c!r}, {h!r},  // {j} resid {res:.1e} ulp |r| <= {rmax:.5f}")
 print("max |r|", max(r[3] for r in rows))
+
+
+def economised_series(a=0.0077945, n=4000):
+    """Degree-4 q(r) of half_ln64t (kLn64C): Taylor to r^4 plus the r^5 term
+    -r^5/14 Chebyshev-economised on |r| <= a; prints the coefficients and the
+    largest absolute error of 0.5 ln(1+r) = r/2 - r^2 q(r) (mpmath, 40 digits)."""
+    import mpmath as mp
+    mp.mp.dps = 40
+    a = mp.mpf(a)
+    c = [mp.mpf(1) / 12, -mp.mpf(1) / 10 - 20 * a ** 2 / 224, mp.mpf(1) / 8,
+         -mp.mpf(1) / 6 + 5 * a ** 4 / 224, mp.mpf(1) / 4]
+    cd = [float(x) for x in c]
+    worst = 0
+    for i in range(-n, n + 1):
+        r = a * i / n
+        q = cd[0]
+        for k in cd[1:]:
+            q = r * q + k
+        worst = max(worst, abs(mp.log(1 + r) / 2 - (r / 2 - r * r * q)))
+    print("kLn64C series:", [repr(x) for x in cd], "max abs error", float(worst))
+
+
+if len(sys.argv) > 2 and sys.argv[2] == "series":
+    economised_series()
