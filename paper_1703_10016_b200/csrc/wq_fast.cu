@@ -225,14 +225,13 @@ __device__ __forceinline__ double k1_gen(double qx, double qy, double qJ2, doubl
   return half_ln64t(R, tab);
 }
 
-// fast path: 1/p^2 at a known address, R's high word folded into min/max
-__device__ __forceinline__ double k1_fast(double qx, double qy, double2 rxy, double ip, int& hmin,
-                                          int& hmax, const double2* tab) {
+// fast path: 1/p^2 at a known address; R's high word less that of DBL_MIN folded into
+// one unsigned max (zero, subnormal, negative, inf and NaN all land >= 0x7fe00000)
+__device__ __forceinline__ double k1_fast(double qx, double qy, double2 rxy, double ip,
+                                          unsigned& hmx, const double2* tab) {
   const double dx = qx - rxy.x, dy = qy - rxy.y;
   const double R = fma(dx, dx, dy * dy) * ip;
-  const int h = __double2hiint(R);
-  hmin = min(hmin, h);
-  hmax = max(hmax, h);
+  hmx = max(hmx, (unsigned)__double2hiint(R) - 0x00100000u);
   return half_ln64t(R, tab);
 }
 
@@ -262,14 +261,14 @@ __device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const
   // fast-path state: ip(q, r) = invp2[SGN (q0 - r0 + q - r)] = pA[-SGN r'] with r' = r - 2 jb
   const double* __restrict__ pA = sm.invp2 + SGN * (q0 - r0 + qA - 2 * jb);
   const double* __restrict__ pB = sm.invp2 + SGN * (q0 - r0 + qB - 2 * jb);
-  int hmin = 0x7fffffff, hmax = (int)0x80000000;
+  unsigned hmx = 0u;
   // fast path: 1/p^2 of the next column's two new r nodes is loaded one column ahead
   double ipA0 = 0.0, ipA1 = 0.0, ipB0 = 0.0, ipB1 = 0.0;
   auto eval = [&](int r, int rr, double& vA, double& vB, double ipa, double ipb) {
     const double2 p = rxy[r];
     if (FAST) {
-      vA = k1_fast(xA, yA, p, ipa, hmin, hmax, tab);
-      if (TWO) vB = k1_fast(xB, yB, p, ipb, hmin, hmax, tab);
+      vA = k1_fast(xA, yA, p, ipa, hmx, tab);
+      if (TWO) vB = k1_fast(xB, yB, p, ipb, hmx, tab);
     } else {
       const double rs = MODE != WQ_K1_TABLE ? rsv[r] : 0.0;
       vA = k1_gen<MODE>(xA, yA, J2A, sA, qaA, p, rs, ra, sm.invp2, sm.period, tab, bad);
@@ -327,7 +326,7 @@ __device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const
       wB[w] = wB[w + 2];
     }
   }
-  if (FAST) bad |= (hmin < 0x00100000) | (hmax >= 0x7ff00000);
+  if (FAST) bad |= hmx >= 0x7fe00000u;
 }
 
 template <int P, int MODE, int UNR>
