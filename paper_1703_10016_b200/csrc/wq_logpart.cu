@@ -389,52 +389,101 @@ __global__ void transpose_kernel(const double* in, int64_t rows, int64_t cols, d
 }
 
 // P[m][i] = alpha P[m][i] - sum_t F[m][(s_i + t) mod nf] S_i[t]; each CTA keeps
-// the S band of its 128 columns i in registers and sweeps GF_ROWS rows m
+// the S band of its 128 columns i in registers and sweeps GF_ROWS rows m, GF_B rows
+// per batch with every load of the batch issued before its FMAs (the per-row loop
+// was DRAM-latency bound: one P load in flight per thread)
 constexpr int GF_ROWS = 32;
 constexpr int GF_MAXWS = 16;
-__global__ void gather_fs_kernel(wq_logpart_t lp, double alpha, const double* F, double* P) {
+constexpr int GF_B = 4;
+template <int WS>
+__global__ void __launch_bounds__(128) gather_fs_kernel(wq_logpart_t lp, double alpha,
+                                                        const double* F, double* P) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t m0 = (int64_t)blockIdx.y * GF_ROWS;
   if (i >= lp.n_rows) return;
-  const int64_t nf = lp.n_fine;
-  double sw[GF_MAXWS];
-  int64_t col[GF_MAXWS];
+  const int64_t nf = lp.n_fine, nr = lp.n_rows;
+  double sw[WS];
+  int col[WS];
 #pragma unroll
-  for (int t = 0; t < GF_MAXWS; ++t) {
-    sw[t] = t < lp.ws ? lp.s_w[i * lp.ws + t] : 0.0;
-    col[t] = t < lp.ws ? pmod(lp.s_start[i] + t, nf) : 0;
+  for (int t = 0; t < WS; ++t) {
+    sw[t] = lp.s_w[i * WS + t];
+    col[t] = (int)pmod(lp.s_start[i] + t, nf);
   }
   const int64_t m1 = m0 + GF_ROWS < nf ? m0 + GF_ROWS : nf;
-  for (int64_t m = m0; m < m1; ++m) {
-    double acc = alpha * P[m * lp.n_rows + i];
-    const double* fr = F + m * nf;
+  for (int64_t m = m0; m < m1; m += GF_B) {
+    double acc[GF_B], fv[GF_B][WS];
 #pragma unroll
-    for (int t = 0; t < GF_MAXWS; ++t)
-      if (t < lp.ws && sw[t] != 0.0) acc = fma(-fr[col[t]], sw[t], acc);
-    P[m * lp.n_rows + i] = acc;
+    for (int u = 0; u < GF_B; ++u) {
+      const int64_t mm = m + u < m1 ? m + u : m1 - 1;   // clamped (duplicate, not stored)
+      acc[u] = P[mm * nr + i];
+      const double* fr = F + mm * nf;
+#pragma unroll
+      for (int t = 0; t < WS; ++t) fv[u][t] = __ldg(fr + col[t]);
+    }
+#pragma unroll
+    for (int u = 0; u < GF_B; ++u) {
+      double a = alpha * acc[u];
+#pragma unroll
+      for (int t = 0; t < WS; ++t) a = fma(-fv[u][t], sw[t], a);
+      if (m + u < m1) P[(m + u) * nr + i] = a;
+    }
   }
 }
 
 // X[j][i] (+)= sum_t S_j[t] Phi[(s_j + t) mod nf][i]; each CTA sweeps ST_ROWS
-// consecutive j, whose Phi rows overlap (L1 reuse)
+// consecutive j (their Phi rows overlap: L1 reuse), ST_B rows j per batch with the
+// batch's loads issued before its FMAs
 constexpr int ST_ROWS = 16;
-__global__ void add_st_phi_kernel(wq_logpart_t lp, const double* Phi, int64_t row0, int64_t row1,
-                                  double* X, int64_t ldx, int accumulate) {
+constexpr int ST_B = 4;
+template <int WS>
+__global__ void __launch_bounds__(128) add_st_phi_kernel(wq_logpart_t lp, const double* Phi,
+                                                         int64_t row0, int64_t row1, double* X,
+                                                         int64_t ldx, int accumulate) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t j0 = row0 + (int64_t)blockIdx.y * ST_ROWS;
   if (i >= lp.n_rows) return;
+  const int64_t nf = lp.n_fine, nr = lp.n_rows;
   const int64_t j1 = j0 + ST_ROWS < row1 ? j0 + ST_ROWS : row1;
-  for (int64_t j = j0; j < j1; ++j) {
-    double acc = 0.0;
-    const int64_t sj = pmod(lp.s_start[j], lp.n_fine);   // unwrapped start -> [0, nf)
-    for (int t = 0; t < lp.ws; ++t) {
-      const double s = lp.s_w[j * lp.ws + t];
-      if (s != 0.0) acc = fma(s, Phi[wrap1(sj + t, lp.n_fine) * lp.n_rows + i], acc);
+  for (int64_t j = j0; j < j1; j += ST_B) {
+    double pv[ST_B][WS], xv[ST_B];
+#pragma unroll
+    for (int u = 0; u < ST_B; ++u) {
+      const int64_t jj = j + u < j1 ? j + u : j1 - 1;
+      const int64_t sj = pmod(lp.s_start[jj], nf);   // unwrapped start -> [0, nf)
+#pragma unroll
+      for (int t = 0; t < WS; ++t) pv[u][t] = __ldg(Phi + wrap1(sj + t, nf) * nr + i);
+      xv[u] = accumulate ? X[(jj - row0) * ldx + i] : 0.0;
     }
-    double* dst = X + (j - row0) * ldx + i;
-    *dst = accumulate ? *dst + acc : acc;
+#pragma unroll
+    for (int u = 0; u < ST_B; ++u) {
+      const int64_t jj = j + u < j1 ? j + u : j1 - 1;
+      double acc = 0.0;
+#pragma unroll
+      for (int t = 0; t < WS; ++t) acc = fma(lp.s_w[jj * WS + t], pv[u][t], acc);
+      if (j + u < j1) X[(j + u - row0) * ldx + i] = xv[u] + acc;
+    }
   }
 }
+
+#define WQ_WS_SWITCH(ws, CALL) \
+  switch (ws) {                \
+    case 1: CALL(1); break;    \
+    case 2: CALL(2); break;    \
+    case 3: CALL(3); break;    \
+    case 4: CALL(4); break;    \
+    case 5: CALL(5); break;    \
+    case 6: CALL(6); break;    \
+    case 7: CALL(7); break;    \
+    case 8: CALL(8); break;    \
+    case 9: CALL(9); break;    \
+    case 10: CALL(10); break;  \
+    case 11: CALL(11); break;  \
+    case 12: CALL(12); break;  \
+    case 13: CALL(13); break;  \
+    case 14: CALL(14); break;  \
+    case 15: CALL(15); break;  \
+    case 16: CALL(16); break;  \
+  }
 
 }  // namespace wq
 
@@ -556,12 +605,14 @@ int wq_gather_fs(const wq_logpart_t* lp, double alpha, const double* F, double* 
     set_error("wq_gather_fs: bad arguments");
     return WQ_EINVAL;
   }
-  if (lp->ws > GF_MAXWS) {
-    set_error("wq_gather_fs: S band wider than %d", GF_MAXWS);
+  if (lp->ws > GF_MAXWS || lp->ws < 1) {
+    set_error("wq_gather_fs: S band width %lld outside [1, %d]", (long long)lp->ws, GF_MAXWS);
     return WQ_EUNSUPPORTED;
   }
   dim3 grid(ceil_div(lp->n_rows, 128), ceil_div(lp->n_fine, GF_ROWS));
-  gather_fs_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, alpha, F, P);
+#define WQ_GF(W) gather_fs_kernel<W><<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, alpha, F, P)
+  WQ_WS_SWITCH(lp->ws, WQ_GF)
+#undef WQ_GF
   return check_launch("wq_gather_fs");
 }
 
@@ -571,9 +622,16 @@ int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64
     set_error("wq_add_st_phi: bad arguments");
     return WQ_EINVAL;
   }
+  if (lp->ws > GF_MAXWS || lp->ws < 1) {
+    set_error("wq_add_st_phi: S band width %lld outside [1, %d]", (long long)lp->ws, GF_MAXWS);
+    return WQ_EUNSUPPORTED;
+  }
   dim3 grid(ceil_div(lp->n_rows, 128), ceil_div(row1 - row0, ST_ROWS));
-  add_st_phi_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, Phi, row0, row1, X, ldx,
-                                                            accumulate);
+#define WQ_ST(W)                                                                     \
+  add_st_phi_kernel<W><<<grid, 128, 0, (cudaStream_t)stream>>>(*lp, Phi, row0, row1, X, ldx, \
+                                                               accumulate)
+  WQ_WS_SWITCH(lp->ws, WQ_ST)
+#undef WQ_ST
   return check_launch("wq_add_st_phi");
 }
 
