@@ -418,6 +418,12 @@ def _k1_vanishes(disc) -> bool:
 _K1_SHORTCUT = True   # IK1 = 0 on unit-speed straight segments (_k1_vanishes)
 
 
+def _ik1_skipped(disc) -> bool:
+    """IK1 is identically zero and not evaluated (callers then write the log
+    part without accumulating, so X is neither zero-filled nor re-read)."""
+    return _K1_SHORTCUT and _k1_vanishes(disc)
+
+
 def _ik1_into(disc, X, accumulate=False, row0=0, row1=None):
     """IK1 (all rows, or rows [row0, row1) x all columns with row0 on a
     64-row tile boundary) into X."""
@@ -649,7 +655,9 @@ def general_rows_into(disc, X_rows, row0: int, row1: int, F=None):
     st = _lib.stream_handle()
     N, NE = disc.space.dim, disc.refined.basis.dim
     nr = row1 - row0
-    _ik1_into(disc, X_rows, accumulate=False, row0=row0, row1=row1)
+    skip = _ik1_skipped(disc)
+    if not skip:
+        _ik1_into(disc, X_rows, accumulate=False, row0=row0, row1=row1)
     T, D = _theta_d(disc, lp, d, rows=(row0, row1))
     if F is None:
         F = _fit_f(disc, lp, d, D)
@@ -660,7 +668,7 @@ def general_rows_into(disc, X_rows, row0: int, row1: int, F=None):
     PhiT = torch.empty((nr, NE), dtype=torch.float64, device="cuda")
     _lib.call("wq_transpose", _lib.ptr(T), NE, nr, _lib.ptr(PhiT), st)
     _lib.call("wq_phi_s_rows", ctypes_ref(d["struct"]), _lib.ptr(PhiT), row0, row1,
-              _lib.ptr(X_rows), X_rows.stride(0), 1, st)
+              _lib.ptr(X_rows), X_rows.stride(0), 0 if skip else 1, st)
     return X_rows
 
 
@@ -1025,8 +1033,10 @@ def _assemble_into(disc: Discretization, X, scaled: bool = True):
     alpha = -1.0 / (2.0 * TWO_PI) if scaled else 0.5
     if _use_v2(disc):
         return _assemble_v2(disc, X, alpha)
-    _ik1_into(disc, X, accumulate=False)
-    _ik2_x2_into(disc, X, accumulate=True)
+    skip = _ik1_skipped(disc)
+    if not skip:
+        _ik1_into(disc, X, accumulate=False)
+    _ik2_x2_into(disc, X, accumulate=not skip)
     _lib.call("wq_symmetrize", _lib.ptr(X), X.shape[0], alpha, _lib.stream_handle())
     return X
 
