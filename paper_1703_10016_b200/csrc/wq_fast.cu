@@ -549,13 +549,19 @@ __device__ __forceinline__ void s_contract_acc(const double* Phs, const double* 
   }
 }
 
-constexpr int T2STRIDE = 66;  // orientation hand-off tile (== 2 mod 16: conflict-free transposed reads)
+// orientation hand-off tile: stride 70 (== 6 mod 8: the transposed 8-byte reads of rows
+// 2c + e hit distinct banks) with odd rows shifted by 2 more doubles, so two consecutive
+// rows start 8 apart mod 16 and the 16-byte row-fragment loads / stores are conflict-free
+// too (each row arrives by its own bulk copy, so the row starts are free)
+constexpr int T2STRIDE = 70;
+constexpr int T2EXTRA = 8;
+__device__ __forceinline__ int tst_row(int a) { return a * T2STRIDE + ((a & 1) ? 2 : 0); }
 
 template <int P>
 struct X2Smem {
   using C = X2Cfg<P>;
   static constexpr int SROW = C::WS <= 8 ? 8 : 16;
-  static constexpr int TOTAL = C::ZROWS * C::ZSTRIDE + FT * PSTRIDE + FT * T2STRIDE + FT * SROW +
+  static constexpr int TOTAL = C::ZROWS * C::ZSTRIDE + FT * PSTRIDE + FT * T2STRIDE + T2EXTRA + FT * SROW +
                                8 * (C::KS / 4) * 32 + 2;  // + 2 mbarriers (window, IK1 tile)
 };
 
@@ -578,7 +584,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
   double* Zsm = smem;                              // ZROWS * ZSTRIDE
   double* Phs = Zsm + C::ZROWS * C::ZSTRIDE;       // FT * PSTRIDE (also output staging, stride 65)
   double* Tst = Phs + FT * PSTRIDE;                // FT * T2STRIDE: IK1(I,J), then T
-  double* Ssm = Tst + FT * T2STRIDE;               // FT * SROW (S band rows)
+  double* Ssm = Tst + FT * T2STRIDE + T2EXTRA;     // FT * SROW (S band rows)
   double* Bfr = Ssm + FT * SROW;                   // 8 * KS/4 * 32 (fragment order, alpha S)
   uint64_t* bar = reinterpret_cast<uint64_t*>(Bfr + 8 * (C::KS / 4) * 32);
   const int64_t n = N;
@@ -611,8 +617,8 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
     {
       for (int k = tid; k < FT * FT; k += X2_THREADS) {
         const int a = k >> 6, b = k & 63;
-        if (a < ni && b < nj) cp_async8(Tst + a * T2STRIDE + b, src + a * ldx + b);
-        else Tst[a * T2STRIDE + b] = 0.0;
+        if (a < ni && b < nj) cp_async8(Tst + tst_row(a) + b, src + a * ldx + b);
+        else Tst[tst_row(a) + b] = 0.0;
       }
     }
   }
@@ -674,7 +680,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
         __syncwarp();
         const uint64_t pol = l2_evict_first();   // the IK1 tile is read once
         for (int a = tid; a < FT; a += 32)
-          bulk_g2s_hint(Tst + a * T2STRIDE, src + a * ldx, FT * 8, bar + 1, pol);
+          bulk_g2s_hint(Tst + tst_row(a), src + a * ldx, FT * 8, bar + 1, pol);
       }
       __syncthreads();
       x2_mark(1 + 3 * orient);
@@ -716,7 +722,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
       for (int jb = 0; jb < 8; ++jb) {
         if (with_ik1) {
           const double2 t =
-              *reinterpret_cast<const double2*>(Tst + (8 * warp + r) * T2STRIDE + 8 * jb + 2 * c);
+              *reinterpret_cast<const double2*>(Tst + tst_row(8 * warp + r) + 8 * jb + 2 * c);
           acc[jb][0] = aw * t.x;
           acc[jb][1] = aw * t.y;
         } else {
@@ -727,7 +733,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
 #pragma unroll
       for (int ib = 0; ib < 8; ++ib)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) acc[ib][e] = Tst[(8 * ib + 2 * c + e) * T2STRIDE + 8 * warp + r];
+        for (int e = 0; e < 2; ++e) acc[ib][e] = Tst[tst_row(8 * ib + 2 * c + e) + 8 * warp + r];
     }
     __syncthreads();
     x2_mark(2 + 3 * orient);
@@ -737,7 +743,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
       // T[i][j] (each lane rewrites the entries it read)
 #pragma unroll
       for (int jb = 0; jb < 8; ++jb)
-        *reinterpret_cast<double2*>(Tst + (8 * warp + r) * T2STRIDE + 8 * jb + 2 * c) =
+        *reinterpret_cast<double2*>(Tst + tst_row(8 * warp + r) + 8 * jb + 2 * c) =
             make_double2(acc[jb][0], acc[jb][1]);
     }
   }
@@ -746,7 +752,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
     // unsymmetrised row block: X(I,J) = alpha (w IK1 + X2(I,J)) = T
     for (int k = tid; k < FT * FT; k += X2_THREADS) {
       const int a = k >> 6, b = k & 63;
-      if (a < ni && b < nj) X[(I0 - row_off + a) * ldx + J0 + b] = Tst[a * T2STRIDE + b];
+      if (a < ni && b < nj) X[(I0 - row_off + a) * ldx + J0 + b] = Tst[tst_row(a) + b];
     }
     return;
   }
@@ -760,7 +766,7 @@ __device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Ue
     constexpr int OSA = 72, OSB = 66;
     double* Oji = Phs;             // A(J,I)[j][i]
     double* Oij = Phs + FT * OSA;  // A(I,J)[i][j] = A(J,I)[j][i]
-    static_assert(FT * (OSA + OSB) <= FT * PSTRIDE + FT * T2STRIDE, "output staging overflows");
+    static_assert(FT * (OSA + OSB) <= FT * PSTRIDE + FT * T2STRIDE + T2EXTRA, "output staging overflows");
 #pragma unroll
     for (int ib = 0; ib < 8; ++ib) {
       *reinterpret_cast<double2*>(Oji + (8 * warp + r) * OSA + 8 * ib + 2 * c) =
