@@ -144,8 +144,8 @@ static __device__ const double kTang64[128] = {
 // Chebyshev-economised onto r^3 and r on |r| <= a = 0.0077945 (the table's largest |r|):
 // r^5 ~ (20 a^2 r^3 - 5 a^4 r) / 16.  Truncation error of 0.5 ln(1+r): <= 8.7e-18
 // absolute (`python tools/tang_table.py 64 series`), one DFMA less per ln.
-static __constant__ double kLn64C[7] = {0.08333333333333333, -0.10000542448484374, 0.125,
-                                        -0.16666666658427656, 0.25, HLN2_A, HLN2_B};
+static __constant__ double kLn64C[6] = {0.08333333333333333, -0.10000542448484374, 0.125,
+                                        -0.16666666658427656, 0.25, 0.34657359027997264};
 
 __device__ __forceinline__ double half_ln64t(double x, const double2* __restrict__ tab) {
   const int hi = __double2hiint(x);
@@ -157,11 +157,12 @@ __device__ __forceinline__ double half_ln64t(double x, const double2* __restrict
   q = fma(r, q, kLn64C[2]);
   q = fma(r, q, kLn64C[3]);
   q = fma(r, q, kLn64C[4]);
-  // 0.5 ln x = de A + (t.y + de B + r (0.5 - r q)), A = HLN2_A (de A exact): 9 FP64
-  // operations; max error 1.3e-16 of max(|0.5 ln x|, 1) (exact-rounding emulation)
+  // 0.5 ln x = de (0.5 ln 2) + (t.y + r (0.5 - r q)), 0.5 ln 2 rounded to a double (its
+  // error de * 2.8e-17 scales with the result): 8 FP64 operations; max error 1.7e-16 of
+  // max(|0.5 ln x|, 1) (exact-rounding emulation, tools/ln_emulate.py)
   const double de = (double)((hi >> 20) - 1023);  // I2F: the conversion pipe is idle here
   const double u = fma(-r, q, 0.5);
-  const double w = fma(r, u, fma(de, kLn64C[6], t.y));
+  const double w = fma(r, u, t.y);
   return fma(de, kLn64C[5], w);
 }
 

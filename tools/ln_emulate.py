@@ -27,13 +27,13 @@ def old(x):
     r2=mul(r,r); de=float((hi>>20)-1023)
     thi=fma(de,A,ty[k])
     return add(thi, fma(r,0.5,fma(-r2,q,mul(de,B))))
-def new(x):
+def new(x):   # the current half_ln64t: 8 FP64 operations
     hi,m=parts(x); k=(hi>>14)&63
     r=fma(m,tx[k],-1.0)
     q=fma(r,C[0],C[1]); q=fma(r,q,C[2]); q=fma(r,q,C[3]); q=fma(r,q,C[4])
     u=fma(-r,q,0.5); de=float((hi>>20)-1023)
-    w=fma(de,B,ty[k]); w=fma(r,u,w)
-    return fma(de,A,w)
+    w=fma(r,u,ty[k])
+    return fma(de,float(mp.log(2)/2),w)
 random.seed(1)
 eo=en=0
 for n in range(30000):
