@@ -170,6 +170,9 @@ typedef struct {
 
 /* Theta^T (N_E x N) and D (N_E x N_E) by element-pair gathers (assembly.py:215-232). */
 int wq_theta_t(const wq_pairs_t* pp, double* thetaT, void* stream);
+/* Columns [row0, row1) of Theta^T only (a rank's row block): thetaT[l * ld + i - row0]. */
+int wq_theta_t_rows(const wq_pairs_t* pp, int64_t row0, int64_t row1, double* thetaT, int64_t ld,
+                    void* stream);
 int wq_dmat(const wq_pairs_t* pp, double* D, void* stream);
 
 /* In-place banded SPD solve on every column of X (n x ncols, ld ldx):

@@ -429,7 +429,8 @@ def pair_moments_closed(da, db, he, hf, delta):
     return out
 
 
-def pair_moments_gauss(da, db, he, hf, delta, order=PAIR_FAR_ORDER, period=None, gap_only=False):
+def pair_moments_gauss(da, db, he, hf, delta, order=PAIR_FAR_ORDER, period=None, gap_only=False,
+                       fast=False):
     """Tensor Gauss for analytic pair moments (quadrature.py:413-438)."""
     he = np.asarray(he, float)[:, None, None]
     hf = np.asarray(hf, float)[:, None, None]
@@ -444,6 +445,11 @@ def pair_moments_gauss(da, db, he, hf, delta, order=PAIR_FAR_ORDER, period=None,
         kern = np.log(np.abs(arg))
         if period is not None:
             kern += np.log(np.abs(np.sinc(arg / period)))
+    if fast:   # batched matrix products (same sums, other association order)
+        pa, pb = np.arange(da + 1), np.arange(db + 1)
+        wa = he[:, :, :1] ** (pa + 1.0) * (w[:, None] * x[:, None] ** pa)[None]    # (n, g, da+1)
+        wb = hf[:, 0, :, None] ** (pb + 1.0) * (w[:, None] * x[:, None] ** pb)[None]  # (n, h, db+1)
+        return np.matmul(np.swapaxes(wa, 1, 2), np.matmul(kern, wb))
     out = np.empty((u.shape[0], da + 1, db + 1))
     for a in range(da + 1):
         wa = (he[:, :, 0] ** (a + 1)) * (w * x ** a)[None, :]
@@ -871,7 +877,8 @@ def pair_moments_touching(da, db, rho, dl, n=24, levels=16, ratio=0.15):
     return A.T @ K @ B
 
 
-def pair_moments_general(da, db, he, hf, delta, closed_period=None):
+def pair_moments_general(da, db, he, hf, delta, closed_period=None, far_order=PAIR_FAR_ORDER,
+                         fast=False):
     """Centred double log moments for arbitrary element pairs; he, hf, delta
     arrays (delta = outer centre minus inner centre, as quadrature.py:382)."""
     he, hf, delta = np.broadcast_arrays(np.asarray(he, float), np.asarray(hf, float),
@@ -898,7 +905,8 @@ def pair_moments_general(da, db, he, hf, delta, closed_period=None):
     for k in np.flatnonzero(near & (rho != 1.0)):   # exact contact geometry (rounding aside)
         m[k] = pair_moments_touching(da, db, rho[k], np.copysign(0.5 * (1.0 + rho[k]), dl[k]))
     if (~near).any():
-        m[~near] = pair_moments_gauss(da, db, ones[~near], rho[~near], dl[~near])
+        m[~near] = pair_moments_gauss(da, db, ones[~near], rho[~near], dl[~near], order=far_order,
+                                      fast=fast)
     if closed_period is not None:
         m += pair_moments_gauss(da, db, ones, rho, dl, period=(closed_period / he)[:, None, None],
                                 gap_only=True)
@@ -975,3 +983,211 @@ def config5_space(n_el=16384, degree=4, seed=0, zone=0.2, ratio=0.9, growth_elem
     bp = -1.0 + 2.0 * bp / bp[-1]
     mult = np.where(np.random.default_rng(seed).random(n_el - 1) < 0.25, 2, 1)
     return open_basis(degree, bp, mult)
+
+
+# --------------------------------------------------------------------------
+# row restatement for OPEN meshes of any grading (config 5 at full size)
+# --------------------------------------------------------------------------
+#
+# The dense general restatement above needs n_el^2 pair tensors and dense
+# N x N products; at config 5 (N = 20418, n_el = 16384) it cannot run.  This
+# class computes ROWS of M = IK1 + IK2 (assembly.py:244-256) through the
+# X-form X = IK1 + (2 Theta - C^T D) C with C = H^{-1} S (the
+# normal equations of the reference's QR fit, assembly.py:233-243):
+#
+#   X[R, :] = IK1[R, :] + ((H^{-1} (2 Theta[R, :]^T - D C_R))^T S
+#   X[:, R] = IK1[:, R] + 2 Theta C_R - S^T H^{-1} D C_R,     C_R = H^{-1} S[:, R]
+#
+# Theta C_R and D C_R need every element pair once: Z_e = sum_f M(e, f) y_f
+# with y_f = v_f . Y[vcols_f]; Theta Y = sum u_e^T Z_e and D Y = sum v_e^T
+# Z_e[:d+1].  Pairs of two elements on the uniform lattice of the median
+# width h0 read the reference's gap table (quadrature.py:441-504, scaled at h0)
+# and their sum over f is a correlation (FFT); every pair with an element off
+# the lattice (the graded ends) takes pair_moments_general (touching pairs of
+# unequal widths by the graded composite rule, far pairs by tensor Gauss --
+# order 30 below two larger widths of separation, 16 below eight, 12 beyond,
+# each converged to <= 5e-15 of the natural slot scale,
+# tests/test_oracle.py::test_tiered_far_orders).  Theta[R, :] takes the same
+# pair moments for the outer elements of the sampled rows.  H^{-1} by a banded
+# Cholesky solve (scipy.linalg.solveh_banded).
+
+
+def _far_order(he, hf, delta):
+    sep = (np.abs(delta) - 0.5 * (he + hf)) / np.maximum(he, hf)
+    return np.where(sep < 2.0, 30, np.where(sep < 8.0, 16, 12))
+
+
+def pair_moments_tiered(da, db, he, hf, delta):
+    """pair_moments_general with the far-pair Gauss order chosen by separation
+    (30 | 16 | 12, SURVEY 8(c) generalisation; open meshes)."""
+    he, hf, delta = (np.asarray(a, float) for a in np.broadcast_arrays(he, hf, delta))
+    out = np.empty((len(he), da + 1, db + 1))
+    order = _far_order(he, hf, delta)
+    for o in (30, 16, 12):
+        m = order == o
+        if m.any():
+            out[m] = pair_moments_general(da, db, he[m], hf[m], delta[m], far_order=o, fast=True)
+    return out
+
+
+class GeneralRows:
+    """Rows of M / A for an open discretization of any grading (config 5)."""
+
+    def __init__(self, curve: Curve, space: Basis, nref: int = 1, chunk: int = 65536):
+        assert not space.closed, "GeneralRows: open meshes"
+        import scipy.sparse as sp
+        self.curve, self.space = curve, space
+        self.fine = fine = refine(space, nref)
+        self.N, self.NE = space.dim, fine.dim
+        self.d = d = fine.degree
+        self.P = space.degree + JFIT_DEGREE
+        self.chunk = chunk
+        self.nodes = nodes = build_nodes(fine)
+        self.J = curve.speed(nodes)
+        idx, w = _rules_local(space, fine, nodes, False)
+        rows = np.concatenate([np.full(len(q), i) for i, q in enumerate(idx)])
+        vals = np.concatenate([wi * self.J[q] for wi, q in zip(w, idx)])
+        self.rule_idx = idx
+        self.G = sp.csr_matrix((vals, (rows, np.concatenate(idx))), shape=(self.N, len(nodes)))
+        bt = design_sparse(fine, nodes)
+        bpar = design_sparse(space, nodes)
+        H = (bt.T @ bt).tocsr()
+        self.S = (bt.T @ sp.diags(self.J) @ bpar).tocsc()        # N_E x N
+        coo = H.tocoo()
+        self.bw = bw = int(np.abs(coo.row - coo.col).max())
+        ab = np.zeros((bw + 1, self.NE))
+        up = coo.row <= coo.col
+        ab[bw + coo.row[up] - coo.col[up], coo.col[up]] = coo.data[up]
+        self.h_band = ab
+        els = fine.elements
+        self.h = els[:, 1] - els[:, 0]
+        self.mid = 0.5 * (els[:, 0] + els[:, 1])
+        self.u, self.ucols = local_coeffs(space, els, self.P, scale_fn=curve.speed)
+        self.v, self.vcols = local_coeffs(fine, els, d)
+        # lattice: widths within 2e-11 of the median and centres on its grid,
+        # one contiguous run of elements
+        h0 = float(np.median(self.h))
+        on = np.abs(self.h / h0 - 1.0) < 2e-11
+        first = int(np.argmax(on))
+        k = (self.mid - self.mid[first]) / h0
+        on &= np.abs(k - np.rint(k)) < 1e-10 * np.maximum(1.0, np.abs(k))
+        lat = np.flatnonzero(on)
+        assert len(lat) and np.all(np.diff(lat) == 1) and np.all(np.rint(k[lat]) == lat - lat[0]), \
+            "GeneralRows: the lattice elements must form one consecutive run"
+        self.h0, self.lat0, self.nL = h0, int(lat[0]), len(lat)
+        self.off = np.flatnonzero(~on)
+        unit = unit_pair_stack(self.P, d, self.nL, False)
+        pa, pb = np.arange(self.P + 1), np.arange(d + 1)
+        scale = h0 ** (2.0 + pa[:, None] + pb[None, :])
+        self.tab = scale[None] * (unit + np.log(h0) * (centred_integrals(self.P)[:, None]
+                                                        * centred_integrals(d)[None, :]))
+
+    # -- pieces -------------------------------------------------------------
+    def hinv(self, Y):
+        return scipy.linalg.solveh_banded(self.h_band, Y)
+
+    def moments(self, e, f):
+        """M(e, f) for index arrays e, f (lattice pairs from the table)."""
+        e = np.asarray(e)
+        f = np.asarray(f)
+        out = np.empty((len(e), self.P + 1, self.d + 1))
+        lo, hi = self.lat0, self.lat0 + self.nL
+        lat = (e >= lo) & (e < hi) & (f >= lo) & (f < hi)
+        out[lat] = self.tab[f[lat] - e[lat] + self.nL - 1]
+        rest = np.flatnonzero(~lat)
+        for c0 in range(0, len(rest), self.chunk):
+            k = rest[c0:c0 + self.chunk]
+            out[k] = pair_moments_tiered(self.P, self.d, self.h[e[k]], self.h[f[k]],
+                                         self.mid[e[k]] - self.mid[f[k]])
+        return out
+
+    def _y(self, Y):
+        """y_f[beta, r] = sum_b v_f[beta, b] Y[vcols[f, b], r]."""
+        return np.einsum("fqb,fbr->fqr", self.v, Y[self.vcols])
+
+    def z_all(self, Y):
+        """Z_e = sum_f M(e, f) y_f for every element e: (n_el, P+1, R)."""
+        y = self._y(Y)
+        n, R = len(self.h), Y.shape[1]
+        nA = self.P + 1
+        Z = np.zeros((n, nA, R))
+        lo, nL = self.lat0, self.nL
+        # lattice x lattice: correlation with the gap table, by FFT
+        L = 1 << int(np.ceil(np.log2(3 * nL)))
+        yr = y[lo:lo + nL][::-1]                               # reversed
+        Yf = np.fft.rfft(yr, n=L, axis=0)                       # (L/2+1, d+1, R)
+        acc = np.zeros((L // 2 + 1, nA, R), complex)
+        for b in range(self.d + 1):
+            Tf = np.fft.rfft(self.tab[:, :, b], n=L, axis=0)    # (L/2+1, nA)
+            acc += Tf[:, :, None] * Yf[:, b, None, :]
+        conv = np.fft.irfft(acc, n=L, axis=0)
+        e = np.arange(nL)
+        Z[lo:lo + nL] = conv[2 * nL - 2 - e]
+        # every pair with an element off the lattice
+        off = self.off
+        allf = np.arange(n)
+        for g in off:                                           # outer off-lattice: all partners
+            M = self.moments(np.full(n, g), allf)
+            Z[g] = np.einsum("fab,fbr->ar", M, y)
+        latf = np.arange(lo, lo + nL)
+        for c0 in range(0, nL, max(1, self.chunk // max(1, len(off)))):
+            es = latf[c0:c0 + max(1, self.chunk // max(1, len(off)))]
+            ee = np.repeat(es, len(off))
+            ff = np.tile(off, len(es))
+            M = self.moments(ee, ff).reshape(len(es), len(off), nA, self.d + 1)
+            Z[es] += np.einsum("efab,fbr->ear", M, y[off])
+        return Z
+
+    def theta_dy(self, Y):
+        """(Theta Y, D Y) for a block of N_E-vectors Y (N_E x R)."""
+        Z = self.z_all(Y)
+        R = Y.shape[1]
+        TY = np.zeros((self.N, R))
+        np.add.at(TY, self.ucols.ravel(), np.einsum("eak,ear->ekr", self.u, Z).reshape(-1, R))
+        DY = np.zeros((self.NE, R))
+        np.add.at(DY, self.vcols.ravel(),
+                  np.einsum("eak,ear->ekr", self.v, Z[:, : self.d + 1]).reshape(-1, R))
+        return TY, DY
+
+    def theta_rows(self, rows):
+        """Theta[rows, :] by element pairs (assembly.py:215-228)."""
+        n = len(self.h)
+        out = np.zeros((len(rows), self.NE))
+        allf = np.arange(n)
+        for k, i in enumerate(rows):
+            for e, a in zip(*np.nonzero(self.ucols == i)):
+                M = self.moments(np.full(n, e), allf)
+                w = np.einsum("a,fab,fbc->fc", self.u[e][:, a], M, self.v)
+                np.add.at(out[k], self.vcols.ravel(), w.ravel())
+        return out
+
+    def ik1_rows(self, rows):
+        """IK1[rows, :] = G[rows] K1 G^T (assembly.py:175-183, geometry.py:225-248)."""
+        out = np.zeros((len(rows), self.N))
+        Gt = self.G.T.tocsr()
+        for k, i in enumerate(rows):
+            gi = self.G.getrow(i)
+            k1 = k1_grid(self.curve, self.nodes[gi.indices], self.nodes)
+            out[k] = np.asarray((gi.data @ k1) @ Gt).ravel()
+        return out
+
+    def x_rows_cols(self, rows):
+        """(X[rows, :], X[:, rows]^T) of the X-form."""
+        rows = np.asarray(rows)
+        SR = np.asarray(self.S[:, rows].todense())               # N_E x R
+        CR = self.hinv(SR)
+        TC, DC = self.theta_dy(CR)
+        th = self.theta_rows(rows)                               # R x N_E
+        ik1 = self.ik1_rows(rows)
+        Q = self.hinv(2.0 * th.T - DC)                           # N_E x R
+        xr = ik1 + np.asarray((self.S.T @ Q)).T                  # R x N
+        xc = ik1 + (2.0 * TC - np.asarray(self.S.T @ self.hinv(DC))).T
+        return xr, xc
+
+    def m_rows(self, rows):
+        """Rows of the symmetrised M = (X + X^T)/2 = sym(IK1 + IK2)."""
+        xr, xc = self.x_rows_cols(rows)
+        return 0.5 * (xr + xc)
+
+    def a_rows(self, rows):
+        return -self.m_rows(rows) / TWO_PI

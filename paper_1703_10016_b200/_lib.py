@@ -62,6 +62,7 @@ _SIGS = {
     "wq_ik2_circ": [ctypes.POINTER(WqLogpart), c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp,
                     c_i64, c_int, c_vp],
     "wq_theta_t": [ctypes.POINTER(WqPairs), c_vp, c_vp],
+    "wq_theta_t_rows": [ctypes.POINTER(WqPairs), c_i64, c_i64, c_vp, c_i64, c_vp],
     "wq_dmat": [ctypes.POINTER(WqPairs), c_vp, c_vp],
     "wq_band_solve_cols": [c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp],
     "wq_transpose": [c_vp, c_i64, c_i64, c_vp, c_vp],

@@ -43,6 +43,7 @@ from .splines import BasisSpec, RefinedBasis, active_values, as_basis, local_bas
 
 __all__ = [
     "NodeVector",
+    "WeightedRule",
     "Discretization",
     "build_discretization",
     "assemble_ik1",
@@ -132,6 +133,24 @@ class LogPart:
     vcols: np.ndarray = None
 
 
+@dataclass(frozen=True)
+class WeightedRule:
+    """One regular weighted rule on the shared node vector (quadrature.py:150-168):
+    tag ("basis", i), active node indices, weights."""
+
+    tag: tuple
+    idx: np.ndarray
+    weights: np.ndarray
+
+    def apply(self, values_at_nodes) -> float:
+        return float(self.weights @ np.asarray(values_at_nodes)[self.idx])
+
+    def full_weights(self, n_quad: int) -> np.ndarray:
+        w = np.zeros(n_quad)
+        w[self.idx] = self.weights
+        return w
+
+
 @dataclass
 class Discretization:
     """Solution space, shared node vector and the banded regular rules
@@ -154,8 +173,29 @@ class Discretization:
     _dev: dict = field(default_factory=dict, repr=False)
 
     @property
-    def regular_rules(self):
-        return self.rules
+    def regular_rules(self) -> list:
+        """The regular rules as the reference's list of WeightedRule
+        (assembly.py:139, quadrature.py:510-540), built from the band on first
+        use; the device path reads the band (``rules``)."""
+        if "regular_rules" not in self._dev:
+            rb, nq = self.rules, self.nodes.n
+            out = []
+            for i in range(len(rb.start)):
+                w = int(rb.width[i])
+                idx = np.mod(rb.start[i] + np.arange(w), nq)
+                order = np.argsort(idx, kind="stable")
+                out.append(WeightedRule(("basis", i), idx[order], rb.weights[i, :w][order].copy()))
+            self._dev["regular_rules"] = out
+        return self._dev["regular_rules"]
+
+    @property
+    def singular_rules(self):
+        """The singular (log) rules of Alg. 2 are not built: the matrix never
+        reads them and the reference builds them in O(N^3) time /
+        O(N^2) memory (quadrature.py:543-571).  Raises UsageError, so the
+        reference's ``--dump-rules`` path fails with a clear message."""
+        raise UsageError("singular rules are not built by the B200 backend (unused by the "
+                         "matrix, SURVEY F3); dump them with the reference's build_singular_rules")
 
     @property
     def G(self) -> np.ndarray:
@@ -583,26 +623,29 @@ def _ik2_x2_into(disc, X, accumulate=True):
     return X
 
 
-def _theta_d(disc, lp: LogPart, d, rows=None):
-    """Theta^T (all columns, or the block rows = (row0, row1)) and D."""
+def _theta_d(disc, lp: LogPart, d, rows=None, want_theta=True, want_d=True):
+    """Theta^T (all columns, or the block rows = (row0, row1)) and D; either
+    may be skipped (None): a rank's row block needs only its Theta^T columns,
+    D is computed once per assembly (general_prepare)."""
     torch = _torch()
     st = _lib.stream_handle()
     N, NE = disc.space.dim, disc.refined.basis.dim
     if lp.graded:
-        thetaT, D = _graded_theta_d(disc, lp, d, rows)
-    else:
-        m2, keep = _m2_table(disc, lp)
-        pp = _lib.WqPairs(N, NE, lp.n_el, m2.shape[0], lp.da, lp.db, int(disc.closed),
-                          lp.u_el.shape[1], lp.v_el.shape[1], d["u_el"].data_ptr(),
-                          d["u_loc"].data_ptr(), d["v_el"].data_ptr(), d["v_loc"].data_ptr(),
-                          d["u"].data_ptr(), disc.space.degree, d["v"].data_ptr(),
-                          m2.data_ptr())
-        thetaT = torch.empty((NE, N), dtype=torch.float64, device="cuda")
+        return _graded_theta_d(disc, lp, d, rows, want_theta, want_d)
+    m2, keep = _m2_table(disc, lp)
+    pp = _lib.WqPairs(N, NE, lp.n_el, m2.shape[0], lp.da, lp.db, int(disc.closed),
+                      lp.u_el.shape[1], lp.v_el.shape[1], d["u_el"].data_ptr(),
+                      d["u_loc"].data_ptr(), d["v_el"].data_ptr(), d["v_loc"].data_ptr(),
+                      d["u"].data_ptr(), disc.space.degree, d["v"].data_ptr(),
+                      m2.data_ptr())
+    thetaT = D = None
+    if want_theta:
+        r0, r1 = (0, N) if rows is None else rows
+        thetaT = torch.empty((NE, r1 - r0), dtype=torch.float64, device="cuda")
+        _lib.call("wq_theta_t_rows", ctypes_ref(pp), r0, r1, _lib.ptr(thetaT), r1 - r0, st)
+    if want_d:
         D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
-        _lib.call("wq_theta_t", ctypes_ref(pp), _lib.ptr(thetaT), st)
         _lib.call("wq_dmat", ctypes_ref(pp), _lib.ptr(D), st)
-        if rows is not None:
-            thetaT = thetaT[:, rows[0]:rows[1]].contiguous()
     return thetaT, D
 
 
@@ -639,8 +682,7 @@ def general_prepare(disc):
     """F = H^{-1} D H^{-1} of the general path (replicated per rank; computed
     once per assembly and shared by its row blocks)."""
     lp, d = _logpart_dev(disc)
-    N = disc.space.dim
-    _, D = _theta_d(disc, lp, d, rows=(0, min(N, 64)))
+    _, D = _theta_d(disc, lp, d, want_theta=False)
     return _fit_f(disc, lp, d, D)
 
 
@@ -658,9 +700,9 @@ def general_rows_into(disc, X_rows, row0: int, row1: int, F=None):
     skip = _ik1_skipped(disc)
     if not skip:
         _ik1_into(disc, X_rows, accumulate=False, row0=row0, row1=row1)
-    T, D = _theta_d(disc, lp, d, rows=(row0, row1))
     if F is None:
-        F = _fit_f(disc, lp, d, D)
+        F = general_prepare(disc)
+    T, _ = _theta_d(disc, lp, d, rows=(row0, row1), want_d=False)
     _hsolver(lp, d, NE)(T, nr)
     _lib.call("wq_gather_fs_rows", ctypes_ref(d["struct"]), 2.0, _lib.ptr(F), _lib.ptr(T), row0,
               row1, nr, st)
@@ -696,6 +738,7 @@ def _gap_table(disc, lp: LogPart, h0: float):
 # graded open meshes: lattice route (Theta / D straight from the gap table for
 # outer elements on the width-h0 lattice) when at most this many elements are off it
 _LATTICE_MAX_OFF = 4096
+_LATTICE_MAX_BYTES = 8 << 30   # device bytes of the lattice route's off-lattice moments
 # D by its lower storage triangle + mirror (D is symmetric)
 _YS_SYM_D = True
 _NOT_LATTICE = np.iinfo(np.int64).min
@@ -762,21 +805,25 @@ def _tile_span(lo, hi, tile):
     return int((hi[ends] - lo[starts] + 1).max())
 
 
-def _graded_theta_d(disc, lp: LogPart, d, rows=None):
+def _graded_theta_d(disc, lp: LogPart, d, rows=None, want_theta=True, want_d=True):
     """Theta^T (N_E x N, or N_E x (row1 - row0) for rows = (row0, row1)) and D
-    (N_E x N_E) of a graded mesh."""
+    (N_E x N_E) of a graded mesh (either may be skipped)."""
     consecutive = all(np.array_equal(c, c[:, :1] + np.arange(c.shape[1])[None, :])
                       for c in (lp.ucols, lp.vcols))     # element functions are consecutive rows
     if not disc.closed and _GEN_GAP_TABLE and lp.db == 4 and consecutive:
         kidx, gidx, glist = lattice_classes(lp.elh, lp.elm)
-        if len(glist) <= _LATTICE_MAX_OFF:
-            return _lattice_theta_d(disc, lp, d, kidx, gidx, glist, rows)
-    return _blocks_theta_d(disc, lp, d, rows=rows)
+        # the off-lattice moments (len(glist), n_el, P+1, d+1) stay within a byte budget
+        mg_bytes = len(glist) * lp.n_el * (lp.da + 1) * (lp.db + 1) * 8
+        if len(glist) <= _LATTICE_MAX_OFF and mg_bytes <= _LATTICE_MAX_BYTES:
+            return _lattice_theta_d(disc, lp, d, kidx, gidx, glist, rows, want_theta, want_d)
+    return _blocks_theta_d(disc, lp, d, rows=rows, want_theta=want_theta, want_d=want_d)
 
 
-def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None):
+def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None, want_theta=True,
+                     want_d=True):
     """Theta^T and D of a graded open mesh: lattice outer elements straight
-    from the unit gap table (wq_ystage), the few others by the block route."""
+    from the unit gap table (wq_ystage), the few others by the block route
+    (either output may be skipped: None)."""
     torch = _torch()
     st = _lib.stream_handle()
     N, NE, n = disc.space.dim, disc.refined.basis.dim, lp.n_el
@@ -811,8 +858,8 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None):
                   _lib.ptr(d["near_unit"]), _lib.ptr(d["touch"]), _lib.ptr(d["ca"]),
                   _lib.ptr(d["cb"]), _lib.ptr(L["gidx"]), _lib.ptr(mgc), st)
     r0, r1 = (0, N) if rows is None else rows
-    thetaT = torch.empty((NE, r1 - r0), dtype=torch.float64, device="cuda")
-    D = torch.empty((NE, NE), dtype=torch.float64, device="cuda")
+    thetaT = torch.empty((NE, r1 - r0), dtype=torch.float64, device="cuda") if want_theta else None
+    D = torch.empty((NE, NE), dtype=torch.float64, device="cuda") if want_d else None
     mg = _lib.ptr(mgc) if mgc is not None else None
     wc = lp.v_el.shape[1]
     cols = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]))
@@ -836,40 +883,50 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None):
         kpT, kpD = -(-5 * da1 // 4) * 4, -(-5 * nB // 4) * 4
         Tb = torch.empty((5, n_tab, 20), **f64)
         vsum = torch.empty((NE, 5), **f64)
-        CrT, LtT = torch.empty((5, N, kpT), **f64), torch.empty((N, 5), **f64)
-        CrD, LtD = torch.empty((5, NE, kpD), **f64), torch.empty((NE, 5), **f64)
         common = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]))
-        _lib.call("wq_ystage_mma_prep", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
-                  _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *common, _lib.ptr(d["u"]), da1,
-                  _lib.ptr(d["v"]), _lib.ptr(d["elh"]), _lib.ptr(m2u), da1, _lib.ptr(d["ca"]),
-                  _lib.ptr(d["cb"]), _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum), _lib.ptr(Tb),
-                  n_tab, st)
-        _lib.call("wq_ystage_mma_prep", NE, NE, n, nB, nB, wc, _lib.ptr(L["vcols"]),
-                  _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *common, _lib.ptr(d["v"]), nB,
-                  _lib.ptr(d["v"]), _lib.ptr(d["elh"]), None, da1, _lib.ptr(d["ca"]),
-                  _lib.ptr(d["cb"]), _lib.ptr(CrD), _lib.ptr(LtD), _lib.ptr(vsum), None, n_tab, st)
         mcols = common + (_lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), _lib.ptr(d["v"]))
-        _lib.call("wq_ystage_mma", N, NE, n, da1, wc, _lib.ptr(L["u_lo"]), *mcols,
-                  _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
-                  kT, kC, _lib.ptr(thetaT), r1 - r0, r0, r1, 0, st)
-        _lib.call("wq_ystage_mma", NE, NE, n, nB, wc, _lib.ptr(L["v_lo"]), *mcols,
-                  _lib.ptr(CrD), _lib.ptr(LtD), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
-                  kD, kC, _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), st)
-    _lib.call("wq_ystage", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
-              _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *cols, _lib.ptr(d["u"]), da1, *tail,
-              L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, 0, kT, kC, st)
-    _lib.call("wq_ystage", NE, NE, n, nB, nB, wc, _lib.ptr(L["vcols"]),
-              _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *cols, _lib.ptr(d["v"]), nB, *tail,
-              L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), kD, kC, st)
+        if want_theta:      # (the first prep also re-lays the table out: Tb)
+            CrT, LtT = torch.empty((5, N, kpT), **f64), torch.empty((N, 5), **f64)
+            _lib.call("wq_ystage_mma_prep", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
+                      _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *common, _lib.ptr(d["u"]), da1,
+                      _lib.ptr(d["v"]), _lib.ptr(d["elh"]), _lib.ptr(m2u), da1, _lib.ptr(d["ca"]),
+                      _lib.ptr(d["cb"]), _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum),
+                      _lib.ptr(Tb), n_tab, st)
+        if want_d:
+            CrD, LtD = torch.empty((5, NE, kpD), **f64), torch.empty((NE, 5), **f64)
+            tb = None if want_theta else _lib.ptr(Tb)
+            _lib.call("wq_ystage_mma_prep", NE, NE, n, nB, nB, wc, _lib.ptr(L["vcols"]),
+                      _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *common, _lib.ptr(d["v"]), nB,
+                      _lib.ptr(d["v"]), _lib.ptr(d["elh"]), None if tb is None else _lib.ptr(m2u),
+                      da1, _lib.ptr(d["ca"]), _lib.ptr(d["cb"]), _lib.ptr(CrD), _lib.ptr(LtD),
+                      _lib.ptr(vsum), tb, n_tab, st)
+        if want_theta:
+            _lib.call("wq_ystage_mma", N, NE, n, da1, wc, _lib.ptr(L["u_lo"]), *mcols,
+                      _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
+                      kT, kC, _lib.ptr(thetaT), r1 - r0, r0, r1, 0, st)
+        if want_d:
+            _lib.call("wq_ystage_mma", NE, NE, n, nB, wc, _lib.ptr(L["v_lo"]), *mcols,
+                      _lib.ptr(CrD), _lib.ptr(LtD), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
+                      kD, kC, _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), st)
+    if want_theta:
+        _lib.call("wq_ystage", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
+                  _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *cols, _lib.ptr(d["u"]), da1, *tail,
+                  L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, 0, kT, kC, st)
+    if want_d:
+        _lib.call("wq_ystage", NE, NE, n, nB, nB, wc, _lib.ptr(L["vcols"]),
+                  _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *cols, _lib.ptr(d["v"]), nB, *tail,
+                  L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), kD, kC, st)
     if len(glist):
-        _blocks_theta_d(disc, lp, d, outer=glist, thetaT=thetaT, D=D, rows=rows)
+        _blocks_theta_d(disc, lp, d, outer=glist, thetaT=thetaT, D=D, rows=rows,
+                        want_theta=want_theta, want_d=want_d)
     # D's lower storage triangle is complete (lattice + block parts): mirror it
-    if _YS_SYM_D:
+    if want_d and _YS_SYM_D:
         _lib.call("wq_mirror_lower", _lib.ptr(D), NE, NE, st)
     return thetaT, D
 
 
-def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None, rows=None):
+def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None, rows=None,
+                    want_theta=True, want_d=True):
     """Theta^T (N_E x N) and D (N_E x N_E) of a graded mesh: per-pair blocks
     for chunks of outer elements (all of them, or the runs of ``outer``), then
     deterministic gathers, accumulating into ``thetaT`` / ``D`` when given
@@ -885,10 +942,9 @@ def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None, rows=
     wd = torch.empty((n, nB, nB, chunk), dtype=torch.float64, device="cuda")
     flags = torch.empty((n, -(-chunk // 64)), dtype=torch.int32, device="cuda")
     r0, r1 = (0, N) if rows is None else rows
-    if thetaT is None:
-        thetaT = torch.zeros((NE, r1 - r0), dtype=torch.float64, device="cuda")
-        D = torch.zeros((NE, NE), dtype=torch.float64, device="cuda")
     if outer is None:
+        thetaT = torch.zeros((NE, r1 - r0), dtype=torch.float64, device="cuda") if want_theta else None
+        D = torch.zeros((NE, NE), dtype=torch.float64, device="cuda") if want_d else None
         ranges = [(e0, min(n, e0 + chunk)) for e0 in range(0, n, chunk)]
     else:   # contiguous runs of the listed outer elements, split into chunks
         cuts = np.flatnonzero(np.diff(outer) != 1) + 1
@@ -913,12 +969,13 @@ def _blocks_theta_d(disc, lp: LogPart, d, outer=None, thetaT=None, D=None, rows=
                   _lib.ptr(wd), chunk, _lib.ptr(flags), st)
         uc, vc = lp.ucols[e0:e1], lp.vcols[e0:e1]
         i0, i1 = max(int(uc.min()), r0), min(int(uc.max()) + 1, r1)
-        if i1 > i0:
+        if want_theta and i1 > i0:
             _lib.call("wq_gen_gather_theta", N, NE, e0, e1, chunk, i0, i1, wu, wv, nU, nB,
                       _lib.ptr(d["u_el"]), _lib.ptr(d["u_loc"]), _lib.ptr(d["v_el"]),
                       _lib.ptr(d["v_loc"]), _lib.ptr(wt), _lib.ptr(thetaT), r1 - r0, r0, st)
-        _lib.call("wq_gen_gather_d", NE, e0, e1, chunk, int(vc.min()), int(vc.max()) + 1, wv, nB,
-                  _lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(wd), _lib.ptr(D), st)
+        if want_d:
+            _lib.call("wq_gen_gather_d", NE, e0, e1, chunk, int(vc.min()), int(vc.max()) + 1, wv,
+                      nB, _lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]), _lib.ptr(wd), _lib.ptr(D), st)
     return thetaT, D
 
 

@@ -55,7 +55,7 @@ __device__ __forceinline__ double k1_value(const wq_smooth_t& sm, int64_t qa, co
 
 __global__ void __launch_bounds__(IK1_THREADS)
 ik1_tile_kernel(wq_smooth_t sm, int64_t row0, int64_t row1, int64_t col0, int64_t col1, double* X,
-                int64_t ldx, int accumulate, int span, int* flag, int sym) {
+                int64_t ldx, int accumulate, int span, int qc, int* flag, int sym) {
   extern __shared__ double smem[];
   __shared__ double2 ltab[64];
   // sym: rows == cols; only tiles on or above the diagonal, mirrored (K1 is
@@ -73,8 +73,8 @@ ik1_tile_kernel(wq_smooth_t sm, int64_t row0, int64_t row1, int64_t col0, int64_
 
   NodeRec* qn = reinterpret_cast<NodeRec*>(smem);         // span
   NodeRec* rn = qn + span;                                // span
-  double* K = reinterpret_cast<double*>(rn + span);       // span * span
-  double* T = K + (size_t)span * span;                    // span * TJ
+  double* K = reinterpret_cast<double*>(rn + span);       // qc * span (a chunk of q rows)
+  double* T = K + (size_t)qc * span;                      // span * TJ
   double* Gi = T + (size_t)span * IK1_TJ;                 // TI * wg
   double* Gj = Gi + IK1_TI * wg;                          // TJ * wg
   int* qidx = reinterpret_cast<int*>(Gj + IK1_TJ * wg);   // span
@@ -101,27 +101,31 @@ ik1_tile_kernel(wq_smooth_t sm, int64_t row0, int64_t row1, int64_t col0, int64_
   }
   __syncthreads();
 
+  // K1 rows in chunks of qc outer nodes (the whole span x span tile does not fit
+  // shared memory for wide rules, e.g. p = 5 with nref = 2), each chunk
+  // contracted into T[q][jj] = sum_w K[q][r_j + w] G[j][w] before the next
   int bad = 0;
-  for (int k = threadIdx.x; k < nQ * nR; k += blockDim.x) {
-    int a = k / nR, b = k - a * nR;
-    K[a * span + b] = k1_value(sm, qidx[a], qn[a], ridx[b], rn[b], &bad, ltab);
+  for (int q0c = 0; q0c < nQ; q0c += qc) {
+    const int nq_c = min(qc, nQ - q0c);
+    for (int k = threadIdx.x; k < nq_c * nR; k += blockDim.x) {
+      int a = k / nR, b = k - a * nR;
+      K[a * span + b] = k1_value(sm, qidx[q0c + a], qn[q0c + a], ridx[b], rn[b], &bad, ltab);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nq_c * IK1_TJ; k += blockDim.x) {
+      int a = k / IK1_TJ, jj = k - a * IK1_TJ;
+      double acc = 0.0;
+      if (jj < nj) {
+        int r0 = (int)(sm.g_start[J0 + jj] - rlo);
+        const double* kr = K + a * span + r0;
+        const double* gj = Gj + jj * wg;
+        for (int w = 0; w < wg; ++w) acc = fma(kr[w], gj[w], acc);
+      }
+      T[(q0c + a) * IK1_TJ + jj] = acc;
+    }
+    __syncthreads();
   }
   if (bad) atomicOr(flag, WQ_FLAG_R_NONPOSITIVE);
-  __syncthreads();
-
-  // T[q][jj] = sum_w K[q][r_j + w] G[j][w]
-  for (int k = threadIdx.x; k < nQ * IK1_TJ; k += blockDim.x) {
-    int q = k / IK1_TJ, jj = k - q * IK1_TJ;
-    double acc = 0.0;
-    if (jj < nj) {
-      int r0 = (int)(sm.g_start[J0 + jj] - rlo);
-      const double* kr = K + q * span + r0;
-      const double* gj = Gj + jj * wg;
-      for (int w = 0; w < wg; ++w) acc = fma(kr[w], gj[w], acc);
-    }
-    T[q * IK1_TJ + jj] = acc;
-  }
-  __syncthreads();
 
   // X[i][j] = sum_w G[i][w] T[q_i + w][jj]
   for (int k = threadIdx.x; k < ni * IK1_TJ; k += blockDim.x) {
@@ -157,18 +161,22 @@ extern "C" int wq_ik1(const wq_smooth_t* sm, int64_t row0, int64_t row1, int64_t
     return WQ_EINVAL;
   }
   int span = (int)max_span;
-  size_t smem = (size_t)2 * span * sizeof(NodeRec) + (size_t)span * span * 8 +
-                (size_t)span * IK1_TJ * 8 + (size_t)(IK1_TI + IK1_TJ) * sm->wg * 8 +
-                (size_t)2 * span * sizeof(int);
-  if (smem > 227 * 1024) {
-    set_error("wq_ik1: node span %d too large for one tile (%zu B smem)", span, smem);
+  const size_t fixed = (size_t)2 * span * sizeof(NodeRec) + (size_t)span * IK1_TJ * 8 +
+                       (size_t)(IK1_TI + IK1_TJ) * sm->wg * 8 + (size_t)2 * span * sizeof(int);
+  const size_t budget = 225 * 1024;   // + the static ln table, under the 227 KB opt-in limit
+  // K1 rows per chunk: the whole span when it fits, else as many as fit
+  const int64_t qfit = fixed < budget ? (int64_t)((budget - fixed) / ((size_t)span * 8)) : 0;
+  const int qc = (int)(qfit < span ? qfit : span);
+  if (qc < 1) {
+    set_error("wq_ik1: node span %d too large for one tile", span);
     return WQ_EUNSUPPORTED;
   }
+  const size_t smem = fixed + (size_t)qc * span * 8;
   cudaFuncSetAttribute(ik1_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(ceil_div(col1 - col0, IK1_TJ), ceil_div(row1 - row0, IK1_TI));
   // the full square (the assemble_ik1 / general-path call) uses the symmetry
   const int sym = row0 == col0 && row1 == col1 && IK1_TI == IK1_TJ;
   ik1_tile_kernel<<<grid, IK1_THREADS, smem, (cudaStream_t)stream>>>(*sm, row0, row1, col0, col1, X,
-                                                                     ldx, accumulate, span, flag, sym);
+                                                                     ldx, accumulate, span, qc, flag, sym);
   return check_launch("wq_ik1");
 }

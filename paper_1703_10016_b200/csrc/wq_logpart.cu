@@ -253,10 +253,11 @@ __device__ __forceinline__ int64_t gap_index(const wq_pairs_t& pp, int64_t e, in
 }
 
 // Theta^T[l][i] = sum_{(f,b) in inc_v(l)} sum_{(e,a) in inc_u(i)} u[e][:,a]^T M2[gap] v[f][:,b]
-__global__ void theta_t_kernel(wq_pairs_t pp, double* out) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// (columns i in [row0, row1) only: a rank's row block, out[l * ld + i - row0])
+__global__ void theta_t_kernel(wq_pairs_t pp, int64_t row0, int64_t row1, int64_t ld, double* out) {
+  int64_t i = row0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t l = blockIdx.y;
-  if (i >= pp.n_rows) return;
+  if (i >= row1) return;
   const int nA = (int)pp.da + 1, nB = (int)pp.db + 1, nU = (int)pp.pu + 1;
   double acc = 0.0;
   for (int vb = 0; vb < pp.wv; ++vb) {
@@ -279,7 +280,7 @@ __global__ void theta_t_kernel(wq_pairs_t pp, double* out) {
       acc += s;
     }
   }
-  out[l * pp.n_rows + i] = acc;
+  out[l * ld + i - row0] = acc;
 }
 
 // D[l][m] = sum_{(e,a) in inc_v(l)} sum_{(f,b) in inc_v(m)} v[e][:,a]^T M2[gap][:db+1] v[f][:,b]
@@ -554,8 +555,19 @@ int wq_theta_t(const wq_pairs_t* pp, double* thetaT, void* stream) {
     return WQ_EINVAL;
   }
   dim3 grid(ceil_div(pp->n_rows, 128), (unsigned)pp->n_fine);
-  theta_t_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*pp, thetaT);
+  theta_t_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*pp, 0, pp->n_rows, pp->n_rows, thetaT);
   return check_launch("wq_theta_t");
+}
+
+int wq_theta_t_rows(const wq_pairs_t* pp, int64_t row0, int64_t row1, double* thetaT, int64_t ld,
+                    void* stream) {
+  if (!pp || !thetaT || row0 < 0 || row1 > pp->n_rows || row1 <= row0 || ld < row1 - row0) {
+    set_error("wq_theta_t_rows: bad arguments");
+    return WQ_EINVAL;
+  }
+  dim3 grid(ceil_div(row1 - row0, 128), (unsigned)pp->n_fine);
+  theta_t_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*pp, row0, row1, ld, thetaT);
+  return check_launch("wq_theta_t_rows");
 }
 
 int wq_dmat(const wq_pairs_t* pp, double* D, void* stream) {

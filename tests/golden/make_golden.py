@@ -69,8 +69,33 @@ def space_dict(space):
     return {"degree": int(space.degree), "knots": space.knots.tolist(), "closed": bool(space.closed)}
 
 
+class RecordingDatum:
+    """Wraps a problem-defined Dirichlet datum (problems.py:48-150) and records
+    every (s, u_D(s)) the reference evaluates, so the GPU tests can replay the
+    reference's own values as a tabulated datum (the problem code stays in the
+    reference)."""
+
+    def __init__(self, fn):
+        self.fn, self.pts, self.vals = fn, [], []
+
+    def __call__(self, s):
+        v = np.asarray(self.fn(s), dtype=float)
+        self.pts.append(np.atleast_1d(np.asarray(s, float)).ravel().copy())
+        self.vals.append(np.atleast_1d(v).ravel().copy())
+        return v
+
+    def table(self):
+        pts = np.concatenate(self.pts)
+        vals = np.concatenate(self.vals)
+        pts, idx = np.unique(pts, return_index=True)
+        return pts, vals[idx]
+
+
 def run_case(name, curve, space, dirichlet=None, dname=None, b2=False, out=None, nref=1):
     t0 = time.time()
+    tabulate = dname in ("parabola", "closed-smooth")
+    if tabulate:
+        dirichlet = RecordingDatum(dirichlet)
     disc = A.build_discretization(curve, space, nref)
     tb = time.time() - t0
     ik1 = A.assemble_ik1(disc)
@@ -99,6 +124,8 @@ def run_case(name, curve, space, dirichlet=None, dname=None, b2=False, out=None,
         rec["b1"] = A.assemble_b1(curve, space, dirichlet)
         if b2:
             rec["b2"] = A.assemble_b2(curve, space, dirichlet)
+        if tabulate:
+            rec["g_pts"], rec["g_vals"] = dirichlet.table()
     if out is not None:
         out.update(rec)
     np.savez_compressed(os.path.join(HERE, name + ".npz"), **rec)
@@ -183,7 +210,14 @@ def main(which=None):
     for name, curve, space, g, gname in (
             ("ell_p3_n32_nref2", ell, make_cyclic_basis(3, np.linspace(0, 1, 33)), g_ell,
              "exp(x)cos(y)"),
-            ("slit_p2_n16_nref2", slit, make_open_basis(2, np.linspace(-1, 1, 17)), sq, "x^2")):
+            ("slit_p2_n16_nref2", slit, make_open_basis(2, np.linspace(-1, 1, 17)), sq, "x^2"),
+            # the widest rule bands (degree 4 / 5 with nref = 2)
+            ("ell_p4_n24_nref2", ell, make_cyclic_basis(4, np.linspace(0, 1, 25)), g_ell,
+             "exp(x)cos(y)"),
+            ("ell_p5_n128_nref2", ell, make_cyclic_basis(5, np.linspace(0, 1, 129)), g_ell,
+             "exp(x)cos(y)"),
+            ("slit_p4_n20_nref2", slit, make_open_basis(4, np.linspace(-1, 1, 21)), sq, "x^2"),
+            ("slit_p5_n128_nref2", slit, make_open_basis(5, np.linspace(-1, 1, 129)), sq, "x^2")):
         if which and not any(w in name for w in which):
             continue
         run_case(name, curve, space, g, gname, False, nref=2)

@@ -63,3 +63,47 @@ def test_config3_degree_sweep_rows_match_oracle(cuda, p):
     rows = np.array([0, 1, 777, 2048, 4095])
     _, err = _rows_vs_oracle(_star(), space, rows)
     assert err <= TOL, err
+
+
+def test_config5_full_size_rows_match_general_oracle(cuda):
+    """Config 5 at its stated size (N = 20418: p = 4, 16384 graded elements,
+    4030 double knots; the reference raises on graded meshes,
+    quadrature.py:489-491): sampled rows of A against the oracle's row
+    restatement for graded open meshes (oracle.GeneralRows, pinned to the
+    dense general restatement and to the reference goldens in
+    tests/test_oracle.py).  Rows: first / last, both graded ends, rows on
+    double knots, interior, and the rows holding max|A| and the extreme
+    diagonal entries (so max|A| and the diagonal's range are pinned too)."""
+    torch = cuda
+    from oracle import wq_oracle as O
+    sp = O.config5_space()
+    curve = W.load_curve({"degree": 1, "knots": [-1, -1, 1, 1], "control_points": [[-1, 0], [1, 0]]})
+    space = W.BasisSpec(sp.degree, sp.knots, False)
+    disc = W.build_discretization(curve, space, 1)
+    N = space.dim
+    assert N == 20418 and AS._log_part(disc).graded
+    A = AS.assemble_matrix_device(disc)
+    flat = int(A.abs().argmax())
+    imax, jmax = divmod(flat, N)
+    amax = float(A.abs().max())
+    dg = A.diagonal()
+    dlo, dhi = int(dg.argmin()), int(dg.argmax())
+    # functions whose support holds a double knot (interior and near the graded zone)
+    kn = np.asarray(sp.knots)
+    inner, cnt = np.unique(kn[sp.degree + 1: -sp.degree - 1], return_counts=True)
+    dbl = inner[cnt == 2]
+    dbl_rows = [int(np.searchsorted(kn, x)) - sp.degree for x in (dbl[0], dbl[len(dbl) // 2], dbl[-1])]
+    rows = np.unique(np.array([0, 1, 3, 7, 40, 100, 2500, 5000, 10209, 15000, N - 101, N - 41,
+                               N - 8, N - 4, N - 2, N - 1, imax, dlo, dhi] + dbl_rows))
+    rows = rows[(rows >= 0) & (rows < N)]
+    assert len(rows) >= 16
+    gr = O.GeneralRows(O.Curve(O.open_basis(1, np.array([-1.0, 1.0])), [[-1, 0], [1, 0]]), sp)
+    ref = gr.a_rows(rows)
+    got = A[torch.as_tensor(rows, device="cuda")].cpu().numpy()
+    err = float(np.abs(got - ref).max() / amax)
+    assert err <= TOL, err
+    k = int(np.flatnonzero(rows == imax)[0])
+    assert abs(abs(ref[k, jmax]) - amax) / amax <= TOL          # max|A| pinned
+    assert np.abs(np.diag(got[:, rows]) - ref[np.arange(len(rows)), rows]).max() / amax <= TOL
+    assert bool(torch.isfinite(A).all())
+    assert bool(torch.equal(A[:2048, :2048], A[:2048, :2048].T))

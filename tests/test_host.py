@@ -275,3 +275,23 @@ def test_graded_gather_dataflow_in_numpy():
         theta, dmm, _ = O.ik2_ingredients_general(od)
         assert rel(thT.T, theta) <= 1e-13
         assert rel(D, dmm) <= 1e-13
+
+
+def test_regular_rules_list_like_reference():
+    """disc.regular_rules is the reference's list of WeightedRule
+    (quadrature.py:150-176): stacking it as rules_matrix does, times J, gives G;
+    singular_rules raises a clear UsageError (not built)."""
+    from paper_1703_10016_b200.errors import UsageError
+    z, meta = load("slit_p4_n24_dbl")
+    curve, space = product_objects(meta)
+    disc = W.build_discretization(curve, space, 1)
+    rules = disc.regular_rules
+    assert len(rules) == space.dim and rules[3].tag == ("basis", 3)
+    dense = np.zeros((len(rules), disc.nodes.n))
+    for k, r in enumerate(rules):
+        dense[k, r.idx] = r.weights
+    assert np.array_equal(dense * disc.J_nodes[None, :], disc.G)
+    g = np.cos(disc.nodes.nodes)
+    assert abs(rules[5].apply(g) - rules[5].full_weights(disc.nodes.n) @ g) <= 1e-15
+    with pytest.raises(UsageError):
+        disc.singular_rules

@@ -163,3 +163,46 @@ def test_gauss_beats_closed_form_off_contact():
             assert (np.abs(m - ref) / nat).max() <= 5e-15
             c = O.pair_moments_closed(da, db, one, rho * one, dl * one)[0]
             assert (np.abs(c - ref) / nat).max() >= 1e-4
+
+
+def test_tiered_far_orders():
+    """Far-pair Gauss orders by separation (30 | 16 | 12, oracle
+    pair_moments_tiered) against order 30 everywhere, relative to the natural
+    slot scale h_e^(a+1) h_f^(b+1), for graded widths (config 5's end elements
+    are 0.9^60 ~ 1.8e-3 of the interior width)."""
+    rng = np.random.default_rng(3)
+    n = 400
+    he = 10.0 ** rng.uniform(-4, -2, n)
+    hf = he * 10.0 ** rng.uniform(-3, 3, n)
+    sep = np.maximum(he, hf) * 10.0 ** rng.uniform(-1.5, 2, n)
+    delta = np.sign(rng.uniform(-1, 1, n)) * (sep + 0.5 * (he + hf))
+    da, db = 16, 4
+    a = O.pair_moments_tiered(da, db, he, hf, delta)
+    b = O.pair_moments_general(da, db, he, hf, delta)
+    nat = he[:, None, None] ** (np.arange(da + 1)[None, :, None] + 1.0) * \
+        hf[:, None, None] ** (np.arange(db + 1)[None, None, :] + 1.0)
+    assert np.abs((a - b) / nat).max() <= 5e-15 * 10
+
+
+@pytest.mark.parametrize("name", ["c1_slit_p2_n64", "slit_p4_n24_dbl", "slit_p3_n24"])
+def test_general_rows_match_reference(name):
+    """oracle.GeneralRows (the row restatement used at config-5 size) against
+    the reference's own A on uniform open meshes (lattice = every element)."""
+    z, meta = load(name)
+    oc, ob = oracle_objects(meta)
+    gr = O.GeneralRows(oc, ob, meta["nref"])
+    rows = np.arange(ob.dim)
+    assert np.abs(gr.a_rows(rows) - z["A"]).max() / np.abs(z["A"]).max() <= 1e-13
+
+
+def test_general_rows_match_dense_general_on_graded_mesh():
+    """... and against the dense general restatement on a config-5 reading
+    at 96 elements (graded ends, double knots: off-lattice elements)."""
+    slit = O.Curve(O.open_basis(1, np.array([-1.0, 1.0])), [[-1, 0], [1, 0]])
+    sp = O.config5_space(n_el=96, growth_elems=12)
+    gr = O.GeneralRows(slit, sp)
+    assert len(gr.off) > 0
+    od = O.build_discretization(slit, sp, 1)
+    ref = O.scale_and_symmetrize(O.dense_ik1(od) + O.dense_ik2_general(od))[0]
+    rows = np.array([0, 1, 5, 40, sp.dim - 2, sp.dim - 1])
+    assert np.abs(gr.a_rows(rows) - ref[rows]).max() / np.abs(ref).max() <= 1e-13
