@@ -394,7 +394,7 @@ __global__ void transpose_kernel(const double* in, int64_t rows, int64_t cols, d
 // per batch with every load of the batch issued before its FMAs (the per-row loop
 // was DRAM-latency bound: one P load in flight per thread)
 constexpr int GF_ROWS = 32;
-constexpr int GF_MAXWS = 16;
+constexpr int GF_MAXWS = 20;   // 3p + 2 fine functions per S column: nref = 2 up to p = 6
 constexpr int GF_B = 4;
 template <int WS>
 __global__ void __launch_bounds__(128) gather_fs_kernel(wq_logpart_t lp, double alpha,
@@ -484,6 +484,10 @@ __global__ void __launch_bounds__(128) add_st_phi_kernel(wq_logpart_t lp, const 
     case 14: CALL(14); break;  \
     case 15: CALL(15); break;  \
     case 16: CALL(16); break;  \
+    case 17: CALL(17); break;  \
+    case 18: CALL(18); break;  \
+    case 19: CALL(19); break;  \
+    case 20: CALL(20); break;  \
   }
 
 }  // namespace wq
