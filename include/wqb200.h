@@ -404,6 +404,18 @@ int wq_mirror_lower(double* out, int64_t n, int64_t ld, void* stream);
  * symmetric multi-GPU path: each rank assembles the upper tile pairs of its rows). */
 int wq_mirror_upper(double* out, int64_t n, int64_t ld, void* stream);
 
+/* Packed upper-triangle blocks (multi-GPU all-gather of the symmetric
+ * assembly, half the bytes of full rows): the upper tiles A(I, J), J >= I, of
+ * the 64 x 64 tile pairs [p0, p1) in row-by-row pair order, tile-major
+ * (pair p at (p - p0) * 4096 doubles, row-major 64 x 64; entries outside an
+ * edge tile unused).
+ * wq_pack_pairs: A (ld) -> packed.
+ * wq_unpack_pairs: packed -> A(I, J) and its transpose into A(J, I). */
+int wq_pack_pairs(const double* A, int64_t n, int64_t ld, int64_t p0, int64_t p1, double* packed,
+                  void* stream);
+int wq_unpack_pairs(const double* packed, int64_t n, int64_t p0, int64_t p1, double* A, int64_t ld,
+                    void* stream);
+
 /* General-path row blocks (multi-GPU; X-form, assembly.py:233-245):
  * wq_gather_fs_rows: P[m][i - i0] = alpha P[m][i - i0] - sum_t F[m][s_i + t] S_i[t],
  *   i in [i0, i1), P with leading dimension ldp (the block's Theta^T columns);

@@ -44,6 +44,20 @@ __device__ __forceinline__ bool near_pair_j2(const wq_smooth_t& sm, int64_t qa, 
   return true;
 }
 
+// upper-triangle tile pair index -> (bi, bj), bi <= bj; tile row bi holds nb - bi
+// pairs, pairs numbered row by row
+__device__ __forceinline__ void tri_index(int64_t t, int nb, int& bi, int& bj) {
+  double B = 2.0 * nb + 1.0;
+  int b = (int)floor((B - sqrt(B * B - 8.0 * (double)t)) * 0.5);
+  if (b < 0) b = 0;
+  if (b > nb - 1) b = nb - 1;
+  auto start = [nb](int64_t x) { return x * nb - x * (x - 1) / 2; };
+  while (b > 0 && start(b) > t) --b;
+  while (b + 1 < nb && start(b + 1) <= t) ++b;
+  bi = b;
+  bj = b + (int)(t - start(b));
+}
+
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kTwoPi = 6.28318530717958647692;
 

@@ -126,20 +126,6 @@ __device__ __forceinline__ double half_ln(double x, const double* __restrict__ t
   return t_hi + fma(r, 0.5, fma(r2, q, t_lo));
 }
 
-// upper-triangle tile pair index -> (bi, bj), bi <= bj, row bi holds nb - bi pairs
-__device__ __forceinline__ void tri_index(int64_t t, int nb, int& bi, int& bj) {
-  double B = 2.0 * nb + 1.0;
-  int b = (int)floor((B - sqrt(B * B - 8.0 * (double)t)) * 0.5);
-  if (b < 0) b = 0;
-  if (b > nb - 1) b = nb - 1;
-  auto start = [nb](int64_t x) { return x * nb - x * (x - 1) / 2; };
-  while (b > 0 && start(b) > t) --b;
-  while (b + 1 < nb && start(b + 1) <= t) ++b;
-  bi = b;
-  bj = b + (int)(t - start(b));
-}
-
-
 // ---------------------------------------------------------------------------
 // ik1_sym_kernel: closed uniform nodes, rule i on nodes 2(i-p)+1 .. 2(i-p)+2p+1
 // ---------------------------------------------------------------------------

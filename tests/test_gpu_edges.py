@@ -56,20 +56,10 @@ def test_partial_edge_tiles(cuda, p, N):
     AS._assemble_v2(disc, X, -1.0 / (4 * np.pi), chunks=5)
     torch.cuda.synchronize()
     assert torch.equal(X, A)
-    # symmetric multi-GPU row blocks, two ranks emulated in turn
-    sub, n_pad = D.cyclic_blocks(N, 2, 2)
-    G = torch.full((n_pad, N), float("nan"), dtype=torch.float64, device="cuda")
-    for rank in range(2):
-        B = torch.full((n_pad, N), float("nan"), dtype=torch.float64, device="cuda")
-        for c in range(2):
-            b = c * 2 + rank
-            r0, r1 = b * sub, min((b + 1) * sub, N)
-            if r1 > r0:
-                D.upper_rows_device(disc, B, r0, r1)
-                G[r0:r1] = B[r0:r1]
-    _lib.call("wq_mirror_upper", _lib.ptr(G), N, G.stride(0), _lib.stream_handle())
-    torch.cuda.synchronize()
-    assert torch.equal(G[:N], A)
+    # symmetric multi-GPU path (packed upper tiles), three ranks emulated in turn
+    from test_gpu_parity import emulate_packed_ranks
+    bufs, _ = emulate_packed_ranks(disc, 3, 2)
+    assert all(torch.equal(B, A) for B in bufs)
     # unsymmetrised row blocks (rect tiles) + epilogue
     bounds, per = D.row_blocks(N, 2)
     Xr = torch.zeros((per * 2, N), dtype=torch.float64, device="cuda")
