@@ -205,9 +205,82 @@ def committed_traffic(dom):
         return None
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_ladder(sizes, with_ebe=True, ebe_max=1024):
+    """The UNMODIFIED reference (``wqbem`` installed into baseline/_ref) through
+    its own public API on this host's cores: build_discretization
+    (rule_seconds, assembly.py:147-172), assemble_weighted_matrix cold (first
+    call, pair-table lru_cache empty) and warm, with the reference's own
+    seconds (assembly.py:248-259), and the element-by-element
+    assemble_baseline_matrix(ng=12) with its own timer (assembly.py:418-538),
+    on the ellipse p = 3 ladder (N = 1024 is config 2) and config 1; plus a
+    power-law fit of the weighted path's seconds to config 4 (N = 32768),
+    labelled as an extrapolation (the reference cannot run it)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "wqbem")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref)"}
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import wqbem
+    from wqbem import assembly as RA
+    from wqbem.geometry import load_curve
+    from wqbem.splines import make_cyclic_basis, make_open_basis
+    th = 2 * np.pi * np.arange(16) / 16
+    ell = load_curve({"degree": 3, "closed": True, "breakpoints": np.linspace(0, 1, 17).tolist(),
+                      "control_points": np.column_stack([2 * np.cos(th), np.sin(th)]).tolist()})
+    slit = load_curve({"degree": 1, "knots": [-1, -1, 1, 1], "control_points": [[-1, 0], [1, 0]]})
+    cases = [("C1 slit p=2", slit, make_open_basis(2, np.linspace(-1, 1, 65)))]
+    cases += [(f"ellipse p=3 N={n}" + (" (C2)" if n == 1024 else ""), ell,
+               make_cyclic_basis(3, np.linspace(0, 1, n + 1))) for n in sizes]
+    rows = []
+    for name, curve, space in cases:
+        N = space.dim
+        t0 = time.perf_counter()
+        disc = RA.build_discretization(curve, space, 1)
+        build_s = time.perf_counter() - t0
+        from wqbem import quadrature as RQ
+        for fn in (getattr(RQ, "_unit_pair_stack", None),):
+            if fn is not None and hasattr(fn, "cache_clear"):
+                fn.cache_clear()
+        _, _, cold = RA.assemble_weighted_matrix(disc)
+        _, _, warm = RA.assemble_weighted_matrix(disc)
+        rec = {"case": name, "N": N, "build_s": build_s, "rule_seconds": disc.rule_seconds,
+               "weighted_cold_s": cold, "weighted_warm_s": warm,
+               "weighted_entries_per_s": N * N / warm}
+        if with_ebe and N <= ebe_max:
+            _, _, ebe = RA.assemble_baseline_matrix(curve, space, ng=12)
+            rec.update(ebe_s=ebe, ebe_entries_per_s=N * N / ebe)
+        rows.append(rec)
+        del disc
+    lad = [r for r in rows if r["case"].startswith("ellipse")]
+    fit = None
+    lad = lad[-2:]    # the two largest sizes: closest to the asymptotic law (N^2.5-3, SURVEY 3.3)
+    if len(lad) >= 2:
+        x = np.log([r["N"] for r in lad])
+        y = np.log([r["weighted_warm_s"] for r in lad])
+        k, c = np.polyfit(x, y, 1)
+        t4 = float(np.exp(c + k * np.log(32768)))
+        fit = {"law": f"seconds ~ N^{k:.2f} (fit over N = {[r['N'] for r in lad]})",
+               "c4_seconds_extrapolated": t4, "c4_entries_per_s_extrapolated": 32768 ** 2 / t4,
+               "label": "EXTRAPOLATION: the reference cannot run C4 (550 GB pair tensor, SURVEY F6)"}
+        e = [r for r in rows if r["case"].startswith("ellipse") and "ebe_s" in r][-2:]
+        if len(e) >= 2:
+            k2, c2 = np.polyfit(np.log([r["N"] for r in e]), np.log([r["ebe_s"] for r in e]), 1)
+            t5 = float(np.exp(c2 + k2 * np.log(32768)))
+            fit.update(ebe_law=f"seconds ~ N^{k2:.2f}", ebe_c4_seconds_extrapolated=t5,
+                       ebe_c4_entries_per_s_extrapolated=32768 ** 2 / t5)
+    return {"package": f"wqbem {wqbem.__version__} (unmodified, baseline/_ref)",
+            "cores": os.cpu_count(),
+            "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS", "unset (all cores)"),
+            "cases": rows, "c4_fit": fit}
+
+
 def run_reference(args):
     """CPU oracle port (reference algorithm, row-block restatement) on a
-    bounded row sample of the same workload; rank 0 only."""
+    bounded row sample of the same workload; rank 0 only.  The line also
+    carries the unmodified reference timed on the ladder it can run
+    (``reference_ladder``)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -246,6 +319,10 @@ def run_reference(args):
                                    f"the reference's warm path)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.ref_ladder:
+        t0 = time.perf_counter()
+        line["reference_ladder"] = reference_ladder([int(x) for x in args.ref_ladder.split(",")])
+        line["reference_ladder"]["wall_s"] = time.perf_counter() - t0
     print(json.dumps(line), flush=True)
 
 
@@ -292,7 +369,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--chunks", type=int, default=4,
                     help="N > 1: pair-range chunks per rank (all-gather pipelining depth)")
-    ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--ref-rows", type=int, default=8)
+    ap.add_argument("--ref-ladder", default="256,512,1024",
+                    help="--impl reference: N of the unmodified-reference ladder ('' = skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--launcher-check", action="store_true",
                     help="only check the one-rank-per-GPU launch (CPU, gloo)")
