@@ -47,8 +47,9 @@ __device__ __forceinline__ bool near_pair_j2(const wq_smooth_t& sm, int64_t qa, 
 // upper-triangle tile pair index -> (bi, bj), bi <= bj; tile row bi holds nb - bi
 // pairs, pairs numbered row by row
 __device__ __forceinline__ void tri_index(int64_t t, int nb, int& bi, int& bj) {
-  double B = 2.0 * nb + 1.0;
-  int b = (int)floor((B - sqrt(B * B - 8.0 * (double)t)) * 0.5);
+  // float estimate (MUFU), corrected exactly by the integer loops below
+  const float B = 2.0f * (float)nb + 1.0f;
+  int b = (int)floorf((B - sqrtf(fmaxf(B * B - 8.0f * (float)t, 0.0f))) * 0.5f);
   if (b < 0) b = 0;
   if (b > nb - 1) b = nb - 1;
   auto start = [nb](int64_t x) { return x * nb - x * (x - 1) / 2; };

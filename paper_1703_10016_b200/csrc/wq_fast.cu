@@ -22,6 +22,7 @@
 //
 // Both kernels are deterministic (no atomics on values).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -813,6 +814,282 @@ x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __rest
              rect ? (int64_t)tile_row0 * FT : 0, smem);
 }
 
+// ---------------------------------------------------------------------------
+// x2 v5 (x2v4_kernel): both Z' windows requested at CTA start (one mbarrier each);
+// the IK1 tile, the banded S fragments and the output tiles go straight between
+// global memory and registers in the DMMA accumulator layout (every access
+// sector-efficient: 64-byte row segments); only Phi and the orientation hand-off
+// T live in shared memory (~85 KB, 2 CTAs per SM).
+//
+//   phi (DMMA)  Phi[i][m] = sum_K Zext-window[..][K] Uext[i][K] in skewed
+//               coordinates, stored as Phs[i][m] (stride 76)
+//   S   (DMMA)  warp w owns one 8-column block of the output (j = 8w..8w+7 in
+//               orientation 0, i in orientation 1): its band B fragments are loaded
+//               once into registers and the warp sweeps the 8 row blocks with A
+//               fragments from Phs
+// Orientation 0 gives T = alpha (w IK1(I,J) + X2(I,J)) (accumulators start from
+// alpha w IK1); T goes through shared memory to the orientation-1 layout, whose
+// accumulators start from T^T and add alpha X2(J,I): A(J,I), stored to rows J
+// and, transposed, to rows I.  One tile pair per CTA: co-resident CTAs stay out
+// of phase, so one CTA's staging / hand-off / stores overlap the other's DMMAs (a
+// persistent grid of 2 CTAs per SM that refilled each window for its next pair
+// as soon as phi had read it ran the two CTAs in lock step: 9.2 vs 8.3 ms).
+// ---------------------------------------------------------------------------
+
+// loads issued where written (volatile: not sunk to their first use, so their HBM / L2
+// latency overlaps the phi DMMAs that follow)
+__device__ __forceinline__ double2 ld_cs_v2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_cs(const double* p) {
+  double v;
+  asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_nc(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+constexpr int X5_TS = 66;   // T hand-off [i][j] row stride (16-byte row-fragment stores)
+
+template <int P>
+struct X4Smem {
+  using C = X2Cfg<P>;
+  static constexpr int ZW = C::ZROWS * C::ZSTRIDE;                    // one Z' window
+  static constexpr int PH = FT * PSTRIDE;                             // Phi, then T
+  static_assert(FT * X5_TS <= PH, "T hand-off overflows the Phi buffer");
+  static constexpr int TOTAL = 2 * ZW + PH + 4;                       // + mbarriers
+};
+
+// first table row of the skewed Z' window of orientation o of tile pair (bi, bj)
+template <int P>
+__device__ __forceinline__ int64_t x5_gmin(int o, int bi, int bj) {
+  using C = X2Cfg<P>;
+  const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
+  const int64_t R0 = o == 0 ? I0 : J0;
+  const int64_t M0 = (o == 0 ? J0 : I0) - C::D;
+  return M0 - (R0 + 63) + P - C::AMAX;
+}
+
+// ZROWS contiguous table rows from gmin (mod n) into dst on the TMA engine (two pieces at
+// the seam), completing on bar
+template <int P>
+__device__ __forceinline__ void x5_window(double* dst, const double* Zext, int64_t n, int64_t gmin,
+                                          uint64_t* bar) {
+  using C = X2Cfg<P>;
+  constexpr unsigned RB = C::ZSTRIDE * 8;
+  int64_t g0 = gmin % n;
+  if (g0 < 0) g0 += n;
+  const uint64_t pol = l2_evict_last();    // the Z' table is re-read by every tile pair
+  const int64_t first = min((int64_t)C::ZROWS, n - g0);
+  mbar_arrive_expect_tx(bar, C::ZROWS * RB);
+  bulk_g2s_hint(dst, Zext + g0 * C::ZSTRIDE, (unsigned)first * RB, bar, pol);
+  if (first < C::ZROWS)
+    bulk_g2s_hint(dst + first * C::ZSTRIDE, Zext, (unsigned)(C::ZROWS - first) * RB, bar, pol);
+}
+
+template <int P>
+__global__ void __launch_bounds__(X2_THREADS, 2)
+x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
+            const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
+            int nb, int tile_row0, int64_t pair0) {
+  using C = X2Cfg<P>;
+  using L = X4Smem<P>;
+  constexpr int KS4 = C::KS / 4;
+  extern __shared__ double smem[];
+  double* Zs0 = smem;
+  double* Zs1 = Zs0 + L::ZW;
+  double* Phs = Zs1 + L::ZW;          // Phi[i][m] (both orientations), then the T hand-off
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Phs + L::PH);
+  const int64_t n = N;
+  const bool rect = tile_row0 >= 0;
+  const int64_t row_off = rect ? (int64_t)tile_row0 * FT : 0;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int r = lane >> 2, c = lane & 3;
+  const int norient = rect ? 1 : 2;
+  const bool with_ik1 = w_ik1 != 0.0;
+  const bool zbulk = n >= C::ZROWS;
+  int bi, bj;
+  tile_of_block(nb, tile_row0, pair0, bi, bj);
+  const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
+  const int ni = (int)min((int64_t)FT, N - I0);
+  const int nj = (int)min((int64_t)FT, N - J0);
+  const int64_t gmin[2] = {x5_gmin<P>(0, bi, bj), x5_gmin<P>(1, bi, bj)};
+
+  // Z' windows of both orientations, requested at once
+  if (zbulk) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int o = 0; o < norient; ++o) x5_window<P>(o == 0 ? Zs0 : Zs1, Zext, n, gmin[o], bar + o);
+  } else {
+    constexpr int CH = C::ZSTRIDE / 2;  // 16-byte chunks per table row
+    for (int o = 0; o < norient; ++o) {
+      double* dst = o == 0 ? Zs0 : Zs1;
+      int64_t g0 = gmin[o] % n;
+      if (g0 < 0) g0 += n;
+      for (int k = tid; k < C::ZROWS * CH; k += X2_THREADS) {
+        const int row = k / CH, cc = 2 * (k - row * CH);
+        int64_t g = g0 + row;
+        while (g >= n) g -= n;
+        cp_async16(dst + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
+      }
+    }
+  }
+  // Phi's pad columns (read by the band contraction against zero B entries) must be finite
+  for (int k = tid; k < FT * (PSTRIDE - C::SPAN); k += X2_THREADS)
+    Phs[(k / (PSTRIDE - C::SPAN)) * PSTRIDE + C::SPAN + k % (PSTRIDE - C::SPAN)] = 0.0;
+
+  // accumulators of orientation 0: lane (i = 8 ib + r, j = 8 warp + 2c + e); the raw IK1
+  // tile now (scaled by alpha w after phi0, when the loads have landed)
+  double acc[8][2];
+  {
+    const int jj = 8 * warp + 2 * c;
+    const double* src = X + (I0 - row_off) * ldx + J0 + jj;
+    const bool vec = with_ik1 && ni == FT && nj == FT && (ldx & 1) == 0 &&
+                     (reinterpret_cast<uintptr_t>(X + J0) & 15) == 0;
+#pragma unroll
+    for (int ib = 0; ib < 8; ++ib) {
+      const int ii = 8 * ib + r;
+      if (vec) {
+        const double2 v = ld_cs_v2(src + ii * ldx);
+        acc[ib][0] = v.x;
+        acc[ib][1] = v.y;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          acc[ib][e] = (with_ik1 && ii < ni && jj + e < nj) ? ld_cs(src + ii * ldx + e) : 0.0;
+      }
+    }
+  }
+
+  // one orientation: 0 = Phi rows I over the J range with band S_J, 1 = rows J over I, S_I
+  auto orient = [&](const int o) {
+    const int64_t R0 = o == 0 ? I0 : J0;
+    const int64_t M0 = (o == 0 ? J0 : I0) - C::D;
+    // B fragments of the alpha S band for this warp's column block (raw now, scaled after
+    // phi, when the loads have landed): bS[s] = S_{C0 + 8 warp + r}[4 s + c - r]
+    double bS[KS4];
+    {
+      const int64_t C0 = o == 0 ? J0 : I0;
+      const int nc = o == 0 ? nj : ni;
+      const int row = 8 * warp + r;
+#pragma unroll
+      for (int s2 = 0; s2 < KS4; ++s2) {
+        const int t = 4 * s2 + c - r;
+        bS[s2] = (t >= 0 && t <= 2 * C::D && row < nc) ? ld_nc(sw + (C0 + row) * C::WS + t) : 0.0;
+      }
+    }
+    if (zbulk) {
+      mbar_wait(bar + o, 0);
+    } else if (o == 0) {
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    phi_block<P>(Uext, N, o == 0 ? Zs0 : Zs1, Phs, M0, R0, gmin[o], warp);
+#pragma unroll
+    for (int s2 = 0; s2 < KS4; ++s2) bS[s2] *= alpha;
+    if (o == 0) {
+      const double aw = alpha * w_ik1;
+#pragma unroll
+      for (int rb = 0; rb < 8; ++rb) {
+        acc[rb][0] *= aw;
+        acc[rb][1] *= aw;
+      }
+    }
+    __syncthreads();
+    // band contraction (DMMA; the warp's band B fragments stay in registers):
+    // acc[rb][e] += sum_s Phs[8 rb + r][8 warp + 4 s + c] bS[s]
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb) {
+#pragma unroll
+      for (int s2 = 0; s2 < KS4; ++s2) {
+        const double a = Phs[(8 * rb + r) * PSTRIDE + 8 * warp + 4 * s2 + c];
+        dmma(acc[rb][0], acc[rb][1], a, bS[s2]);
+      }
+    }
+  };
+  orient(0);
+  if (rect) {
+    // unsymmetrised row block: X(I,J) = alpha (w IK1 + X2(I,J)) = T
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb) {
+      const int ii = 8 * rb + r;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jj = 8 * warp + 2 * c + e;
+        if (ii < ni && jj < nj) X[(I0 - row_off + ii) * ldx + J0 + jj] = acc[rb][e];
+      }
+    }
+    return;
+  }
+  {
+    // T[i][j] (i = 8 rb + r, j = 8 warp + 2c + e) -> acc of orientation 1: lane
+    // (j = 8 rb + r, i = 8 warp + 2c + e) starts from T[i][j]
+    __syncthreads();                         // Phi0 fully read
+    double* Tsm = Phs;
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb)
+      *reinterpret_cast<double2*>(Tsm + (8 * rb + r) * X5_TS + 8 * warp + 2 * c) =
+          make_double2(acc[rb][0], acc[rb][1]);
+    __syncthreads();
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) acc[rb][e] = Tsm[(8 * warp + 2 * c + e) * X5_TS + 8 * rb + r];
+    __syncthreads();                         // T read before Phi1 overwrites it
+  }
+  orient(1);
+
+  // acc[rb][e] = A(J,I)[j = 8 rb + r][i = 8 warp + 2c + e]: rows J (16-byte pieces, 64-byte
+  // row segments per 4 lanes) and the transpose into rows I (8-byte pieces, 64-byte segments)
+  const int i = 8 * warp + 2 * c;
+  const bool full = ni == FT && nj == FT && (ldx & 1) == 0 &&
+                    (reinterpret_cast<uintptr_t>(X + I0) & 15) == 0;
+  if (bi != bj) {
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb) {
+      const int j = 8 * rb + r;
+      double* rowJ = X + (J0 + j) * ldx + I0 + i;
+      if (full) {
+        __stcs(reinterpret_cast<double2*>(rowJ), make_double2(acc[rb][0], acc[rb][1]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (j < nj && i + e < ni) __stcs(rowJ + e, acc[rb][e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int rb = 0; rb < 8; ++rb) {
+        const int j = 8 * rb + r;
+        if (j < nj && i + e < ni) __stcs(X + (I0 + i + e) * ldx + J0 + j, acc[rb][e]);
+      }
+  } else {
+    // diagonal tile: entry (j, i) with i <= j written to both (j, i) and (i, j), so A is
+    // exactly symmetric
+#pragma unroll
+    for (int rb = 0; rb < 8; ++rb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = 8 * rb + r;
+        if (j < nj && i + e < ni && i + e <= j) {
+          __stcs(X + (J0 + j) * ldx + I0 + i + e, acc[rb][e]);
+          __stcs(X + (I0 + i + e) * ldx + J0 + j, acc[rb][e]);
+        }
+      }
+  }
+}
+
 // DMMA loop probe (tools only): the phi_block inner loop on resident shared
 // data, mode 0 as in the kernel, 1 without the B (Uext) loads, 2 without the
 // A (Zsm) loads, 3 neither.
@@ -955,19 +1232,31 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
   return check_launch("wq_ik1_sym");
 }
 
+static int g_x2_version = -1;
+
 template <int P>
 static int launch_x2(int64_t N, const double* Uext, const double* Zext, const double* s_w,
                      double alpha, double w_ik1, double* X, int64_t ldx, cudaStream_t st,
                      int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
-  using C = X2Cfg<P>;
-  const size_t smem = (size_t)X2Smem<P>::TOTAL * 8;
-  cudaFuncSetAttribute(x2_pairs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (g_x2_version < 0) {
+    const char* v = getenv("WQB200_X2");
+    g_x2_version = v ? atoi(v) : 4;
+  }
   const int nb = ceil_div(N, FT);
   const int64_t all = (int64_t)nb * (nb + 1) / 2;
   if (pair1 < 0 || pair1 > all) pair1 = all;
   if (pair0 < 0) pair0 = 0;
   const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
   if (blocks <= 0) return WQ_OK;
+  if (g_x2_version == 4) {
+    const size_t smem = (size_t)X4Smem<P>::TOTAL * 8;
+    cudaFuncSetAttribute(x2v4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    x2v4_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
+                                                               ldx, nb, tile_row0, pair0);
+    return check_launch("wq_x2_pairs");
+  }
+  const size_t smem = (size_t)X2Smem<P>::TOTAL * 8;
+  cudaFuncSetAttribute(x2_pairs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   x2_pairs_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
                                                                  ldx, nb, tile_row0, pair0);
   return check_launch("wq_x2_pairs");
