@@ -856,6 +856,24 @@ __device__ __forceinline__ double ld_nc(const double* p) {
 
 constexpr int X5_TS = 66;   // T hand-off [i][j] row stride (16-byte row-fragment stores)
 
+#ifdef WQ_X2_TIMELINE
+// tools build only (tools/x2_timeline_build.sh): per-CTA phase clocks and SM id
+__device__ long long* g_x2_tl = nullptr;
+#define X5_TL(k)                                                                          \
+  do {                                                                                    \
+    if (threadIdx.x == 0 && g_x2_tl) {                                                    \
+      g_x2_tl[(int64_t)blockIdx.x * 10 + (k)] = clock64();                                \
+      if ((k) == 0) {                                                                     \
+        unsigned sm;                                                                      \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));                                   \
+        g_x2_tl[(int64_t)blockIdx.x * 10 + 9] = sm;                                        \
+      }                                                                                   \
+    }                                                                                     \
+  } while (0)
+#else
+#define X5_TL(k) do {} while (0)
+#endif
+
 template <int P>
 struct X4Smem {
   using C = X2Cfg<P>;
@@ -920,6 +938,7 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
   const int ni = (int)min((int64_t)FT, N - I0);
   const int nj = (int)min((int64_t)FT, N - J0);
   const int64_t gmin[2] = {x5_gmin<P>(0, bi, bj), x5_gmin<P>(1, bi, bj)};
+  X5_TL(0);
 
   // Z' windows of both orientations, requested at once
   if (zbulk) {
@@ -994,6 +1013,7 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
       cp_async_wait_all();
       __syncthreads();
     }
+    X5_TL(1 + 4 * o);
     phi_block<P>(Uext, N, o == 0 ? Zs0 : Zs1, Phs, M0, R0, gmin[o], warp);
 #pragma unroll
     for (int s2 = 0; s2 < KS4; ++s2) bS[s2] *= alpha;
@@ -1006,6 +1026,7 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
       }
     }
     __syncthreads();
+    X5_TL(2 + 4 * o);
     // band contraction (DMMA; the warp's band B fragments stay in registers):
     // acc[rb][e] += sum_s Phs[8 rb + r][8 warp + 4 s + c] bS[s]
 #pragma unroll
@@ -1018,6 +1039,7 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
     }
   };
   orient(0);
+  X5_TL(3);
   if (rect) {
     // unsymmetrised row block: X(I,J) = alpha (w IK1 + X2(I,J)) = T
 #pragma unroll
@@ -1047,7 +1069,9 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
       for (int e = 0; e < 2; ++e) acc[rb][e] = Tsm[(8 * warp + 2 * c + e) * X5_TS + 8 * rb + r];
     __syncthreads();                         // T read before Phi1 overwrites it
   }
+  X5_TL(4);
   orient(1);
+  X5_TL(7);
 
   // acc[rb][e] = A(J,I)[j = 8 rb + r][i = 8 warp + 2c + e]: rows J (16-byte pieces, 64-byte
   // row segments per 4 lanes) and the transpose into rows I (8-byte pieces, 64-byte segments)
@@ -1088,6 +1112,7 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
         }
       }
   }
+  X5_TL(8);
 }
 
 // DMMA loop probe (tools only): the phi_block inner loop on resident shared
@@ -1434,6 +1459,13 @@ int wq_debug_x2_timing(long long* buf) {
   }
   return WQ_OK;
 }
+
+#ifdef WQ_X2_TIMELINE
+int wq_debug_x2_timeline(long long* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(g_x2_tl, &buf, sizeof(buf));
+  return e == cudaSuccess ? WQ_OK : WQ_ECUDA;
+}
+#endif
 
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream) {
   selftest_dmma_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(A, B, C);
