@@ -175,6 +175,13 @@ int wq_theta_t_rows(const wq_pairs_t* pp, int64_t row0, int64_t row1, double* th
                     void* stream);
 int wq_dmat(const wq_pairs_t* pp, double* D, void* stream);
 
+/* Segmented variant (parallel over columns x row segments of seg rows): a segment
+ * starts from the state reconstructed from the k0 preceding rows run from zero
+ * (exact to rounding once k0 exceeds the decay length of L^{-1}); state: workspace
+ * of (ceil(n/seg) - 1) * bw * ncols doubles. */
+int wq_band_solve_seg(int64_t n, int64_t bw, const double* Lb, double* X, int64_t ncols,
+                      int64_t ldx, int64_t seg, int64_t k0, double* state, void* stream);
+
 /* In-place banded SPD solve on every column of X (n x ncols, ld ldx):
  * X <- H^{-1} X with H = L L^T, Lb[k][j] = L[k][k-j], j = 0..bw. */
 int wq_band_solve_cols(int64_t n, int64_t bw, const double* Lb, double* X, int64_t ncols,

@@ -102,6 +102,7 @@ _SIGS = {
     "wq_phi_s_rows": [ctypes.POINTER(WqLogpart), c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_vp],
     "wq_gen_gather_d": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,
                         c_vp, c_vp],
+    "wq_band_solve_seg": [c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
     "wq_band_solve_win": [c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp],
     "wq_gen_near_moments": [c_i64, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,
                             c_vp, c_vp, c_vp, c_vp],

@@ -131,6 +131,7 @@ class LogPart:
     near_cnt: np.ndarray = None    # (n_el,) number of near inner elements
     ucols: np.ndarray = None
     vcols: np.ndarray = None
+    seg_k0: int = None             # warm-up rows of the segmented H^{-1} solves
 
 
 @dataclass(frozen=True)
@@ -649,12 +650,35 @@ def _theta_d(disc, lp: LogPart, d, rows=None, want_theta=True, want_d=True):
     return thetaT, D
 
 
+# segmented banded solves (columns x row segments in parallel) from this many rows on
+_SEG_ROWS = 1024
+_SEG_MIN_N = 2048
+
+
+def _seg_warmup(lp: LogPart) -> int:
+    """Warm-up rows of the segmented solves: the measured decay length of the
+    factor's inverse to 1e-20 (precompute.inverse_decay_rows) plus a margin,
+    or -1 (sequential solves) when it does not decay within 2048 rows."""
+    if lp.seg_k0 is None:
+        k = PC.inverse_decay_rows(lp.Lb, lp.bw)
+        lp.seg_k0 = -1 if k < 0 else -(-(k + 32) // 16) * 16
+    return lp.seg_k0
+
+
 def _hsolver(lp: LogPart, d, NE):
     """Y <- H^{-1} Y on ncols columns (banded / arrow Cholesky of the fit)."""
     st = _lib.stream_handle()
 
     def hsolve(Y, ncols):
-        if lp.L21 is None and lp.bw <= 8:
+        k0 = _seg_warmup(lp) if lp.L21 is None and lp.bw <= 8 and NE >= _SEG_MIN_N else -1
+        if k0 >= 0:
+            torch = _torch()
+            nseg = -(-NE // _SEG_ROWS)
+            state = torch.empty(max(1, (nseg - 1) * lp.bw * ncols), dtype=torch.float64,
+                                device="cuda")
+            _lib.call("wq_band_solve_seg", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(Y), ncols,
+                      Y.stride(0), _SEG_ROWS, k0, _lib.ptr(state), st)
+        elif lp.L21 is None and lp.bw <= 8:
             _lib.call("wq_band_solve_win", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(Y), ncols,
                       Y.stride(0), st)
         elif lp.L21 is None:

@@ -618,3 +618,42 @@ def fit_cholesky(H, bw: int, closed: bool):
     if diag.min() ** 2 <= RANK_RTOL ** 2 * diag.max() ** 2:
         raise ConstructionError("node vector does not resolve the refined space")
     return Lb, bw, L21, L22
+
+
+def inverse_decay_rows(Lb: np.ndarray, bw: int, tol: float = 1e-20, probes: int = 9,
+                       window: int = 2048) -> int:
+    """Rows after which a column of L^{-1} and of L^{-T} (L the banded factor,
+    Lb[k, j] = L[k, k-j]) has fallen below ``tol`` of its peak, maximised over
+    unit-vector probes spread along the band (forward and backward); -1 when a
+    probe does not decay within ``window`` rows.  Sizes the warm-up of the
+    segmented device solves (wq_band_solve_seg)."""
+    import scipy.linalg
+    m = Lb.shape[0]
+    lo = np.zeros((bw + 1, m))
+    for j in range(bw + 1):
+        lo[j, : m - j] = Lb[j:, j]
+    worst = 0
+    for k in np.unique(np.linspace(0, m - 1, probes).astype(int)):
+        # (probes near the ends see fewer rows; the interior ones bound the decay)
+        for fwd in (True, False):
+            n = min(window, m - k) if fwd else min(window, k + 1)
+            if n < 2:
+                continue
+            e = np.zeros(n)
+            if fwd:       # L x = e_k restricted to rows k .. k + n - 1 (the same decay)
+                sub = lo[:, k:k + n].copy()
+                e[0] = 1.0
+                x = np.abs(scipy.linalg.solve_banded((bw, 0), sub, e))
+            else:         # L^T x = e_k on rows k - n + 1 .. k, read backwards
+                sub = np.zeros((bw + 1, n))
+                for j in range(bw + 1):   # upper band of L^T: row r, column r + j holds L[r + j, r]
+                    sub[bw - j, j:] = lo[j, k - n + 1: k + 1 - j]
+                e[-1] = 1.0
+                x = np.abs(scipy.linalg.solve_banded((0, bw), sub, e))[::-1]
+            last = int(np.flatnonzero(x >= tol * x.max())[-1])   # last entry still above tol
+            if last >= n - 1:
+                if n == window:
+                    return -1          # no decay within the window
+                continue               # cut short by the end of the band: no information
+            worst = max(worst, last + 1)
+    return worst

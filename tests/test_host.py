@@ -295,3 +295,25 @@ def test_regular_rules_list_like_reference():
     assert abs(rules[5].apply(g) - rules[5].full_weights(disc.nodes.n) @ g) <= 1e-15
     with pytest.raises(UsageError):
         disc.singular_rules
+
+
+def test_inverse_decay_rows_bounds_dense_inverse():
+    """precompute.inverse_decay_rows (warm-up of the segmented device solves)
+    bounds where the columns of L^{-1} and L^{-T} fall below 1e-20 of their peak,
+    against dense inverses of the fit factor of a config-5 reading."""
+    from oracle import wq_oracle as O
+    from paper_1703_10016_b200 import assembly as AS, precompute as PC
+    sp = O.config5_space(n_el=512)
+    curve = W.load_curve({"degree": 1, "knots": [-1, -1, 1, 1], "control_points": [[-1, 0], [1, 0]]})
+    disc = W.build_discretization(curve, W.BasisSpec(sp.degree, sp.knots, False), 1)
+    lp = AS._log_part(disc)
+    k = PC.inverse_decay_rows(lp.Lb, lp.bw)
+    assert 0 < k < 200
+    m = lp.Lb.shape[0]
+    L = np.zeros((m, m))
+    for j in range(lp.bw + 1):
+        L[np.arange(j, m), np.arange(m - j)] = lp.Lb[j:, j]
+    Li = np.linalg.inv(L)
+    for c in range(0, m - k, 37):
+        col = np.abs(Li[c:, c])
+        assert np.all(col[k:] < 1e-19 * col.max())
