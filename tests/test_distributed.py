@@ -15,6 +15,13 @@ import torch.multiprocessing as mp
 from paper_1703_10016_b200.distributed import cyclic_blocks, gather_rows, pipeline_rows, row_blocks
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 @pytest.mark.parametrize("n,world", [(1, 1), (64, 2), (130, 2), (32768, 8), (4096, 3), (65, 8)])
 def test_row_blocks_cover_exactly(n, world):
     bounds, per = row_blocks(n, world)
@@ -48,7 +55,7 @@ def _worker(rank, world, port, n, out):
 @pytest.mark.parametrize("n", [130, 256])
 def test_gloo_allgather_assembles_full_matrix(n):
     world = 2
-    port = 29500 + (os.getpid() % 2000)
+    port = free_port()
     out = mp.Manager().dict()
     mp.spawn(_worker, args=(world, port, n, out), nprocs=world, join=True)
     assert dict(out) == {0: 1, 1: 1}
@@ -89,7 +96,7 @@ def _pipe_worker(rank, world, port, n, chunks, out):
 @pytest.mark.parametrize("n,chunks", [(130, 3), (300, 2)])
 def test_gloo_pipelined_allgather(n, chunks):
     world = 2
-    port = 31500 + (os.getpid() % 2000)
+    port = free_port()
     out = mp.Manager().dict()
     mp.spawn(_pipe_worker, args=(world, port, n, chunks, out), nprocs=world, join=True)
     assert dict(out) == {0: 1, 1: 1}
@@ -184,7 +191,7 @@ def _packed_worker(rank, world, port, n, chunks, out):
 @pytest.mark.parametrize("n,chunks", [(130, 2), (300, 3), (256, 1)])
 def test_gloo_packed_upper_allgather(n, chunks):
     world = 2
-    port = 33500 + (os.getpid() % 2000)
+    port = free_port()
     out = mp.Manager().dict()
     mp.spawn(_packed_worker, args=(world, port, n, chunks, out), nprocs=world, join=True)
     res = dict(out)
