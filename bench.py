@@ -658,10 +658,34 @@ def end_to_end(torch, dist, W, AS, D, disc, X, args, world, rank, chunks):
         tt = _t.tensor([t], dtype=_t.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
-    return {"value": N * N / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": t * 1e3,
-            "path": "assemble_matrix_to_host (streamed row blocks)" if world == 1 else
-                    "assemble_distributed_pipelined + per-rank D2H of a 1/N row share"}
+    out = {"value": N * N / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
+           "d2h_bytes_per_step": int(d2h), "ms_per_step": t * 1e3,
+           "path": "assemble_matrix_to_host (streamed row blocks)" if world == 1 else
+                   "assemble_distributed_pipelined + per-rank D2H of a 1/N row share"}
+    if world == 1:
+        out["cold_call"] = cold_call(torch, W, AS, args, host, X)
+    return out
+
+
+def cold_call(torch, W, AS, args, host, X):
+    """One complete drop-in call from the curve and space objects, nothing
+    cached: build_discretization (O(N) host precompute), the log-part host
+    ingredients, the uploads, the device assembly with the pair table cold, and
+    the streamed D2H of A -- what a user's first assemble call costs."""
+    curve, space = workload(args.n_el, args.p, args.geometry)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    disc = W.build_discretization(curve, space, 1)
+    t1 = time.perf_counter()
+    AS._log_part(disc)
+    t2 = time.perf_counter()
+    W.assemble_matrix_to_host(disc, out=host, work=X)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    N = space.dim
+    return {"value": N * N / (t3 - t0), "unit": UNIT, "ms": (t3 - t0) * 1e3,
+            "build_discretization_ms": (t1 - t0) * 1e3, "log_part_host_ms": (t2 - t1) * 1e3,
+            "upload_assemble_d2h_ms": (t3 - t2) * 1e3}
 
 
 SURVEY_W_C5 = 5.46e11         # SURVEY 8(d): algorithmic flop-eq of the C5 assembly

@@ -233,6 +233,11 @@ def regular_rule_band(parent: BasisSpec, fine: BasisSpec, nodes: np.ndarray) -> 
                 if len(np.unique(jidx[sel[k], :sj][lm[k]])) > sn:
                     raise ConstructionError(
                         f"rank-deficient local collocation matrix for weight {int(sel[k])}")
+        # identical local systems (every rule of a uniform mesh, up to the ends) are solved
+        # once: the same inputs give the same bits
+        key = np.concatenate([Am.reshape(len(sel), -1), bm], axis=1)
+        ukey, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+        Am, bm = Am[first], bm[first]
         u_, s_, vt = np.linalg.svd(Am, full_matrices=False)
         if np.any(s_[:, -1] <= max(sj, sn) * np.finfo(float).eps * s_[:, 0]):
             raise ConstructionError("rank-deficient local collocation matrix for a weight")
@@ -240,7 +245,7 @@ def regular_rule_band(parent: BasisSpec, fine: BasisSpec, nodes: np.ndarray) -> 
         resid = np.linalg.norm(np.einsum("kjc,kc->kj", Am, w) - bm, axis=1)
         if np.any(resid > EXACTNESS_TOL):
             raise ConstructionError(f"regular rule exactness residual {resid.max():.2e}")
-        weights[sel, :sn] = w
+        weights[sel, :sn] = w[inv.ravel()]
     return RuleBand(start=n_start, width=n_len, weights=weights, WG=WN)
 
 

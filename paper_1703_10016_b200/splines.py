@@ -209,8 +209,12 @@ def refine_uniform(basis, nref: int) -> RefinedBasis:
     if nref < 1:
         raise ConstructionError("nref must be >= 1")
     bp = basis.breakpoints
-    pieces = [np.linspace(lo, hi, nref + 1)[:-1] for lo, hi in zip(bp[:-1], bp[1:])]
-    nbp = np.concatenate(pieces + [bp[-1:]])
+    # np.linspace(lo, hi, nref + 1)[:-1] per element, vectorised with linspace's own
+    # arithmetic (k * ((hi - lo) / nref) + lo), so the breakpoints are bit-identical
+    lo, hi = bp[:-1], bp[1:]
+    step = (hi - lo) / nref
+    pieces = np.arange(nref, dtype=float)[None, :] * step[:, None] + lo[:, None]
+    nbp = np.concatenate([pieces.ravel(), bp[-1:]])
     nm = np.ones(len(nbp), dtype=int)
     nm[::nref] = basis.multiplicities
     if basis.closed:
