@@ -199,7 +199,7 @@ def committed_traffic(dom):
         return None
     try:
         data = json.load(open(files[-1]))
-        key = {"ik1": "ik1_sym_kernel", "ik2": "x2_pairs_kernel"}[dom]
+        key = {"ik1": "ik1_sym_kernel", "ik2": "x2v4_kernel"}[dom]
         return data[key]["total"]
     except (OSError, ValueError, KeyError):
         return None
@@ -481,7 +481,7 @@ def main():
     dom = "ik1" if split[1] >= split[2] else "ik2"
     dom_ms = split[1] if dom == "ik1" else split[2]
     achieved = fl[dom] / (dom_ms * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2_pairs_kernel"}[dom],
+    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2v4_kernel"}[dom],
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": "measured DFMA probe (wq_fp64_peak, burst); MEASURED_PEAKS.json has "
                                "no FP64 entry", "peak_datasheet": FP64_DATASHEET_TFLOPS,

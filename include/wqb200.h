@@ -71,10 +71,6 @@ const char* wq_last_error(void);
  * in practice). */
 int wq_fp64_peak(int64_t iters, int blocks, double* out, void* stream);
 
-/* FP64 tensor-core probe: blocks x 8 warps x iters x 8 DMMA m8n8k4 (512 flops
- * each); mode 1 adds 32 DFMA per lane per iteration (pipe-overlap probe). */
-int wq_dmma_peak(int64_t iters, int blocks, int mode, double* out, void* stream);
-
 /*
  * IK1 rows/cols block (replaces assemble_ik1, assembly.py:175-183, with the
  * K1 grid of geometry.py:225-248 evaluated in-kernel and never stored):
@@ -260,15 +256,6 @@ int wq_x2_pairs_range(int64_t N, int p, int nA, int nApad, int ws, int ktot, int
 /* Self-test hooks (unit tests): the IK1 kernel's table 0.5*ln vs libdevice; one DMMA 8x8x4. */
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream);
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream);
-/* Throughput probe of 0.5*ln (tools): mode 0 table ln, 1 without I2F, 2 libdevice. */
-int wq_probe_log(int64_t iters, int blocks, int mode, double* out, void* stream);
-/* DMMA inner-loop probe (tools): blocks x 8 warps x iters x 180 DMMA (p = 3 layout). */
-int wq_probe_phi(int iters, int blocks, int mode, const double* Uext, double* out, void* stream);
-/* Tuning knob of ik1_sym: 1 = column loop unrolled 4 (default), 2 = unrolled 2. */
-int wq_set_ik1_passes(int npass);
-/* Profiling hook: per-CTA phase clock64 stamps of wq_x2_pairs (8 per CTA) into
- * buf (device memory), or NULL to disable. */
-int wq_debug_x2_timing(long long* buf);
 
 /* Epilogue (assembly.py:262-271): A = alpha * (X + X^T), in place, n x n. */
 int wq_symmetrize(double* X, int64_t n, double alpha, void* stream);

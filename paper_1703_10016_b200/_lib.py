@@ -51,7 +51,6 @@ _SIGS = {
     "wq_version": [],
     "wq_last_error": [],
     "wq_fp64_peak": [c_i64, c_int, c_vp, c_vp],
-    "wq_dmma_peak": [c_i64, c_int, c_int, c_vp, c_vp],
     "wq_ik1": [ctypes.POINTER(WqSmooth), c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_int, c_i64,
                c_vp, c_vp],
     "wq_ik1_band": [ctypes.POINTER(WqSmooth), c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp],
@@ -85,10 +84,6 @@ _SIGS = {
     "wq_b2_inner": [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "wq_selftest_log": [c_i64, c_vp, c_vp, c_vp, c_vp],
     "wq_selftest_dmma": [c_vp, c_vp, c_vp, c_vp],
-    "wq_debug_x2_timing": [c_vp],
-    "wq_set_ik1_passes": [c_int],
-    "wq_probe_log": [c_i64, c_int, c_int, c_vp, c_vp],
-    "wq_probe_phi": [c_int, c_int, c_int, c_vp, c_vp, c_vp],
     "wq_gen_pair_blocks": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_vp,
                            c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                            c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp],

@@ -114,33 +114,6 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(int64_t iters, double se
   if (r == 12345.678) out[blockIdx.x] = r;  // keep the chains alive
 }
 
-// FP64 tensor-core (DMMA m8n8k4) probe; mode 1 also runs 4 DFMA chains per
-// lane alongside (does the DFMA pipe overlap the DMMA pipe?).
-__global__ void __launch_bounds__(256) dmma_peak_kernel(int64_t iters, int mode, double* out) {
-  double a = 1.0 + threadIdx.x * 1e-3, b = 0.5;
-  double c[8][2];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) c[k][0] = c[k][1] = 0.0;
-  double f0 = a, f1 = a + 1, f2 = a + 2, f3 = a + 3;
-  const double m = 0.999999999, cc = 1e-9;
-  for (int64_t it = 0; it < iters; ++it) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
-    }
-    if (mode) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        f0 = fma(f0, m, cc); f1 = fma(f1, m, cc); f2 = fma(f2, m, cc); f3 = fma(f3, m, cc);
-      }
-    }
-  }
-  double r = f0 + f1 + f2 + f3;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) r += c[k][0] + c[k][1];
-  if (r == 12345.678) out[blockIdx.x] = r;
-}
 
 }  // namespace wq
 
@@ -160,15 +133,6 @@ int wq_fp64_peak(int64_t iters, int blocks, double* out, void* stream) {
 }
 
 const char* wq_last_error(void) { return g_err; }
-
-int wq_dmma_peak(int64_t iters, int blocks, int mode, double* out, void* stream) {
-  if (iters <= 0 || blocks <= 0 || !out) {
-    set_error("wq_dmma_peak: bad arguments");
-    return WQ_EINVAL;
-  }
-  dmma_peak_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, mode, out);
-  return check_launch("wq_dmma_peak");
-}
 
 int wq_symmetrize(double* X, int64_t n, double alpha, void* stream) {
   if (!X || n <= 0) {

@@ -1,24 +1,23 @@
-// v3 closed-uniform (circulant) assembly: two sm_100a kernels over the
+// Closed-uniform (circulant) assembly: two sm_100a kernels over the
 // UPPER-TRIANGLE tile pairs (I <= J) of the N x N matrix (64 x 64 tiles).
 //
 //  ik1_sym_kernel   IK1(I,J) = G_I K1 G_J^T (assemble_ik1, assembly.py:175-183;
-//                   K1_grid, geometry.py:225-248).  Each thread owns one outer
-//                   node q and sweeps the inner nodes r of half the tile with
-//                   a sliding register window of 2p+1 kernel values: K1 is
-//                   evaluated once per node pair (+8% halo), on the FP64 pipe
-//                   (table ln, conflict-free 16-entry table), never stored to
-//                   HBM or shared memory; the first banded contraction happens
-//                   in registers, the second reads T = K1 G^T from shared
-//                   memory with another sliding window.  Only the upper tile
-//                   (I,J) is written (IK1 is symmetric).
-//  x2_pairs_kernel  X2(I,J) and X2(J,I) of the log part (assemble_ik2,
+//                   K1_grid, geometry.py:225-248).  Each thread owns two outer
+//                   nodes and sweeps the inner nodes of half the tile with
+//                   sliding register windows of 2p+1 kernel values: K1 is
+//                   evaluated once per node pair (+8% halo) on the FP64 pipe
+//                   (accurate-table ln, wq_log.cuh), never stored to HBM; the
+//                   first banded contraction happens in registers, the second
+//                   reads T = K1 G^T from shared memory with another sliding
+//                   window.  Only the upper tile (I,J) is written (IK1 is
+//                   symmetric).
+//  x2v4_kernel      X2(I,J) and X2(J,I) of the log part (assemble_ik2,
 //                   assembly.py:186-245, X-form) on the FP64 tensor cores
 //                   (DMMA m8n8k4): Phi = Zext * Uext^T in skewed (diagonal)
-//                   coordinates, the banded S contraction as a second DMMA,
-//                   then the fused epilogue
+//                   coordinates from TMA-staged Z' windows, the banded S
+//                   contraction as a second DMMA, then the fused epilogue
 //                     A(I,J) = alpha (w IK1(I,J) + X2(I,J) + X2(J,I)^T),
 //                     A(J,I) = A(I,J)^T      (scale_and_symmetrize, :262-271).
-//                   Shared staging by cp.async; 2 CTAs per SM.
 //
 // Both kernels are deterministic (no atomics on values).
 #include <math.h>
@@ -35,108 +34,8 @@ namespace wq {
 constexpr int FT = 64;  // tile rows/cols
 
 // ---------------------------------------------------------------------------
-// 0.5*ln(x), x > 0 normal: x = 2^e m, m in [1,2); c_j = 1/mid_j on 1024
-// mantissa bins (24 KB table in shared memory: the kernel arguments of
-// neighbouring lanes are close, so lookups are mostly broadcasts); r = m c_j - 1
-// with one FMA rounding (|r| < 2^-11); ln(1+r) by its degree-5 series
-// (truncation < 3e-21); -ln c_j as a double-double.
-// ---------------------------------------------------------------------------
-
-constexpr int LOGBITS = 10;              // 1024-entry table (read through L1)
-constexpr int LOGTAB = 1 << LOGBITS;
-__device__ double g_logtab[3 * LOGTAB];
-__device__ double g_logtab16[3 * 16];  // 16-entry table: spans the 32 banks once (smem)  // c_j | 0.5*(-ln c_j)_hi | 0.5*(-ln c_j)_lo
-static bool g_logtab_ready[64];
-
-static int upload_logtab(const void* sym, int bins) {
-  double* tab = new double[3 * bins];
-  for (int j = 0; j < bins; ++j) {
-    long double mid = 1.0L + (j + 0.5L) / bins;
-    double c = (double)(1.0L / mid);
-    long double nl = -logl((long double)c);
-    double hi = (double)nl;
-    double lo = (double)(nl - (long double)hi);
-    tab[j] = c;
-    tab[bins + j] = 0.5 * hi;
-    tab[2 * bins + j] = 0.5 * lo;
-  }
-  cudaError_t e = cudaMemcpyToSymbol(sym, tab, sizeof(double) * 3 * bins);
-  delete[] tab;
-  if (e != cudaSuccess) {
-    set_error("log table upload: %s", cudaGetErrorString(e));
-    return WQ_ECUDA;
-  }
-  return WQ_OK;
-}
-
-int ensure_logtab();
-
-// device address of the 16-entry table (for kernels in other translation units)
-int logtab16_device(const double** out) {
-  int rc = ensure_logtab();
-  if (rc) return rc;
-  void* p = nullptr;
-  cudaError_t e = cudaGetSymbolAddress(&p, g_logtab16);
-  if (e != cudaSuccess) {
-    set_error("log table address: %s", cudaGetErrorString(e));
-    return WQ_ECUDA;
-  }
-  *out = static_cast<const double*>(p);
-  return WQ_OK;
-}
-
-int ensure_logtab() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && g_logtab_ready[dev]) return WQ_OK;
-  int rc = upload_logtab(g_logtab, LOGTAB);
-  if (rc) return rc;
-  rc = upload_logtab(g_logtab16, 16);
-  if (rc) return rc;
-  if (dev >= 0 && dev < 64) g_logtab_ready[dev] = true;
-  return WQ_OK;
-}
-
-
-
-__device__ __forceinline__ double half_ln(double x, const double* __restrict__ tab) {
-  const int hi = __double2hiint(x);
-  const int lo = __double2loint(x);
-  const int e = (hi >> 20) - 1023;
-  const int j = (hi >> (20 - LOGBITS)) & (LOGTAB - 1);
-  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-  const double r = fma(m, tab[j], -1.0);  // |r| < 2^-(LOGBITS+1)
-  // 0.5 ln(1+r) = 0.5 r + r^2 q(r), q = 0.5 sum_{k>=2} (-1)^(k+1) r^(k-2) / k, truncated
-  // at the degree where r^(deg+1)/(deg+1) < 1.2e-19 (degree 9 for 16 bins, 5 for 1024)
-  double q;
-  if constexpr (LOGBITS >= 10) {
-    q = fma(r, 0.5 / 5.0, -0.5 / 4.0);
-  } else {
-    q = fma(r, 0.5 / 9.0, -0.5 / 8.0);
-    q = fma(r, q, 0.5 / 7.0);
-    q = fma(r, q, -0.5 / 6.0);
-    q = fma(r, q, 0.5 / 5.0);
-    q = fma(r, q, -0.5 / 4.0);
-  }
-  q = fma(r, q, 0.5 / 3.0);
-  q = fma(r, q, -0.25);
-  const double r2 = r * r;
-  const double de = (double)e;
-  const double t_hi = fma(de, HLN2_A, tab[LOGTAB + j]);
-  const double t_lo = fma(de, HLN2_B, tab[2 * LOGTAB + j]);
-  return t_hi + fma(r, 0.5, fma(r2, q, t_lo));
-}
-
-// ---------------------------------------------------------------------------
 // ik1_sym_kernel: closed uniform nodes, rule i on nodes 2(i-p)+1 .. 2(i-p)+2p+1
 // ---------------------------------------------------------------------------
-
-// optional per-CTA phase timestamps (clock64), set by wq_debug_x2_timing (tools only)
-__device__ long long* g_x2_dbg = nullptr;
-__device__ __forceinline__ void x2_mark(int slot) {
-  long long* d = g_x2_dbg;
-  if (d != nullptr && threadIdx.x == 0) d[(int64_t)blockIdx.x * 8 + slot] = clock64();
-}
 
 // Tile mapping: sym (tile_row0 < 0): upper-triangle pairs of an nb x nb tile grid;
 // rect: tile rows tile_row0 .. + gridDim.x / nbj, all nbj tile columns, output rows
@@ -453,7 +352,6 @@ struct X2Cfg {
 constexpr int X2_THREADS = 256;
 
 constexpr int PSTRIDE = 76;  // Phi smem row stride (== 12 mod 16), >= SPAN and 56 + KS
-constexpr int TSTRIDE = 65;  // transpose staging stride
 
 // Phi[m][i] for m in [M0, M0 + SPAN), i in the tile rows starting at R0 (Uext rows),
 // written to Phs[i][m - M0]
@@ -516,302 +414,6 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64
       if (mm >= 0 && mm < C::SPAN) Phs[il * PSTRIDE + mm] = acc[kb][e];
     }
   }
-}
-
-// acc[b][.] += sum_m Phs[a][m] S_b[m - b + d]; warp owns row block `warp`
-template <int P>
-__device__ __forceinline__ void s_contract_acc(const double* Phs, const double* Bfr,
-                                               double (&acc)[8][2], int warp) {
-  using C = X2Cfg<P>;
-  const int lane = threadIdx.x & 31;
-  const int r = lane >> 2, c = lane & 3;
-#pragma unroll
-  for (int jb = 0; jb < 8; ++jb) {
-#pragma unroll
-    for (int s = 0; s < C::KS / 4; ++s) {
-      const double a = Phs[(8 * warp + r) * PSTRIDE + 8 * jb + 4 * s + c];
-      const double b = Bfr[(jb * (C::KS / 4) + s) * 32 + lane];
-      dmma(acc[jb][0], acc[jb][1], a, b);
-    }
-  }
-}
-
-// orientation hand-off tile: stride 70 (== 6 mod 8: the transposed 8-byte reads of rows
-// 2c + e hit distinct banks) with odd rows shifted by 2 more doubles, so two consecutive
-// rows start 8 apart mod 16 and the 16-byte row-fragment loads / stores are conflict-free
-// too (each row arrives by its own bulk copy, so the row starts are free)
-constexpr int T2STRIDE = 70;
-constexpr int T2EXTRA = 8;
-__device__ __forceinline__ int tst_row(int a) { return a * T2STRIDE + ((a & 1) ? 2 : 0); }
-
-template <int P>
-struct X2Smem {
-  using C = X2Cfg<P>;
-  static constexpr int SROW = C::WS <= 8 ? 8 : 16;
-  static constexpr int TOTAL = C::ZROWS * C::ZSTRIDE + FT * PSTRIDE + FT * T2STRIDE + T2EXTRA + FT * SROW +
-                               8 * (C::KS / 4) * 32 + 2;  // + 2 mbarriers (window, IK1 tile)
-};
-
-// One tile pair (bi, bj) of the log part + fused symmetric epilogue (or, rect,
-// the unsymmetrised row block).  The epilogue runs inside the DMMA
-// accumulators: orientation 0 starts from alpha w IK1(I,J) and contracts with
-// alpha S_J, giving T = alpha (w IK1 + X2(I,J)) (kept in shared memory);
-// orientation 1 starts from T^T and contracts with alpha S_I, giving
-// A(J,I) = alpha (w IK1 + X2(I,J) + X2(J,I)^T)^T directly, so no FP64
-// instructions compete with the neighbour CTA's DMMAs in the epilogue.
-template <int P>
-__device__ __forceinline__ void x2_tile(int64_t N, const double* __restrict__ Uext,
-                                        const double* __restrict__ Zext,
-                                        const double* __restrict__ sw, double alpha, double w_ik1,
-                                        double* X, int64_t ldx, int bi, int bj, bool rect,
-                                        int64_t row_off, double* smem) {
-  using C = X2Cfg<P>;
-  using L = X2Smem<P>;
-  constexpr int SROW = L::SROW;
-  double* Zsm = smem;                              // ZROWS * ZSTRIDE
-  double* Phs = Zsm + C::ZROWS * C::ZSTRIDE;       // FT * PSTRIDE (also output staging, stride 65)
-  double* Tst = Phs + FT * PSTRIDE;                // FT * T2STRIDE: IK1(I,J), then T
-  double* Ssm = Tst + FT * T2STRIDE + T2EXTRA;     // FT * SROW (S band rows)
-  double* Bfr = Ssm + FT * SROW;                   // 8 * KS/4 * 32 (fragment order, alpha S)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Bfr + 8 * (C::KS / 4) * 32);
-  const int64_t n = N;
-  const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
-  const int ni = (int)min((int64_t)FT, N - I0);
-  const int nj = (int)min((int64_t)FT, N - J0);
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int r = lane >> 2, c = lane & 3;
-  const bool with_ik1 = w_ik1 != 0.0;
-
-  x2_mark(0);
-  // bulk (TMA) staging needs whole 16-byte-aligned rows and a table of >= ZROWS rows
-  const bool zbulk = n >= C::ZROWS;
-  const double* src = X + (I0 - row_off) * ldx + J0;
-  const bool tbulk = with_ik1 && zbulk && ni == FT && nj == FT && (ldx & 1) == 0 &&
-                     (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  if (zbulk) {
-    if (tid == 0) {
-      mbar_init(bar, 1);
-      mbar_init(bar + 1, 1);
-    }
-    fence_proxy_async();
-    __syncthreads();
-  }
-  // IK1(I,J) tile -> Tst: 64 row copies on the TMA engine (issued after the
-  // orientation-0 window below, which is needed first), or cp.async
-  if (tbulk) {
-  } else if (with_ik1) {
-    {
-      for (int k = tid; k < FT * FT; k += X2_THREADS) {
-        const int a = k >> 6, b = k & 63;
-        if (a < ni && b < nj) cp_async8(Tst + tst_row(a) + b, src + a * ldx + b);
-        else Tst[tst_row(a) + b] = 0.0;
-      }
-    }
-  }
-  // Phs pad columns must be finite (they multiply zero B entries)
-  for (int k = tid; k < FT * (PSTRIDE - C::SPAN); k += X2_THREADS) {
-    const int row = k / (PSTRIDE - C::SPAN), col = C::SPAN + k % (PSTRIDE - C::SPAN);
-    Phs[row * PSTRIDE + col] = 0.0;
-  }
-
-  double acc[8][2];
-  const int norient = rect ? 1 : 2;
-  for (int orient = 0; orient < norient; ++orient) {
-    // 0: Phi rows = I, m over J-range, contraction with S_J -> X2(I,J)
-    // 1: Phi rows = J, m over I-range, contraction with S_I -> X2(J,I)
-    const int64_t R0 = orient == 0 ? I0 : J0;
-    const int64_t C0 = orient == 0 ? J0 : I0;
-    const int nc = orient == 0 ? nj : ni;
-    const int64_t M0 = C0 - C::D;
-    const int64_t gmin = M0 - (R0 + 63) + P - C::AMAX;
-    if (orient == 1) {
-      fence_proxy_async();  // generic reads of Zsm before the async-proxy overwrite
-      __syncthreads();      // Zsm / Phs / Bfr reuse, T complete
-    }
-    int64_t g0 = gmin % n;
-    if (g0 < 0) g0 += n;
-    constexpr int NBF = 8 * (C::KS / 4) * 32;
-    constexpr int BPT = (NBF + X2_THREADS - 1) / X2_THREADS;
-    if (zbulk) {
-      // skewed Z' window: ZROWS contiguous table rows (two pieces at the seam)
-      if (tid == 0) {
-        constexpr unsigned RB = C::ZSTRIDE * 8;
-        const int64_t first = min((int64_t)C::ZROWS, n - g0);
-        mbar_arrive_expect_tx(bar, C::ZROWS * RB);
-        const uint64_t pol = l2_evict_last();    // the Z' table is re-read by every tile pair
-        bulk_g2s_hint(Zsm, Zext + g0 * C::ZSTRIDE, (unsigned)first * RB, bar, pol);
-        if (first < C::ZROWS)
-          bulk_g2s_hint(Zsm + first * C::ZSTRIDE, Zext, (unsigned)(C::ZROWS - first) * RB, bar, pol);
-      }
-      // alpha S band in B-fragment order, Bfr[jb][s][lane] = alpha S_{8jb+r}[4s+c-r],
-      // straight from global memory while the copies fly
-      double bv[BPT];
-#pragma unroll
-      for (int u = 0; u < BPT; ++u) {
-        const int k = tid + u * X2_THREADS;
-        const int ln = k & 31, s = (k >> 5) % (C::KS / 4), jb = (k >> 5) / (C::KS / 4);
-        const int rr = ln >> 2, cc = ln & 3;
-        const int t = 4 * s + cc - rr, row = 8 * jb + rr;
-        bv[u] = (k < NBF && t >= 0 && t <= 2 * C::D && row < nc) ? __ldg(sw + (C0 + row) * C::WS + t)
-                                                                  : 0.0;
-      }
-      // (stored after phi: only s_contract reads Bfr, so the loads' latency -- long for the
-      // orientation-0 S_J rows -- hides behind phi instead of delaying it)
-      if (orient == 0 && with_ik1 && !tbulk) cp_async_wait_all();
-      mbar_wait(bar, (unsigned)orient);
-      if (orient == 0 && tbulk && tid < 32) {
-        // own barrier, requested once the window is in: the tile is first needed after
-        // phi0, so its HBM latency hides behind phi0 without delaying the window
-        if (tid == 0) mbar_arrive_expect_tx(bar + 1, FT * FT * 8);
-        __syncwarp();
-        const uint64_t pol = l2_evict_first();   // the IK1 tile is read once
-        for (int a = tid; a < FT; a += 32)
-          bulk_g2s_hint(Tst + tst_row(a), src + a * ldx, FT * 8, bar + 1, pol);
-      }
-      __syncthreads();
-      x2_mark(1 + 3 * orient);
-      phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
-#pragma unroll
-      for (int u = 0; u < BPT; ++u)
-        if (tid + u * X2_THREADS < NBF) Bfr[tid + u * X2_THREADS] = alpha * bv[u];
-    } else {
-      constexpr int CH = C::ZSTRIDE / 2;  // 16-byte chunks per table row
-      for (int k = tid; k < C::ZROWS * CH; k += X2_THREADS) {
-        const int row = k / CH, cc = 2 * (k - row * CH);
-        int64_t g = g0 + row;
-        while (g >= n) g -= n;
-        cp_async16(Zsm + row * C::ZSTRIDE + cc, Zext + g * C::ZSTRIDE + cc);
-      }
-      for (int k = tid; k < FT * SROW; k += X2_THREADS) {
-        const int row = k / SROW, t = k - row * SROW;
-        const bool ok = row < nc && t < C::WS;
-        cp_async8_zfill(Ssm + k, sw + (ok ? (C0 + row) * C::WS + t : 0), ok);
-      }
-      cp_async_wait_all();
-      __syncthreads();
-      for (int k = tid; k < NBF; k += X2_THREADS) {
-        const int ln = k & 31, s = (k >> 5) % (C::KS / 4), jb = (k >> 5) / (C::KS / 4);
-        const int rr = ln >> 2, cc = ln & 3;
-        const int t = 4 * s + cc - rr;
-        Bfr[k] = (t >= 0 && t <= 2 * C::D) ? alpha * Ssm[(8 * jb + rr) * SROW + t] : 0.0;
-      }
-      __syncthreads();
-      x2_mark(1 + 3 * orient);
-      phi_block<P>(Uext, N, Zsm, Phs, M0, R0, gmin, warp);
-    }
-    // accumulator start: orientation 0 alpha w IK1(I,J) (lane: i = 8warp + r,
-    // j = 8jb + 2c + e); orientation 1 T^T (lane: j = 8warp + r, i = 8ib + 2c + e)
-    if (orient == 0) {
-      if (tbulk) mbar_wait(bar + 1, 0);
-      const double aw = alpha * w_ik1;
-#pragma unroll
-      for (int jb = 0; jb < 8; ++jb) {
-        if (with_ik1) {
-          const double2 t =
-              *reinterpret_cast<const double2*>(Tst + tst_row(8 * warp + r) + 8 * jb + 2 * c);
-          acc[jb][0] = aw * t.x;
-          acc[jb][1] = aw * t.y;
-        } else {
-          acc[jb][0] = acc[jb][1] = 0.0;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int ib = 0; ib < 8; ++ib)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) acc[ib][e] = Tst[tst_row(8 * ib + 2 * c + e) + 8 * warp + r];
-    }
-    __syncthreads();
-    x2_mark(2 + 3 * orient);
-    s_contract_acc<P>(Phs, Bfr, acc, warp);
-    x2_mark(3 + 3 * orient);
-    if (orient == 0) {
-      // T[i][j] (each lane rewrites the entries it read)
-#pragma unroll
-      for (int jb = 0; jb < 8; ++jb)
-        *reinterpret_cast<double2*>(Tst + tst_row(8 * warp + r) + 8 * jb + 2 * c) =
-            make_double2(acc[jb][0], acc[jb][1]);
-    }
-  }
-  __syncthreads();
-  if (rect) {
-    // unsymmetrised row block: X(I,J) = alpha (w IK1 + X2(I,J)) = T
-    for (int k = tid; k < FT * FT; k += X2_THREADS) {
-      const int a = k >> 6, b = k & 63;
-      if (a < ni && b < nj) X[(I0 - row_off + a) * ldx + J0 + b] = Tst[tst_row(a) + b];
-    }
-    return;
-  }
-  // acc holds A(J,I) (lane: j = 8warp + r, i = 8ib + 2c + e)
-  const bool sbulk = zbulk && bi != bj && ni == FT && nj == FT && (ldx & 1) == 0 &&
-                     (reinterpret_cast<uintptr_t>(X) & 15) == 0;
-  if (sbulk) {
-    // both output tiles staged row-contiguous (16-byte aligned rows) in the Phs | Tst
-    // region, then 128 row copies shared -> global on the TMA engine.  Strides: 72 (== 8
-    // mod 16) for the 16-byte row-fragment stores, 66 (== 2 mod 16) for the transposed ones
-    constexpr int OSA = 72, OSB = 66;
-    double* Oji = Phs;             // A(J,I)[j][i]
-    double* Oij = Phs + FT * OSA;  // A(I,J)[i][j] = A(J,I)[j][i]
-    static_assert(FT * (OSA + OSB) <= FT * PSTRIDE + FT * T2STRIDE + T2EXTRA, "output staging overflows");
-#pragma unroll
-    for (int ib = 0; ib < 8; ++ib) {
-      *reinterpret_cast<double2*>(Oji + (8 * warp + r) * OSA + 8 * ib + 2 * c) =
-          make_double2(acc[ib][0], acc[ib][1]);
-#pragma unroll
-      for (int e = 0; e < 2; ++e) Oij[(8 * ib + 2 * c + e) * OSB + 8 * warp + r] = acc[ib][e];
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid < 2 * FT) {
-      const int a = tid & (FT - 1);
-      const bool ji = tid < FT;
-      double* dst = ji ? X + (J0 + a) * ldx + I0 : X + (I0 + a) * ldx + J0;
-      const double* srcs = ji ? Oji + a * OSA : Oij + a * OSB;
-      bulk_s2g_hint(dst, srcs, FT * 8, l2_evict_first());   // A is written once
-      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-    }
-    x2_mark(7);
-    return;
-  }
-#pragma unroll
-  for (int ib = 0; ib < 8; ++ib)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) Phs[(8 * warp + r) * TSTRIDE + 8 * ib + 2 * c + e] = acc[ib][e];
-  __syncthreads();
-  // A(J,I) rows (coalesced), A(I,J) = transpose; diagonal tiles mirror their
-  // lower-staged triangle so A is exactly symmetric
-  if (bi != bj) {
-    for (int k = tid; k < FT * FT; k += X2_THREADS) {
-      const int a = k >> 6, b = k & 63;  // row J0 + a, col I0 + b
-      if (a < nj && b < ni) X[(J0 + a) * ldx + I0 + b] = Phs[a * TSTRIDE + b];
-    }
-  }
-  for (int k = tid; k < FT * FT; k += X2_THREADS) {
-    const int a = k >> 6, b = k & 63;  // row I0 + a, col J0 + b
-    if (a < ni && b < nj) {
-      const double v = (bi == bj && b > a) ? Phs[a * TSTRIDE + b] : Phs[b * TSTRIDE + a];
-      X[(I0 + a) * ldx + J0 + b] = v;
-    }
-  }
-  x2_mark(7);
-}
-
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
-template <int P>
-__global__ void __launch_bounds__(X2_THREADS, 2)
-x2_pairs_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
-                const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
-                int nb, int tile_row0, int64_t pair0) {
-  extern __shared__ double smem[];
-  int bi, bj;
-  tile_of_block(nb, tile_row0, pair0, bi, bj);
-  const bool rect = tile_row0 >= 0;
-  x2_tile<P>(N, Uext, Zext, sw, alpha, w_ik1, X, ldx, bi, bj, rect,
-             rect ? (int64_t)tile_row0 * FT : 0, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1115,51 +717,6 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
   X5_TL(8);
 }
 
-// DMMA loop probe (tools only): the phi_block inner loop on resident shared
-// data, mode 0 as in the kernel, 1 without the B (Uext) loads, 2 without the
-// A (Zsm) loads, 3 neither.
-template <int MODE>
-__global__ void __launch_bounds__(256) probe_phi_kernel(int iters, const double* __restrict__ Uext,
-                                                        double* out) {
-  using C = X2Cfg<3>;
-  __shared__ double Zsm[C::ZROWS * C::ZSTRIDE];
-  for (int k = threadIdx.x; k < C::ZROWS * C::ZSTRIDE; k += 256) Zsm[k] = 1e-3 * (k % 17);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = lane >> 2, c = lane & 3;
-  double acc[C::NKB][2];
-#pragma unroll
-  for (int kb = 0; kb < C::NKB; ++kb) acc[kb][0] = acc[kb][1] = 0.0;
-  const double* urow = Uext + (blockIdx.x * 64 + 8 * warp + r) * C::KTOT + c;
-  const int zbase = 56 - 8 * warp + r + C::AMAX;
-  for (int it = 0; it < iters; ++it) {
-    double bq[C::PF];
-#pragma unroll
-    for (int s = 0; s < C::PF; ++s) bq[s] = MODE & 1 ? 0.5 : __ldg(urow + 4 * s);
-#pragma unroll
-    for (int s = 0; s < C::NSTEPS; ++s) {
-      int off, col;
-      if (s < C::SZ) {
-        off = (4 * s) / C::NAPAD;
-        col = (4 * s - off * C::NAPAD) + c;
-      } else {
-        off = 4 * (s - C::SZ) + c;
-        col = C::NAPAD;
-      }
-      const double b = bq[s % C::PF];
-      if (!(MODE & 1) && s + C::PF < C::NSTEPS) bq[s % C::PF] = __ldg(urow + 4 * (s + C::PF));
-      const double* z = Zsm + (zbase - off) * C::ZSTRIDE + col;
-#pragma unroll
-      for (int kb = 0; kb < C::NKB; ++kb)
-        dmma(acc[kb][0], acc[kb][1], MODE & 2 ? 0.25 : z[kb * 8 * C::ZSTRIDE], b);
-    }
-  }
-  double t = 0;
-#pragma unroll
-  for (int kb = 0; kb < C::NKB; ++kb) t += acc[kb][0] + acc[kb][1];
-  if (t == 12345.678) out[blockIdx.x] = t;
-}
-
 // Zext[g] = [Z'[g][0..nA-1], 0.., ff[g] at column nApad, 0..]
 __global__ void zext_kernel(int64_t n, int nA, int nApad, int zstride, const double* Zp,
                             const double* ff, double* Zext) {
@@ -1171,48 +728,6 @@ __global__ void zext_kernel(int64_t n, int nA, int nApad, int zstride, const dou
   if (col < nA) v = Zp[g * nA + col];
   else if (col == nApad) v = ff[g];
   Zext[e] = v;
-}
-
-// throughput probe of the kernel-evaluation building blocks (tools only):
-// mode 0: half_ln; 1: half_ln with the exponent conversion replaced by a DADD
-// trick; 2: libdevice 0.5*log; 3: full K1 (dist^2, x 1/p^2, half_ln)
-__device__ __forceinline__ double half_ln_noi2f(double x, const double* __restrict__ tab) {
-  const int hi = __double2hiint(x);
-  const int lo = __double2loint(x);
-  const int j = (hi >> (20 - LOGBITS)) & (LOGTAB - 1);
-  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-  const double r = fma(m, tab[j], -1.0);
-  double q = fma(r, 0.5 / 5.0, -0.5 / 4.0);
-  q = fma(r, q, 0.5 / 3.0);
-  q = fma(r, q, -0.25);
-  const double r2 = r * r;
-  // exponent as a double: 2^52 + biased exponent, minus (2^52 + 1023)
-  const double de = __hiloint2double(0x43300000, (hi >> 20) & 0x7ff) - 4503599627371519.0;
-  const double t_hi = fma(de, HLN2_A, tab[LOGTAB + j]);
-  const double t_lo = fma(de, HLN2_B, tab[2 * LOGTAB + j]);
-  return t_hi + fma(r, 0.5, fma(r2, q, t_lo));
-}
-
-__global__ void __launch_bounds__(256) probe_log_kernel(int64_t iters, int mode, double* out) {
-  __shared__ double tab[3 * LOGTAB];
-  for (int k = threadIdx.x; k < 3 * LOGTAB; k += blockDim.x) tab[k] = g_logtab[k];
-  __syncthreads();
-  double x0 = 1.5 + threadIdx.x * 1e-3, x1 = x0 + 0.25, x2 = x0 + 0.5, x3 = x0 + 0.75;
-  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-  for (int64_t it = 0; it < iters; ++it) {
-    if (mode == 0) {
-      a0 += half_ln(x0, tab); a1 += half_ln(x1, tab); a2 += half_ln(x2, tab); a3 += half_ln(x3, tab);
-    } else if (mode == 1) {
-      a0 += half_ln_noi2f(x0, tab); a1 += half_ln_noi2f(x1, tab);
-      a2 += half_ln_noi2f(x2, tab); a3 += half_ln_noi2f(x3, tab);
-    } else {
-      a0 += 0.5 * log(x0); a1 += 0.5 * log(x1); a2 += 0.5 * log(x2); a3 += 0.5 * log(x3);
-    }
-    x0 = fma(x0, 1.0000001, 1e-9); x1 = fma(x1, 1.0000001, 1e-9);
-    x2 = fma(x2, 1.0000001, 1e-9); x3 = fma(x3, 1.0000001, 1e-9);
-  }
-  double r = a0 + a1 + a2 + a3;
-  if (r == 12345.678) out[blockIdx.x] = r;
 }
 
 // self-test hooks: fast ln vs libdevice, and a DMMA fragment-layout check
@@ -1234,8 +749,6 @@ __global__ void selftest_dmma_kernel(const double* A, const double* B, double* C
   C[r * 8 + 2 * c + 1] = c1;
 }
 
-static int g_ik1_tab = 0;  // ik1_sym_kernel column loop: 0 unrolled 4, 1 unrolled 2
-
 template <int P, int MODE>
 static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, cudaStream_t st,
                       int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
@@ -1245,7 +758,7 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
     return WQ_EINVAL;
   }
   const size_t smem = (size_t)Ik4Cfg<P, MODE>::TOTAL * 8;
-  auto kern = g_ik1_tab == 1 ? ik1_sym_kernel<P, MODE, 1> : ik1_sym_kernel<P, MODE, 0>;
+  auto kern = ik1_sym_kernel<P, MODE, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nb = ceil_div(sm->n_rows, FT);
   const int64_t all = (int64_t)nb * (nb + 1) / 2;
@@ -1257,33 +770,20 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
   return check_launch("wq_ik1_sym");
 }
 
-static int g_x2_version = -1;
-
 template <int P>
 static int launch_x2(int64_t N, const double* Uext, const double* Zext, const double* s_w,
                      double alpha, double w_ik1, double* X, int64_t ldx, cudaStream_t st,
                      int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
-  if (g_x2_version < 0) {
-    const char* v = getenv("WQB200_X2");
-    g_x2_version = v ? atoi(v) : 4;
-  }
   const int nb = ceil_div(N, FT);
   const int64_t all = (int64_t)nb * (nb + 1) / 2;
   if (pair1 < 0 || pair1 > all) pair1 = all;
   if (pair0 < 0) pair0 = 0;
   const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
   if (blocks <= 0) return WQ_OK;
-  if (g_x2_version == 4) {
-    const size_t smem = (size_t)X4Smem<P>::TOTAL * 8;
-    cudaFuncSetAttribute(x2v4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    x2v4_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
-                                                               ldx, nb, tile_row0, pair0);
-    return check_launch("wq_x2_pairs");
-  }
-  const size_t smem = (size_t)X2Smem<P>::TOTAL * 8;
-  cudaFuncSetAttribute(x2_pairs_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  x2_pairs_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
-                                                                 ldx, nb, tile_row0, pair0);
+  const size_t smem = (size_t)X4Smem<P>::TOTAL * 8;
+  cudaFuncSetAttribute(x2v4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  x2v4_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
+                                                             ldx, nb, tile_row0, pair0);
   return check_launch("wq_x2_pairs");
 }
 
@@ -1307,8 +807,6 @@ static int ik1_dispatch(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag
     set_error("wq_ik1_sym: table mode without invp2");
     return WQ_EINVAL;
   }
-  int rc = ensure_logtab();
-  if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int p = (int)(sm->wg - 1) / 2;
   const bool tab = sm->k1_mode == WQ_K1_TABLE;
@@ -1418,46 +916,8 @@ int wq_x2_rows(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
 }
 
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream) {
-  int rc = ensure_logtab();
-  if (rc) return rc;
   selftest_log_kernel<<<ceil_div(n, 256), 256, 0, (cudaStream_t)stream>>>(n, x, out_fast, out_ref);
   return check_launch("wq_selftest_log");
-}
-
-int wq_probe_log(int64_t iters, int blocks, int mode, double* out, void* stream) {
-  int rc = ensure_logtab();
-  if (rc) return rc;
-  probe_log_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(iters, mode, out);
-  return check_launch("wq_probe_log");
-}
-
-int wq_probe_phi(int iters, int blocks, int mode, const double* Uext, double* out, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  switch (mode) {
-    case 0: probe_phi_kernel<0><<<blocks, 256, 0, st>>>(iters, Uext, out); break;
-    case 1: probe_phi_kernel<1><<<blocks, 256, 0, st>>>(iters, Uext, out); break;
-    case 2: probe_phi_kernel<2><<<blocks, 256, 0, st>>>(iters, Uext, out); break;
-    default: probe_phi_kernel<3><<<blocks, 256, 0, st>>>(iters, Uext, out); break;
-  }
-  return check_launch("wq_probe_phi");
-}
-
-int wq_set_ik1_passes(int mode) {
-  if (mode < 1 || mode > 2) {
-    set_error("wq_set_ik1_passes: 1 (column loop unrolled 4) or 2 (unrolled 2)");
-    return WQ_EINVAL;
-  }
-  g_ik1_tab = mode - 1;
-  return WQ_OK;
-}
-
-int wq_debug_x2_timing(long long* buf) {
-  cudaError_t e = cudaMemcpyToSymbol(g_x2_dbg, &buf, sizeof(buf));
-  if (e != cudaSuccess) {
-    set_error("wq_debug_x2_timing: %s", cudaGetErrorString(e));
-    return WQ_ECUDA;
-  }
-  return WQ_OK;
 }
 
 #ifdef WQ_X2_TIMELINE

@@ -166,7 +166,4 @@ __device__ __forceinline__ double half_ln64t(double x, const double2* __restrict
   return fma(de, kLn64C[5], w);
 }
 
-// device address of the 16-entry table (wq_fast.cu; uploads it on first use)
-int logtab16_device(const double** out);
-
 }  // namespace wq
