@@ -253,6 +253,16 @@ int wq_x2_pairs_range(int64_t N, int p, int nA, int nApad, int ws, int ktot, int
                       double w_ik1, int64_t pair0, int64_t pair1, double* X, int64_t ldx,
                       void* stream);
 
+/* The same kernels over an explicit list of upper-triangle tile-pair indices
+ * (device array, npairs entries): the single-process multi-GPU host path gives
+ * each GPU the pairs that complete its own rows. */
+int wq_ik1_pair_list(const wq_smooth_t* sm, const int64_t* plist, int64_t npairs, double* X,
+                     int64_t ldx, int* flag, void* stream);
+int wq_x2_pair_list(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+                    const double* Uext, const double* Zext, const double* s_w, double alpha,
+                    double w_ik1, const int64_t* plist, int64_t npairs, double* X, int64_t ldx,
+                    void* stream);
+
 /* Self-test hooks (unit tests): the IK1 kernel's table 0.5*ln vs libdevice; one DMMA 8x8x4. */
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream);
 int wq_selftest_dmma(const double* A, const double* B, double* C, void* stream);

@@ -82,6 +82,9 @@ _SIGS = {
     "wq_x2_rows": [c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_dbl, c_dbl,
                    c_i64, c_i64, c_vp, c_i64, c_vp],
     "wq_b2_inner": [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+    "wq_ik1_pair_list": [ctypes.POINTER(WqSmooth), c_vp, c_i64, c_vp, c_i64, c_vp, c_vp],
+    "wq_x2_pair_list": [c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_dbl,
+                        c_dbl, c_vp, c_i64, c_vp, c_i64, c_vp],
     "wq_selftest_log": [c_i64, c_vp, c_vp, c_vp, c_vp],
     "wq_selftest_dmma": [c_vp, c_vp, c_vp, c_vp],
     "wq_gen_pair_blocks": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_dbl, c_vp, c_vp,

@@ -376,7 +376,11 @@ def _torch():
 
 
 def _dev(disc: Discretization, key, make):
+    """Per-device cache of the discretization's device data (the current CUDA
+    device is part of the key: the multi-GPU host path keeps one copy per GPU)."""
+    import torch
     d = disc._dev
+    key = (torch.cuda.current_device(), key)
     if key not in d:
         d[key] = make()
     return d[key]
@@ -1207,25 +1211,33 @@ def pinned_host_matrix(n: int, m: int = None):
             os.sched_setaffinity(0, old)
 
 
+_COPY_STREAMS = {}
+
+
 def _copy_stream(torch):
-    if not hasattr(_copy_stream, "s"):
-        _copy_stream.s = torch.cuda.Stream()
-    return _copy_stream.s
+    dev = torch.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAMS[dev]
 
 
 def assemble_matrix_to_host(disc: Discretization, out=None, scaled: bool = True,
-                            chunks: int = 32, work=None):
+                            chunks: int = 32, work=None, devices=None):
     """A (scaled) or M into a host tensor, streaming finished row blocks to the
     host while the next ones are assembled (closed uniform meshes: tile pairs
     are processed in tile-row order, so once the pairs of tile rows < R are
     done, rows < 64 R are final).  ``out``: (N, N) float64 CPU tensor, pinned
     for full PCIe speed (allocated when None).  Other meshes assemble, then
     copy.  ``work``: optional (N, N) device buffer for the assembly (else one is
-    cached on the discretization).  Returns ``out`` after the last copy."""
+    cached on the discretization).  ``devices``: several CUDA devices assemble
+    in one process, each its own share of the rows over its own PCIe link
+    (``_to_host_multi``).  Returns ``out`` after the last copy."""
     torch = _torch()
     N = disc.space.dim
     if out is None:
         out = pinned_host_matrix(N)
+    if devices is not None and len(devices) > 1:
+        return _to_host_multi(disc, out, scaled, chunks, list(devices))
     X = work if work is not None else _dev(disc, "host_stage", lambda: _new_square(disc))
     if not _use_v2(disc) or chunks <= 1:
         _assemble_into(disc, X, scaled)
@@ -1262,6 +1274,81 @@ def assemble_matrix_to_host(disc: Discretization, out=None, scaled: bool = True,
         done = end
     cs.synchronize()
     _check_flag(sm)
+    return out
+
+
+def _own_row_pairs(nb: int, t0: int, t1: int) -> np.ndarray:
+    """Upper-triangle tile pairs (J, I), J < t0 <= I < t1, in pair order: the
+    pairs whose mirrors complete the left part of tile rows [t0, t1)."""
+    if t0 == 0 or t1 <= t0:
+        return np.zeros(0, np.int64)
+    J = np.arange(t0, dtype=np.int64)
+    first = J * nb - J * (J - 1) // 2 + (t0 - J)          # pair (J, t0)
+    return (first[:, None] + np.arange(t1 - t0, dtype=np.int64)[None, :]).ravel()
+
+
+def _to_host_multi(disc: Discretization, out, scaled: bool, chunks: int, devices):
+    """Single-process multi-GPU host path (closed uniform meshes): the tile rows
+    are split evenly over ``devices``; device d computes every tile pair that
+    touches its rows -- the pairs (J, I), J < t0, whose mirrors complete the left
+    part of its rows (an explicit pair list), then its own upper pairs in
+    tile-row chunks -- in its own (N, N) buffer, and streams each finished row
+    chunk to the shared pinned host array over its own PCIe link.  The same
+    device may appear twice (two buffers on one GPU: the bit-identity test).
+    Other meshes: the first device assembles, then copies."""
+    torch = _torch()
+    N = disc.space.dim
+    if not _use_v2(disc):
+        with torch.cuda.device(devices[0]):
+            return assemble_matrix_to_host(disc, out=out, scaled=scaled, chunks=1)
+    alpha = -1.0 / (2.0 * TWO_PI) if scaled else 0.5
+    T = _lib.WQ_FTILE
+    nb = -(-N // T)
+    k = len(devices)
+    bounds = [nb * d // k for d in range(k + 1)]
+    start = lambda r: r * nb - r * (r - 1) // 2     # first pair of tile row r
+    pending = []
+    for slot, dev in enumerate(devices):
+        t0, t1 = bounds[slot], bounds[slot + 1]
+        if t1 <= t0:
+            continue
+        with torch.cuda.device(dev):
+            lp, d = _logpart_dev(disc)
+            sm = _smooth(disc)
+            X = _dev(disc, ("host_multi", slot), lambda: _new_square(disc))
+            plist = _dev(disc, ("host_pairs", slot, nb, t0, t1),
+                         lambda: _to_dev(torch, _own_row_pairs(nb, t0, t1)))
+            main = torch.cuda.current_stream()
+            st = _lib.stream_handle(main)
+            Zext = _zext_table(disc)
+            x2args = (N, disc.space.degree, lp.da + 1, lp.nApad, lp.s_w.shape[1],
+                      lp.uext.shape[1], lp.zstride, _lib.ptr(d["uext"]), _lib.ptr(Zext),
+                      _lib.ptr(d["s_w"]), alpha, 2.0)
+            if plist.numel():
+                _lib.call("wq_ik1_pair_list", ctypes_ref(sm["struct"]), _lib.ptr(plist),
+                          plist.numel(), _lib.ptr(X), X.stride(0), _lib.ptr(sm["flag"]), st)
+                _lib.call("wq_x2_pair_list", *x2args, _lib.ptr(plist), plist.numel(), _lib.ptr(X),
+                          X.stride(0), st)
+            cs = _copy_stream(torch)
+            cs.wait_stream(main)
+            rows_per = max(1, -(-(t1 - t0) // max(1, chunks // k)))
+            for r0 in range(t0, t1, rows_per):
+                r1 = min(t1, r0 + rows_per)
+                _lib.call("wq_ik1_pairs", ctypes_ref(sm["struct"]), start(r0), start(r1), _lib.ptr(X),
+                          X.stride(0), _lib.ptr(sm["flag"]), st)
+                _lib.call("wq_x2_pairs_range", *x2args, start(r0), start(r1), _lib.ptr(X), X.stride(0),
+                          st)
+                ev = torch.cuda.Event()
+                ev.record(main)
+                cs.wait_event(ev)
+                a, b = r0 * T, min(N, r1 * T)
+                with torch.cuda.stream(cs):
+                    out[a:b].copy_(X[a:b], non_blocking=True)
+            pending.append((dev, cs, sm))
+    for dev, cs, sm in pending:
+        with torch.cuda.device(dev):
+            cs.synchronize()
+            _check_flag(sm)
     return out
 
 

@@ -40,8 +40,11 @@ constexpr int FT = 64;  // tile rows/cols
 // Tile mapping: sym (tile_row0 < 0): upper-triangle pairs of an nb x nb tile grid;
 // rect: tile rows tile_row0 .. + gridDim.x / nbj, all nbj tile columns, output rows
 // offset by tile_row0 * FT (a rank's row block).
-__device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int64_t pair0, int& bi, int& bj) {
-  if (tile_row0 < 0) {
+__device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int64_t pair0,
+                                              const int64_t* plist, int& bi, int& bj) {
+  if (plist) {                 // explicit list of upper-triangle pair indices
+    tri_index(plist[blockIdx.x], nb, bi, bj);
+  } else if (tile_row0 < 0) {
     tri_index(pair0 + blockIdx.x, nb, bi, bj);
   } else {
     bi = tile_row0 + (int)(blockIdx.x / nb);
@@ -313,11 +316,11 @@ __device__ __forceinline__ void ik1_tile_v5(const wq_smooth_t& sm, int bi, int b
 
 template <int P, int MODE, int TAB>
 __global__ void __launch_bounds__(IK4_THREADS, 3)
-ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, double* X, int64_t ldx,
-               int* flag) {
+ik1_sym_kernel(wq_smooth_t sm, int nb, int tile_row0, int64_t pair0, const int64_t* plist, double* X,
+               int64_t ldx, int* flag) {
   extern __shared__ double dsm[];
   int bi, bj;
-  tile_of_block(nb, tile_row0, pair0, bi, bj);
+  tile_of_block(nb, tile_row0, pair0, plist, bi, bj);
   const int64_t row_off = tile_row0 < 0 ? 0 : (int64_t)tile_row0 * FT;
   int bad = 0;
   ik1_tile_v5<P, MODE, TAB == 1 ? 2 : 4>(sm, bi, bj, row_off, X, ldx, bad, dsm);
@@ -516,7 +519,7 @@ template <int P>
 __global__ void __launch_bounds__(X2_THREADS, 2)
 x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
             const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
-            int nb, int tile_row0, int64_t pair0) {
+            int nb, int tile_row0, int64_t pair0, const int64_t* plist) {
   using C = X2Cfg<P>;
   using L = X4Smem<P>;
   constexpr int KS4 = C::KS / 4;
@@ -535,7 +538,7 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
   const bool with_ik1 = w_ik1 != 0.0;
   const bool zbulk = n >= C::ZROWS;
   int bi, bj;
-  tile_of_block(nb, tile_row0, pair0, bi, bj);
+  tile_of_block(nb, tile_row0, pair0, plist, bi, bj);
   const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
   const int ni = (int)min((int64_t)FT, N - I0);
   const int nj = (int)min((int64_t)FT, N - J0);
@@ -751,7 +754,8 @@ __global__ void selftest_dmma_kernel(const double* A, const double* B, double* C
 
 template <int P, int MODE>
 static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, cudaStream_t st,
-                      int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
+                      int tile_row0, int tile_row1, int64_t pair0, int64_t pair1,
+                      const int64_t* plist) {
   using C = Ik4Cfg<P, MODE>;
   if (sm->wg != C::WG) {
     set_error("wq_ik1_sym: rule band width %lld != 2p+1", (long long)sm->wg);
@@ -766,14 +770,15 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
   if (pair0 < 0) pair0 = 0;
   const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
   if (blocks <= 0) return WQ_OK;
-  kern<<<(unsigned)blocks, IK4_THREADS, smem, st>>>(*sm, nb, tile_row0, pair0, X, ldx, flag);
+  kern<<<(unsigned)blocks, IK4_THREADS, smem, st>>>(*sm, nb, tile_row0, pair0, plist, X, ldx, flag);
   return check_launch("wq_ik1_sym");
 }
 
 template <int P>
 static int launch_x2(int64_t N, const double* Uext, const double* Zext, const double* s_w,
                      double alpha, double w_ik1, double* X, int64_t ldx, cudaStream_t st,
-                     int tile_row0, int tile_row1, int64_t pair0, int64_t pair1) {
+                     int tile_row0, int tile_row1, int64_t pair0, int64_t pair1,
+                     const int64_t* plist) {
   const int nb = ceil_div(N, FT);
   const int64_t all = (int64_t)nb * (nb + 1) / 2;
   if (pair1 < 0 || pair1 > all) pair1 = all;
@@ -783,7 +788,7 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
   const size_t smem = (size_t)X4Smem<P>::TOTAL * 8;
   cudaFuncSetAttribute(x2v4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   x2v4_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
-                                                             ldx, nb, tile_row0, pair0);
+                                                             ldx, nb, tile_row0, pair0, plist);
   return check_launch("wq_x2_pairs");
 }
 
@@ -794,7 +799,8 @@ using namespace wq;
 extern "C" {
 
 static int ik1_dispatch(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, void* stream,
-                        int tile_row0, int tile_row1, int64_t pair0 = -1, int64_t pair1 = -1) {
+                        int tile_row0, int tile_row1, int64_t pair0 = -1, int64_t pair1 = -1,
+                        const int64_t* plist = nullptr) {
   if (!sm || !X || !flag || sm->n_rows <= 0 || !sm->closed) {
     set_error("wq_ik1_sym: bad arguments (closed uniform meshes only)");
     return WQ_EINVAL;
@@ -812,8 +818,8 @@ static int ik1_dispatch(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag
   const bool tab = sm->k1_mode == WQ_K1_TABLE;
 #define WQ_IK1_CASE(PP)                                                                          \
   case PP:                                                                                       \
-    return tab ? launch_ik1<PP, WQ_K1_TABLE>(sm, X, ldx, flag, st, tile_row0, tile_row1, pair0, pair1) \
-               : launch_ik1<PP, WQ_K1_CLOSED>(sm, X, ldx, flag, st, tile_row0, tile_row1, pair0, pair1);
+    return tab ? launch_ik1<PP, WQ_K1_TABLE>(sm, X, ldx, flag, st, tile_row0, tile_row1, pair0, pair1, plist) \
+               : launch_ik1<PP, WQ_K1_CLOSED>(sm, X, ldx, flag, st, tile_row0, tile_row1, pair0, pair1, plist);
   switch (p) {
     WQ_IK1_CASE(2)
     WQ_IK1_CASE(3)
@@ -861,7 +867,8 @@ int wq_zext(int64_t n, int nA, int nApad, int zstride, const double* Zp, const d
 static int x2_dispatch(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
                        const double* Uext, const double* Zext, const double* s_w, double alpha,
                        double w_ik1, double* X, int64_t ldx, void* stream, int tile_row0,
-                       int tile_row1, int64_t pair0 = -1, int64_t pair1 = -1) {
+                       int tile_row1, int64_t pair0 = -1, int64_t pair1 = -1,
+                       const int64_t* plist = nullptr) {
   if (N <= 0 || !Uext || !Zext || !s_w || !X) {
     set_error("wq_x2_pairs: bad arguments");
     return WQ_EINVAL;
@@ -875,7 +882,7 @@ static int x2_dispatch(int64_t N, int p, int nA, int nApad, int ws, int ktot, in
       return WQ_EINVAL;                                                                        \
     }                                                                                          \
     return launch_x2<PP>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, st, tile_row0, tile_row1, \
-                         pair0, pair1);
+                         pair0, pair1, plist);
   switch (p) {
     WQ_X2_CASE(2)
     WQ_X2_CASE(3)
@@ -913,6 +920,29 @@ int wq_x2_rows(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstrid
   }
   return x2_dispatch(N, p, nA, nApad, ws, ktot, zstride, Uext, Zext, s_w, alpha, w_ik1, Xrows, ldx,
                      stream, (int)tile_row0, (int)tile_row1);
+}
+
+int wq_ik1_pair_list(const wq_smooth_t* sm, const int64_t* plist, int64_t npairs, double* X,
+                     int64_t ldx, int* flag, void* stream) {
+  if (!plist || npairs < 0) {
+    set_error("wq_ik1_pair_list: bad pair list");
+    return WQ_EINVAL;
+  }
+  if (npairs == 0) return WQ_OK;
+  return ik1_dispatch(sm, X, ldx, flag, stream, -1, -1, 0, npairs, plist);
+}
+
+int wq_x2_pair_list(int64_t N, int p, int nA, int nApad, int ws, int ktot, int zstride,
+                    const double* Uext, const double* Zext, const double* s_w, double alpha,
+                    double w_ik1, const int64_t* plist, int64_t npairs, double* X, int64_t ldx,
+                    void* stream) {
+  if (!plist || npairs < 0) {
+    set_error("wq_x2_pair_list: bad pair list");
+    return WQ_EINVAL;
+  }
+  if (npairs == 0) return WQ_OK;
+  return x2_dispatch(N, p, nA, nApad, ws, ktot, zstride, Uext, Zext, s_w, alpha, w_ik1, X, ldx,
+                     stream, -1, -1, 0, npairs, plist);
 }
 
 int wq_selftest_log(int64_t n, const double* x, double* out_fast, double* out_ref, void* stream) {
