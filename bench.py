@@ -190,6 +190,22 @@ def kernel_flops(disc):
     return {"ik1": ik1, "ik2": ik2}
 
 
+def x2_executed_flops(disc):
+    """FP64 tensor flops x2v4_kernel issues per launch: per tile pair 8 warps x 2
+    orientations x (phi NSTEPS x NKB + band 8 x KS/4) DMMA m8n8k4 of 512 flops
+    (wq_fast.cu X2Cfg)."""
+    p = disc.space.degree
+    NA = p + 13
+    NAPAD = -(-NA // 4) * 4
+    WSPAD = -(-(2 * p + 1) // 4) * 4
+    nsteps = ((p + 1) * NAPAD + WSPAD) // 4
+    nkb = (64 + 2 * p + 14) // 8
+    ks4 = -(-(8 + 2 * p) // 4)
+    nb = -(-disc.space.dim // 64)
+    pairs = nb * (nb + 1) // 2
+    return float(pairs * 8 * 2 * (nsteps * nkb + 8 * ks4) * 512)
+
+
 def committed_traffic(dom):
     """dram read+write bytes per launch of the dominant kernel from the
     committed ncu --set full capture (profiles/r*_traffic.json), or None."""
@@ -481,8 +497,13 @@ def main():
     dom = "ik1" if split[1] >= split[2] else "ik2"
     dom_ms = split[1] if dom == "ik1" else split[2]
     achieved = fl[dom] / (dom_ms * 1e-3) / 1e12
+    executed = x2_executed_flops(disc) if dom == "ik2" else None
     roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2v4_kernel"}[dom],
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "executed_flop_per_launch": executed,
+                "executed_frac": (executed / (dom_ms * 1e-3) / 1e12 / peak) if executed else None,
+                "executed_note": "DMMA flops the kernel issues (skew and band padding included), "
+                                 "executed / time / peak ~ the DMMA pipe's active fraction",
                 "peak_source": "measured DFMA probe (wq_fp64_peak, burst); MEASURED_PEAKS.json has "
                                "no FP64 entry", "peak_datasheet": FP64_DATASHEET_TFLOPS,
                 "traffic": committed_traffic(dom), "traffic_unit": "bytes per launch (ncu, profiles/)"}
@@ -779,6 +800,33 @@ def run_c5(args):
     if k1_skipped:
         nq, wbar = disc.nodes.n, 2 * space.degree + 1
         W -= 67.0 * nq * nq + 2.0 * wbar * (nq * N + N * N)
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        # public API with host buffers: H2D of the O(N) inputs from pinned memory, assembly,
+        # D2H of the 3.3 GB matrix into a pinned host array
+        sm = AS._smooth(disc)
+        lp, dd = AS._logpart_dev(disc)
+        inputs = [v for v in list(sm.values()) + list(dd.values())
+                  if isinstance(v, torch.Tensor) and v.is_cuda and v.numel() > 1]
+        pinned = [t.cpu().pin_memory() for t in inputs]
+        host = AS.pinned_host_matrix(N)
+        W_ = __import__("paper_1703_10016_b200")
+        W_.assemble_matrix_to_host(disc, out=host, work=X)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for src, dst in zip(pinned, inputs):
+                dst.copy_(src, non_blocking=True)
+            W_.assemble_matrix_to_host(disc, out=host, work=X)
+            torch.cuda.synchronize()
+        t_e2e = (time.perf_counter() - t0) / args.e2e_steps
+        e2e = {"value": N * N / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in pinned)),
+               "d2h_bytes_per_step": int(N * N * 8), "ms_per_step": t_e2e * 1e3,
+               "path": "assemble_matrix_to_host (assemble, then one D2H copy)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_c5(args)
     if rank == 0:
         line = {
             "metric": METRIC, "value": N * N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
@@ -803,12 +851,36 @@ def run_c5(args):
                          "unit": "TFLOP/s per GPU", "W_flop": W,
                          "frac": W / (ms * 1e-3) / 1e12 / world / peak, "traffic": None},
             "precompute_s": precompute_s,
-            "e2e": None,
-            "cpu_baseline": None,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def cpu_baseline_c5(args, rows: int = 2):
+    """C5 on this host: the oracle's row restatement for graded open meshes
+    (oracle.GeneralRows: pair moments by the reference recipe, FFT correlation
+    on the width lattice, banded fit solves), timed on a bounded row sample;
+    its O(N) setup (rules, gap table) reported separately."""
+    try:
+        from oracle import wq_oracle as O
+    except ImportError:
+        return None
+    sp = O.config5_space()
+    slit = O.Curve(O.open_basis(1, np.array([-1.0, 1.0])), [[-1, 0], [1, 0]])
+    t0 = time.perf_counter()
+    gr = O.GeneralRows(slit, sp)
+    setup = time.perf_counter() - t0
+    sample = np.random.default_rng(2).integers(0, sp.dim, rows)
+    t0 = time.perf_counter()
+    gr.a_rows(sample)
+    t = time.perf_counter() - t0
+    return {"value": rows * sp.dim / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{rows} rows of A ({rows * sp.dim} entries) via oracle.GeneralRows, {t:.1f}s "
+                      f"(its per-call Theta / D matvecs over every element pair dominate); setup "
+                      f"{setup:.1f}s untimed; the reference itself raises on graded meshes"}
 
 
 def cpu_baseline(args, N):
