@@ -785,7 +785,11 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
   if (pair0 < 0) pair0 = 0;
   const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
   if (blocks <= 0) return WQ_OK;
+#ifdef WQ_X2_ONE_CTA   // tools build only: one CTA per SM (occupancy experiment)
+  const size_t smem = 120 * 1024;
+#else
   const size_t smem = (size_t)X4Smem<P>::TOTAL * 8;
+#endif
   cudaFuncSetAttribute(x2v4_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   x2v4_kernel<P><<<(unsigned)blocks, X2_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X,
                                                              ldx, nb, tile_row0, pair0, plist);
