@@ -290,8 +290,10 @@ def kbar_grid(curve: Curve, s, t):
 # --------------------------------------------------------------------------
 
 
-def build_nodes(fine: Basis):
-    """Shared node vector (quadrature.py:87-146)."""
+def build_nodes(fine: Basis, end_fix: bool = False):
+    """Shared node vector (quadrature.py:87-146); ``end_fix``: the opt-in
+    deviation that keeps the extra points of a repeated knot next to an open
+    end element (the reference drops them, quadrature.py:106-108)."""
     d = fine.degree
     els = fine.elements
     pts = [fine.breakpoints]
@@ -301,7 +303,11 @@ def build_nodes(fine: Basis):
         extra[0] = extra[-1] = fine.seam_multiplicity - 1
     n_inner = 1 + extra[:-1] + extra[1:]
     if not fine.closed:
-        n_inner[0] = n_inner[-1] = d
+        if end_fix and len(els) > 1:
+            n_inner[0] = d + extra[1]
+            n_inner[-1] = d + extra[-2]
+        else:
+            n_inner[0] = n_inner[-1] = d
     if np.all(n_inner == 1):
         mids = 0.5 * (els[:, 0] + els[:, 1])
         if fine.closed:
@@ -373,12 +379,12 @@ class Disc:
     J: np.ndarray
 
 
-def build_discretization(curve, space, nref=1) -> Disc:
+def build_discretization(curve, space, nref=1, end_fix=False) -> Disc:
     """assembly.py:147-172 (singular rules omitted: unused by the matrix)."""
     curve = curve if isinstance(curve, Curve) else Curve.from_reference(curve)
     space = as_basis(space)
     fine = refine(space, nref)
-    nodes = build_nodes(fine)
+    nodes = build_nodes(fine, end_fix)
     W = regular_rules(space, fine, nodes)
     J = curve.speed(nodes)
     return Disc(curve, space, fine, nodes, W, W * J[None, :], design(space, nodes).T, J)
@@ -1033,7 +1039,8 @@ def pair_moments_tiered(da, db, he, hf, delta):
 class GeneralRows:
     """Rows of M / A for an open discretization of any grading (config 5)."""
 
-    def __init__(self, curve: Curve, space: Basis, nref: int = 1, chunk: int = 65536):
+    def __init__(self, curve: Curve, space: Basis, nref: int = 1, chunk: int = 65536,
+                 end_fix: bool = False):
         assert not space.closed, "GeneralRows: open meshes"
         import scipy.sparse as sp
         self.curve, self.space = curve, space
@@ -1042,7 +1049,7 @@ class GeneralRows:
         self.d = d = fine.degree
         self.P = space.degree + JFIT_DEGREE
         self.chunk = chunk
-        self.nodes = nodes = build_nodes(fine)
+        self.nodes = nodes = build_nodes(fine, end_fix)
         self.J = curve.speed(nodes)
         idx, w = _rules_local(space, fine, nodes, False)
         rows = np.concatenate([np.full(len(q), i) for i, q in enumerate(idx)])

@@ -219,16 +219,22 @@ class Discretization:
         return self.space.closed
 
 
-def build_discretization(curve, space, nref: int) -> Discretization:
+def build_discretization(curve, space, nref: int, *, end_node_fix: bool = False) -> Discretization:
     """Refine, build nodes and the banded regular rules, and sample the curve
-    at the nodes (assembly.py:147-172), in O(N) host time."""
+    at the nodes (assembly.py:147-172), in O(N) host time.
+
+    ``end_node_fix`` (keyword-only, opt-in deviation from the reference): keep
+    the extra nodes a repeated knot next to an open end element asks for, which
+    the reference drops (quadrature.py:106-108) and then fails on with a
+    rank-deficient last rule (ConstructionError, quadrature.py:528-531); see
+    ``precompute.build_nodes``."""
     curve = as_curve(curve)
     space = as_basis(space)
     _check_space(curve, space)
     t0 = time.perf_counter()
     refined = refine_uniform(space, nref)
     fine = refined.basis
-    nodes = PC.build_nodes(fine)
+    nodes = PC.build_nodes(fine, end_fix=end_node_fix)
     rules = PC.regular_rule_band(space, fine, nodes)
     rule_seconds = time.perf_counter() - t0
     b = curve.basis

@@ -45,11 +45,18 @@ PERIODIC_CORR_ORDER = 24  # quadrature.py:53 (closed-domain weight correction)
 # -- nodes ---------------------------------------------------------------------
 
 
-def build_nodes(fine: BasisSpec) -> np.ndarray:
+def build_nodes(fine: BasisSpec, end_fix: bool = False) -> np.ndarray:
     """Breakpoints + midpoints, d+2 points in open end elements, extra points
     beside multiple knots, deduplicated at 1e-12 L (quadrature.py:87-146).
     The O(N^3) SVD rank check is replaced by the banded/circulant SPD check
-    of the fit normal matrix (``fit_bands``)."""
+    of the fit normal matrix (``fit_bands``).
+
+    ``end_fix`` (opt-in deviation): the reference gives an open
+    end element exactly d interior points (quadrature.py:106-108), dropping the
+    m - 1 extra points its inner breakpoint of multiplicity m asks for, so a
+    repeated knot next to an end element leaves the last regular rule
+    rank-deficient (quadrature.py:528-531, ConstructionError).  With end_fix the
+    end element keeps both: d + (m - 1) interior points."""
     d = fine.degree
     els = fine.elements
     pts = [fine.breakpoints]
@@ -59,7 +66,11 @@ def build_nodes(fine: BasisSpec) -> np.ndarray:
         extra[0] = extra[-1] = fine.seam_multiplicity - 1
     n_inner = 1 + extra[:-1] + extra[1:]
     if not fine.closed:
-        n_inner[0] = n_inner[-1] = d
+        if end_fix and len(els) > 1:
+            n_inner[0] = d + extra[1]
+            n_inner[-1] = d + extra[-2]
+        else:
+            n_inner[0] = n_inner[-1] = d
     if np.all(n_inner == 1):
         mids = 0.5 * (els[:, 0] + els[:, 1])
         if fine.closed:

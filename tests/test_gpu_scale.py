@@ -107,3 +107,27 @@ def test_config5_full_size_rows_match_general_oracle(cuda):
     assert np.abs(np.diag(got[:, rows]) - ref[np.arange(len(rows)), rows]).max() / amax <= TOL
     assert bool(torch.isfinite(A).all())
     assert bool(torch.equal(A[:2048, :2048], A[:2048, :2048].T))
+
+
+@pytest.mark.parametrize("n_el", [64, 1024])
+def test_end_node_fix_graded_meshes(cuda, n_el):
+    """The opt-in end-element node fix on config-5 readings the
+    reference cannot build (a double knot next to the last element): A against
+    the restatement built with the same nodes (dense at 64 elements, sampled
+    rows of GeneralRows at 1024)."""
+    from oracle import wq_oracle as O
+    curve = W.load_curve({"degree": 1, "knots": [-1, -1, 1, 1], "control_points": [[-1, 0], [1, 0]]})
+    sp = O.config5_space(n_el=n_el, growth_elems=12 if n_el == 64 else 60)
+    space = W.BasisSpec(sp.degree, sp.knots, False)
+    disc = W.build_discretization(curve, space, 1, end_node_fix=True)
+    A = AS.assemble_matrix_device(disc).cpu().numpy()
+    oc = O.Curve(O.open_basis(1, np.array([-1.0, 1.0])), [[-1, 0], [1, 0]])
+    if n_el == 64:
+        od = O.build_discretization(oc, sp, 1, end_fix=True)
+        ref = O.scale_and_symmetrize(O.dense_ik1(od) + O.dense_ik2_general(od))[0]
+        assert np.abs(A - ref).max() / np.abs(ref).max() <= TOL
+    else:
+        rows = np.array([0, 1, 7, 500, space.dim - 8, space.dim - 2, space.dim - 1])
+        ref = O.GeneralRows(oc, sp, end_fix=True).a_rows(rows)
+        assert np.abs(A[rows] - ref).max() / np.abs(A).max() <= TOL
+    assert np.array_equal(A, A.T)

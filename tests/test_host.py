@@ -317,3 +317,24 @@ def test_inverse_decay_rows_bounds_dense_inverse():
     for c in range(0, m - k, 37):
         col = np.abs(Li[c:, c])
         assert np.all(col[k:] < 1e-19 * col.max())
+
+
+def test_end_node_fix_opt_in():
+    """A repeated knot next to an open end element: the reference drops the
+    extra end-element nodes (quadrature.py:106-108) and then raises on the
+    rank-deficient last rule (quadrature.py:528-531) -- the default here does
+    the same; the opt-in end_node_fix keeps them and the rules are exact."""
+    from oracle import wq_oracle as O
+    from paper_1703_10016_b200.errors import ConstructionError
+    curve = W.load_curve({"degree": 1, "knots": [-1, -1, 1, 1], "control_points": [[-1, 0], [1, 0]]})
+    sp = O.config5_space(n_el=64, growth_elems=12)
+    assert sp.multiplicities[-2] == 2
+    space = W.BasisSpec(sp.degree, sp.knots, False)
+    with pytest.raises(ConstructionError):
+        W.build_discretization(curve, space, 1)
+    disc = W.build_discretization(curve, space, 1, end_node_fix=True)
+    n_default = len(O.build_nodes(sp))
+    assert disc.nodes.n == n_default + 1
+    od = O.build_discretization(O.Curve(curve.basis, curve.control_points), sp, 1, end_fix=True)
+    assert np.array_equal(od.nodes, disc.nodes.nodes)
+    assert np.abs(disc.G - od.G).max() <= 1e-9 * np.abs(od.G).max()
