@@ -630,7 +630,11 @@ template <int BW, bool FWD>
 __device__ __forceinline__ void band_sweep_range(int64_t n, const double* Lb, double* x, int64_t ldx,
                                                  bool live, int64_t i0, int64_t i1, double (&w)[BW],
                                                  bool store) {
-  constexpr int RB = 16, DEPTH = 3;
+  // columns x segments threads: occupancy, not a deep per-thread prefetch, hides the HBM
+  // latency, so the register ring stays short (RB 8 x DEPTH 2: 3 solves 11.5 -> 10.0 ms at
+  // C5; 16 x 2: 11.1, 8 x 3: 12.1, 4 x 2: 9.9; the factor rows of a whole segment staged
+  // once in shared memory instead of per batch: 10.1)
+  constexpr int RB = 8, DEPTH = 2;
   __shared__ double cf[RB][BW + 1];   // [r][0] = 1/diag, [r][j] = -off-diagonal
   // sweep index i -> row: forward k = i, backward k = n - 1 - i
   auto row = [n](int64_t i) -> int64_t { return FWD ? i : n - 1 - i; };

@@ -434,7 +434,10 @@ __global__ void __launch_bounds__(128) gather_fs_kernel(wq_logpart_t lp, double 
 // X[j][i] (+)= sum_t S_j[t] Phi[(s_j + t) mod nf][i]; each CTA sweeps ST_ROWS
 // consecutive j (their Phi rows overlap: L1 reuse), ST_B rows j per batch with the
 // batch's loads issued before its FMAs
-constexpr int ST_ROWS = 16;
+#ifndef WQ_ST_ROWS
+#define WQ_ST_ROWS 16
+#endif
+constexpr int ST_ROWS = WQ_ST_ROWS;
 constexpr int ST_B = 4;
 template <int WS>
 __global__ void __launch_bounds__(128) add_st_phi_kernel(wq_logpart_t lp, const double* Phi,
