@@ -443,28 +443,48 @@ template <int WS>
 __global__ void __launch_bounds__(128) add_st_phi_kernel(wq_logpart_t lp, const double* Phi,
                                                          int64_t row0, int64_t row1, double* X,
                                                          int64_t ldx, int accumulate) {
+  // the CTA's rows j: wrapped band start and weights staged once (broadcast reads), so
+  // the per-entry work is WS loads + WS FMAs with pointer increments (the int64 modulo
+  // and wrap per load made the kernel issue-bound: 75 % issue at 1.6 TB/s)
+  __shared__ int64_t sst[ST_ROWS];
+  __shared__ double ssw[ST_ROWS][WS];
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t j0 = row0 + (int64_t)blockIdx.y * ST_ROWS;
-  if (i >= lp.n_rows) return;
   const int64_t nf = lp.n_fine, nr = lp.n_rows;
   const int64_t j1 = j0 + ST_ROWS < row1 ? j0 + ST_ROWS : row1;
+  for (int k = threadIdx.x; k < ST_ROWS * (WS + 1); k += blockDim.x) {
+    const int u = k / (WS + 1), t = k - u * (WS + 1);
+    const int64_t jj = j0 + u < j1 ? j0 + u : j1 - 1;
+    if (t == WS) sst[u] = pmod(lp.s_start[jj], nf);
+    else ssw[u][t] = lp.s_w[jj * WS + t];
+  }
+  __syncthreads();
+  if (i >= nr) return;
   for (int64_t j = j0; j < j1; j += ST_B) {
     double pv[ST_B][WS], xv[ST_B];
 #pragma unroll
     for (int u = 0; u < ST_B; ++u) {
-      const int64_t jj = j + u < j1 ? j + u : j1 - 1;
-      const int64_t sj = pmod(lp.s_start[jj], nf);   // unwrapped start -> [0, nf)
+      const int uu = (int)(j - j0) + u < (int)(j1 - j0) ? (int)(j - j0) + u : (int)(j1 - j0) - 1;
+      const int64_t sj = sst[uu];
+      if (sj + WS <= nf) {
+        const double* p = Phi + sj * nr + i;
 #pragma unroll
-      for (int t = 0; t < WS; ++t) pv[u][t] = __ldg(Phi + wrap1(sj + t, nf) * nr + i);
-      xv[u] = accumulate ? X[(jj - row0) * ldx + i] : 0.0;
+        for (int t = 0; t < WS; ++t, p += nr) pv[u][t] = __ldg(p);
+      } else {
+#pragma unroll
+        for (int t = 0; t < WS; ++t) pv[u][t] = __ldg(Phi + wrap1(sj + t, nf) * nr + i);
+      }
+      xv[u] = accumulate ? X[(j0 + uu - row0) * ldx + i] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < ST_B; ++u) {
-      const int64_t jj = j + u < j1 ? j + u : j1 - 1;
+      const int uu = (int)(j - j0) + u;
       double acc = 0.0;
+      if (uu < (int)(j1 - j0)) {
 #pragma unroll
-      for (int t = 0; t < WS; ++t) acc = fma(lp.s_w[jj * WS + t], pv[u][t], acc);
-      if (j + u < j1) X[(j + u - row0) * ldx + i] = xv[u] + acc;
+        for (int t = 0; t < WS; ++t) acc = fma(ssw[uu][t], pv[u][t], acc);
+        X[(j0 + uu - row0) * ldx + i] = xv[u] + acc;
+      }
     }
   }
 }
