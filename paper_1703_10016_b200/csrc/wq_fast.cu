@@ -62,15 +62,16 @@ __device__ __forceinline__ void tile_of_block(int nb, int tile_row0, int64_t pai
 //    warp one leftover node per lane), so
 //    every r-node load ({x, y} as one 16-byte load) and every rule-weight load
 //    (16-byte loads of a padded row) serves both;
-//  * the ln uses a 64-bin accurate table (one 16-byte load, degree-7 series,
-//    exponent by an exact DADD instead of I2F);
+//  * the ln uses a 64-bin accurate table (one 16-byte load, degree-4
+//    economised series, exponent by I2F on the idle conversion pipe:
+//    8 FP64 operations, wq_log.cuh);
 //  * tile pairs whose node ranges neither wrap at the seam nor touch (all
 //    but O(nb) of them) take a fast path: the node-index gap is q - r + const
 //    with one sign across the tile, so 1/p^2 is read through one per-thread
 //    pointer walked with the r loop (immediate offsets), no diagonal select,
 //    and the R-validity test is a running integer min/max of R's high word.
 //  The rest (and the closed-form distance mode) take the general path with
-//  a running node index.  ~21.5 FP64 and ~12 other instructions per value.
+//  a running node index.  ~16.5 FP64 and ~13 other instructions per value.
 // 160 threads, 3 CTAs per SM at p = 3 (75.3 KB shared memory each).
 // ---------------------------------------------------------------------------
 
