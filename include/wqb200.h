@@ -213,7 +213,10 @@ int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64
  *   reading IK1(I,J) from X (written by wq_ik1_sym), where
  *   X2[i,j] = sum_t S[j-d+t, j] Phi[j-d+t, i],
  *   Phi[m,i] = sum_K Uext[i][K] Zrow(m-i, K),  Uext[i] = [2U[i][a][al] (a*nApad+al),
- *   -S[i-d+t, i] (tu*nApad + t), 0 ..] (ktot columns).
+ *   -S[i-d+t, i] (tu*nApad + t), 0 ..] (ktot columns).  Uext is passed in DMMA
+ *   B-fragment order: element (i, K) at ((i/8 * ktot/4 + K/4) * 8 + i%8) * 4 + K%4,
+ *   rows padded with zeros to a multiple of 8 (ceil(N/8) * 8 * ktot doubles), so each
+ *   warp reads one contiguous 256-byte fragment per row group and k-step.
  *   alpha = -1/(4 pi), w_ik1 = 2 gives A; alpha = 1/2 gives M = (X + X^T)/2.
  */
 #define WQ_FTILE 64

@@ -545,6 +545,17 @@ def _m2_table(disc, lp: LogPart):
     return make()
 
 
+def _uext_fragments(uext):
+    """Uext in the DMMA B-fragment order the x2 kernel reads (include/wqb200.h):
+    [row group of 8][k-step of 4 columns][row in group][column in step], rows padded
+    with zeros to a multiple of 8, so a warp's fragment is one contiguous 256-byte load."""
+    N, ktot = uext.shape
+    G = -(-N // 8)
+    pad = np.zeros((8 * G, ktot))
+    pad[:N] = uext
+    return np.ascontiguousarray(pad.reshape(G, 8, ktot // 4, 4).transpose(0, 2, 1, 3))
+
+
 def _logpart_dev(disc):
     torch = _torch()
     lp = _log_part(disc)
@@ -558,7 +569,7 @@ def _logpart_dev(disc):
             d["U"] = _to_dev(torch, lp.U)
             d["v0"] = _to_dev(torch, lp.v0)
             d["taps"] = _to_dev(torch, lp.hinv_taps)
-            d["uext"] = _to_dev(torch, lp.uext)
+            d["uext"] = _to_dev(torch, _uext_fragments(lp.uext))
             tu = lp.U.shape[1]
             d["struct"] = _lib.WqLogpart(N, lp.n_el, lp.da, tu, lp.s_w.shape[1],
                                          d["e_start"].data_ptr(), d["U"].data_ptr(),

@@ -350,7 +350,7 @@ struct X2Cfg {
   static constexpr int NKB = (SPAN + 7 + 7) / 8;       // 8-row k blocks per row group
   static constexpr int ZROWS = 56 + 8 * NKB + AMAX;
   static constexpr int KS = ((8 + 2 * D) + 3) / 4 * 4;  // S-contraction K
-  static constexpr int PF = 12;                         // B-fragment prefetch depth
+  static constexpr int PF = 5;                          // B-fragment prefetch depth (k-steps)
 };
 
 constexpr int X2_THREADS = 256;
@@ -358,27 +358,38 @@ constexpr int X2_THREADS = 256;
 constexpr int PSTRIDE = 76;  // Phi smem row stride (== 12 mod 16), >= SPAN and 56 + KS
 
 // Phi[m][i] for m in [M0, M0 + SPAN), i in the tile rows starting at R0 (Uext rows),
-// written to Phs[i][m - M0]
+// written to Phs[i][m - M0].  Skewed coordinates: row group G (8 functions) needs the table
+// blocks zb = 7 - G .. 7 - G + NKB - 1 (block zb = window rows 8 zb + AMAX - off ..); adjacent
+// groups share all but one of them, so warp (g, h) = (warp / 2, warp % 2) takes BOTH groups
+// 2g and 2g + 1 over half of the blocks: NH + 1 A fragments from shared memory feed 2 NH
+// DMMAs per k-step (12 loads for 20 DMMAs at p = 3 instead of 20).  B fragments come from
+// the fragment-ordered Uext (one coalesced 256-byte load per group and k-step).
 template <int P>
-__device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64_t N,
-                                          const double* Zsm, double* Phs, int64_t M0, int64_t R0,
-                                          int64_t gmin, int warp) {
+__device__ __forceinline__ void phi_block(const double* __restrict__ Ufrag, int64_t N,
+                                          const double* Zsm, double* Phs, int64_t R0, int warp) {
   using C = X2Cfg<P>;
+  constexpr int NH0 = (C::NKB + 1) / 2, NH1 = C::NKB - NH0;   // blocks per half
+  constexpr int PF = C::PF;
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, c = lane & 3;
-  const int64_t kb0 = M0 - (R0 + 8 * warp + 7);
-  double acc[C::NKB][2];
+  const int g = warp >> 1, h = warp & 1;
+  const int nh = h ? NH1 : NH0;
+  double accA[NH0][2], accB[NH0][2];   // group 2g (A fragments j + 1), group 2g + 1 (j)
 #pragma unroll
-  for (int kb = 0; kb < C::NKB; ++kb) acc[kb][0] = acc[kb][1] = 0.0;
-  const int64_t row = R0 + 8 * warp + r;
-  const double* __restrict__ urow = Uext + (row < N ? row : 0) * C::KTOT + c;
-  const bool valid = row < N;
-  double bq[C::PF];
+  for (int j = 0; j < NH0; ++j) accA[j][0] = accA[j][1] = accB[j][0] = accB[j][1] = 0.0;
+  // B fragments: group G of the tile at Ufrag[((R0 / 8 + G) * NSTEPS + s) * 32 + lane]
+  const int64_t grpA = R0 / 8 + 2 * g;
+  const bool vA = 8 * grpA < N, vB = 8 * (grpA + 1) < N;
+  const double* __restrict__ uA = Ufrag + (vA ? grpA : 0) * (C::NSTEPS * 32) + lane;
+  const double* __restrict__ uB = Ufrag + (vB ? grpA + 1 : 0) * (C::NSTEPS * 32) + lane;
+  double bqA[PF], bqB[PF];
 #pragma unroll
-  for (int s = 0; s < C::PF; ++s) bq[s] = valid ? __ldg(urow + 4 * s) : 0.0;
-  const int zbase = (int)(kb0 + r + P - gmin);
-  // A fragments of k-step s: Zsm[(zbase + 8 kb - off(s)) * ZSTRIDE + col(s)], kb = 0..NKB-1;
-  // software-pipelined one k-step ahead so the DMMAs never wait on their LDS
+  for (int s = 0; s < PF; ++s) {
+    bqA[s] = vA ? __ldg(uA + 32 * s) : 0.0;
+    bqB[s] = vB ? __ldg(uB + 32 * s) : 0.0;
+  }
+  // A fragment j of k-step s: window row 8 (6 - 2g + h NH0 + j) + r + AMAX - off(s), column col(s)
+  const int zbase = 8 * (6 - 2 * g + h * NH0) + r + C::AMAX;
   auto zptr = [&](int s) -> const double* {
     int off, col;
     if (s < C::SZ) {
@@ -390,11 +401,12 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64
     }
     return Zsm + (zbase - off) * C::ZSTRIDE + col;
   };
-  double afr[2][C::NKB];
+  double afr[2][NH0 + 1];
   {
     const double* z = zptr(0);
 #pragma unroll
-    for (int kb = 0; kb < C::NKB; ++kb) afr[0][kb] = z[kb * 8 * C::ZSTRIDE];
+    for (int j = 0; j <= NH0; ++j)
+      if (NH0 == NH1 || j <= nh) afr[0][j] = z[j * 8 * C::ZSTRIDE];
   }
 #pragma unroll
   for (int s = 0; s < C::NSTEPS; ++s) {
@@ -402,20 +414,36 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Uext, int64
     if (s + 1 < C::NSTEPS) {
       const double* z = zptr(s + 1);
 #pragma unroll
-      for (int kb = 0; kb < C::NKB; ++kb) afr[cur ^ 1][kb] = z[kb * 8 * C::ZSTRIDE];
+      for (int j = 0; j <= NH0; ++j)
+        if (NH0 == NH1 || j <= nh) afr[cur ^ 1][j] = z[j * 8 * C::ZSTRIDE];
     }
-    const double b = bq[s % C::PF];
-    if (s + C::PF < C::NSTEPS) bq[s % C::PF] = valid ? __ldg(urow + 4 * (s + C::PF)) : 0.0;
+    const double ba = bqA[s % PF], bb = bqB[s % PF];
+    if (s + PF < C::NSTEPS) {
+      bqA[s % PF] = vA ? __ldg(uA + 32 * (s + PF)) : 0.0;
+      bqB[s % PF] = vB ? __ldg(uB + 32 * (s + PF)) : 0.0;
+    }
 #pragma unroll
-    for (int kb = 0; kb < C::NKB; ++kb) dmma(acc[kb][0], acc[kb][1], afr[cur][kb], b);
+    for (int j = 0; j < NH0; ++j) {
+      if (NH0 == NH1 || j < nh) {
+        dmma(accB[j][0], accB[j][1], afr[cur][j], bb);
+        dmma(accA[j][0], accA[j][1], afr[cur][j + 1], ba);
+      }
+    }
   }
+  // accA[j]: group 2g, block kb = h NH0 + j; accB[j]: group 2g + 1, same kb.
+  // Entry (r, 2c + e) of block kb of group G is Phi[m][i], i = 8G + 2c + e,
+  // m - M0 = 8 kb + r + (2c + e) - 7
 #pragma unroll
-  for (int kb = 0; kb < C::NKB; ++kb) {
+  for (int j = 0; j < NH0; ++j) {
+    if (NH0 == NH1 || j < nh) {
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int il = 8 * warp + 2 * c + e;
-      const int mm = (int)(kb0 + 8 * kb + r + R0 + il - M0);
-      if (mm >= 0 && mm < C::SPAN) Phs[il * PSTRIDE + mm] = acc[kb][e];
+      for (int e = 0; e < 2; ++e) {
+        const int mm = 8 * (h * NH0 + j) + r + 2 * c + e - 7;
+        if (mm >= 0 && mm < C::SPAN) {
+          Phs[(16 * g + 2 * c + e) * PSTRIDE + mm] = accA[j][e];
+          Phs[(16 * g + 8 + 2 * c + e) * PSTRIDE + mm] = accB[j][e];
+        }
+      }
     }
   }
 }
@@ -599,7 +627,6 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
   // one orientation: 0 = Phi rows I over the J range with band S_J, 1 = rows J over I, S_I
   auto orient = [&](const int o) {
     const int64_t R0 = o == 0 ? I0 : J0;
-    const int64_t M0 = (o == 0 ? J0 : I0) - C::D;
     // B fragments of the alpha S band for this warp's column block (raw now, scaled after
     // phi, when the loads have landed): bS[s] = S_{C0 + 8 warp + r}[4 s + c - r]
     double bS[KS4];
@@ -620,7 +647,7 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
       __syncthreads();
     }
     X5_TL(1 + 4 * o);
-    phi_block<P>(Uext, N, o == 0 ? Zs0 : Zs1, Phs, M0, R0, gmin[o], warp);
+    phi_block<P>(Uext, N, o == 0 ? Zs0 : Zs1, Phs, R0, warp);
 #pragma unroll
     for (int s2 = 0; s2 < KS4; ++s2) bS[s2] *= alpha;
     if (o == 0) {
