@@ -364,9 +364,15 @@ constexpr int PSTRIDE = 76;  // Phi smem row stride (== 12 mod 16), >= SPAN and 
 // 2g and 2g + 1 over half of the blocks: NH + 1 A fragments from shared memory feed 2 NH
 // DMMAs per k-step (12 loads for 20 DMMAs at p = 3 instead of 20).  B fragments come from
 // the fragment-ordered Uext (one coalesced 256-byte load per group and k-step).
-template <int P>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// before_store() runs after the last DMMA and before the first write to Phs
+template <int P, class Hook = NoHook>
 __device__ __forceinline__ void phi_block(const double* __restrict__ Ufrag, int64_t N,
-                                          const double* Zsm, double* Phs, int64_t R0, int warp) {
+                                          const double* Zsm, double* Phs, int64_t R0, int warp,
+                                          Hook before_store = Hook()) {
   using C = X2Cfg<P>;
   constexpr int NH0 = (C::NKB + 1) / 2, NH1 = C::NKB - NH0;   // blocks per half
   constexpr int PF = C::PF;
@@ -430,6 +436,7 @@ __device__ __forceinline__ void phi_block(const double* __restrict__ Ufrag, int6
       }
     }
   }
+  before_store();
   // accA[j]: group 2g, block kb = h NH0 + j; accB[j]: group 2g + 1, same kb.
   // Entry (r, 2c + e) of block kb of group G is Phi[m][i], i = 8G + 2c + e,
   // m - M0 = 8 kb + r + (2c + e) - 7
@@ -504,8 +511,15 @@ __device__ long long* g_x2_tl = nullptr;
       }                                                                                   \
     }                                                                                     \
   } while (0)
+// x2ws: stamps of pair k == 20 of every CTA: slots 0-9 Phi group (thread 0), 16-23 epilogue
+#define XW_TL(slot)                                                                       \
+  do {                                                                                    \
+    if (k == 20 && (threadIdx.x & 255) == 0 && g_x2_tl)                                   \
+      g_x2_tl[(int64_t)blockIdx.x * 32 + (slot)] = clock64();                             \
+  } while (0)
 #else
 #define X5_TL(k) do {} while (0)
+#define XW_TL(slot) do {} while (0)
 #endif
 
 template <int P>
@@ -530,12 +544,21 @@ __device__ __forceinline__ int64_t x5_gmin(int o, int bi, int bj) {
 // ZROWS contiguous table rows from gmin (mod n) into dst on the TMA engine (two pieces at
 // the seam), completing on bar
 template <int P>
+__device__ __forceinline__ void x5_window_at(double* dst, const double* Zext, int64_t n, int64_t g0,
+                                             uint64_t* bar);
+
+template <int P>
 __device__ __forceinline__ void x5_window(double* dst, const double* Zext, int64_t n, int64_t gmin,
                                           uint64_t* bar) {
+  x5_window_at<P>(dst, Zext, n, pmod(gmin, n), bar);
+}
+
+// the same from the reduced first row g0 = gmin mod n
+template <int P>
+__device__ __forceinline__ void x5_window_at(double* dst, const double* Zext, int64_t n, int64_t g0,
+                                             uint64_t* bar) {
   using C = X2Cfg<P>;
   constexpr unsigned RB = C::ZSTRIDE * 8;
-  int64_t g0 = gmin % n;
-  if (g0 < 0) g0 += n;
   const uint64_t pol = l2_evict_last();    // the Z' table is re-read by every tile pair
   const int64_t first = min((int64_t)C::ZROWS, n - g0);
   mbar_arrive_expect_tx(bar, C::ZROWS * RB);
@@ -748,6 +771,261 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
   X5_TL(8);
 }
 
+// ---------------------------------------------------------------------------
+// x2 v6 (x2ws_kernel): warp-specialised persistent variant of x2v4_kernel for full
+// upper-triangle sweeps.  One CTA of 16 warps per SM walks the tile pairs
+// blockIdx.x, + gridDim.x, ...:
+//   warps 0-7  (Phi group)      phi0(k), phi1(k), phi0(k+1), ... back to back: the DMMA
+//                               stream never stops for staging, hand-off or stores, and the
+//                               warps never meet at a barrier, so they drift apart and one
+//                               warp's fragment prologue / Phi stores hide under the others'
+//                               DMMAs.
+//   warps 8-15 (epilogue group) per pair: IK1 tile and S band into registers, band
+//                               contraction 0 from Phs[0], T hand-off through its own
+//                               buffer, band contraction 1 from Phs[1], stores of A(J,I)
+//                               and A(I,J) - all while the Phi group computes the next Phi.
+//                               Its first thread re-requests Z' window o (TMA) for the next
+//                               pair as soon as Phs[o] is full (every Phi warp has then read
+//                               the window), a whole phase ahead of its use.
+// Hand-over by shared-memory mbarriers (arrive by one lane per warp after __syncwarp, wait by
+// parity): wfull for the windows, pfull / pempty for the two Phi buffers.
+// Same arithmetic, in the same order, as x2v4_kernel: bit-identical results.
+// ---------------------------------------------------------------------------
+
+constexpr int XW_THREADS = 512;
+constexpr int XW_BAR_EPI = 1;   // named barrier of the epilogue group (T hand-off)
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// the warp's shared-memory accesses are ordered before the arrive of its first lane
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+
+template <int P>
+struct XwSmem {
+  using C = X2Cfg<P>;
+  static constexpr int ZW = C::ZROWS * C::ZSTRIDE;   // one Z' window
+  static constexpr int PH = FT * PSTRIDE;            // one Phi buffer
+  static constexpr int TS = FT * X5_TS;              // T hand-off
+  static constexpr int TOTAL = 2 * ZW + 2 * PH + TS + 6;   // + 6 mbarriers
+};
+
+template <int P>
+__global__ void __launch_bounds__(XW_THREADS, 1)
+x2ws_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict__ Zext,
+            const double* __restrict__ sw, double alpha, double w_ik1, double* X, int64_t ldx,
+            int nb, int64_t pair0, int64_t npairs, const int64_t* plist) {
+  using C = X2Cfg<P>;
+  using L = XwSmem<P>;
+  constexpr int KS4 = C::KS / 4;
+  extern __shared__ double smem[];
+  double* Tsm = smem + 2 * L::ZW + 2 * L::PH;
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(Tsm + L::TS);   // [2] window o landed (tx)
+  uint64_t* pfull = wfull + 2;                                  // [2] Phs[o] written by 8 Phi warps
+  uint64_t* pempty = wfull + 4;                                 // [2] Phs[o] read by 8 epilogue warps
+  const int tid = threadIdx.x;
+  const int64_t mine = (npairs - blockIdx.x + gridDim.x - 1) / gridDim.x;   // pairs of this CTA
+  auto pair_of = [&](int64_t k, int& bi, int& bj) {
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    tri_index(plist ? plist[t] : pair0 + t, nb, bi, bj);
+  };
+  if (tid == 0) {
+    for (int o = 0; o < 2; ++o) {
+      mbar_init(wfull + o, 1);
+      mbar_init(pfull + o, 8);
+      mbar_init(pempty + o, 8);
+    }
+  }
+  // Phi's pad columns (read by the band contraction against zero B entries) must be finite
+  for (int k = tid; k < 2 * FT * (PSTRIDE - C::SPAN); k += XW_THREADS) {
+    const int b = k / (FT * (PSTRIDE - C::SPAN)), q = k % (FT * (PSTRIDE - C::SPAN));
+    smem[2 * L::ZW + b * L::PH + (q / (PSTRIDE - C::SPAN)) * PSTRIDE + C::SPAN +
+         q % (PSTRIDE - C::SPAN)] = 0.0;
+  }
+  __syncthreads();
+  if (mine <= 0) return;
+
+  if (tid < 256) {
+    // ------------------------------ Phi group ------------------------------
+    const int warp = tid >> 5;
+    for (int64_t k = 0; k < mine; ++k) {
+      int bi, bj;
+      pair_of(k, bi, bj);
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const int64_t R0 = (int64_t)(o == 0 ? bi : bj) * FT;
+        XW_TL(5 * o);
+        mbar_wait(wfull + o, (unsigned)(k & 1));
+        XW_TL(5 * o + 1);
+        phi_block<P>(Uext, N, smem + o * L::ZW, smem + 2 * L::ZW + o * L::PH, R0, warp, [&]() {
+          XW_TL(5 * o + 2);
+          // Phs[o] is free once the epilogue group has contracted the previous pair's Phi
+          if (k > 0) mbar_wait(pempty + o, (unsigned)((k - 1) & 1));
+          XW_TL(5 * o + 3);
+        });
+        warp_arrive(pfull + o);
+        XW_TL(5 * o + 4);
+      }
+    }
+  } else {
+    // ---------------------------- epilogue group ---------------------------
+    const int et = tid - 256;
+    const int lane = et & 31, warp = et >> 5;
+    const int r = lane >> 2, c = lane & 3;
+    const bool with_ik1 = w_ik1 != 0.0;
+    // raw IK1 tile of pair (bi, bj) in the orientation-0 accumulator layout:
+    // lane (i = 8 ib + r, j = 8 warp + 2c + e)
+    auto load_ik1 = [&](int bi, int bj, double (&t)[8][2]) {
+      const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
+      const int ni = (int)min((int64_t)FT, N - I0);
+      const int nj = (int)min((int64_t)FT, N - J0);
+      const int jj = 8 * warp + 2 * c;
+      const double* src = X + I0 * ldx + J0 + jj;
+      const bool vec = with_ik1 && ni == FT && nj == FT && (ldx & 1) == 0 &&
+                       (reinterpret_cast<uintptr_t>(X + J0) & 15) == 0;
+#pragma unroll
+      for (int ib = 0; ib < 8; ++ib) {
+        const int ii = 8 * ib + r;
+        if (vec) {
+          const double2 v = ld_cs_v2(src + ii * ldx);
+          t[ib][0] = v.x;
+          t[ib][1] = v.y;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            t[ib][e] = (with_ik1 && ii < ni && jj + e < nj) ? ld_cs(src + ii * ldx + e) : 0.0;
+        }
+      }
+    };
+    int bi, bj;
+    pair_of(0, bi, bj);
+    if (et == 0)
+      for (int o = 0; o < 2; ++o)
+        x5_window<P>(smem + o * L::ZW, Zext, N, x5_gmin<P>(o, bi, bj), wfull + o);
+    double acc[8][2], nxt[8][2];
+    load_ik1(bi, bj, nxt);
+    for (int64_t k = 0; k < mine; ++k) {
+      int nbi = 0, nbj = 0;
+      const bool more = k + 1 < mine;
+      if (more) pair_of(k + 1, nbi, nbj);
+      // first rows of the next pair's windows, reduced now so that the requests below are short
+      int64_t g0n[2] = {0, 0};
+      if (et == 0 && more)
+        for (int o = 0; o < 2; ++o) g0n[o] = pmod(x5_gmin<P>(o, nbi, nbj), N);
+      XW_TL(15);
+      const int64_t I0 = (int64_t)bi * FT, J0 = (int64_t)bj * FT;
+      const int ni = (int)min((int64_t)FT, N - I0);
+      const int nj = (int)min((int64_t)FT, N - J0);
+      // band B fragments of both orientations: bS[o][s] = alpha S_{C0 + 8 warp + r}[4 s + c - r]
+      double bS[2][KS4];
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const int64_t C0 = o == 0 ? J0 : I0;
+        const int nc = o == 0 ? nj : ni;
+        const int row = 8 * warp + r;
+#pragma unroll
+        for (int s2 = 0; s2 < KS4; ++s2) {
+          const int t = 4 * s2 + c - r;
+          bS[o][s2] = (t >= 0 && t <= 2 * C::D && row < nc) ? ld_nc(sw + (C0 + row) * C::WS + t) : 0.0;
+        }
+      }
+      auto contract = [&](const int o) {
+        XW_TL(16 + 3 * o);
+        mbar_wait(pfull + o, (unsigned)(k & 1));
+        // Phs[o] full: every Phi warp has read window o, so it can be refilled for the next pair
+        if (et == 0 && more) x5_window_at<P>(smem + o * L::ZW, Zext, N, g0n[o], wfull + o);
+        XW_TL(17 + 3 * o);
+        const double* ph = smem + 2 * L::ZW + o * L::PH;
+#pragma unroll
+        for (int rb = 0; rb < 8; ++rb) {
+#pragma unroll
+          for (int s2 = 0; s2 < KS4; ++s2) {
+            const double a = ph[(8 * rb + r) * PSTRIDE + 8 * warp + 4 * s2 + c];
+            dmma(acc[rb][0], acc[rb][1], a, bS[o][s2]);
+          }
+        }
+        warp_arrive(pempty + o);
+        XW_TL(18 + 3 * o);
+      };
+      {
+        // the tile was requested before the previous pair's stores
+        const double aw = alpha * w_ik1;
+#pragma unroll
+        for (int rb = 0; rb < 8; ++rb) {
+          acc[rb][0] = nxt[rb][0] * aw;
+          acc[rb][1] = nxt[rb][1] * aw;
+        }
+#pragma unroll
+        for (int o = 0; o < 2; ++o)
+#pragma unroll
+          for (int s2 = 0; s2 < KS4; ++s2) bS[o][s2] *= alpha;
+      }
+      contract(0);
+      // T[i][j] (i = 8 rb + r, j = 8 warp + 2c + e) -> acc of orientation 1: lane
+      // (j = 8 rb + r, i = 8 warp + 2c + e) starts from T[i][j]
+#pragma unroll
+      for (int rb = 0; rb < 8; ++rb)
+        *reinterpret_cast<double2*>(Tsm + (8 * rb + r) * X5_TS + 8 * warp + 2 * c) =
+            make_double2(acc[rb][0], acc[rb][1]);
+      named_sync(XW_BAR_EPI, 256);
+#pragma unroll
+      for (int rb = 0; rb < 8; ++rb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[rb][e] = Tsm[(8 * warp + 2 * c + e) * X5_TS + 8 * rb + r];
+      named_sync(XW_BAR_EPI, 256);               // T read before the next pair overwrites it
+      contract(1);
+      // the next pair's IK1 tile: its HBM latency hides under the stores below
+      if (more) load_ik1(nbi, nbj, nxt);
+
+      // acc[rb][e] = A(J,I)[j = 8 rb + r][i = 8 warp + 2c + e]: rows J and, transposed, rows I
+      const int i = 8 * warp + 2 * c;
+      const bool full = ni == FT && nj == FT && (ldx & 1) == 0 &&
+                        (reinterpret_cast<uintptr_t>(X + I0) & 15) == 0;
+      if (bi != bj) {
+#pragma unroll
+        for (int rb = 0; rb < 8; ++rb) {
+          const int j = 8 * rb + r;
+          double* rowJ = X + (J0 + j) * ldx + I0 + i;
+          if (full) {
+            __stcs(reinterpret_cast<double2*>(rowJ), make_double2(acc[rb][0], acc[rb][1]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (j < nj && i + e < ni) __stcs(rowJ + e, acc[rb][e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int rb = 0; rb < 8; ++rb) {
+            const int j = 8 * rb + r;
+            if (j < nj && i + e < ni) __stcs(X + (I0 + i + e) * ldx + J0 + j, acc[rb][e]);
+          }
+      } else {
+#pragma unroll
+        for (int rb = 0; rb < 8; ++rb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = 8 * rb + r;
+            if (j < nj && i + e < ni && i + e <= j) {
+              __stcs(X + (J0 + j) * ldx + I0 + i + e, acc[rb][e]);
+              __stcs(X + (I0 + i + e) * ldx + J0 + j, acc[rb][e]);
+            }
+          }
+      }
+      XW_TL(22);
+      bi = nbi;
+      bj = nbj;
+    }
+  }
+}
+
 // Zext[g] = [Z'[g][0..nA-1], 0.., ff[g] at column nApad, 0..]
 __global__ void zext_kernel(int64_t n, int nA, int nApad, int zstride, const double* Zp,
                             const double* ff, double* Zext) {
@@ -802,6 +1080,15 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
   return check_launch("wq_ik1_sym");
 }
 
+// fewer pairs than this go to the one-pair-per-CTA kernel (two CTAs per SM)
+static int64_t x2ws_min_pairs() {
+  static const int64_t v = [] {
+    const char* e = getenv("WQB200_X2WS_MIN_PAIRS");   // A/B tools only
+    return e ? (int64_t)atoll(e) : (int64_t)592;
+  }();
+  return v;
+}
+
 template <int P>
 static int launch_x2(int64_t N, const double* Uext, const double* Zext, const double* s_w,
                      double alpha, double w_ik1, double* X, int64_t ldx, cudaStream_t st,
@@ -813,6 +1100,18 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
   if (pair0 < 0) pair0 = 0;
   const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
   if (blocks <= 0) return WQ_OK;
+  // full sweeps of the upper triangle: the warp-specialised persistent kernel, one CTA per SM
+  if (tile_row0 < 0 && N >= X2Cfg<P>::ZROWS && blocks >= x2ws_min_pairs()) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = (size_t)XwSmem<P>::TOTAL * 8;
+    cudaFuncSetAttribute(x2ws_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks, sms);
+    x2ws_kernel<P><<<grid, XW_THREADS, smem, st>>>(N, Uext, Zext, s_w, alpha, w_ik1, X, ldx, nb,
+                                                   pair0, blocks, plist);
+    return check_launch("wq_x2_pairs");
+  }
 #ifdef WQ_X2_ONE_CTA   // tools build only: one CTA per SM (occupancy experiment)
   const size_t smem = 120 * 1024;
 #else

@@ -17,7 +17,7 @@ def ik1():
     _lib.call("wq_ik1_sym", AS.ctypes_ref(sm["struct"]), _lib.ptr(X), N, sm["span64"], _lib.ptr(sm["flag"]), _lib.stream_handle())
 def x2():
     _lib.call("wq_x2_pairs", N, 3, lp.da + 1, lp.nApad, lp.s_w.shape[1], lp.uext.shape[1], lp.zstride,
-              _lib.ptr(d["uext"]), _lib.ptr(zext), _lib.ptr(d["s_w"]), alpha, 2.0, _lib.ptr(X), N, _lib.stream_handle())
+              _lib.ptr(d["uext"]), _lib.ptr(zext), _lib.ptr(d["s_w"]), alpha, float(os.environ.get("W_IK1", "2.0")), _lib.ptr(X), N, _lib.stream_handle())
 def step():
     AS._assemble_into(disc, X)
 def t(fn, reps=5):
