@@ -191,9 +191,9 @@ def kernel_flops(disc):
 
 
 def x2_executed_flops(disc):
-    """FP64 tensor flops x2v4_kernel issues per launch: per tile pair 8 warps x 2
-    orientations x (phi NSTEPS x NKB + band 8 x KS/4) DMMA m8n8k4 of 512 flops
-    (wq_fast.cu X2Cfg)."""
+    """FP64 tensor flops the x2 kernel (x2ws_kernel; x2v4_kernel issues the same) executes
+    per launch: per tile pair 2 orientations x 8 (phi NSTEPS x NKB + band 8 x KS/4) DMMA
+    m8n8k4 of 512 flops (wq_fast.cu X2Cfg)."""
     p = disc.space.degree
     NA = p + 13
     NAPAD = -(-NA // 4) * 4
@@ -215,7 +215,7 @@ def committed_traffic(dom):
         return None
     try:
         data = json.load(open(files[-1]))
-        key = {"ik1": "ik1_sym_kernel", "ik2": "x2v4_kernel"}[dom]
+        key = {"ik1": "ik1_sym_kernel", "ik2": "x2ws_kernel"}[dom]
         return data[key]["total"]
     except (OSError, ValueError, KeyError):
         return None
@@ -498,7 +498,7 @@ def main():
     dom_ms = split[1] if dom == "ik1" else split[2]
     achieved = fl[dom] / (dom_ms * 1e-3) / 1e12
     executed = x2_executed_flops(disc) if dom == "ik2" else None
-    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2v4_kernel"}[dom],
+    roofline = {"bound": "fp64", "kernel": {"ik1": "ik1_sym_kernel", "ik2": "x2ws_kernel"}[dom],
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "executed_flop_per_launch": executed,
                 "executed_frac": (executed / (dom_ms * 1e-3) / 1e12 / peak) if executed else None,

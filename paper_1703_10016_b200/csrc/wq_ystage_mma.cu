@@ -95,6 +95,11 @@ __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int
   const double* tsrc = A.Tb + (gbase + A.n_el - 1 + YM_TFRONT) * YM_ZST;
   const int64_t emax_w = A.r_emin[R0 + 8 * warp + 7];
   const int zoff = (int)(emax_all - emax_w) + (YM_NS - 1);   // window row of skew k = fa - emax_w
+  // skew blocks this warp needs: its functions read rows fl - ef, fl < the tile's element span,
+  // -ef <= the spread of the warp's first elements (YM_NKB covers the host-checked maxima;
+  // with repeated knots 64 functions span far fewer elements)
+  const int fspan = (int)(A.c_emax[C0 + YM_T - 1] - fa) + 1;
+  const int nkb = min(YM_NKB, (fspan + (int)(emax_w - A.r_emin[R0 + 8 * warp]) + 7) >> 3);
 
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -164,7 +169,8 @@ __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int
       if (t + C::PF < C::NSTEPS) bq[t % C::PF] = __ldg(brow + 4 * (t + C::PF));
       const double* z = zl - s * YM_ZST + al;
 #pragma unroll
-      for (int kb = 0; kb < YM_NKB; ++kb) dmma(acc[kb][0], acc[kb][1], z[8 * kb * YM_ZST], bfrag);
+      for (int kb = 0; kb < YM_NKB; ++kb)
+        if (kb < nkb) dmma(acc[kb][0], acc[kb][1], z[8 * kb * YM_ZST], bfrag);
     }
     fence_proxy_async();
     __syncthreads();   // every warp is done with this window (and with Phs of b - 1)
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int fl = 8 * kb + rl + ef[e];
-        if (fl >= 0 && fl < YM_FSP) Phs[(8 * warp + 2 * cl + e) * YM_PST + fl] = acc[kb][e];
+        if (fl >= 0 && fl < fspan) Phs[(8 * warp + 2 * cl + e) * YM_PST + fl] = acc[kb][e];
       }
     __syncthreads();
     // ---- column contraction: Out[c][r] += sum_{(f,b') in inc(c)} Y_b[r][f] v_f[b][b'] ----
