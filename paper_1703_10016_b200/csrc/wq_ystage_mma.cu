@@ -18,6 +18,8 @@
 // the table window of each b arrives by a 1-D TMA bulk copy.  Deterministic.
 // Citations: quadrature.py:441-504 (unit-table recipe, scaling 497-500),
 // assembly.py:186-245 (Theta / D assembly).
+#include <type_traits>
+
 #include "wq_async.cuh"
 #include "wq_common.cuh"
 
@@ -160,18 +162,25 @@ __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int
 #pragma unroll
     for (int kb = 0; kb < YM_NKB; ++kb) acc[kb][0] = acc[kb][1] = 0.0;
     const double* zl = zb + (zoff + rl) * YM_ZST;
+    // NK = the blocks this warp needs (a compile-time count per branch: no predicated DMMAs)
+    auto gemm = [&](auto nk) {
+      constexpr int NK = decltype(nk)::value;
 #pragma unroll
-    for (int t = 0; t < C::NSTEPS; ++t) {
-      // this lane's contraction index k = 4t + cl = s NAL + al (padding: zero B, any finite A)
-      const int kk = min(4 * t + cl, YM_NS * NAL - 1);
-      const int s = kk / NAL, al = kk - s * NAL;
-      const double bfrag = bq[t % C::PF];
-      if (t + C::PF < C::NSTEPS) bq[t % C::PF] = __ldg(brow + 4 * (t + C::PF));
-      const double* z = zl - s * YM_ZST + al;
+      for (int t = 0; t < C::NSTEPS; ++t) {
+        // this lane's contraction index k = 4t + cl = s NAL + al (padding: zero B, any finite A)
+        const int kk = min(4 * t + cl, YM_NS * NAL - 1);
+        const int s = kk / NAL, al = kk - s * NAL;
+        const double bfrag = bq[t % C::PF];
+        if (t + C::PF < C::NSTEPS) bq[t % C::PF] = __ldg(brow + 4 * (t + C::PF));
+        const double* z = zl - s * YM_ZST + al;
 #pragma unroll
-      for (int kb = 0; kb < YM_NKB; ++kb)
-        if (kb < nkb) dmma(acc[kb][0], acc[kb][1], z[8 * kb * YM_ZST], bfrag);
-    }
+        for (int kb = 0; kb < NK; ++kb) dmma(acc[kb][0], acc[kb][1], z[8 * kb * YM_ZST], bfrag);
+      }
+    };
+    if (nkb <= YM_NKB - 3) gemm(std::integral_constant<int, YM_NKB - 3>());
+    else if (nkb == YM_NKB - 2) gemm(std::integral_constant<int, YM_NKB - 2>());
+    else if (nkb == YM_NKB - 1) gemm(std::integral_constant<int, YM_NKB - 1>());
+    else gemm(std::integral_constant<int, YM_NKB>());
     fence_proxy_async();
     __syncthreads();   // every warp is done with this window (and with Phs of b - 1)
     if (tid == 0 && b + 2 < YM_NB) {

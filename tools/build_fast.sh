@@ -1,7 +1,7 @@
 #!/bin/bash
 # incremental build (tools only): compile the .cu files that changed, in parallel, and link
 # paper_1703_10016_b200/libwqb200.so (or $1).  __graft_entry__.build() is the reference build.
-set -e
+set -u; TAG=${TAG:-}; EXTRA=${EXTRA:-}
 cd "$(dirname "$0")/.."
 OUT=${1:-paper_1703_10016_b200/libwqb200.so}
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I include $EXTRA"
