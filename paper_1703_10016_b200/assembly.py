@@ -634,11 +634,11 @@ def _ik2_x2_into(disc, X, accumulate=True):
         return _ik2_x2_rows(disc, X, 0, N, accumulate)
     NE = disc.refined.basis.dim
     thetaT, D = _theta_d(disc, lp, d)
-    F = _fit_f(disc, lp, d, D)
-    hsolve = _hsolver(lp, d, NE)
-    # Phi = 2 H^{-1} Theta^T - F S
-    hsolve(thetaT, N)
-    _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(F), _lib.ptr(thetaT), st)
+    E = _fit_dh(disc, lp, d, D)
+    # Phi = H^{-1} (2 Theta^T - D H^{-1} S)  (= 2 H^{-1} Theta^T - F S, F = H^{-1} D H^{-1}:
+    # one banded solve fewer than forming F)
+    _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(E), _lib.ptr(thetaT), st)
+    _hsolver(lp, d, NE)(thetaT, N)
     # X[j][i] (+)= sum_m S[m, j] Phi[m, i]  (= X2^T)
     _lib.call("wq_add_st_phi", ctypes_ref(d["struct"]), _lib.ptr(thetaT), 0, N, _lib.ptr(X),
               X.stride(0), int(accumulate), st)
@@ -711,32 +711,32 @@ def _hsolver(lp: LogPart, d, NE):
     return hsolve
 
 
-def _fit_f(disc, lp: LogPart, d, D):
-    """F = H^{-1} D H^{-1} (D is overwritten by H^{-1} D)."""
+def _fit_dh(disc, lp: LogPart, d, D):
+    """E = D H^{-1} = (H^{-1} D)^T, D symmetric (D is overwritten by H^{-1} D).  The fit term
+    C^T D C = S^T (H^{-1} D H^{-1}) S enters Phi as H^{-1} (E S), so the second solve of
+    F = H^{-1} D H^{-1} merges with the solve of Theta^T (assembly.py:233-245 in X-form)."""
     torch = _torch()
     NE = disc.refined.basis.dim
-    hsolve = _hsolver(lp, d, NE)
-    hsolve(D, NE)
-    F = torch.empty_like(D)
-    _lib.call("wq_transpose", _lib.ptr(D), NE, NE, _lib.ptr(F), _lib.stream_handle())
-    hsolve(F, NE)
-    return F
+    _hsolver(lp, d, NE)(D, NE)
+    E = torch.empty_like(D)
+    _lib.call("wq_transpose", _lib.ptr(D), NE, NE, _lib.ptr(E), _lib.stream_handle())
+    return E
 
 
 def general_prepare(disc):
-    """F = H^{-1} D H^{-1} of the general path (replicated per rank; computed
-    once per assembly and shared by its row blocks)."""
+    """E = D H^{-1} of the general path (replicated per rank; computed once per
+    assembly and shared by its row blocks)."""
     lp, d = _logpart_dev(disc)
     _, D = _theta_d(disc, lp, d, want_theta=False)
-    return _fit_f(disc, lp, d, D)
+    return _fit_dh(disc, lp, d, D)
 
 
 def general_rows_into(disc, X_rows, row0: int, row1: int, F=None):
     """Rows [row0, row1) of the unsymmetrised X = IK1 + X2 of the general
     (non-circulant) path into X_rows (leading dimension N): IK1 rows, the
-    block's Theta^T columns, replicated D and F, Phi = 2 H^{-1} Theta^T - F S on
-    the block's columns, X2[i][j] = sum_t S_j[t] Phi[s_j + t][i].  No
-    communication."""
+    block's Theta^T columns, replicated D and E = D H^{-1} (passed as F),
+    Phi = H^{-1} (2 Theta^T - E S) on the block's columns,
+    X2[i][j] = sum_t S_j[t] Phi[s_j + t][i].  No communication."""
     lp, d = _logpart_dev(disc)
     sm = _smooth(disc)
     st = _lib.stream_handle()
@@ -748,9 +748,9 @@ def general_rows_into(disc, X_rows, row0: int, row1: int, F=None):
     if F is None:
         F = general_prepare(disc)
     T, _ = _theta_d(disc, lp, d, rows=(row0, row1), want_d=False)
-    _hsolver(lp, d, NE)(T, nr)
     _lib.call("wq_gather_fs_rows", ctypes_ref(d["struct"]), 2.0, _lib.ptr(F), _lib.ptr(T), row0,
               row1, nr, st)
+    _hsolver(lp, d, NE)(T, nr)
     torch = _torch()
     PhiT = torch.empty((nr, NE), dtype=torch.float64, device="cuda")
     _lib.call("wq_transpose", _lib.ptr(T), NE, nr, _lib.ptr(PhiT), st)
