@@ -20,6 +20,8 @@
 // Closed meshes add the periodic gap term log|sinc(r / L)| (quadrature.py:
 // 459-468) -- far pairs use log|L/pi sin(pi r / L)|, its exact sum with log|r|.
 // Every output is a fixed-order sum (deterministic; no atomics).
+#include <algorithm>
+
 #include "wq_common.cuh"
 #include "wq_log.cuh"
 
@@ -237,11 +239,16 @@ pair_table_kernel(GenArgs A) {
 
 // Far pairs off the table: tensor Gauss on the contracted integrand, one
 // thread per outer element e, the inner element f's weighted polynomial values
-// at every tier's nodes in shared memory.  Persistent over (f, 64 outer
-// elements) tiles; with a gap table only the tiles pair_table_kernel flagged.
+// at every tier's nodes in shared memory.  Persistent: a CTA keeps one block of 64
+// outer elements and walks the inner elements f (with a gap table only the tiles
+// pair_table_kernel flagged).  The outer polynomials at the far tier's nodes --
+// w_g U_e(x_g), w_g V_e(x_g), the same for every f -- are evaluated once per CTA into
+// shared memory (thread-minor): evaluating them per pair from global memory (85 + 25
+// strided loads per node) bound the kernel by L1/L2 traffic.
 template <int NP>
 __global__ void __launch_bounds__(FP_THREADS)
-pair_far_kernel(GenArgs A, int64_t ntiles, int nbx) {
+pair_far_kernel(GenArgs A, int64_t nf, int nbx) {
+  extern __shared__ double far_uv[];   // [GT2][2 NP][FP_THREADS]: far-tier w_g U_e, w_g V_e
   __shared__ double Vt[GTSUM][NP];   // h_f w_h V_f(h_f x_h)
   __shared__ double Yt[GTSUM];       // h_f x_h
   __shared__ double Gx[GTSUM], Gw[GTSUM];
@@ -252,13 +259,43 @@ pair_far_kernel(GenArgs A, int64_t ntiles, int nbx) {
     Gw[g] = A.gw[g];
   }
   for (int k = threadIdx.x; k < 128; k += FP_THREADS) reinterpret_cast<double*>(lntab)[k] = kTang64[k];
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if (A.m2u && !A.tile_flag[tile]) continue;
-    __syncthreads();   // previous tile's tables are dead; Gx/Gw visible
-    const int64_t f = tile / nbx;
-    const int64_t e = A.e0 + (tile % nbx) * FP_THREADS + threadIdx.x;
+  const int ebk = blockIdx.x % nbx;                 // this CTA's block of outer elements
+  const int64_t e = A.e0 + (int64_t)ebk * FP_THREADS + threadIdx.x;
+  const bool have_e = e < A.e1;
+  const double he = have_e ? A.elh[e] : 1.0;
+  const double* ue = A.u + (have_e ? e : A.e0) * nA * NP;
+  const double* ve = A.v + (have_e ? e : A.e0) * NP * NP;
+  // outer polynomials at node x (weight wx) of tier node g
+  auto outer = [&](int g, double (&uu)[NP], double (&vv)[NP]) {
+    const double x = he * Gx[g], wx = he * Gw[g];
+#pragma unroll
+    for (int a = 0; a < NP; ++a) {
+      double s = 0.0;
+      for (int al = nA - 1; al >= 0; --al) s = fma(s, x, __ldg(ue + al * NP + a));
+      uu[a] = wx * s;
+      s = 0.0;
+#pragma unroll
+      for (int al = NP - 1; al >= 0; --al) s = fma(s, x, __ldg(ve + al * NP + a));
+      vv[a] = wx * s;
+    }
+  };
+  __syncthreads();                                  // Gx / Gw visible
+  if (have_e) {
+    for (int g = 0; g < GT2; ++g) {
+      double uu[NP], vv[NP];
+      outer(GT0 + GT1 + g, uu, vv);
+#pragma unroll
+      for (int a = 0; a < NP; ++a) {
+        far_uv[(g * 2 * NP + a) * FP_THREADS + threadIdx.x] = uu[a];
+        far_uv[(g * 2 * NP + NP + a) * FP_THREADS + threadIdx.x] = vv[a];
+      }
+    }
+  }
+  for (int64_t f = blockIdx.x / nbx; f < nf; f += gridDim.x / nbx) {
+    if (A.m2u && !A.tile_flag[f * nbx + ebk]) continue;
+    __syncthreads();   // previous tile's tables are dead
     const double hf = A.elh[f];
-    bool mine = e < A.e1 && !is_near(A, e, f);
+    bool mine = have_e && !is_near(A, e, f);
     double gap;
     if (mine && A.m2u && snapped_gap(A.elh[e], hf, A.elm[e] - A.elm[f], &gap) &&
         fabs(gap) <= (double)(A.n_el - 1))
@@ -276,7 +313,6 @@ pair_far_kernel(GenArgs A, int64_t ntiles, int nbx) {
     }
     __syncthreads();
     if (mine) {
-      const double he = A.elh[e];
       const double delta = wrap_delta(A, A.elm[e] - A.elm[f]);
       const double sep = fabs(delta) - 0.5 * (he + hf);
       const double hm = fmax(he, hf);
@@ -284,8 +320,7 @@ pair_far_kernel(GenArgs A, int64_t ntiles, int nbx) {
       // <= 5e-15 of the natural slot scale at degree 16 x 4 for every tier)
       const int t0 = sep < 2.0 * hm ? 0 : (sep < 8.0 * hm ? GT0 : GT0 + GT1);
       const int ng = sep < 2.0 * hm ? GT0 : (sep < 8.0 * hm ? GT1 : GT2);
-      const double* ue = A.u + e * nA * NP;
-      const double* ve = A.v + e * NP * NP;
+      const bool far = t0 == GT0 + GT1;
       double wT[NP][NP], wD[NP][NP];
 #pragma unroll
       for (int a = 0; a < NP; ++a)
@@ -295,17 +330,16 @@ pair_far_kernel(GenArgs A, int64_t ntiles, int nbx) {
       const double invL = closed ? 1.0 / A.period : 0.0;
       const double lnLpi = closed ? log(A.period / kPi) : 0.0;
       for (int g = 0; g < ng; ++g) {
-        const double x = he * Gx[t0 + g], wx = he * Gw[t0 + g];
+        const double x = he * Gx[t0 + g];
         double uu[NP], vv[NP];
+        if (far) {
 #pragma unroll
-        for (int a = 0; a < NP; ++a) {
-          double s = 0.0;
-          for (int al = nA - 1; al >= 0; --al) s = fma(s, x, __ldg(ue + al * NP + a));
-          uu[a] = wx * s;
-          s = 0.0;
-#pragma unroll
-          for (int al = NP - 1; al >= 0; --al) s = fma(s, x, __ldg(ve + al * NP + a));
-          vv[a] = wx * s;
+          for (int a = 0; a < NP; ++a) {
+            uu[a] = far_uv[(g * 2 * NP + a) * FP_THREADS + threadIdx.x];
+            vv[a] = far_uv[(g * 2 * NP + NP + a) * FP_THREADS + threadIdx.x];
+          }
+        } else {
+          outer(t0 + g, uu, vv);
         }
         const double base = -x - delta;   // r = y - x - delta
         double t[NP];
@@ -775,13 +809,21 @@ int wq_gen_pair_blocks(int64_t n_el, int64_t e0, int64_t e1, int da, int db, int
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t fgrid = ntiles < (int64_t)sms * 8 ? ntiles : (int64_t)sms * 8;
+  // persistent grid: a multiple of the outer blocks (each CTA keeps one), ~3 CTAs per SM (61 KB each at p = 4)
+  const int64_t per = std::max<int64_t>(1, std::min<int64_t>(n_el, (int64_t)sms * 3 / g1.x));
+  const int64_t fgrid = per * g1.x;
+  (void)ntiles;
 #define WQ_GEN_CASE(NP)                                                                      \
   case NP:                                                                                   \
     if (m2u) {                                                                               \
       pair_table_kernel<NP><<<g1, FP_THREADS, 0, st>>>(A);                                   \
     }                                                                                        \
-    pair_far_kernel<NP><<<(unsigned)fgrid, FP_THREADS, 0, st>>>(A, ntiles, (int)g1.x);      \
+    {                                                                                        \
+      const size_t fsm = (size_t)GT2 * 2 * NP * FP_THREADS * sizeof(double);                 \
+      cudaFuncSetAttribute(pair_far_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)fsm);                                                        \
+      pair_far_kernel<NP><<<(unsigned)fgrid, FP_THREADS, fsm, st>>>(A, n_el, (int)g1.x);     \
+    }                                                                                        \
     break;
   switch (np1) {
     WQ_GEN_CASE(2)

@@ -312,6 +312,77 @@ gen_moments_far_kernel(int64_t n_el, int da1, int nb, const int64_t* glist, cons
   for (int s = 0; s < da1 * nb; ++s) out[s] = M[s];
 }
 
+// The same with the DA1 x NB moments of a pair in registers (the kernel above keeps them in
+// shared memory: 2 x 85 shared accesses per outer Gauss node and pair made it shared-memory
+// bound) and the inner element's weighted powers w_h y_h^b staged once per CTA (f is fixed per
+// CTA), so a pair costs ng^2 ln + ng^2 NB + ng DA1 NB FMAs and no per-thread shared traffic.
+template <int DA1, int NB>
+__global__ void __launch_bounds__(GM_THREADS)
+gen_moments_far_reg_kernel(int64_t n_el, const int64_t* glist, const int* gidx, const double* elh,
+                           const double* elm, const int64_t* near_lo, const int64_t* near_cnt,
+                           const double* gx, const double* gw, double* mgc) {
+  constexpr int NG = 30 + 16 + 12;
+  __shared__ double2 lntab[64];                   // accurate-table ln (wq_log.cuh)
+  __shared__ double Wt[NG][NB];                   // h_f w_h (h_f x_h)^b
+  __shared__ double Yt[NG], Gx[NG], Gw[NG];
+  const int j = blockIdx.y;                       // index in G
+  const int64_t f = glist[j];
+  const double hf = elh[f];
+  for (int q = threadIdx.x; q < 128; q += GM_THREADS) reinterpret_cast<double*>(lntab)[q] = kTang64[q];
+  for (int h = threadIdx.x; h < NG; h += GM_THREADS) {
+    const double y = hf * gx[h];
+    double w = hf * gw[h];
+    Gx[h] = gx[h];
+    Gw[h] = gw[h];
+    Yt[h] = y;
+#pragma unroll
+    for (int b = 0; b < NB; ++b, w *= y) Wt[h][b] = w;
+  }
+  __syncthreads();
+  const int64_t e = (int64_t)blockIdx.x * GM_THREADS + threadIdx.x;
+  if (e >= n_el || gidx[e] >= 0) return;          // outer in G: block route
+  int64_t k = f - near_lo[e];
+  if (k < 0) k += n_el;
+  if (k < near_cnt[e]) return;                    // touching: near kernel
+  const double he = elh[e];
+  const double delta = elm[e] - elm[f];
+  const double sep = fabs(delta) - 0.5 * (he + hf);
+  const double hm = fmax(he, hf);
+  const int t0 = sep < 2.0 * hm ? 0 : (sep < 8.0 * hm ? 30 : 46);
+  const int ng = sep < 2.0 * hm ? 30 : (sep < 8.0 * hm ? 16 : 12);
+  double M[DA1][NB];
+#pragma unroll
+  for (int a = 0; a < DA1; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) M[a][b] = 0.0;
+  for (int g = 0; g < ng; ++g) {
+    const double x = he * Gx[t0 + g];
+    const double base = -x - delta;
+    double t[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) t[b] = 0.0;
+#pragma unroll 4
+    for (int h = 0; h < ng; ++h) {
+      // separated pair: y - x - delta != 0
+      const double kv = 2.0 * half_ln64t(fabs(Yt[t0 + h] + base), lntab);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) t[b] = fma(Wt[t0 + h][b], kv, t[b]);
+    }
+    double wa = he * Gw[t0 + g];
+#pragma unroll
+    for (int a = 0; a < DA1; ++a) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) M[a][b] = fma(wa, t[b], M[a][b]);
+      wa *= x;
+    }
+  }
+  double* out = mgc + ((int64_t)j * n_el + e) * (DA1 * NB);
+#pragma unroll
+  for (int a = 0; a < DA1; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) out[a * NB + b] = M[a][b];
+}
+
 }  // namespace wq
 
 using namespace wq;
@@ -388,10 +459,15 @@ int wq_gen_moments_far(int64_t n_el, int da1, int nb, int64_t n_g, const int64_t
     set_error("wq_gen_moments_far: bad arguments");
     return WQ_EINVAL;
   }
+  dim3 grid(ceil_div(n_el, GM_THREADS), (unsigned)n_g);
+  if (da1 == 17 && nb == 5) {   // config 5 (p = 4): moments in registers
+    gen_moments_far_reg_kernel<17, 5><<<grid, GM_THREADS, 0, (cudaStream_t)stream>>>(
+        n_el, glist, gidx, elh, elm, near_lo, near_cnt, gx, gw, mgc);
+    return check_launch("wq_gen_moments_far");
+  }
   const size_t smem = (size_t)GM_THREADS * da1 * nb * 8;
   cudaFuncSetAttribute(gen_moments_far_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  dim3 grid(ceil_div(n_el, GM_THREADS), (unsigned)n_g);
   gen_moments_far_kernel<<<grid, GM_THREADS, smem, (cudaStream_t)stream>>>(
       n_el, da1, nb, glist, gidx, elh, elm, near_lo, near_cnt, gx, gw, mgc);
   return check_launch("wq_gen_moments_far");
