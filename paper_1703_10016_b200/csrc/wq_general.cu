@@ -373,6 +373,44 @@ pair_far_kernel(GenArgs A, int64_t nf, int nbx) {
   }
 }
 
+// sum over quadrature nodes n < nnodes of w u^a v^b for every slot (a, b), the nodes dealt to
+// the lanes of the warp and the NA x NB partial sums in registers, then a butterfly sum (all
+// lanes end with the same totals); added to M[a NB + b] (shared, this warp's).  One pass of
+// NA NB FMAs per node instead of a power loop per slot and node on one lane.
+template <int NA, int NB, class NodeFn>
+__device__ __forceinline__ void warp_node_moments(int nnodes, NodeFn node, double* M, int lane) {
+  double m[NA][NB];
+#pragma unroll
+  for (int a = 0; a < NA; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) m[a][b] = 0.0;
+  for (int n = lane; n < nnodes; n += 32) {
+    double w, u, v;
+    node(n, w, u, v);
+    double ua = w;
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      double t = ua;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        m[a][b] += t;
+        t *= v;
+      }
+      ua *= u;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NA; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double x = m[a][b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == (a * NB + b) % 32) M[a * NB + b] += x;
+    }
+  __syncwarp();
+}
+
 constexpr int TOUCH_XI = 16, TOUCH_ETA = 30, TOUCH_LOG = 14;
 constexpr int NP_WARPS = 4;
 
@@ -439,47 +477,76 @@ pair_near_kernel(GenArgs A, int max_near) {
     const double* w30 = x30 + TOUCH_ETA;
     const double* xl = w30 + TOUCH_ETA;
     const double* wl = xl + TOUCH_LOG;
-    for (int tri = 0; tri < 2; ++tri) {
-      for (int q = 0; q < TOUCH_ETA; ++q) {
-        const double eta = x30[q];
-        const double g = tri == 0 ? log1p(rho * eta) : log(rho + eta);
-        for (int jx = 0; jx < TOUCH_XI + TOUCH_LOG; ++jx) {
-          const bool lg = jx >= TOUCH_XI;
-          const double xi = lg ? xl[jx - TOUCH_XI] : x16[jx];
-          const double wx = w30[q] * rho * xi * (lg ? -wl[jx - TOUCH_XI] : w16[jx] * g);
-          double u, v;
-          if (tri == 0) {
-            u = sig * (xi - 0.5);
-            v = -sig * rho * (xi * eta - 0.5);
-          } else {
-            u = sig * (xi * eta - 0.5);
-            v = -sig * rho * (xi - 0.5);
-          }
-          for (int j = 0; j < SL; ++j) {
-            if (sa[j] < 0) continue;
-            double t = wx;
-            for (int i = 0; i < sa[j]; ++i) t *= u;
-            for (int i = 0; i < sb[j]; ++i) t *= v;
-            acc[j] += t;
-          }
+    auto touch_node = [&](int n, double& w, double& u, double& v) {
+      const int tri = n / (TOUCH_ETA * (TOUCH_XI + TOUCH_LOG));
+      const int q = (n / (TOUCH_XI + TOUCH_LOG)) % TOUCH_ETA, jx = n % (TOUCH_XI + TOUCH_LOG);
+      const double eta = x30[q];
+      const double g = tri == 0 ? log1p(rho * eta) : log(rho + eta);
+      const bool lg = jx >= TOUCH_XI;
+      const double xi = lg ? xl[jx - TOUCH_XI] : x16[jx];
+      w = w30[q] * rho * xi * (lg ? -wl[jx - TOUCH_XI] : w16[jx] * g);
+      if (tri == 0) {
+        u = sig * (xi - 0.5);
+        v = -sig * rho * (xi * eta - 0.5);
+      } else {
+        u = sig * (xi * eta - 0.5);
+        v = -sig * rho * (xi - 0.5);
+      }
+    };
+    constexpr int TOUCH_NODES = 2 * TOUCH_ETA * (TOUCH_XI + TOUCH_LOG);
+    const bool fast = (nA == 17 && nB == 5) || (nA == 16 && nB == 4);
+    if (fast) {
+      // nodes over the lanes, slots in registers (the per-slot loop below ran ~1e5 dependent
+      // multiplies on each lane of one warp per pair: the launch was bound by that latency)
+      for (int i = lane; i < ns; i += 32) M[i] = 0.0;
+      __syncwarp();
+      if (nA == 17) warp_node_moments<17, 5>(TOUCH_NODES, touch_node, M, lane);
+      else warp_node_moments<16, 4>(TOUCH_NODES, touch_node, M, lane);
+      for (int j = 0; j < SL; ++j)
+        if (sa[j] >= 0) acc[j] = M[lane + 32 * j];
+      __syncwarp();
+    } else {
+      for (int n = 0; n < TOUCH_NODES; ++n) {
+        double wx, u, v;
+        touch_node(n, wx, u, v);
+        for (int j = 0; j < SL; ++j) {
+          if (sa[j] < 0) continue;
+          double t = wx;
+          for (int i = 0; i < sa[j]; ++i) t *= u;
+          for (int i = 0; i < sb[j]; ++i) t *= v;
+          acc[j] += t;
         }
       }
     }
   }
   if (A.closed) {  // periodic gap term, 30 x 30 Gauss (quadrature.py:459-468)
     const double per = A.period / he;
-    for (int g = 0; g < GT0; ++g) {
-      const double xg = A.gx[g];
-      for (int h = 0; h < GT0; ++h) {
-        const double xh = A.gx[h];
-        const double yy = ((rho * xh - xg) - dl) / per;
-        const double kv = yy == 0.0 ? 0.0 : log(fabs(sinpi(yy) / (kPi * yy)));
-        const double w = A.gw[g] * A.gw[h] * rho * kv;
+    auto per_node = [&](int n, double& w, double& u, double& v) {
+      const int g = n / GT0, h = n % GT0;
+      const double xg = A.gx[g], xh = A.gx[h];
+      const double yy = ((rho * xh - xg) - dl) / per;
+      const double kv = yy == 0.0 ? 0.0 : log(fabs(sinpi(yy) / (kPi * yy)));
+      w = A.gw[g] * A.gw[h] * rho * kv;
+      u = xg;
+      v = rho * xh;
+    };
+    if ((nA == 17 && nB == 5) || (nA == 16 && nB == 4)) {
+      for (int i = lane; i < ns; i += 32) M[i] = 0.0;
+      __syncwarp();
+      if (nA == 17) warp_node_moments<17, 5>(GT0 * GT0, per_node, M, lane);
+      else warp_node_moments<16, 4>(GT0 * GT0, per_node, M, lane);
+      for (int j = 0; j < SL; ++j)
+        if (sa[j] >= 0) acc[j] += M[lane + 32 * j];
+      __syncwarp();
+    } else {
+      for (int n = 0; n < GT0 * GT0; ++n) {
+        double w, xg, rxh;
+        per_node(n, w, xg, rxh);
         for (int j = 0; j < SL; ++j) {
           if (sa[j] < 0) continue;
           double t = w;
           for (int i = 0; i < sa[j]; ++i) t *= xg;
-          for (int i = 0; i < sb[j]; ++i) t *= rho * xh;
+          for (int i = 0; i < sb[j]; ++i) t *= rxh;
           acc[j] += t;
         }
       }
