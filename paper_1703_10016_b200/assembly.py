@@ -931,14 +931,14 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None, want_th
         common = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]))
         mcols = common + (_lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), _lib.ptr(d["v"]))
         if want_theta:      # (the first prep also re-lays the table out: Tb)
-            CrT, LtT = torch.empty((5, N, kpT), **f64), torch.empty((N, 5), **f64)
+            CrT, LtT = torch.empty((5, -(-N // 8) * 8, kpT), **f64), torch.empty((N, 5), **f64)
             _lib.call("wq_ystage_mma_prep", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
                       _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *common, _lib.ptr(d["u"]), da1,
                       _lib.ptr(d["v"]), _lib.ptr(d["elh"]), _lib.ptr(m2u), da1, _lib.ptr(d["ca"]),
                       _lib.ptr(d["cb"]), _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum),
                       _lib.ptr(Tb), n_tab, st)
         if want_d:
-            CrD, LtD = torch.empty((5, NE, kpD), **f64), torch.empty((NE, 5), **f64)
+            CrD, LtD = torch.empty((5, -(-NE // 8) * 8, kpD), **f64), torch.empty((NE, 5), **f64)
             tb = None if want_theta else _lib.ptr(Tb)
             _lib.call("wq_ystage_mma_prep", NE, NE, n, nB, nB, wc, _lib.ptr(L["vcols"]),
                       _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *common, _lib.ptr(d["v"]), nB,

@@ -49,7 +49,8 @@ struct YmArgs {
   const int64_t* c_emin;
   const int64_t* c_emax;
   const double* v;         // (n_el, NB, NB) column coefficients v_f[be][b]
-  const double* Cr;        // (NB, n_rows, KP) B operand: Cs_{e_r+s}[al][a] h^b at k = s NAL + al
+  const double* Cr;        // (NB, ceil8(n_rows), KP) B operand: Cs_{e_r+s}[al][a] h^b at k = s NAL + al,
+                           // in DMMA B-fragment order [row / 8][k / 4][row % 8][k % 4]
   const double* LtR;       // (n_rows, NB)
   const double* vsum;      // (n_cols, NB)
   const double* Tb;        // (NB, n_tab, ZST) table slices, row g + n_el - 1 + TFRONT
@@ -143,18 +144,18 @@ __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int
     }
   }
   // the skewed output rows of this lane's functions: f = k + e_func
-  const int64_t rowf = R0 + 8 * warp + rl;                 // B-operand row
-  const double* __restrict__ brow0 = A.Cr + rowf * C::KP + cl;
+  // B-operand fragments of the warp's row group: one coalesced 256-byte load per k-step
+  const double* __restrict__ brow0 = A.Cr + ((R0 + 8 * warp) / 8) * (C::NSTEPS * 32) + lane;
   int ef[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) ef[e] = (int)(A.r_emin[R0 + 8 * warp + 2 * cl + e] - emax_w);
 
   for (int b = 0; b < YM_NB; ++b) {
     const double* zb = Zsm + (b & 1) * ZW;
-    const double* __restrict__ brow = brow0 + (int64_t)b * n_rows * C::KP;
+    const double* __restrict__ brow = brow0 + (int64_t)b * n_rows * C::KP;   // n_rows: padded to 8
     double bq[C::PF];
 #pragma unroll
-    for (int t = 0; t < C::PF; ++t) bq[t] = __ldg(brow + 4 * t);
+    for (int t = 0; t < C::PF; ++t) bq[t] = __ldg(brow + 32 * t);
     mbar_wait(bar + (b & 1), (unsigned)((b >> 1) & 1));
 
     // ---- Y_b in skewed coordinates: acc[kb] = rows k = fa - emax_w + 8 kb + rl ----
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int
         const int kk = min(4 * t + cl, YM_NS * NAL - 1);
         const int s = kk / NAL, al = kk - s * NAL;
         const double bfrag = bq[t % C::PF];
-        if (t + C::PF < C::NSTEPS) bq[t % C::PF] = __ldg(brow + 4 * (t + C::PF));
+        if (t + C::PF < C::NSTEPS) bq[t % C::PF] = __ldg(brow + 32 * (t + C::PF));
         const double* z = zl - s * YM_ZST + al;
 #pragma unroll
         for (int kb = 0; kb < NK; ++kb) dmma(acc[kb][0], acc[kb][1], z[8 * kb * YM_ZST], bfrag);
@@ -237,10 +238,20 @@ __global__ void ystage_mma_prep_rows(int64_t n_rows, int nal, int kp, int nloc,
                                      const double* elh, const double* ca, const double* cb,
                                      double* Cr, double* LtR) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n_rows) return;
+  const int64_t nrp = (n_rows + 7) / 8 * 8;   // rows padded to whole fragments
+  // element (b, r, k) in B-fragment order
+  auto at = [&](int b, int64_t rr, int k) -> double& {
+    return Cr[(int64_t)b * nrp * kp + ((rr / 8) * (kp / 4) + k / 4) * 32 + (rr % 8) * 4 + k % 4];
+  };
+  if (r >= n_rows) {
+    if (r < nrp)
+      for (int k = 0; k < kp; ++k)
+        for (int b = 0; b < YM_NB; ++b) at(b, r, k) = 0.0;
+    return;
+  }
   double lt[YM_NB] = {0, 0, 0, 0, 0};
   for (int k = YM_NS * nal; k < kp; ++k)
-    for (int b = 0; b < YM_NB; ++b) Cr[((int64_t)b * n_rows + r) * kp + k] = 0.0;
+    for (int b = 0; b < YM_NB; ++b) at(b, r, k) = 0.0;
   for (int s = 0; s < YM_NS; ++s) {
     const int64_t e = r_emin[r] + s;
     int a = -1;
@@ -253,7 +264,7 @@ __global__ void ystage_mma_prep_rows(int64_t n_rows, int nal, int kp, int nloc,
       const double c = a >= 0 ? coef[(e * ldal + al) * nloc + a] * p : 0.0;
       sc = fma(ca[al], c, sc);
       double hb = 1.0;
-      for (int b = 0; b < YM_NB; ++b, hb *= h) Cr[((int64_t)b * n_rows + r) * kp + s * nal + al] = c * hb;
+      for (int b = 0; b < YM_NB; ++b, hb *= h) at(b, r, s * nal + al) = c * hb;
     }
     if (a >= 0) {
       const double lh = log(h);
@@ -312,7 +323,7 @@ int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, in
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int kp = (YM_NS * nal + 3) / 4 * 4;
-  ystage_mma_prep_rows<<<ceil_div(n_rows, 128), 128, 0, st>>>(n_rows, nal, kp, nloc, e_rows,
+  ystage_mma_prep_rows<<<ceil_div(n_rows + 7, 128), 128, 0, st>>>(n_rows, nal, kp, nloc, e_rows,
                                                                 r_emin, r_emax, coef, ldal, elh,
                                                                 ca, cb, Cr, LtR);
   ystage_mma_prep_cols<<<ceil_div(n_cols, 128), 128, 0, st>>>(n_cols, wc, c_el, c_loc, v, vsum);
@@ -345,7 +356,7 @@ int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
     const size_t smem = (size_t)YmCfg<NA>::SMEM * 8;                                             \
     cudaFuncSetAttribute(ystage_mma_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                          (int)smem);                                                             \
-    ystage_mma_kernel<NA><<<grid, YM_THREADS, smem, st>>>(A, n_rows);                            \
+    ystage_mma_kernel<NA><<<grid, YM_THREADS, smem, st>>>(A, (n_rows + 7) / 8 * 8);              \
   }
   if (nal == 17) WQ_YM_LAUNCH(17) else WQ_YM_LAUNCH(5)
 #undef WQ_YM_LAUNCH
