@@ -389,7 +389,9 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
  * contraction and the ln h term (LtR, vsum) follow in shared memory.  wq_ystage given the
  * same row_ko / col_ko skips exactly these tiles.  nal: 17 (Theta, p = 4) or 5 (D).
  * n_tab >= 2 n_el - 1 + 160.
- * wq_ystage_mma_prep fills Cr (5 x n_rows x kp, kp = 5 nal rounded up to 4), LtR
+ * wq_ystage_mma_prep fills Cr (5 x ceil8(n_rows) x kp doubles, kp = 5 nal rounded up to 4,
+ * rows padded with zeros to a multiple of 8, each power b in DMMA B-fragment order
+ * [row / 8][k / 4][row % 8][k % 4]: one contiguous 256-byte fragment per row group and k-step), LtR
  * (n_rows x 5), vsum (n_cols x 5) and, when Tb is not NULL, Tb (5 x n_tab x 20) from m2u.
  */
 int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, int wc,
