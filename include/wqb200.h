@@ -196,6 +196,13 @@ int wq_transpose(const double* in, int64_t rows, int64_t cols, double* out, void
 /* Phi[m][i] = alpha * P[m][i] - sum_t F[m][(s_start[i]+t) mod nf] S[s_start[i]+t, i]  (in place on P) */
 int wq_gather_fs(const wq_logpart_t* lp, double alpha, const double* F, double* P, void* stream);
 
+/* The same with F = Y^T read straight from Y (N_E x N_E; no transposed copy):
+ *   Phi[m][i] = alpha * P[m][i] - sum_t Y[(s_start[i]+t) mod nf][m] S[s_start[i]+t, i].
+ * max_span >= s_start[min(i0 + 63, N - 1)] - s_start[i0] + ws for every 64-column block i0
+ * (the Y rows one block stages); WQ_EUNSUPPORTED when they do not fit in shared memory. */
+int wq_gather_yts(const wq_logpart_t* lp, double alpha, const double* Y, double* P,
+                  int64_t max_span, void* stream);
+
 /* X[j][i] (+)= sum_t S[s_start[j]+t, j] Phi[(s_start[j]+t) mod nf][i], all i, j rows [row0,row1). */
 int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64_t row1,
                   double* X, int64_t ldx, int accumulate, void* stream);

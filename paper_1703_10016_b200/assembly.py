@@ -110,6 +110,7 @@ class LogPart:
     v0: np.ndarray = None          # (db+1, db+1)
     hinv_taps: np.ndarray = None   # (2K+1,)
     uext: np.ndarray = None        # (N, ktot) [2U | -S_i | 0] for the DMMA kernel
+    s_span: int = None             # fit rows under the S bands of 64 columns (lazy)
     nApad: int = 0
     zstride: int = 0
     # general
@@ -634,10 +635,17 @@ def _ik2_x2_into(disc, X, accumulate=True):
         return _ik2_x2_rows(disc, X, 0, N, accumulate)
     NE = disc.refined.basis.dim
     thetaT, D = _theta_d(disc, lp, d)
-    E = _fit_dh(disc, lp, d, D)
     # Phi = H^{-1} (2 Theta^T - D H^{-1} S)  (= 2 H^{-1} Theta^T - F S, F = H^{-1} D H^{-1}:
-    # one banded solve fewer than forming F)
-    _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(E), _lib.ptr(thetaT), st)
+    # one banded solve fewer than forming F); D H^{-1} = (H^{-1} D)^T is read transposed
+    # from H^{-1} D when the band rows of a 64-column block fit in shared memory
+    span = _s_band_span(lp)
+    if span * 33 * 8 <= 200 * 1024 and lp.s_w.shape[1] <= 20:
+        _hsolver(lp, d, NE)(D, NE)
+        _lib.call("wq_gather_yts", ctypes_ref(d["struct"]), 2.0, _lib.ptr(D), _lib.ptr(thetaT),
+                  span, st)
+    else:
+        E = _fit_dh(disc, lp, d, D)
+        _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(E), _lib.ptr(thetaT), st)
     _hsolver(lp, d, NE)(thetaT, N)
     # X[j][i] (+)= sum_m S[m, j] Phi[m, i]  (= X2^T)
     _lib.call("wq_add_st_phi", ctypes_ref(d["struct"]), _lib.ptr(thetaT), 0, N, _lib.ptr(X),
@@ -709,6 +717,16 @@ def _hsolver(lp: LogPart, d, NE):
             _lib.call("wq_cyc_solve_cols", NE, lp.bw, _lib.ptr(d["Lb"]), _lib.ptr(d["L21"]),
                       _lib.ptr(d["L22"]), _lib.ptr(Y), ncols, Y.stride(0), st)
     return hsolve
+
+
+def _s_band_span(lp: LogPart) -> int:
+    """Fit rows touched by the S bands of 64 consecutive columns (wq_gather_yts)."""
+    if lp.s_span is None:
+        ss = np.asarray(lp.s_start, dtype=np.int64)
+        i0 = np.arange(0, len(ss), 64)
+        i1 = np.minimum(i0 + 63, len(ss) - 1)
+        lp.s_span = int((ss[i1] - ss[i0]).max()) + int(lp.s_w.shape[1])
+    return lp.s_span
 
 
 def _fit_dh(disc, lp: LogPart, d, D):

@@ -431,6 +431,51 @@ __global__ void __launch_bounds__(128) gather_fs_kernel(wq_logpart_t lp, double 
   }
 }
 
+// P[m][i] = alpha P[m][i] - sum_t Y[(s_i + t) mod nf][m] S_i[t]: gather_fs with F = Y^T read
+// straight from Y (no transposed copy).  A CTA takes 64 columns i and GY_M rows m: the
+// Y rows its bands touch (s_first .. s_last + WS - 1, `span` of them) x GY_M columns m are
+// staged through shared memory (coalesced 256-byte row pieces in, conflict-free column
+// reads out: row stride GY_M + 1).
+constexpr int GY_I = 64, GY_M = 32, GY_B = 4;
+template <int WS>
+__global__ void __launch_bounds__(128) gather_yts_kernel(wq_logpart_t lp, double alpha,
+                                                         const double* Y, double* P, int span) {
+  extern __shared__ double ysm[];   // [span][GY_M + 1]
+  const int64_t nf = lp.n_fine, nr = lp.n_rows;
+  const int64_t i0 = (int64_t)blockIdx.x * GY_I, m0 = (int64_t)blockIdx.y * GY_M;
+  const int64_t ilast = min(i0 + GY_I, nr) - 1;
+  const int64_t sfirst = lp.s_start[i0];
+  const int rows = (int)(lp.s_start[ilast] - sfirst) + WS;   // <= span (host-checked)
+  const int mcnt = (int)min((int64_t)GY_M, nf - m0);
+  for (int k = threadIdx.x; k < rows * GY_M; k += blockDim.x) {
+    const int r = k / GY_M, mm = k - r * GY_M;
+    if (r < span && mm < mcnt) ysm[r * (GY_M + 1) + mm] = __ldg(Y + pmod(sfirst + r, nf) * nf + m0 + mm);
+  }
+  __syncthreads();
+  const int il = threadIdx.x & (GY_I - 1), half = threadIdx.x >> 6;
+  const int64_t i = i0 + il;
+  if (i >= nr) return;
+  double sw[WS];
+#pragma unroll
+  for (int t = 0; t < WS; ++t) sw[t] = lp.s_w[i * WS + t];
+  const double* yb = ysm + (int)(lp.s_start[i] - sfirst) * (GY_M + 1);
+  const int mh0 = half * (GY_M / 2), mh1 = min(mcnt, mh0 + GY_M / 2);
+  for (int mm = mh0; mm < mh1; mm += GY_B) {
+    double pv[GY_B];
+#pragma unroll
+    for (int u = 0; u < GY_B; ++u) pv[u] = mm + u < mh1 ? P[(m0 + mm + u) * nr + i] : 0.0;
+#pragma unroll
+    for (int u = 0; u < GY_B; ++u) {
+      if (mm + u < mh1) {
+        double a = alpha * pv[u];
+#pragma unroll
+        for (int t = 0; t < WS; ++t) a = fma(-yb[t * (GY_M + 1) + mm + u], sw[t], a);
+        P[(m0 + mm + u) * nr + i] = a;
+      }
+    }
+  }
+}
+
 // X[j][i] (+)= sum_t S_j[t] Phi[(s_j + t) mod nf][i]; each CTA sweeps ST_ROWS
 // consecutive j (their Phi rows overlap: L1 reuse), ST_B rows j per batch with the
 // batch's loads issued before its FMAs
@@ -653,6 +698,31 @@ int wq_gather_fs(const wq_logpart_t* lp, double alpha, const double* F, double* 
   WQ_WS_SWITCH(lp->ws, WQ_GF)
 #undef WQ_GF
   return check_launch("wq_gather_fs");
+}
+
+int wq_gather_yts(const wq_logpart_t* lp, double alpha, const double* Y, double* P,
+                  int64_t max_span, void* stream) {
+  if (!lp || !Y || !P || max_span < 1) {
+    set_error("wq_gather_yts: bad arguments");
+    return WQ_EINVAL;
+  }
+  const size_t smem = (size_t)max_span * (GY_M + 1) * sizeof(double);
+  if (lp->ws > GF_MAXWS || lp->ws < 1 || smem > 200 * 1024) {
+    set_error("wq_gather_yts: S band width %lld or band span %lld unsupported", (long long)lp->ws,
+              (long long)max_span);
+    return WQ_EUNSUPPORTED;
+  }
+  dim3 grid(ceil_div(lp->n_rows, GY_I), ceil_div(lp->n_fine, GY_M));
+#define WQ_GY(W)                                                                                \
+  {                                                                                             \
+    cudaFuncSetAttribute(gather_yts_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                         (int)smem);                                                            \
+    gather_yts_kernel<W><<<grid, 128, smem, (cudaStream_t)stream>>>(*lp, alpha, Y, P,           \
+                                                                    (int)max_span);             \
+  }
+  WQ_WS_SWITCH(lp->ws, WQ_GY)
+#undef WQ_GY
+  return check_launch("wq_gather_yts");
 }
 
 int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64_t row1, double* X,
