@@ -207,6 +207,12 @@ int wq_gather_yts(const wq_logpart_t* lp, double alpha, const double* Y, double*
 int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64_t row1,
                   double* X, int64_t ldx, int accumulate, void* stream);
 
+/* wq_add_st_phi over all rows followed by wq_symmetrize, fused (X2^T is never written):
+ *   A = alpha (X + X^T), X[j][i] = (X_in[j][i] if accumulate) + sum_t S[s_start[j]+t, j] Phi[(s_start[j]+t) mod nf][i],
+ * in place on the N x N matrix X (leading dimension N). */
+int wq_st_phi_sym(const wq_logpart_t* lp, const double* Phi, double* X, double alpha,
+                  int accumulate, void* stream);
+
 /*
  * v2 circulant pipeline (closed uniform simple-knot meshes, nref = 1), tiles of
  * WQ_FTILE rows over the upper-triangle tile pairs (I <= J):

@@ -68,6 +68,7 @@ _SIGS = {
     "wq_cyc_solve_cols": [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp],
     "wq_gather_fs": [ctypes.POINTER(WqLogpart), c_dbl, c_vp, c_vp, c_vp],
     "wq_gather_yts": [ctypes.POINTER(WqLogpart), c_dbl, c_vp, c_vp, c_i64, c_vp],
+    "wq_st_phi_sym": [ctypes.POINTER(WqLogpart), c_vp, c_vp, c_dbl, c_int, c_vp],
     "wq_add_st_phi": [ctypes.POINTER(WqLogpart), c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_vp],
     "wq_symmetrize": [c_vp, c_i64, c_dbl, c_vp],
     "wq_absmax_defect": [c_vp, c_i64, c_vp, c_vp],

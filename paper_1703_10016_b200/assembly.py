@@ -625,14 +625,19 @@ def _ik2_x2_rows(disc, X, row0, row1, accumulate=True, tables=None):
     return X
 
 
-def _ik2_x2_into(disc, X, accumulate=True):
-    """X (+)= X2 (circulant: X2 itself; general: X2^T -- callers symmetrise)."""
+def _ik2_x2_into(disc, X, accumulate=True, sym_alpha=None):
+    """X (+)= X2 (circulant: X2 itself; general: X2^T -- callers symmetrise).
+    With sym_alpha the symmetrisation is included: X <- sym_alpha (X' + X'^T),
+    X' = (X if accumulate) + X2 (general path: fused into the last kernel)."""
     torch = _torch()
     lp, d = _logpart_dev(disc)
     N = disc.space.dim
     st = _lib.stream_handle()
     if lp.path == "circulant":
-        return _ik2_x2_rows(disc, X, 0, N, accumulate)
+        _ik2_x2_rows(disc, X, 0, N, accumulate)
+        if sym_alpha is not None:
+            _lib.call("wq_symmetrize", _lib.ptr(X), N, sym_alpha, st)
+        return X
     NE = disc.refined.basis.dim
     thetaT, D = _theta_d(disc, lp, d)
     # Phi = H^{-1} (2 Theta^T - D H^{-1} S)  (= 2 H^{-1} Theta^T - F S, F = H^{-1} D H^{-1}:
@@ -648,8 +653,14 @@ def _ik2_x2_into(disc, X, accumulate=True):
         _lib.call("wq_gather_fs", ctypes_ref(d["struct"]), 2.0, _lib.ptr(E), _lib.ptr(thetaT), st)
     _hsolver(lp, d, NE)(thetaT, N)
     # X[j][i] (+)= sum_m S[m, j] Phi[m, i]  (= X2^T)
+    if sym_alpha is not None and X.stride(0) == N:
+        _lib.call("wq_st_phi_sym", ctypes_ref(d["struct"]), _lib.ptr(thetaT), _lib.ptr(X),
+                  sym_alpha, int(accumulate), st)
+        return X
     _lib.call("wq_add_st_phi", ctypes_ref(d["struct"]), _lib.ptr(thetaT), 0, N, _lib.ptr(X),
               X.stride(0), int(accumulate), st)
+    if sym_alpha is not None:
+        _lib.call("wq_symmetrize", _lib.ptr(X), N, sym_alpha, st)
     return X
 
 
@@ -1156,8 +1167,7 @@ def _assemble_into(disc: Discretization, X, scaled: bool = True):
     skip = _ik1_skipped(disc)
     if not skip:
         _ik1_into(disc, X, accumulate=False)
-    _ik2_x2_into(disc, X, accumulate=not skip)
-    _lib.call("wq_symmetrize", _lib.ptr(X), X.shape[0], alpha, _lib.stream_handle())
+    _ik2_x2_into(disc, X, accumulate=not skip, sym_alpha=alpha)
     return X
 
 
@@ -1402,8 +1412,7 @@ def assemble_ik2(disc: Discretization) -> np.ndarray:
     if _use_v2(disc):
         _assemble_v2(disc, X, 0.5, w_ik1=0.0)
         return X.cpu().numpy()
-    _ik2_x2_into(disc, X, accumulate=False)
-    _lib.call("wq_symmetrize", _lib.ptr(X), X.shape[0], 0.5, _lib.stream_handle())
+    _ik2_x2_into(disc, X, accumulate=False, sym_alpha=0.5)
     return X.cpu().numpy()
 
 

@@ -534,6 +534,66 @@ __global__ void __launch_bounds__(128) add_st_phi_kernel(wq_logpart_t lp, const 
   }
 }
 
+// A = alpha (X + X^T), X[j][i] = (X_in[j][i] if accumulate) + sum_t S_j[t] Phi[(s_j + t) mod nf][i]
+// (add_st_phi followed by symmetrize, fused: X2^T is never written).  One CTA per 32 x 32 tile
+// pair (bi <= bj); each thread forms 4 entries of both tiles (band sums over coalesced Phi row
+// pieces), the transposed partners meet in shared memory.  In place on X.
+template <int WS>
+__global__ void __launch_bounds__(256) st_phi_sym_kernel(wq_logpart_t lp, const double* Phi,
+                                                         double* X, double alpha, int accumulate,
+                                                         int nb) {
+  __shared__ double a[32][33];
+  __shared__ double b[32][33];
+  __shared__ int64_t sst[64];
+  __shared__ double ssw[64][WS];
+  const int64_t n = lp.n_rows, nf = lp.n_fine;
+  int bi, bj;
+  tri_index(blockIdx.x, nb, bi, bj);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  const int64_t r0 = (int64_t)bi * 32, c0 = (int64_t)bj * 32;
+  // bands of the rows r0 .. r0+31 (first half) and c0 .. c0+31 (second half)
+  for (int k = threadIdx.x; k < 64 * (WS + 1); k += 256) {
+    const int u = k / (WS + 1), t = k - u * (WS + 1);
+    int64_t j = (u < 32 ? r0 : c0 - 32) + u;
+    if (j >= n) j = n - 1;
+    if (t == WS) sst[u] = pmod(lp.s_start[j], nf);
+    else ssw[u][t] = lp.s_w[j * WS + t];
+  }
+  __syncthreads();
+  // band sum of row slot u (0..63) at column col
+  auto band = [&](int u, int64_t col) {
+    const int64_t sj = sst[u];
+    double acc = 0.0;
+    if (sj + WS <= nf) {
+      const double* p = Phi + sj * n + col;
+#pragma unroll
+      for (int t = 0; t < WS; ++t, p += n) acc = fma(ssw[u][t], __ldg(p), acc);
+    } else {
+#pragma unroll
+      for (int t = 0; t < WS; ++t) acc = fma(ssw[u][t], __ldg(Phi + wrap1(sj + t, nf) * n + col), acc);
+    }
+    return acc;
+  };
+#pragma unroll
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = r0 + y, c = c0 + tx;
+    double va = 0.0, vb = 0.0;
+    if (r < n && c < n) va = (accumulate ? X[r * n + c] : 0.0) + band(y, c);
+    const int64_t r2 = c0 + y, c2 = r0 + tx;
+    if (r2 < n && c2 < n) vb = (accumulate ? X[r2 * n + c2] : 0.0) + band(32 + y, c2);
+    a[y][tx] = va;
+    b[y][tx] = vb;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int y = ty; y < 32; y += 8) {
+    const int64_t r = r0 + y, c = c0 + tx;
+    if (r < n && c < n) X[r * n + c] = alpha * (a[y][tx] + b[tx][y]);
+    const int64_t r2 = c0 + y, c2 = r0 + tx;
+    if (bi != bj && r2 < n && c2 < n) X[r2 * n + c2] = alpha * (b[y][tx] + a[tx][y]);
+  }
+}
+
 #define WQ_WS_SWITCH(ws, CALL) \
   switch (ws) {                \
     case 1: CALL(1); break;    \
@@ -723,6 +783,25 @@ int wq_gather_yts(const wq_logpart_t* lp, double alpha, const double* Y, double*
   WQ_WS_SWITCH(lp->ws, WQ_GY)
 #undef WQ_GY
   return check_launch("wq_gather_yts");
+}
+
+int wq_st_phi_sym(const wq_logpart_t* lp, const double* Phi, double* X, double alpha,
+                  int accumulate, void* stream) {
+  if (!lp || !Phi || !X) {
+    set_error("wq_st_phi_sym: bad arguments");
+    return WQ_EINVAL;
+  }
+  if (lp->ws > GF_MAXWS || lp->ws < 1) {
+    set_error("wq_st_phi_sym: S band width %lld outside [1, %d]", (long long)lp->ws, GF_MAXWS);
+    return WQ_EUNSUPPORTED;
+  }
+  const int nb = ceil_div(lp->n_rows, 32);
+  const int64_t tiles = (int64_t)nb * (nb + 1) / 2;
+#define WQ_SPS(W) \
+  st_phi_sym_kernel<W><<<(unsigned)tiles, 256, 0, (cudaStream_t)stream>>>(*lp, Phi, X, alpha, accumulate, nb)
+  WQ_WS_SWITCH(lp->ws, WQ_SPS)
+#undef WQ_SPS
+  return check_launch("wq_st_phi_sym");
 }
 
 int wq_add_st_phi(const wq_logpart_t* lp, const double* Phi, int64_t row0, int64_t row1, double* X,
