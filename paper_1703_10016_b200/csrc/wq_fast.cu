@@ -795,17 +795,6 @@ x2v4_kernel(int64_t N, const double* __restrict__ Uext, const double* __restrict
 constexpr int XW_THREADS = 512;
 constexpr int XW_BAR_EPI = 1;   // named barrier of the epilogue group (T hand-off)
 
-__device__ __forceinline__ void named_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-// the warp's shared-memory accesses are ordered before the arrive of its first lane
-__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
-}
 
 template <int P>
 struct XwSmem {

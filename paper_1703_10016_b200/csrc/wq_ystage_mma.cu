@@ -14,8 +14,10 @@
 // powers, packed densely, and one GEMM per column power b; Out accumulates the column
 // contraction of each Y_b in shared memory, and the ln h_e term enters as
 //   Out[c][r] += sum_b LtR[r][b] vsum[c][b].
-// One CTA = 64 row functions x 64 column functions, 8 warps x 8 row functions;
-// the table window of each b arrives by a 1-D TMA bulk copy.  Deterministic.
+// One tile = 64 row functions x 64 column functions, 8 GEMM warps x 8 row functions and 8
+// contraction warps; the table window of each b arrives by a 1-D TMA bulk copy.  Each warp
+// runs only the skew blocks it needs (64 functions span 48-61 elements with 25 % repeated
+// knots: 7-9 of the 10 blocks the host-checked maxima allow).  Deterministic.
 // Citations: quadrature.py:441-504 (unit-table recipe, scaling 497-500),
 // assembly.py:186-245 (Theta / D assembly).
 #include <type_traits>
@@ -26,7 +28,6 @@
 namespace wq {
 
 constexpr int YM_T = 64;             // row / column functions per tile
-constexpr int YM_THREADS = 256;
 constexpr int YM_NS = 5;             // shifts (elements per row support), p = 4
 constexpr int YM_NB = 5;             // column polynomial slots (d + 1)
 constexpr int YM_ZST = 20;           // table row stride (== 4 mod 16: conflict-free fragments)
@@ -67,164 +68,256 @@ struct YmCfg {
   static constexpr int KP = (YM_NS * NAL + 3) / 4 * 4;   // contraction (s, al) packed densely
   static constexpr int NSTEPS = KP / 4;
   static constexpr int PF = NSTEPS < YM_PF ? NSTEPS : YM_PF;
-  // Zsm[2] | Phs | Cv (column incidences' v_f[b][b'] per b) | 2 mbarriers | Ci (ints)
-  static constexpr int SMEM = 2 * YM_ZR * YM_ZST + YM_T * YM_PST + YM_T * YM_WCM * YM_NB + 2 +
-                              YM_T * YM_WCM / 2;
+};
+
+// ---------------------------------------------------------------------------
+// ystage_ws_kernel: warp-specialised and persistent (the scheme of x2ws_kernel, wq_fast.cu):
+// one CTA of 16 warps per SM walks the pure tiles.  Warps 0-7 (the GEMM group)
+// run the skewed DMMA loops of the 5 column powers of tile after tile back to back and
+// scatter each Y_b into one of two Phs buffers; warps 8-15 (the contraction group) contract
+// it with the columns' v (CUDA cores, registers), keep Out[c][r] in registers across the 5
+// powers and write the finished tile while the GEMM group is already on the next one.
+// "Phase" = one (tile, power): buffers ph & 1, mbarrier parity (ph >> 1) & 1; wfull (table
+// window landed, TMA), pfull / pempty (Y_b written / contracted).  The first contraction
+// thread requests the window of phase ph + 2 as soon as pfull of phase ph completes (every
+// GEMM warp has then read that window buffer).  (Round 2 replaced a one-tile-per-CTA kernel
+// with CTA-wide barriers between the GEMM, scatter and contraction of every power; this one is
+// bit-identical to it and 2.5 % faster.)
+// ---------------------------------------------------------------------------
+constexpr int YW_THREADS = 512;
+constexpr int YW_BAR_E = 1;   // named barrier of the contraction group
+
+template <int NAL>
+struct YwCfg {
+  using C = YmCfg<NAL>;
+  static constexpr int ZW = YM_ZR * YM_ZST;
+  static constexpr int PH = YM_T * YM_PST;
+  static constexpr int CV = YM_T * YM_WCM * YM_NB;
+  static constexpr int OS = YM_T * (YM_T + 1);
+  // Zsm[2] | Phs[2] | Cv | Os | 6 mbarriers | Ci (ints)
+  static constexpr int SMEM = 2 * ZW + 2 * PH + CV + OS + 6 + YM_T * YM_WCM / 2 + 1;
 };
 
 template <int NAL>
-__global__ void __launch_bounds__(YM_THREADS, 2) ystage_mma_kernel(YmArgs A, int64_t n_rows) {
+__global__ void __launch_bounds__(YW_THREADS, 1)
+ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
   using C = YmCfg<NAL>;
+  using W = YwCfg<NAL>;
   extern __shared__ double sm[];
-  // column tiles fastest: the CTAs in flight share a row tile, so its B operand (Cr, 45 KB
-  // per power) is fetched from HBM once and then served from L2
-  const int ct = blockIdx.x, rt = blockIdx.y;
-  const int ko = A.row_ko[rt];
-  if (ko == YM_NOT_PURE || A.col_ko[ct] != ko) return;   // CUDA-core kernel handles the tile
-  const int64_t R0 = A.row0 + (int64_t)rt * YM_T, C0 = (int64_t)ct * YM_T;
-  if (A.sym && C0 + YM_T - 1 < R0) return;   // strictly below the diagonal: mirrored later
-  constexpr int ZW = YM_ZR * YM_ZST;
-  double* Zsm = sm;                          // [2][ZR][ZST] (double-buffered over b)
-  double* Phs = Zsm + 2 * ZW;                // [T][PST]: Y_b[r][f - fa]
-  double* Cv = Phs + YM_T * YM_PST;          // [T c][WCM][NB]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Cv + YM_T * YM_WCM * YM_NB);   // [2]
-  int* Ci = reinterpret_cast<int*>(bar + 2);   // [T c][WCM]: f - fa, or -1
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rl = lane >> 2, cl = lane & 3;
-
-  const int64_t fa = A.c_emin[C0];
-  const int64_t emax_all = A.r_emin[R0 + YM_T - 1];
-  const int64_t gbase = fa - emax_all - (YM_NS - 1);   // first staged gap
-  const double* tsrc = A.Tb + (gbase + A.n_el - 1 + YM_TFRONT) * YM_ZST;
-  const int64_t emax_w = A.r_emin[R0 + 8 * warp + 7];
-  const int zoff = (int)(emax_all - emax_w) + (YM_NS - 1);   // window row of skew k = fa - emax_w
-  // skew blocks this warp needs: its functions read rows fl - ef, fl < the tile's element span,
-  // -ef <= the spread of the warp's first elements (YM_NKB covers the host-checked maxima;
-  // with repeated knots 64 functions span far fewer elements)
-  const int fspan = (int)(A.c_emax[C0 + YM_T - 1] - fa) + 1;
-  const int nkb = min(YM_NKB, (fspan + (int)(emax_w - A.r_emin[R0 + 8 * warp]) + 7) >> 3);
-
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-  }
-  fence_proxy_async();
-  __syncthreads();
+  double* Zsm = sm;                               // [2][ZR][ZST]
+  double* Phs = Zsm + 2 * W::ZW;                  // [2][T][PST]
+  double* Cv = Phs + 2 * W::PH;                   // [T c][WCM][NB]
+  double* Os = Cv + W::CV;                        // [T c][T + 1]
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(Os + W::OS);
+  uint64_t* pfull = wfull + 2;
+  uint64_t* pempty = wfull + 4;
+  int* Ci = reinterpret_cast<int*>(wfull + 6);    // [T c][WCM]
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (int64_t)ntx * nty;
+  // the tiles this kernel owns, in the order every thread of the CTA walks them
+  auto pure = [&](int64_t q) {
+    const int ct = (int)(q % ntx), rt = (int)(q / ntx);
+    const int ko = A.row_ko[rt];
+    if (ko == YM_NOT_PURE || A.col_ko[ct] != ko) return false;
+    const int64_t R0 = A.row0 + (int64_t)rt * YM_T, C0 = (int64_t)ct * YM_T;
+    return !(A.sym && C0 + YM_T - 1 < R0);        // strictly below the diagonal: mirrored later
+  };
+  auto next_pure = [&](int64_t q) {               // first owned pure tile at or after q
+    while (q < ntiles && !pure(q)) q += gridDim.x;
+    return q;
+  };
+  // table rows of tile q's window (power 0)
+  auto window_src = [&](int64_t q) {
+    const int ct = (int)(q % ntx), rt = (int)(q / ntx);
+    const int64_t R0 = A.row0 + (int64_t)rt * YM_T, C0 = (int64_t)ct * YM_T;
+    const int64_t gbase = A.c_emin[C0] - A.r_emin[R0 + YM_T - 1] - (YM_NS - 1);
+    return A.Tb + (gbase + A.n_el - 1 + YM_TFRONT) * YM_ZST;
+  };
   if (tid == 0)
     for (int b = 0; b < 2; ++b) {
-      mbar_arrive_expect_tx(bar + b, ZW * 8);
-      bulk_g2s(Zsm + b * ZW, tsrc + (int64_t)b * A.n_tab * YM_ZST, ZW * 8, bar + b);
+      mbar_init(wfull + b, 1);
+      mbar_init(pfull + b, 8);
+      mbar_init(pempty + b, 8);
     }
-  // column incidences of the tile, once: element offset and v_f[b][b'] for every b
-  for (int k = tid; k < YM_T * YM_WCM; k += YM_THREADS) {
-    const int c = k / YM_WCM, w = k - c * YM_WCM;
-    const int64_t cc = C0 + c;
-    const int64_t f = w < A.wc ? A.c_el[cc * A.wc + w] : -1;
-    Ci[k] = f >= 0 ? (int)(f - fa) : -1;
-    const int bp = f >= 0 ? (int)A.c_loc[cc * A.wc + w] : 0;
-#pragma unroll
-    for (int b = 0; b < YM_NB; ++b)
-      Cv[k * YM_NB + b] = f >= 0 ? __ldg(A.v + f * (YM_NB * YM_NB) + b * YM_NB + bp) : 0.0;
-  }
-  // Out[c][r] for this thread's column c and rows r = 16 rg + i, in registers; starts from
-  // the ln h term sum_b LtR[r][b] vsum[c][b]
-  const int ocol = tid & 63, rg = tid >> 6;
-  double out[YM_T / 4];
-  {
-    double vs[YM_NB];
-#pragma unroll
-    for (int b = 0; b < YM_NB; ++b) vs[b] = __ldg(A.vsum + (C0 + ocol) * YM_NB + b);
-#pragma unroll
-    for (int i = 0; i < YM_T / 4; ++i) {
-      const int64_t r = R0 + 16 * rg + i;
-      double s = 0.0;
-#pragma unroll
-      for (int b = 0; b < YM_NB; ++b) s = fma(__ldg(A.LtR + r * YM_NB + b), vs[b], s);
-      out[i] = s;
-    }
-  }
-  // the skewed output rows of this lane's functions: f = k + e_func
-  // B-operand fragments of the warp's row group: one coalesced 256-byte load per k-step
-  const double* __restrict__ brow0 = A.Cr + ((R0 + 8 * warp) / 8) * (C::NSTEPS * 32) + lane;
-  int ef[2];
-#pragma unroll
-  for (int e = 0; e < 2; ++e) ef[e] = (int)(A.r_emin[R0 + 8 * warp + 2 * cl + e] - emax_w);
+  fence_proxy_async();
+  __syncthreads();
+  const int64_t q0 = next_pure(blockIdx.x);
+  if (q0 >= ntiles) return;
 
-  for (int b = 0; b < YM_NB; ++b) {
-    const double* zb = Zsm + (b & 1) * ZW;
-    const double* __restrict__ brow = brow0 + (int64_t)b * n_rows * C::KP;   // n_rows: padded to 8
+  if (tid < 256) {
+    // ------------------------------ GEMM group ------------------------------
+    const int lane = tid & 31, warp = tid >> 5;
+    const int rl = lane >> 2, cl = lane & 3;
+    // per-tile quantities of this warp (loaded a tile ahead: the dependent global loads would
+    // otherwise stall every GEMM warp at each tile start)
+    struct Tile {
+      const double* brow0;   // B fragments of the warp's row group, power 0
+      int zoff, fspan, nkb, ef0, ef1;
+    };
+    auto load_tile = [&](int64_t q) {
+      Tile t;
+      const int ct = (int)(q % ntx), rt = (int)(q / ntx);
+      const int64_t R0 = A.row0 + (int64_t)rt * YM_T, C0 = (int64_t)ct * YM_T;
+      const int64_t fa = A.c_emin[C0];
+      const int64_t emax_all = A.r_emin[R0 + YM_T - 1];
+      const int64_t emax_w = A.r_emin[R0 + 8 * warp + 7];
+      t.zoff = (int)(emax_all - emax_w) + (YM_NS - 1);
+      t.fspan = (int)(A.c_emax[C0 + YM_T - 1] - fa) + 1;
+      t.nkb = min(YM_NKB, (t.fspan + (int)(emax_w - A.r_emin[R0 + 8 * warp]) + 7) >> 3);
+      t.brow0 = A.Cr + ((R0 + 8 * warp) / 8) * (C::NSTEPS * 32) + lane;
+      t.ef0 = (int)(A.r_emin[R0 + 8 * warp + 2 * cl] - emax_w);
+      t.ef1 = (int)(A.r_emin[R0 + 8 * warp + 2 * cl + 1] - emax_w);
+      return t;
+    };
+    unsigned ph = 0;
+    Tile cur = load_tile(q0);
+    // the B-fragment ring runs on across phases and tiles: slot (SHIFT + t) % PF holds k-step t
+    // of the current phase, refilled with the next phase's k-steps as soon as it is consumed
+    // (5 NSTEPS is a multiple of PF, so every tile starts at shift 0)
+    static_assert((YM_NB * C::NSTEPS) % C::PF == 0, "ystage ws: B-fragment ring does not close");
     double bq[C::PF];
 #pragma unroll
-    for (int t = 0; t < C::PF; ++t) bq[t] = __ldg(brow + 32 * t);
-    mbar_wait(bar + (b & 1), (unsigned)((b >> 1) & 1));
-
-    // ---- Y_b in skewed coordinates: acc[kb] = rows k = fa - emax_w + 8 kb + rl ----
-    double acc[YM_NKB][2];
+    for (int t = 0; t < C::PF; ++t) bq[t] = __ldg(cur.brow0 + 32 * t);
+    for (int64_t q = q0; q < ntiles;) {
+      const int64_t qn = next_pure(q + gridDim.x);
+      const Tile nxt = qn < ntiles ? load_tile(qn) : cur;
+      auto phase = [&](auto bc) {
+        constexpr int b = decltype(bc)::value;
+        constexpr int SHIFT = (b * C::NSTEPS) % C::PF;
+        const int buf = ph & 1;
+        const unsigned par = (ph >> 1) & 1;
+        const double* zb = Zsm + buf * W::ZW;
+        const double* __restrict__ brow = cur.brow0 + (int64_t)b * nrp * C::KP;
+        // the next phase's fragments: the next power of this tile, or power 0 of the next tile
+        const double* __restrict__ bnext = b + 1 < YM_NB ? brow + nrp * C::KP : nxt.brow0;
+        mbar_wait(wfull + buf, par);
+        double acc[YM_NKB][2];
 #pragma unroll
-    for (int kb = 0; kb < YM_NKB; ++kb) acc[kb][0] = acc[kb][1] = 0.0;
-    const double* zl = zb + (zoff + rl) * YM_ZST;
-    // NK = the blocks this warp needs (a compile-time count per branch: no predicated DMMAs)
-    auto gemm = [&](auto nk) {
-      constexpr int NK = decltype(nk)::value;
+        for (int kb = 0; kb < YM_NKB; ++kb) acc[kb][0] = acc[kb][1] = 0.0;
+        const double* zl = zb + (cur.zoff + rl) * YM_ZST;
+        auto gemm = [&](auto nk) {
+          constexpr int NK = decltype(nk)::value;
 #pragma unroll
-      for (int t = 0; t < C::NSTEPS; ++t) {
-        // this lane's contraction index k = 4t + cl = s NAL + al (padding: zero B, any finite A)
-        const int kk = min(4 * t + cl, YM_NS * NAL - 1);
-        const int s = kk / NAL, al = kk - s * NAL;
-        const double bfrag = bq[t % C::PF];
-        if (t + C::PF < C::NSTEPS) bq[t % C::PF] = __ldg(brow + 32 * (t + C::PF));
-        const double* z = zl - s * YM_ZST + al;
+          for (int t = 0; t < C::NSTEPS; ++t) {
+            const int kk = min(4 * t + cl, YM_NS * NAL - 1);
+            const int s = kk / NAL, al = kk - s * NAL;
+            const double bfrag = bq[(SHIFT + t) % C::PF];
+            bq[(SHIFT + t) % C::PF] = t + C::PF < C::NSTEPS ? __ldg(brow + 32 * (t + C::PF))
+                                                            : __ldg(bnext + 32 * (t + C::PF - C::NSTEPS));
+            const double* z = zl - s * YM_ZST + al;
 #pragma unroll
-        for (int kb = 0; kb < NK; ++kb) dmma(acc[kb][0], acc[kb][1], z[8 * kb * YM_ZST], bfrag);
-      }
-    };
-    if (nkb <= YM_NKB - 3) gemm(std::integral_constant<int, YM_NKB - 3>());
-    else if (nkb == YM_NKB - 2) gemm(std::integral_constant<int, YM_NKB - 2>());
-    else if (nkb == YM_NKB - 1) gemm(std::integral_constant<int, YM_NKB - 1>());
-    else gemm(std::integral_constant<int, YM_NKB>());
-    fence_proxy_async();
-    __syncthreads();   // every warp is done with this window (and with Phs of b - 1)
-    if (tid == 0 && b + 2 < YM_NB) {
-      mbar_arrive_expect_tx(bar + (b & 1), ZW * 8);
-      bulk_g2s(Zsm + (b & 1) * ZW, tsrc + (int64_t)(b + 2) * A.n_tab * YM_ZST, ZW * 8, bar + (b & 1));
+            for (int kb = 0; kb < NK; ++kb) dmma(acc[kb][0], acc[kb][1], z[8 * kb * YM_ZST], bfrag);
+          }
+        };
+        if (cur.nkb <= YM_NKB - 3) gemm(std::integral_constant<int, YM_NKB - 3>());
+        else if (cur.nkb == YM_NKB - 2) gemm(std::integral_constant<int, YM_NKB - 2>());
+        else if (cur.nkb == YM_NKB - 1) gemm(std::integral_constant<int, YM_NKB - 1>());
+        else gemm(std::integral_constant<int, YM_NKB>());
+        // Phs[buf] is free once the contraction group has used it two phases ago
+        if (ph >= 2) mbar_wait(pempty + buf, par ^ 1);
+        double* P = Phs + buf * W::PH;
+#pragma unroll
+        for (int kb = 0; kb < YM_NKB; ++kb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int fl = 8 * kb + rl + (e ? cur.ef1 : cur.ef0);
+            if (fl >= 0 && fl < cur.fspan) P[(8 * warp + 2 * cl + e) * YM_PST + fl] = acc[kb][e];
+          }
+        warp_arrive(pfull + buf);
+        ++ph;
+      };
+      phase(std::integral_constant<int, 0>());
+      phase(std::integral_constant<int, 1>());
+      phase(std::integral_constant<int, 2>());
+      phase(std::integral_constant<int, 3>());
+      phase(std::integral_constant<int, 4>());
+      cur = nxt;
+      q = qn;
     }
-    // scatter: lane holds Y_b[func = 8 warp + 2 cl + e][f = fa + 8 kb + rl + ef[e]]
-#pragma unroll
-    for (int kb = 0; kb < YM_NKB; ++kb)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int fl = 8 * kb + rl + ef[e];
-        if (fl >= 0 && fl < fspan) Phs[(8 * warp + 2 * cl + e) * YM_PST + fl] = acc[kb][e];
+  } else {
+    // --------------------------- contraction group ---------------------------
+    const int et = tid - 256;
+    const int ocol = et & 63, rg = et >> 6;
+    unsigned ph = 0;
+    if (et == 0)
+      for (int b = 0; b < 2; ++b) {
+        mbar_arrive_expect_tx(wfull + b, W::ZW * 8);
+        bulk_g2s(Zsm + b * W::ZW, window_src(q0) + (int64_t)b * A.n_tab * YM_ZST, W::ZW * 8, wfull + b);
       }
-    __syncthreads();
-    // ---- column contraction: Out[c][r] += sum_{(f,b') in inc(c)} Y_b[r][f] v_f[b][b'] ----
-    // (this thread's column: incidences in registers, one shared load per FMA)
-    {
-      int fi[YM_WCM];
-      double cv[YM_WCM];
+    for (int64_t q = q0; q < ntiles;) {
+      const int64_t qn = next_pure(q + gridDim.x);
+      const int ct = (int)(q % ntx), rt = (int)(q / ntx);
+      const int64_t R0 = A.row0 + (int64_t)rt * YM_T, C0 = (int64_t)ct * YM_T;
+      const int64_t fa = A.c_emin[C0];
+      // column incidences of the tile: element offset and v_f[b][b'] for every b
+      for (int k = et; k < YM_T * YM_WCM; k += 256) {
+        const int c = k / YM_WCM, w = k - c * YM_WCM;
+        const int64_t cc = C0 + c;
+        const int64_t f = w < A.wc ? A.c_el[cc * A.wc + w] : -1;
+        Ci[k] = f >= 0 ? (int)(f - fa) : -1;
+        const int bp = f >= 0 ? (int)A.c_loc[cc * A.wc + w] : 0;
 #pragma unroll
-      for (int w = 0; w < YM_WCM; ++w) {
-        const int f = Ci[ocol * YM_WCM + w];
-        fi[w] = f >= 0 ? f : 0;
-        cv[w] = f >= 0 ? Cv[(ocol * YM_WCM + w) * YM_NB + b] : 0.0;
+        for (int b = 0; b < YM_NB; ++b)
+          Cv[k * YM_NB + b] = f >= 0 ? __ldg(A.v + f * (YM_NB * YM_NB) + b * YM_NB + bp) : 0.0;
       }
-      const double* ph = Phs + 16 * rg * YM_PST;
+      // Out[c][r] for this thread's column c and rows r = 16 rg + i; starts from the ln h term
+      double out[YM_T / 4];
+      {
+        double vs[YM_NB];
 #pragma unroll
-      for (int i = 0; i < YM_T / 4; ++i)
+        for (int b = 0; b < YM_NB; ++b) vs[b] = __ldg(A.vsum + (C0 + ocol) * YM_NB + b);
 #pragma unroll
-        for (int w = 0; w < YM_WCM; ++w) out[i] = fma(ph[i * YM_PST + fi[w]], cv[w], out[i]);
+        for (int i = 0; i < YM_T / 4; ++i) {
+          const int64_t r = R0 + 16 * rg + i;
+          double s = 0.0;
+#pragma unroll
+          for (int b = 0; b < YM_NB; ++b) s = fma(__ldg(A.LtR + r * YM_NB + b), vs[b], s);
+          out[i] = s;
+        }
+      }
+      named_sync(YW_BAR_E, 256);                  // Ci / Cv visible
+      const double* nsrc = qn < ntiles ? window_src(qn) : nullptr;
+      const double* csrc = window_src(q);
+      for (int b = 0; b < YM_NB; ++b, ++ph) {
+        const int buf = ph & 1;
+        const unsigned par = (ph >> 1) & 1;
+        mbar_wait(pfull + buf, par);
+        // every GEMM warp has read window buf: request the window of phase ph + 2 into it
+        if (et == 0) {
+          const double* src = b + 2 < YM_NB ? csrc + (int64_t)(b + 2) * A.n_tab * YM_ZST
+                                            : (nsrc ? nsrc + (int64_t)(b + 2 - YM_NB) * A.n_tab * YM_ZST
+                                                    : nullptr);
+          if (src) {
+            mbar_arrive_expect_tx(wfull + buf, W::ZW * 8);
+            bulk_g2s(Zsm + buf * W::ZW, src, W::ZW * 8, wfull + buf);
+          }
+        }
+        int fi[YM_WCM];
+        double cv[YM_WCM];
+#pragma unroll
+        for (int w = 0; w < YM_WCM; ++w) {
+          const int f = Ci[ocol * YM_WCM + w];
+          fi[w] = f >= 0 ? f : 0;
+          cv[w] = f >= 0 ? Cv[(ocol * YM_WCM + w) * YM_NB + b] : 0.0;
+        }
+        const double* phs = Phs + buf * W::PH + 16 * rg * YM_PST;
+#pragma unroll
+        for (int i = 0; i < YM_T / 4; ++i)
+#pragma unroll
+          for (int w = 0; w < YM_WCM; ++w) out[i] = fma(phs[i * YM_PST + fi[w]], cv[w], out[i]);
+        warp_arrive(pempty + buf);
+      }
+      // Out[c][r] through shared memory so that 64 consecutive r of a column leave together
+#pragma unroll
+      for (int i = 0; i < YM_T / 4; ++i) Os[ocol * (YM_T + 1) + 16 * rg + i] = out[i];
+      named_sync(YW_BAR_E, 256);
+      for (int k = et; k < YM_T * YM_T; k += 256) {
+        const int c = k >> 6, r = k & 63;
+        A.out[(C0 + c) * A.ldo + R0 + r - A.out_row0] = Os[c * (YM_T + 1) + r];
+      }
+      named_sync(YW_BAR_E, 256);                  // Os, Ci, Cv free for the next tile
+      q = qn;
     }
-  }
-  // Out[c][r] through shared memory (the Phs region, stride T + 1) so that 64 consecutive r
-  // of a column leave together
-  __syncthreads();
-  double* Os = Phs;
-#pragma unroll
-  for (int i = 0; i < YM_T / 4; ++i) Os[ocol * (YM_T + 1) + 16 * rg + i] = out[i];
-  __syncthreads();
-  for (int k = tid; k < YM_T * YM_T; k += YM_THREADS) {
-    const int c = k >> 6, r = k & 63;
-    A.out[(C0 + c) * A.ldo + R0 + r - A.out_row0] = Os[c * (YM_T + 1) + r];
   }
 }
 
@@ -351,15 +444,21 @@ int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
   dim3 grid((unsigned)(n_cols / YM_T), (unsigned)((row1 - row0) / YM_T));
   if (grid.x == 0 || grid.y == 0) return WQ_OK;
   cudaStream_t st = (cudaStream_t)stream;
-#define WQ_YM_LAUNCH(NA)                                                                         \
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nt = (int64_t)grid.x * grid.y;
+  const unsigned g = (unsigned)(nt < sms ? nt : sms);
+#define WQ_YW_LAUNCH(NA)                                                                         \
   {                                                                                              \
-    const size_t smem = (size_t)YmCfg<NA>::SMEM * 8;                                             \
-    cudaFuncSetAttribute(ystage_mma_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+    const size_t smem = (size_t)YwCfg<NA>::SMEM * 8;                                             \
+    cudaFuncSetAttribute(ystage_ws_kernel<NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                          (int)smem);                                                             \
-    ystage_mma_kernel<NA><<<grid, YM_THREADS, smem, st>>>(A, (n_rows + 7) / 8 * 8);              \
+    ystage_ws_kernel<NA><<<g, YW_THREADS, smem, st>>>(A, (n_rows + 7) / 8 * 8, (int)grid.x,      \
+                                                      (int)grid.y);                              \
   }
-  if (nal == 17) WQ_YM_LAUNCH(17) else WQ_YM_LAUNCH(5)
-#undef WQ_YM_LAUNCH
+  if (nal == 17) WQ_YW_LAUNCH(17) else WQ_YW_LAUNCH(5)
+#undef WQ_YW_LAUNCH
   return check_launch("wq_ystage_mma");
 }
 
