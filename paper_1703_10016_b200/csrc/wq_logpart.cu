@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(128) gather_fs_kernel(wq_logpart_t lp, double 
 // Y rows its bands touch (s_first .. s_last + WS - 1, `span` of them) x GY_M columns m are
 // staged through shared memory (coalesced 256-byte row pieces in, conflict-free column
 // reads out: row stride GY_M + 1).
-constexpr int GY_I = 64, GY_M = 32, GY_B = 4;
+constexpr int GY_I = 64, GY_M = 32, GY_B = 8;
 template <int WS>
 __global__ void __launch_bounds__(128) gather_yts_kernel(wq_logpart_t lp, double alpha,
                                                          const double* Y, double* P, int span) {
@@ -447,9 +447,16 @@ __global__ void __launch_bounds__(128) gather_yts_kernel(wq_logpart_t lp, double
   const int64_t sfirst = lp.s_start[i0];
   const int rows = (int)(lp.s_start[ilast] - sfirst) + WS;   // <= span (host-checked)
   const int mcnt = (int)min((int64_t)GY_M, nf - m0);
-  for (int k = threadIdx.x; k < rows * GY_M; k += blockDim.x) {
-    const int r = k / GY_M, mm = k - r * GY_M;
-    if (r < span && mm < mcnt) ysm[r * (GY_M + 1) + mm] = __ldg(Y + pmod(sfirst + r, nf) * nf + m0 + mm);
+  {
+    // one warp per staged row (a 256-byte piece of a Y row), the row index reduced once
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t sf = pmod(sfirst, nf);
+    const int rmax = rows < span ? rows : span;
+    for (int r = w; r < rmax; r += 4) {
+      int64_t g = sf + r;
+      while (g >= nf) g -= nf;
+      if (lane < mcnt) ysm[r * (GY_M + 1) + lane] = __ldg(Y + g * nf + m0 + lane);
+    }
   }
   __syncthreads();
   const int il = threadIdx.x & (GY_I - 1), half = threadIdx.x >> 6;
