@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(128) gather_fs_kernel(wq_logpart_t lp, double 
 // Y rows its bands touch (s_first .. s_last + WS - 1, `span` of them) x GY_M columns m are
 // staged through shared memory (coalesced 256-byte row pieces in, conflict-free column
 // reads out: row stride GY_M + 1).
-constexpr int GY_I = 64, GY_M = 32, GY_B = 8;
+constexpr int GY_I = 64, GY_M = 32, GY_B = 4;
 template <int WS>
 __global__ void __launch_bounds__(128) gather_yts_kernel(wq_logpart_t lp, double alpha,
                                                          const double* Y, double* P, int span) {
