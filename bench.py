@@ -542,6 +542,11 @@ def main():
             "distributed_ms": dist_split,
             "roofline": roofline,
             "fp64_roofline_fraction_survey_W": survey_frac,
+            "fp64_roofline_fraction_survey_W_note": (
+                "SURVEY 8(d) fixed W (prices every ln at 44 flop-eq, libdevice's count) / step "
+                "time / peak; the kernels execute 8 FP64 operations per ln, so this figure can "
+                "exceed 1 -- kept for continuity with the survey's target only; "
+                "roofline.frac and roofline.executed_frac are the measured ones"),
             "precompute_s": precompute_s,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -1069,14 +1069,9 @@ static int launch_ik1(const wq_smooth_t* sm, double* X, int64_t ldx, int* flag, 
   return check_launch("wq_ik1_sym");
 }
 
-// fewer pairs than this go to the one-pair-per-CTA kernel (two CTAs per SM)
-static int64_t x2ws_min_pairs() {
-  static const int64_t v = [] {
-    const char* e = getenv("WQB200_X2WS_MIN_PAIRS");   // A/B tools only
-    return e ? (int64_t)atoll(e) : (int64_t)592;
-  }();
-  return v;
-}
+// fewer pairs than this go to the one-pair-per-CTA kernel (two CTAs per SM); from 4 pairs
+// per SM on, the persistent kernel is at least as fast at every size measured (N = 2048 .. 32768)
+constexpr int64_t X2WS_MIN_PAIRS = 592;
 
 template <int P>
 static int launch_x2(int64_t N, const double* Uext, const double* Zext, const double* s_w,
@@ -1090,7 +1085,7 @@ static int launch_x2(int64_t N, const double* Uext, const double* Zext, const do
   const int64_t blocks = tile_row0 < 0 ? pair1 - pair0 : (int64_t)(tile_row1 - tile_row0) * nb;
   if (blocks <= 0) return WQ_OK;
   // full sweeps of the upper triangle: the warp-specialised persistent kernel, one CTA per SM
-  if (tile_row0 < 0 && N >= X2Cfg<P>::ZROWS && blocks >= x2ws_min_pairs()) {
+  if (tile_row0 < 0 && N >= X2Cfg<P>::ZROWS && blocks >= X2WS_MIN_PAIRS) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
