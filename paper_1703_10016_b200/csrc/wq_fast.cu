@@ -178,10 +178,13 @@ __device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const
       ipB1 = __ldg(pB - SGN * (WG - 1));
     }
   }
-#pragma unroll UNR
-  for (int jj = 0; jj < HJ; ++jj) {
-    const int j = jb + jj;
-    const int r = 2 * j + WG - 2;
+  // software pipeline: the two new kernel values (per outer node) of column jj + 1 are
+  // evaluated while column jj is contracted, so their independent chains fill the latency of
+  // the contraction's dependent FMA chain (the kernel is bound by the number of independent
+  // chains in flight per scheduler, not by issue slots or the FP64 pipe)
+  double cA0, cA1, cB0 = 0.0, cB1 = 0.0;
+  auto column = [&](int jj, double& vA0, double& vA1, double& vB0, double& vB1) {
+    const int r = 2 * (jb + jj) + WG - 2;
     const double a0 = ipA0, a1 = ipA1, b0 = ipB0, b1 = ipB1;
     if (FAST && jj + 1 < HJ) {
       const int rn = 2 * (jj + 1) + WG - 2;
@@ -192,8 +195,19 @@ __device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const
         ipB1 = __ldg(pB - SGN * (rn + 1));
       }
     }
-    eval(r, 2 * jj + WG - 2, wA[WG - 2], wB[WG - 2], a0, b0);
-    eval(r + 1, 2 * jj + WG - 1, wA[WG - 1], wB[WG - 1], a1, b1);
+    eval(r, 2 * jj + WG - 2, vA0, vB0, a0, b0);
+    eval(r + 1, 2 * jj + WG - 1, vA1, vB1, a1, b1);
+  };
+  column(0, cA0, cA1, cB0, cB1);
+#pragma unroll UNR
+  for (int jj = 0; jj < HJ; ++jj) {
+    const int j = jb + jj;
+    double nA0 = 0.0, nA1 = 0.0, nB0 = 0.0, nB1 = 0.0;
+    if (jj + 1 < HJ) column(jj + 1, nA0, nA1, nB0, nB1);
+    wA[WG - 2] = cA0;
+    wA[WG - 1] = cA1;
+    wB[WG - 2] = cB0;
+    wB[WG - 1] = cB1;
     const double2* g2 = reinterpret_cast<const double2*>(G + j * GW);
     double g[GW];
 #pragma unroll
@@ -215,6 +229,10 @@ __device__ __forceinline__ void ik1_phase1(double* T1, const double2* rxy, const
       wA[w] = wA[w + 2];
       wB[w] = wB[w + 2];
     }
+    cA0 = nA0;
+    cA1 = nA1;
+    cB0 = nB0;
+    cB1 = nB1;
   }
   if (FAST) bad |= hmx >= 0x7fe00000u;
 }
