@@ -57,13 +57,13 @@ pair_table_kernel(int64_t nel, int closed, int da, int db, double h, const doubl
     w[g] = gw[g_off + g];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < ng * nA; e += blockDim.x) {
-    int g = e / nA, a = e - g * nA;
-    wa[g][a] = w[g] * pow(x[g], (double)a);
-  }
-  for (int e = threadIdx.x; e < ng * nB; e += blockDim.x) {
-    int g = e / nB, b = e - g * nB;
-    wb[g][b] = w[g] * pow(x[g], (double)b);
+  // w_g x_g^a by running products (a pow() per entry was most of this kernel's instructions)
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+    double p = 1.0;
+    for (int a = 0; a < nA; ++a, p *= x[g]) {
+      wa[g][a] = w[g] * p;
+      if (a < nB) wb[g][a] = w[g] * p;
+    }
   }
   const bool near = fabs(keff) <= 1.0;
   for (int e = threadIdx.x; e < nA * nB; e += blockDim.x) {
@@ -109,7 +109,8 @@ pair_table_kernel(int64_t nel, int closed, int da, int db, double h, const doubl
   const double lh = log(h);
   for (int e = threadIdx.x; e < nA * nB; e += blockDim.x) {
     int a = e / nB, b = e - a * nB;
-    double scale = pow(h, 2.0 + (double)a + (double)b);
+    double scale = h * h;                        // h^(2 + a + b)
+    for (int q = 0; q < a + b; ++q) scale *= h;
     m2[k * nA * nB + e] = scale * (acc[a][b] + lh * (ca[a] * cb[b]));
   }
 }
