@@ -150,6 +150,24 @@ class RuleBand:
     WG: int
 
 
+def _unique_rows(key: np.ndarray):
+    """(first, inv) of np.unique(key, axis=0, return_index=True, return_inverse=True) up to
+    the order of the groups: rows are grouped by a 64-bit hash of their bits (a sort of n
+    integers instead of a lexicographic sort of n rows), verified exactly, with the full
+    row sort as the fallback on a hash collision."""
+    key = np.ascontiguousarray(key, dtype=np.float64)
+    bits = key.view(np.uint64)
+    mult = (np.arange(1, key.shape[1] + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) | np.uint64(1)
+    with np.errstate(over="ignore"):
+        h = (bits * mult[None, :]).sum(axis=1, dtype=np.uint64)
+    _, first, inv = np.unique(h, return_index=True, return_inverse=True)
+    inv = inv.ravel()
+    if not np.array_equal(bits[first][inv], bits):
+        _, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+        inv = inv.ravel()
+    return first, inv
+
+
 def regular_rule_band(parent: BasisSpec, fine: BasisSpec, nodes: np.ndarray) -> RuleBand:
     """Minimum-norm weighted rules, one per parent function, exact on every
     fine function overlapping its support (quadrature.py:510-540).
@@ -247,7 +265,7 @@ def regular_rule_band(parent: BasisSpec, fine: BasisSpec, nodes: np.ndarray) -> 
         # identical local systems (every rule of a uniform mesh, up to the ends) are solved
         # once: the same inputs give the same bits
         key = np.concatenate([Am.reshape(len(sel), -1), bm], axis=1)
-        ukey, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+        first, inv = _unique_rows(key)
         Am, bm = Am[first], bm[first]
         u_, s_, vt = np.linalg.svd(Am, full_matrices=False)
         if np.any(s_[:, -1] <= max(sj, sn) * np.finfo(float).eps * s_[:, 0]):
