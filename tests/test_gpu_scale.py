@@ -131,3 +131,25 @@ def test_end_node_fix_graded_meshes(cuda, n_el):
         ref = O.GeneralRows(oc, sp, end_fix=True).a_rows(rows)
         assert np.abs(A[rows] - ref).max() / np.abs(A).max() <= TOL
     assert np.array_equal(A, A.T)
+
+
+def test_persistent_x2_through_pair_ranges_and_lists(cuda):
+    """At N = 4096 (2080 tile pairs) pair ranges and pair lists are long enough for the
+    warp-specialised persistent x2 kernel: the packed multi-GPU path (ranges with an offset,
+    2 ranks emulated in turn) and the single-process multi-device host path (explicit pair
+    lists, 2 buffers on one GPU) must give the bits of the single-launch assembly."""
+    torch = cuda
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_gpu_parity import emulate_packed_ranks
+    space = W.make_cyclic_basis(3, np.linspace(0, 1, 4097))
+    disc = W.build_discretization(_star(), space, 1)
+    ref = AS.assemble_matrix_device(disc)
+    assert torch.equal(ref, ref.T)
+    bufs, pg = emulate_packed_ranks(disc, 2, 1)
+    assert min(p1 - p0 for p0, p1 in (pg.block(0, r) for r in range(2))) >= 592
+    for B in bufs:
+        assert torch.equal(B, ref)
+    out = W.assemble_matrix_to_host(disc, devices=[0, 0], chunks=1)
+    assert torch.equal(out, ref.cpu())
