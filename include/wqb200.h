@@ -406,6 +406,10 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
  * rows padded with zeros to a multiple of 8, each power b in DMMA B-fragment order
  * [row / 8][k / 4][row % 8][k % 4]: one contiguous 256-byte fragment per row group and k-step), LtR
  * (n_rows x 5), vsum (n_cols x 5) and, when Tb is not NULL, Tb (5 x n_tab x 20) from m2u.
+ * wq_ystage_mma_tiles fills the per-column-tile tables the kernel's contraction warps fetch
+ * by TMA a tile ahead: CvT (n_cols / 64 x 64 x 5 x 5 doubles: v_f[b][b'] of the w-th
+ * incidence (f, b') of each column) and CiT (n_cols / 64 x 64 x 5 ints: f minus the first
+ * element of the tile's first column, or -1).
  */
 int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, int wc,
                        const int64_t* e_rows, const int64_t* r_emin, const int64_t* r_emax,
@@ -413,10 +417,14 @@ int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, in
                        const double* v, const double* elh, const double* m2u, int da1,
                        const double* ca, const double* cb, double* Cr, double* LtR,
                        double* vsum, double* Tb, int64_t n_tab, void* stream);
+int wq_ystage_mma_tiles(int64_t n_cols, int wc, const int64_t* c_el, const int64_t* c_loc,
+                        const int64_t* c_emin, const double* v, double* CvT, int* CiT,
+                        void* stream);
 int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
                   const int64_t* r_emin, const int64_t* c_el, const int64_t* c_loc,
                   const int64_t* c_emin, const int64_t* c_emax, const double* v,
-                  const double* Cr, const double* LtR, const double* vsum, const double* Tb,
+                  const double* Cr, const double* LtR, const double* vsum, const double* CvT,
+                  const int* CiT, const double* Tb,
                   int64_t n_tab, const int* row_ko, const int* col_ko, double* out, int64_t ldo,
                   int64_t row0, int64_t row1, int sym, void* stream);
 

@@ -114,8 +114,10 @@ _SIGS = {
     "wq_ystage_mma_prep": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                            c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                            c_vp, c_i64, c_vp],
+    "wq_ystage_mma_tiles": [c_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "wq_ystage_mma": [c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                      c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_int, c_vp],
+                      c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
+                      c_int, c_vp],
 }
 
 EXPORTED = tuple(_SIGS)

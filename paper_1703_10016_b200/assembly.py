@@ -959,6 +959,12 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None, want_th
         vsum = torch.empty((NE, 5), **f64)
         common = (_lib.ptr(d["v_el"]), _lib.ptr(d["v_loc"]))
         mcols = common + (_lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), _lib.ptr(d["v"]))
+        # per-column-tile incidence tables of the contraction warps (TMA, a tile ahead)
+        CvT = torch.empty((NE // _YM_T, _YM_T * 25), **f64)
+        CiT = torch.empty((NE // _YM_T, _YM_T * 5), dtype=torch.int32, device="cuda")
+        _lib.call("wq_ystage_mma_tiles", NE, wc, *common, _lib.ptr(L["v_lo"]), _lib.ptr(d["v"]),
+                  _lib.ptr(CvT), _lib.ptr(CiT), st)
+        ctabs = (_lib.ptr(CvT), _lib.ptr(CiT))
         if want_theta:      # (the first prep also re-lays the table out: Tb)
             CrT, LtT = torch.empty((5, -(-N // 8) * 8, kpT), **f64), torch.empty((N, 5), **f64)
             _lib.call("wq_ystage_mma_prep", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
@@ -976,11 +982,11 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None, want_th
                       _lib.ptr(vsum), tb, n_tab, st)
         if want_theta:
             _lib.call("wq_ystage_mma", N, NE, n, da1, wc, _lib.ptr(L["u_lo"]), *mcols,
-                      _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
+                      _lib.ptr(CrT), _lib.ptr(LtT), _lib.ptr(vsum), *ctabs, _lib.ptr(Tb), n_tab,
                       kT, kC, _lib.ptr(thetaT), r1 - r0, r0, r1, 0, st)
         if want_d:
             _lib.call("wq_ystage_mma", NE, NE, n, nB, wc, _lib.ptr(L["v_lo"]), *mcols,
-                      _lib.ptr(CrD), _lib.ptr(LtD), _lib.ptr(vsum), _lib.ptr(Tb), n_tab,
+                      _lib.ptr(CrD), _lib.ptr(LtD), _lib.ptr(vsum), *ctabs, _lib.ptr(Tb), n_tab,
                       kD, kC, _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), st)
     if want_theta:
         _lib.call("wq_ystage", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),

@@ -54,6 +54,8 @@ struct YmArgs {
                            // in DMMA B-fragment order [row / 8][k / 4][row % 8][k % 4]
   const double* LtR;       // (n_rows, NB)
   const double* vsum;      // (n_cols, NB)
+  const double* CvT;       // (column tiles, T, WCM, NB) v_f[b][b'] of the tile's column incidences
+  const int* CiT;          // (column tiles, T, WCM) element offset f - fa of the incidence, or -1
   const double* Tb;        // (NB, n_tab, ZST) table slices, row g + n_el - 1 + TFRONT
   int64_t n_tab;
   const int* row_ko;       // (row tiles) lattice offset k_e - e of a pure row tile, or NOT_PURE
@@ -84,6 +86,19 @@ struct YmCfg {
 // with CTA-wide barriers between the GEMM, scatter and contraction of every power; this one is
 // bit-identical to it and 2.5 % faster.)
 // ---------------------------------------------------------------------------
+#ifdef WQ_YS_TIMELINE
+// tools build only: clock stamps of the phases of one tile (the 20th of every CTA):
+// slots 0-24 GEMM group (5 per phase), 32-63 contraction group
+__device__ long long* g_ys_tl = nullptr;
+#define YW_TL(slot)                                                                       \
+  do {                                                                                    \
+    if (tcount == 20 && (threadIdx.x & 255) == 0 && g_ys_tl)                              \
+      g_ys_tl[(int64_t)blockIdx.x * 64 + (slot)] = clock64();                             \
+  } while (0)
+#else
+#define YW_TL(slot) do {} while (0)
+#endif
+
 constexpr int YW_THREADS = 512;
 constexpr int YW_BAR_E = 1;   // named barrier of the contraction group
 
@@ -94,8 +109,9 @@ struct YwCfg {
   static constexpr int PH = YM_T * YM_PST;
   static constexpr int CV = YM_T * YM_WCM * YM_NB;
   static constexpr int OS = YM_T * (YM_T + 1);
-  // Zsm[2] | Phs[2] | Cv | Os | 6 mbarriers | Ci (ints)
-  static constexpr int SMEM = 2 * ZW + 2 * PH + CV + OS + 6 + YM_T * YM_WCM / 2 + 1;
+  static constexpr int LT = YM_T * YM_NB;          // LtR rows / vsum rows of a tile
+  // Zsm[2] | Phs[2] | Cv[2] | Os | LtR[2] | vsum[2] | 8 mbarriers | Ci[2] (ints)
+  static constexpr int SMEM = 2 * ZW + 2 * PH + 2 * CV + OS + 4 * LT + 8 + YM_T * YM_WCM;
 };
 
 template <int NAL>
@@ -106,12 +122,15 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
   extern __shared__ double sm[];
   double* Zsm = sm;                               // [2][ZR][ZST]
   double* Phs = Zsm + 2 * W::ZW;                  // [2][T][PST]
-  double* Cv = Phs + 2 * W::PH;                   // [T c][WCM][NB]
-  double* Os = Cv + W::CV;                        // [T c][T + 1]
-  uint64_t* wfull = reinterpret_cast<uint64_t*>(Os + W::OS);
+  double* Cv = Phs + 2 * W::PH;                   // [2][T c][WCM][NB]
+  double* Os = Cv + 2 * W::CV;                    // [T c][T + 1]
+  double* Lts = Os + W::OS;                       // [2][T r][NB]: LtR rows of the tile
+  double* Vss = Lts + 2 * W::LT;                  // [2][T c][NB]: vsum rows of the tile
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(Vss + 2 * W::LT);
   uint64_t* pfull = wfull + 2;
   uint64_t* pempty = wfull + 4;
-  int* Ci = reinterpret_cast<int*>(wfull + 6);    // [T c][WCM]
+  uint64_t* efull = wfull + 6;                    // [2] tile tables landed (TMA)
+  int* Ci = reinterpret_cast<int*>(wfull + 8);    // [2][T c][WCM]
   const int tid = threadIdx.x;
   const int64_t ntiles = (int64_t)ntx * nty;
   // the tiles this kernel owns, in the order every thread of the CTA walks them
@@ -138,6 +157,7 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
       mbar_init(wfull + b, 1);
       mbar_init(pfull + b, 8);
       mbar_init(pempty + b, 8);
+      mbar_init(efull + b, 1);
     }
   fence_proxy_async();
   __syncthreads();
@@ -178,11 +198,13 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
     double bq[C::PF];
 #pragma unroll
     for (int t = 0; t < C::PF; ++t) bq[t] = __ldg(cur.brow0 + 32 * t);
-    for (int64_t q = q0; q < ntiles;) {
+    int tcount = 0;
+    for (int64_t q = q0; q < ntiles; ++tcount) {
       const int64_t qn = next_pure(q + gridDim.x);
       const Tile nxt = qn < ntiles ? load_tile(qn) : cur;
       auto phase = [&](auto bc) {
         constexpr int b = decltype(bc)::value;
+        YW_TL(5 * b);
         constexpr int SHIFT = (b * C::NSTEPS) % C::PF;
         const int buf = ph & 1;
         const unsigned par = (ph >> 1) & 1;
@@ -191,6 +213,7 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
         // the next phase's fragments: the next power of this tile, or power 0 of the next tile
         const double* __restrict__ bnext = b + 1 < YM_NB ? brow + nrp * C::KP : nxt.brow0;
         mbar_wait(wfull + buf, par);
+        YW_TL(5 * b + 1);
         double acc[YM_NKB][2];
 #pragma unroll
         for (int kb = 0; kb < YM_NKB; ++kb) acc[kb][0] = acc[kb][1] = 0.0;
@@ -213,8 +236,10 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
         else if (cur.nkb == YM_NKB - 2) gemm(std::integral_constant<int, YM_NKB - 2>());
         else if (cur.nkb == YM_NKB - 1) gemm(std::integral_constant<int, YM_NKB - 1>());
         else gemm(std::integral_constant<int, YM_NKB>());
+        YW_TL(5 * b + 2);
         // Phs[buf] is free once the contraction group has used it two phases ago
         if (ph >= 2) mbar_wait(pempty + buf, par ^ 1);
+        YW_TL(5 * b + 3);
         double* P = Phs + buf * W::PH;
 #pragma unroll
         for (int kb = 0; kb < YM_NKB; ++kb)
@@ -224,6 +249,7 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
             if (fl >= 0 && fl < cur.fspan) P[(8 * warp + 2 * cl + e) * YM_PST + fl] = acc[kb][e];
           }
         warp_arrive(pfull + buf);
+        YW_TL(5 * b + 4);
         ++ph;
       };
       phase(std::integral_constant<int, 0>());
@@ -239,49 +265,63 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
     const int et = tid - 256;
     const int ocol = et & 63, rg = et >> 6;
     unsigned ph = 0;
-    if (et == 0)
+    // TMA request of tile q's tables into buffers cb: column incidences (CvT / CiT, per
+    // column tile), the tile's LtR rows and vsum rows
+    auto tables = [&](int64_t q, int cb) {
+      const int ct = (int)(q % ntx), rt = (int)(q / ntx);
+      const int64_t R0 = A.row0 + (int64_t)rt * YM_T, C0 = (int64_t)ct * YM_T;
+      constexpr unsigned BCV = W::CV * 8, BCI = YM_T * YM_WCM * 4, BLT = W::LT * 8;
+      mbar_arrive_expect_tx(efull + cb, BCV + BCI + 2 * BLT);
+      bulk_g2s(Cv + cb * W::CV, A.CvT + (int64_t)ct * W::CV, BCV, efull + cb);
+      bulk_g2s(Ci + cb * (YM_T * YM_WCM), A.CiT + (int64_t)ct * (YM_T * YM_WCM), BCI, efull + cb);
+      bulk_g2s(Lts + cb * W::LT, A.LtR + R0 * YM_NB, BLT, efull + cb);
+      bulk_g2s(Vss + cb * W::LT, A.vsum + C0 * YM_NB, BLT, efull + cb);
+    };
+    if (et == 0) {
       for (int b = 0; b < 2; ++b) {
         mbar_arrive_expect_tx(wfull + b, W::ZW * 8);
         bulk_g2s(Zsm + b * W::ZW, window_src(q0) + (int64_t)b * A.n_tab * YM_ZST, W::ZW * 8, wfull + b);
       }
-    for (int64_t q = q0; q < ntiles;) {
+      tables(q0, 0);
+    }
+    int tcount = 0;
+    for (int64_t q = q0; q < ntiles; ++tcount) {
+      YW_TL(32);
       const int64_t qn = next_pure(q + gridDim.x);
       const int ct = (int)(q % ntx), rt = (int)(q / ntx);
       const int64_t R0 = A.row0 + (int64_t)rt * YM_T, C0 = (int64_t)ct * YM_T;
-      const int64_t fa = A.c_emin[C0];
-      // column incidences of the tile: element offset and v_f[b][b'] for every b
-      for (int k = et; k < YM_T * YM_WCM; k += 256) {
-        const int c = k / YM_WCM, w = k - c * YM_WCM;
-        const int64_t cc = C0 + c;
-        const int64_t f = w < A.wc ? A.c_el[cc * A.wc + w] : -1;
-        Ci[k] = f >= 0 ? (int)(f - fa) : -1;
-        const int bp = f >= 0 ? (int)A.c_loc[cc * A.wc + w] : 0;
-#pragma unroll
-        for (int b = 0; b < YM_NB; ++b)
-          Cv[k * YM_NB + b] = f >= 0 ? __ldg(A.v + f * (YM_NB * YM_NB) + b * YM_NB + bp) : 0.0;
-      }
+      YW_TL(33);
+      // the tile's tables (column incidences, LtR rows, vsum rows) were requested a tile ago;
+      // request the next tile's into the other buffers (all contraction threads left them at
+      // the end of the previous tile)
+      const int cbuf = tcount & 1;
+      if (et == 0 && qn < ntiles) tables(qn, cbuf ^ 1);
+      mbar_wait(efull + cbuf, (unsigned)((tcount >> 1) & 1));
+      const int* ci = Ci + cbuf * (YM_T * YM_WCM);
+      const double* cvs = Cv + cbuf * W::CV;
       // Out[c][r] for this thread's column c and rows r = 16 rg + i; starts from the ln h term
       double out[YM_T / 4];
       {
-        double vs[YM_NB];
-#pragma unroll
-        for (int b = 0; b < YM_NB; ++b) vs[b] = __ldg(A.vsum + (C0 + ocol) * YM_NB + b);
+        const double* vs = Vss + cbuf * W::LT + ocol * YM_NB;
+        const double* lt = Lts + cbuf * W::LT + 16 * rg * YM_NB;
 #pragma unroll
         for (int i = 0; i < YM_T / 4; ++i) {
-          const int64_t r = R0 + 16 * rg + i;
           double s = 0.0;
 #pragma unroll
-          for (int b = 0; b < YM_NB; ++b) s = fma(__ldg(A.LtR + r * YM_NB + b), vs[b], s);
+          for (int b = 0; b < YM_NB; ++b) s = fma(lt[i * YM_NB + b], vs[b], s);
           out[i] = s;
         }
       }
-      named_sync(YW_BAR_E, 256);                  // Ci / Cv visible
+      YW_TL(34);
+      YW_TL(35);
       const double* nsrc = qn < ntiles ? window_src(qn) : nullptr;
       const double* csrc = window_src(q);
       for (int b = 0; b < YM_NB; ++b, ++ph) {
         const int buf = ph & 1;
         const unsigned par = (ph >> 1) & 1;
+        YW_TL(36 + 3 * b);
         mbar_wait(pfull + buf, par);
+        YW_TL(37 + 3 * b);
         // every GEMM warp has read window buf: request the window of phase ph + 2 into it
         if (et == 0) {
           const double* src = b + 2 < YM_NB ? csrc + (int64_t)(b + 2) * A.n_tab * YM_ZST
@@ -296,9 +336,9 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
         double cv[YM_WCM];
 #pragma unroll
         for (int w = 0; w < YM_WCM; ++w) {
-          const int f = Ci[ocol * YM_WCM + w];
+          const int f = ci[ocol * YM_WCM + w];
           fi[w] = f >= 0 ? f : 0;
-          cv[w] = f >= 0 ? Cv[(ocol * YM_WCM + w) * YM_NB + b] : 0.0;
+          cv[w] = f >= 0 ? cvs[(ocol * YM_WCM + w) * YM_NB + b] : 0.0;
         }
         const double* phs = Phs + buf * W::PH + 16 * rg * YM_PST;
 #pragma unroll
@@ -306,6 +346,7 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
 #pragma unroll
           for (int w = 0; w < YM_WCM; ++w) out[i] = fma(phs[i * YM_PST + fi[w]], cv[w], out[i]);
         warp_arrive(pempty + buf);
+        YW_TL(38 + 3 * b);
       }
       // Out[c][r] through shared memory so that 64 consecutive r of a column leave together
 #pragma unroll
@@ -315,7 +356,8 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
         const int c = k >> 6, r = k & 63;
         A.out[(C0 + c) * A.ldo + R0 + r - A.out_row0] = Os[c * (YM_T + 1) + r];
       }
-      named_sync(YW_BAR_E, 256);                  // Os, Ci, Cv free for the next tile
+      named_sync(YW_BAR_E, 256);                  // Os and this tile's tables free
+      YW_TL(52);
       q = qn;
     }
   }
@@ -395,11 +437,37 @@ __global__ void ystage_mma_prep_cols(int64_t n_cols, int wc, const int64_t* c_el
   }
 }
 
+// CvT[ct][c][w][b] = v_f[b][b'] and CiT[ct][c][w] = f - fa of the w-th incidence (f, b') of
+// column C0 + c, fa = the first element of the tile's first column (-1 / 0 where none): the
+// contraction group's per-tile tables, one TMA copy each
+__global__ void ystage_mma_prep_tiles(int64_t n_tiles, int wc, const int64_t* c_el,
+                                      const int64_t* c_loc, const int64_t* c_emin, const double* v,
+                                      double* CvT, int* CiT) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_tiles * YM_T * YM_WCM) return;
+  const int64_t ct = k / (YM_T * YM_WCM);
+  const int kk = (int)(k - ct * (YM_T * YM_WCM));
+  const int c = kk / YM_WCM, w = kk - c * YM_WCM;
+  const int64_t cc = ct * YM_T + c;
+  const int64_t f = w < wc ? c_el[cc * wc + w] : -1;
+  CiT[k] = f >= 0 ? (int)(f - c_emin[ct * YM_T]) : -1;
+  const int bp = f >= 0 ? (int)c_loc[cc * wc + w] : 0;
+  for (int b = 0; b < YM_NB; ++b)
+    CvT[k * YM_NB + b] = f >= 0 ? v[f * (YM_NB * YM_NB) + b * YM_NB + bp] : 0.0;
+}
+
 }  // namespace wq
 
 using namespace wq;
 
 extern "C" {
+
+#ifdef WQ_YS_TIMELINE
+int wq_debug_ys_timeline(long long* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(g_ys_tl, &buf, sizeof(buf));
+  return e == cudaSuccess ? WQ_OK : WQ_ECUDA;
+}
+#endif
 
 int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, int wc,
                        const int64_t* e_rows, const int64_t* r_emin, const int64_t* r_emax,
@@ -426,20 +494,34 @@ int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, in
   return check_launch("wq_ystage_mma_prep");
 }
 
+int wq_ystage_mma_tiles(int64_t n_cols, int wc, const int64_t* c_el, const int64_t* c_loc,
+                        const int64_t* c_emin, const double* v, double* CvT, int* CiT,
+                        void* stream) {
+  if (n_cols < YM_T || wc < 1 || wc > YM_WCM || !c_el || !c_loc || !c_emin || !v || !CvT || !CiT) {
+    set_error("wq_ystage_mma_tiles: bad arguments");
+    return WQ_EINVAL;
+  }
+  const int64_t nt = n_cols / YM_T;
+  ystage_mma_prep_tiles<<<ceil_div(nt * YM_T * YM_WCM, 256), 256, 0, (cudaStream_t)stream>>>(
+      nt, wc, c_el, c_loc, c_emin, v, CvT, CiT);
+  return check_launch("wq_ystage_mma_tiles");
+}
+
 int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
                   const int64_t* r_emin, const int64_t* c_el, const int64_t* c_loc,
                   const int64_t* c_emin, const int64_t* c_emax, const double* v,
-                  const double* Cr, const double* LtR, const double* vsum, const double* Tb,
+                  const double* Cr, const double* LtR, const double* vsum, const double* CvT,
+                  const int* CiT, const double* Tb,
                   int64_t n_tab, const int* row_ko, const int* col_ko, double* out, int64_t ldo,
                   int64_t row0, int64_t row1, int sym, void* stream) {
-  if (n_rows <= 0 || n_cols <= 0 || (nal != 17 && nal != 5) || wc < 1 || !r_emin || !c_el ||
+  if (!CvT || !CiT || n_rows <= 0 || n_cols <= 0 || (nal != 17 && nal != 5) || wc < 1 || !r_emin || !c_el ||
       !c_loc || !c_emin || !c_emax || !v || !Cr || !LtR || !vsum || !Tb || !row_ko ||
       !col_ko || !out || row0 < 0 || row0 % YM_T != 0 || row1 > n_rows || row1 <= row0 ||
       wc > YM_WCM || ldo < row1 - row0 || n_tab < 2 * n_el - 1 + YM_ZR + YM_TFRONT) {
     set_error("wq_ystage_mma: bad arguments");
     return WQ_EINVAL;
   }
-  YmArgs A{n_cols, n_el, wc, r_emin, c_el, c_loc, c_emin, c_emax, v, Cr, LtR, vsum, Tb, n_tab,
+  YmArgs A{n_cols, n_el, wc, r_emin, c_el, c_loc, c_emin, c_emax, v, Cr, LtR, vsum, CvT, CiT, Tb, n_tab,
            row_ko, col_ko, out, ldo, row0, row0, sym};
   dim3 grid((unsigned)(n_cols / YM_T), (unsigned)((row1 - row0) / YM_T));
   if (grid.x == 0 || grid.y == 0) return WQ_OK;
