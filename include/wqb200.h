@@ -428,8 +428,11 @@ int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
                   int64_t n_tab, const int* row_ko, const int* col_ko, double* out, int64_t ldo,
                   int64_t row0, int64_t row1, int sym, void* stream);
 
-/* out[j][i] = out[i][j] for i > j (n x n, leading dimension ld). */
-int wq_mirror_lower(double* out, int64_t n, int64_t ld, void* stream);
+/* out[j][i] = out[i][j] for i > j (n x n, leading dimension ld).  With row_ko / col_ko (both or
+ * neither; the arrays given to wq_ystage_mma with sym = 1) the 64 x 64 tiles that kernel owns
+ * are skipped: it writes their mirrors itself. */
+int wq_mirror_lower(double* out, int64_t n, int64_t ld, const int* row_ko, const int* col_ko,
+                    void* stream);
 /* out[c][r] = out[r][c] for c > r: the upper triangle copied onto the lower one (the
  * symmetric multi-GPU path: each rank assembles the upper tile pairs of its rows). */
 int wq_mirror_upper(double* out, int64_t n, int64_t ld, void* stream);

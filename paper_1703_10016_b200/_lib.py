@@ -97,7 +97,7 @@ _SIGS = {
     "wq_mirror_upper": [c_vp, c_i64, c_i64, c_vp],
     "wq_pack_pairs": [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp],
     "wq_unpack_pairs": [c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp],
-    "wq_mirror_lower": [c_vp, c_i64, c_i64, c_vp],
+    "wq_mirror_lower": [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
     "wq_gather_fs_rows": [ctypes.POINTER(WqLogpart), c_dbl, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp],
     "wq_phi_s_rows": [ctypes.POINTER(WqLogpart), c_vp, c_i64, c_i64, c_vp, c_i64, c_int, c_vp],
     "wq_gen_gather_d": [c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,

@@ -1001,7 +1001,8 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None, want_th
                         want_theta=want_theta, want_d=want_d)
     # D's lower storage triangle is complete (lattice + block parts): mirror it
     if want_d and _YS_SYM_D:
-        _lib.call("wq_mirror_lower", _lib.ptr(D), NE, NE, st)
+        # (the tensor-core tiles wrote their mirrors themselves: row_ko / col_ko skip them)
+        _lib.call("wq_mirror_lower", _lib.ptr(D), NE, NE, kD, kC, st)
     return thetaT, D
 
 

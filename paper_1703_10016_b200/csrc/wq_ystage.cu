@@ -228,10 +228,17 @@ ystage_kernel(YsArgs A) {
 
 // out[j][i] = out[i][j] for i > j (copy the lower triangle onto the upper one),
 // 32 x 32 tiles through shared memory
-__global__ void mirror_lower_kernel(double* out, int64_t n, int64_t ld) {
+// (row_ko / col_ko given: the 64 x 64 tiles wq_ystage_mma owns -- storage row tile bi / 2 pure as
+// a column tile, column tile bj / 2 pure as a row tile, equal offsets -- are already mirrored)
+__global__ void mirror_lower_kernel(double* out, int64_t n, int64_t ld, const int* row_ko,
+                                    const int* col_ko, int n_full) {
   __shared__ double t[32][33];
   const int64_t bi = blockIdx.y, bj = blockIdx.x;   // source tile rows bi, cols bj
   if (bj > bi) return;
+  if (row_ko && bi / 2 < n_full && bj / 2 < n_full) {
+    const int ko = row_ko[bj / 2];
+    if (ko != INT32_MIN && col_ko[bi / 2] == ko) return;
+  }
   const int tx = threadIdx.x, ty = threadIdx.y;
   for (int y = ty; y < 32; y += 8) {
     const int64_t r = bi * 32 + y, c = bj * 32 + tx;
@@ -430,13 +437,15 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
   return check_launch("wq_ystage");
 }
 
-int wq_mirror_lower(double* out, int64_t n, int64_t ld, void* stream) {
-  if (!out || n <= 0 || ld < n) {
+int wq_mirror_lower(double* out, int64_t n, int64_t ld, const int* row_ko, const int* col_ko,
+                    void* stream) {
+  if (!out || n <= 0 || ld < n || (row_ko != nullptr) != (col_ko != nullptr)) {
     set_error("wq_mirror_lower: bad arguments");
     return WQ_EINVAL;
   }
   dim3 mg(ceil_div(n, 32), ceil_div(n, 32));
-  mirror_lower_kernel<<<mg, dim3(32, 8), 0, (cudaStream_t)stream>>>(out, n, ld);
+  mirror_lower_kernel<<<mg, dim3(32, 8), 0, (cudaStream_t)stream>>>(out, n, ld, row_ko, col_ko,
+                                                                      (int)(n / 64));
   return check_launch("wq_mirror_lower");
 }
 

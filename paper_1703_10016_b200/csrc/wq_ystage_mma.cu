@@ -352,9 +352,24 @@ ystage_ws_kernel(YmArgs A, int64_t nrp, int ntx, int nty) {
 #pragma unroll
       for (int i = 0; i < YM_T / 4; ++i) Os[ocol * (YM_T + 1) + 16 * rg + i] = out[i];
       named_sync(YW_BAR_E, 256);
-      for (int k = et; k < YM_T * YM_T; k += 256) {
-        const int c = k >> 6, r = k & 63;
-        A.out[(C0 + c) * A.ldo + R0 + r - A.out_row0] = Os[c * (YM_T + 1) + r];
+      if (!A.sym) {
+        for (int k = et; k < YM_T * YM_T; k += 256) {
+          const int c = k >> 6, r = k & 63;
+          A.out[(C0 + c) * A.ldo + R0 + r - A.out_row0] = Os[c * (YM_T + 1) + r];
+        }
+      } else {
+        // symmetric output (D): the storage entry (C0 + c, R0 + r), c >= r on the diagonal
+        // tile, and its mirror (R0 + r, C0 + c) -- both coalesced; no mirror pass over these
+        // tiles afterwards (wq_mirror_lower skips them)
+        const bool diag = C0 == R0;
+        for (int k = et; k < YM_T * YM_T; k += 256) {
+          const int c = k >> 6, r = k & 63;
+          if (!diag || c >= r) A.out[(C0 + c) * A.ldo + R0 + r] = Os[c * (YM_T + 1) + r];
+        }
+        for (int k = et; k < YM_T * YM_T; k += 256) {
+          const int r = k >> 6, c = k & 63;
+          if (!diag || c > r) A.out[(R0 + r) * A.ldo + C0 + c] = Os[c * (YM_T + 1) + r];
+        }
       }
       named_sync(YW_BAR_E, 256);                  // Os and this tile's tables free
       YW_TL(52);
@@ -497,11 +512,16 @@ int wq_ystage_mma_prep(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, in
 int wq_ystage_mma_tiles(int64_t n_cols, int wc, const int64_t* c_el, const int64_t* c_loc,
                         const int64_t* c_emin, const double* v, double* CvT, int* CiT,
                         void* stream) {
-  if (n_cols < YM_T || wc < 1 || wc > YM_WCM || !c_el || !c_loc || !c_emin || !v || !CvT || !CiT) {
+  if (n_cols < 1 || wc < 1 || wc > YM_WCM || !c_el || !c_loc || !c_emin || !v) {
     set_error("wq_ystage_mma_tiles: bad arguments");
     return WQ_EINVAL;
   }
   const int64_t nt = n_cols / YM_T;
+  if (nt == 0) return WQ_OK;          // no full column tile: wq_ystage_mma has no tile either
+  if (!CvT || !CiT) {
+    set_error("wq_ystage_mma_tiles: missing output tables");
+    return WQ_EINVAL;
+  }
   ystage_mma_prep_tiles<<<ceil_div(nt * YM_T * YM_WCM, 256), 256, 0, (cudaStream_t)stream>>>(
       nt, wc, c_el, c_loc, c_emin, v, CvT, CiT);
   return check_launch("wq_ystage_mma_tiles");
@@ -514,10 +534,11 @@ int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
                   const int* CiT, const double* Tb,
                   int64_t n_tab, const int* row_ko, const int* col_ko, double* out, int64_t ldo,
                   int64_t row0, int64_t row1, int sym, void* stream) {
-  if (!CvT || !CiT || n_rows <= 0 || n_cols <= 0 || (nal != 17 && nal != 5) || wc < 1 || !r_emin || !c_el ||
+  if (n_rows <= 0 || n_cols <= 0 || (nal != 17 && nal != 5) || wc < 1 || !r_emin || !c_el ||
       !c_loc || !c_emin || !c_emax || !v || !Cr || !LtR || !vsum || !Tb || !row_ko ||
       !col_ko || !out || row0 < 0 || row0 % YM_T != 0 || row1 > n_rows || row1 <= row0 ||
-      wc > YM_WCM || ldo < row1 - row0 || n_tab < 2 * n_el - 1 + YM_ZR + YM_TFRONT) {
+      wc > YM_WCM || ldo < row1 - row0 || n_tab < 2 * n_el - 1 + YM_ZR + YM_TFRONT ||
+      (sym && (row0 != 0 || row1 != n_rows || n_rows != n_cols || ldo < n_cols))) {
     set_error("wq_ystage_mma: bad arguments");
     return WQ_EINVAL;
   }
@@ -525,6 +546,10 @@ int wq_ystage_mma(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int wc,
            row_ko, col_ko, out, ldo, row0, row0, sym};
   dim3 grid((unsigned)(n_cols / YM_T), (unsigned)((row1 - row0) / YM_T));
   if (grid.x == 0 || grid.y == 0) return WQ_OK;
+  if (!CvT || !CiT) {
+    set_error("wq_ystage_mma: missing tile tables (wq_ystage_mma_tiles)");
+    return WQ_EINVAL;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
