@@ -3,7 +3,10 @@ x2 kernel's bulk-copy threshold (ZROWS rows of the Z' table) with N % 64 != 0,
 so the TMA window path runs together with the cp.async IK1 tile (zero fill),
 the non-bulk output stores and the `row < nc` masks on the S band.  Checked
 against the oracle (dense restatement at N = 200, row-block restatement at
-N = 1000) and through every entry point that launches those tiles."""
+N = 1000 and 2250) and through every entry point that launches those tiles.
+At N = 2250 (666 tile pairs) the single launch runs the warp-specialised
+persistent x2 kernel with a partial last tile, the chunked and per-rank
+launches the one-pair-per-CTA kernel: they must give the same bits."""
 
 import numpy as np
 import pytest
@@ -34,7 +37,7 @@ def _oracle_A(curve, space, N):
 
 
 @pytest.mark.parametrize("p", [2, 3, 4, 5])
-@pytest.mark.parametrize("N", [200, 1000])
+@pytest.mark.parametrize("N", [200, 1000, 2250])
 def test_partial_edge_tiles(cuda, p, N):
     torch = cuda
     from paper_1703_10016_b200 import _lib, distributed as D
