@@ -382,7 +382,10 @@ int wq_gen_moments_far(int64_t n_el, int da1, int nb, int64_t n_g, const int64_t
  * the full range (D): only the storage entries out[c][r] with c >= r are produced
  * (complete them, then wq_mirror_lower; D is symmetric).  Column degree nb - 1 = 4.  Writes
  * (does not accumulate) out; outer elements off the lattice are added afterwards by
- * the block route (wq_gen_pair_blocks + gathers).
+ * the block route (wq_gen_pair_blocks + gathers).  tiles (optional): n_tiles pairs
+ * (16-row tile from row0, 64-column tile) to run instead of the full tile grid -- with
+ * row_ko / col_ko most tiles belong to wq_ystage_mma and a CTA holds ~110 KB of shared
+ * memory, so launching only the others removes a launch slot per skipped tile.
  */
 int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, int wc,
               const int64_t* e_rows, const int64_t* r_emin, const int64_t* r_emax,
@@ -391,7 +394,8 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
               const double* elh, const int64_t* kidx, const int* gidx, const double* m2u,
               int da1, const double* mgc, const double* ca, const double* cb, int64_t fspan,
               int64_t espan, double* out, int64_t ldo, int64_t row0, int64_t row1,
-              int sym_d, const int* row_ko, const int* col_ko, void* stream);
+              int sym_d, const int* row_ko, const int* col_ko, const int* tiles,
+              int64_t n_tiles, void* stream);
 
 /*
  * Tensor-core lattice tiles of wq_ystage (same Theta^T / D entries): for 64-row tiles

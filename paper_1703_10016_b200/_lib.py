@@ -110,7 +110,7 @@ _SIGS = {
                            c_vp, c_vp, c_vp],
     "wq_ystage": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                   c_vp, c_vp, c_int, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,
-                  c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_vp],
+                  c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_vp, c_i64, c_vp],
     "wq_ystage_mma_prep": [c_i64, c_i64, c_i64, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                            c_vp, c_int, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                            c_vp, c_i64, c_vp],

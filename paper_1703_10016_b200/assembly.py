@@ -863,6 +863,22 @@ def _ym_tiles(lo, hi, ko_el, start, stop, rows):
     return np.asarray(out, np.int32)
 
 
+def _ys_tile_list(row_ko, col_ko, n_rows, n_cols, sym):
+    """(16-row tile, 64-column tile) pairs left to wq_ystage once wq_ystage_mma owns the
+    tiles with equal pure offsets; ``sym``: only tiles meeting the storage triangle
+    (last column >= first row).  int32 (n, 2)."""
+    nrt = -(-n_rows // 16)
+    nct = -(-n_cols // _YM_T)
+    rk = np.repeat(np.asarray(row_ko, np.int64), _YM_T // 16)[:nrt]
+    ck = np.asarray(col_ko, np.int64)[:nct]
+    todo = ~((rk[:, None] != _YM_NOT_PURE) & (rk[:, None] == ck[None, :]))
+    if sym:
+        r0 = 16 * np.arange(nrt)[:, None]
+        c_last = np.minimum(_YM_T * (np.arange(nct)[None, :] + 1), n_cols) - 1
+        todo &= c_last >= r0
+    return np.ascontiguousarray(np.argwhere(todo).astype(np.int32))
+
+
 def _support_ranges(el):
     """First / last element of each function's support from a (-1 padded)
     incidence array (open meshes: contiguous)."""
@@ -941,17 +957,24 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None, want_th
             _lib.ptr(m2u), da1, mg, _lib.ptr(d["ca"]), _lib.ptr(d["cb"]))
     mma = _YS_MMA and r0 % _YM_T == 0 and nU == 5 and nB == 5 and da1 == 17 and wc <= 5
     kT = kD = kC = None
+    listT = listD = (None, 0)
     if mma:
         mkey = ("ym", r0, r1)
         if mkey not in L:
             ko_el = np.where(kidx != _NOT_LATTICE, kidx - np.arange(n), _YM_NOT_PURE)
             u_lo, u_hi = _support_ranges(lp.u_el)
             v_lo, v_hi = _support_ranges(lp.v_el)
-            L[mkey] = {"T": _to_dev(torch, _ym_tiles(u_lo, u_hi, ko_el, r0, r1, True)),
-                       "D": _to_dev(torch, _ym_tiles(v_lo, v_hi, ko_el, 0, NE, True)),
-                       "C": _to_dev(torch, _ym_tiles(v_lo, v_hi, ko_el, 0, NE, False))}
+            tT = _ym_tiles(u_lo, u_hi, ko_el, r0, r1, True)
+            tD = _ym_tiles(v_lo, v_hi, ko_el, 0, NE, True)
+            tC = _ym_tiles(v_lo, v_hi, ko_el, 0, NE, False)
+            L[mkey] = {"T": _to_dev(torch, tT), "D": _to_dev(torch, tD), "C": _to_dev(torch, tC),
+                       # the tiles left to the CUDA-core kernel (a few per cent)
+                       "listT": _to_dev(torch, _ys_tile_list(tT, tC, r1 - r0, NE, False)),
+                       "listD": _to_dev(torch, _ys_tile_list(tD, tC, NE, NE, bool(_YS_SYM_D)))}
         Y = L[mkey]
         kT, kD, kC = _lib.ptr(Y["T"]), _lib.ptr(Y["D"]), _lib.ptr(Y["C"])
+        listT = (_lib.ptr(Y["listT"]), Y["listT"].shape[0])
+        listD = (_lib.ptr(Y["listD"]), Y["listD"].shape[0])
         n_tab = 2 * n - 1 + _YM_ZR + _YM_TFRONT
         f64 = dict(dtype=torch.float64, device="cuda")
         kpT, kpD = -(-5 * da1 // 4) * 4, -(-5 * nB // 4) * 4
@@ -988,14 +1011,15 @@ def _lattice_theta_d(disc, lp: LogPart, d, kidx, gidx, glist, rows=None, want_th
             _lib.call("wq_ystage_mma", NE, NE, n, nB, wc, _lib.ptr(L["v_lo"]), *mcols,
                       _lib.ptr(CrD), _lib.ptr(LtD), _lib.ptr(vsum), *ctabs, _lib.ptr(Tb), n_tab,
                       kD, kC, _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), st)
-    if want_theta:
+    # (with the tensor-core tiles taken out, an empty list means nothing is left)
+    if want_theta and not (mma and listT[1] == 0):
         _lib.call("wq_ystage", N, NE, n, da1, nU, wc, _lib.ptr(L["ucols"]),
                   _lib.ptr(L["u_lo"]), _lib.ptr(L["u_hi"]), *cols, _lib.ptr(d["u"]), da1, *tail,
-                  L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, 0, kT, kC, st)
-    if want_d:
+                  L["v_fs"], L["u_es"], _lib.ptr(thetaT), r1 - r0, r0, r1, 0, kT, kC, *listT, st)
+    if want_d and not (mma and listD[1] == 0):
         _lib.call("wq_ystage", NE, NE, n, nB, nB, wc, _lib.ptr(L["vcols"]),
                   _lib.ptr(L["v_lo"]), _lib.ptr(L["v_hi"]), *cols, _lib.ptr(d["v"]), nB, *tail,
-                  L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), kD, kC, st)
+                  L["v_fs"], L["v_es"], _lib.ptr(D), NE, 0, NE, int(_YS_SYM_D), kD, kC, *listD, st)
     if len(glist):
         _blocks_theta_d(disc, lp, d, outer=glist, thetaT=thetaT, D=D, rows=rows,
                         want_theta=want_theta, want_d=want_d)

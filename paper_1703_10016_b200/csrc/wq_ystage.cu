@@ -67,6 +67,9 @@ struct YsArgs {
   const int* row_ko;          // 64-row tiles from out_row0 (wq_ystage_mma) or NULL
   const int* col_ko;          // 64-column tiles; tiles with row_ko == col_ko != NOT_PURE are
                               // done on the tensor cores by wq_ystage_mma
+  const int* tiles;           // (n, 2) (row tile, column tile) of the CTAs to run, or NULL: the
+                              // full grid (every CTA holds ~110 KB of shared memory, so a grid
+                              // of mostly skipped tiles costs a launch slot per skipped tile)
 };
 
 // Thread (inner element f, group of YS_RPT tile rows): Y in registers.
@@ -74,13 +77,15 @@ template <int NB, bool SYM>
 __global__ void __launch_bounds__(YS_THREADS)
 ystage_kernel(YsArgs A) {
   extern __shared__ double sm[];
-  const int64_t R0 = (A.t0 + blockIdx.x) * YS_TR, C0 = (int64_t)blockIdx.y * YS_TC;
+  const int bx = A.tiles ? A.tiles[2 * blockIdx.x] : (int)blockIdx.x;
+  const int by = A.tiles ? A.tiles[2 * blockIdx.x + 1] : (int)blockIdx.y;
+  const int64_t R0 = (A.t0 + bx) * YS_TR, C0 = (int64_t)by * YS_TC;
   const int nr = (int)min((int64_t)YS_TR, A.row_end - R0);
   const int nc = (int)min((int64_t)YS_TC, A.n_cols - C0);
   if (SYM && C0 + nc - 1 < R0) return;   // strictly below the diagonal: mirrored later
   if (A.row_ko) {
     const int ko = A.row_ko[(R0 - A.out_row0) / 64];
-    if (ko != INT32_MIN && A.col_ko[blockIdx.y] == ko) return;   // wq_ystage_mma's tile
+    if (ko != INT32_MIN && A.col_ko[by] == ko) return;   // wq_ystage_mma's tile
   }
   const int64_t ea = A.r_emin[R0], eb = A.r_emax[R0 + nr - 1];
   const int64_t fa = A.c_emin[C0], fb = A.c_emax[C0 + nc - 1];
@@ -403,8 +408,10 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
               const double* elh, const int64_t* kidx, const int* gidx, const double* m2u,
               int da1, const double* mgc, const double* ca, const double* cb, int64_t fspan,
               int64_t espan, double* out, int64_t ldo, int64_t row0, int64_t row1,
-              int sym_d, const int* row_ko, const int* col_ko, void* stream) {
+              int sym_d, const int* row_ko, const int* col_ko, const int* tiles,
+              int64_t n_tiles, void* stream) {
   if (n_rows <= 0 || n_cols <= 0 || nal < 1 || nal > da1 || nloc < 1 || nloc > YS_MAXLOC ||
+      (tiles && n_tiles < 0) ||
       wc < 1 || !e_rows || !r_emin || !r_emax || !c_el || !c_loc || !c_emin || !c_emax ||
       !coef || ldal < nal || !v || nb != YS_NB || !elh || !kidx || !gidx || !m2u || !ca || !cb ||
       fspan < 1 || espan < 1 || !out || row0 < 0 || row1 > n_rows || row1 <= row0 ||
@@ -414,7 +421,7 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
   }
   YsArgs A{n_rows, n_cols, n_el, nal, nloc, wc, e_rows, r_emin, r_emax, c_el, c_loc, c_emin,
            c_emax, coef, ldal, v, elh, kidx, gidx, m2u, da1, mgc, ca, cb, fspan, espan, out,
-           ldo, row0 / YS_TR, row0, row1, 0, row_ko, col_ko};
+           ldo, row0 / YS_TR, row0, row1, 0, row_ko, col_ko, tiles};
   const size_t smem = (size_t)(espan * nal * nloc + espan * nloc * YS_NB + espan * YS_NB +
                                (fspan + espan - 1) * nal * YS_NB + YS_TR * fspan * YS_NB) * 8 +
                       (size_t)espan * nloc * 4;
@@ -429,6 +436,10 @@ int wq_ystage(int64_t n_rows, int64_t n_cols, int64_t n_el, int nal, int nloc, i
   // rows [row0, row1): the last tile may run past row1 (up to n_rows) -- clip
   const int64_t nrow_tiles = ceil_div(row1 - row0, YS_TR);
   dim3 grid((unsigned)nrow_tiles, ceil_div(n_cols, YS_TC));
+  if (tiles) {
+    if (n_tiles == 0) return WQ_OK;
+    grid = dim3((unsigned)n_tiles, 1);
+  }
   // D (rows == cols, full range): only the storage entries out[c][r], c >= r
   // (the caller completes D and mirrors it, wq_mirror_lower)
   A.sym = n_rows == n_cols && row0 == 0 && row1 == n_rows && sym_d;
